@@ -1,0 +1,163 @@
+"""Seeded synthetic inputs shared by the oracle and the CUDA path.
+
+This module holds NO arithmetic of the method (no norm, attention, softmax,
+sampling or commit logic): only model shapes, seeded random tensors and the
+input recipes of DESIGN.md §"Input recipe". Both ``oracle`` and the tests /
+bench that drive the CUDA library take their inputs from here.
+
+Shapes follow BASELINE.json ``configs`` and SURVEY.md §8 "Fixed definitions"
+(Llama-3-8B-shaped layer: D=4096, 32 q / 8 kv heads, d_h=128, V=128256,
+F=14336, RoPE theta 500000, eps 1e-5).
+"""
+from dataclasses import dataclass, replace, asdict
+
+import numpy as np
+import torch
+
+
+@dataclass(frozen=True)
+class ModelConfig:
+    n_layers: int
+    d_model: int
+    n_q_heads: int
+    n_kv_heads: int
+    head_dim: int
+    vocab: int
+    ffn_dim: int            # 0 = no MLP
+    rope_theta: float = 500000.0
+    norm_eps: float = 1e-5
+    page_size: int = 64
+    n_pages: int = 64
+    max_slots: int = 8
+    max_batch: int = 8
+    max_depth: int = 8
+    max_pos: int = 1024
+
+    def with_(self, **kw):
+        return replace(self, **kw)
+
+    def as_dict(self):
+        return asdict(self)
+
+    @property
+    def qkv_rows(self):
+        return (self.n_q_heads + 2 * self.n_kv_heads) * self.head_dim
+
+
+# BASELINE.json configs[0]: toy verify (1 layer, 2 q / 2 kv heads x 64, vocab 512)
+TOY = ModelConfig(n_layers=1, d_model=128, n_q_heads=2, n_kv_heads=2, head_dim=64,
+                  vocab=512, ffn_dim=0, n_pages=64, max_slots=8, max_batch=8,
+                  max_depth=8, max_pos=512)
+# coverage variant with the MLP on (SURVEY.md §8 "toy+mlp")
+TOY_MLP = TOY.with_(ffn_dim=256)
+# BASELINE.json configs[1] (and north-star): Llama-3-8B-shaped single layer + lm-head
+LLAMA = ModelConfig(n_layers=1, d_model=4096, n_q_heads=32, n_kv_heads=8, head_dim=128,
+                    vocab=128256, ffn_dim=14336, n_pages=4608, max_slots=128,
+                    max_batch=128, max_depth=8, max_pos=8192 + 64)
+
+CONFIGS = {"toy": TOY, "toy_mlp": TOY_MLP, "llama": LLAMA}
+
+
+def _gen(seed):
+    g = torch.Generator(device="cpu")
+    g.manual_seed(int(seed))
+    return g
+
+
+def model_weights(cfg, seed=0, std=0.02, embed_std=1.0, norm_one=True):
+    """Random-init weights, bf16, [out, in] row-major, layer-stacked.
+
+    fp32 N(0, std^2) draws rounded once to bf16 by torch's cast (SURVEY.md §8(c)
+    S19: identical values are fed to both paths). Norm gains are 1 (or
+    1 + N(0, 0.1^2) with norm_one=False, to exercise the gain multiply).
+    """
+    g = _gen(seed)
+    L, D, V, F = cfg.n_layers, cfg.d_model, cfg.vocab, cfg.ffn_dim
+    hd = cfg.n_q_heads * cfg.head_dim
+
+    def rn(*shape, s):
+        return (torch.randn(*shape, generator=g, dtype=torch.float32) * s).to(torch.bfloat16)
+
+    def norm(*shape):
+        if norm_one:
+            return torch.ones(*shape, dtype=torch.bfloat16)
+        return (1.0 + 0.1 * torch.randn(*shape, generator=g)).to(torch.bfloat16)
+
+    w = {
+        "embed": rn(V, D, s=embed_std),
+        "attn_norm": norm(L, D),
+        "wqkv": rn(L, cfg.qkv_rows, D, s=std),
+        "wo": rn(L, D, hd, s=std),
+        "ffn_norm": norm(L, D),
+        "w_gate_up": rn(L, 2 * F, D, s=std) if F > 0 else torch.zeros(L, 0, D, dtype=torch.bfloat16),
+        "w_down": rn(L, D, F, s=std) if F > 0 else torch.zeros(L, D, 0, dtype=torch.bfloat16),
+        "final_norm": norm(D),
+        "lm_head": rn(V, D, s=std),
+    }
+    return w
+
+
+def context_kv(cfg, n_tokens, seed, std=1.0):
+    """Synthetic post-RoPE context K/V for one request: [n_layers][n][H_kv][d_h] bf16."""
+    g = _gen(seed)
+    shape = (cfg.n_layers, n_tokens, cfg.n_kv_heads, cfg.head_dim)
+    k = (torch.randn(*shape, generator=g) * std).to(torch.bfloat16)
+    v = (torch.randn(*shape, generator=g) * std).to(torch.bfloat16)
+    return k, v
+
+
+def random_tokens(n, vocab, seed):
+    g = _gen(seed)
+    return torch.randint(0, vocab, (n,), generator=g, dtype=torch.int32)
+
+
+def depths_uniform(batch, kmin, kmax, seed):
+    g = _gen(seed)
+    return torch.randint(kmin, kmax + 1, (batch,), generator=g, dtype=torch.int32)
+
+
+def draft_probs_dense(n_rows, vocab, seed, sharpness=3.0):
+    """Dense draft distributions q [n_rows][V] fp32 (rows sum to 1 in fp64 before the cast).
+
+    q = w / sum(w) with w = exp-distributed weights raised to `sharpness`
+    (a heavy-tailed random simplex point; no softmax involved).
+    """
+    g = _gen(seed)
+    e = -torch.log(torch.rand(n_rows, vocab, generator=g, dtype=torch.float64).clamp_min(1e-300))
+    w = e ** sharpness
+    q = w / w.sum(dim=1, keepdim=True)
+    return q.to(torch.float32)
+
+
+def draft_tokens_from(q_rows, seed):
+    """Draw one draft token per row from q (inverse-CDF on fp64 uniforms)."""
+    g = _gen(seed)
+    q = q_rows.to(torch.float64)
+    cdf = torch.cumsum(q, dim=1)
+    u = torch.rand(q.shape[0], 1, generator=g, dtype=torch.float64) * cdf[:, -1:]
+    tok = torch.searchsorted(cdf, u).clamp_max(q.shape[1] - 1)
+    return tok.view(-1).to(torch.int32)
+
+
+def planted_successor(cfg, weights, seed, beta):
+    """Planted-successor fixture (SURVEY.md §8(d) "Acceptance control").
+
+    Picks a permutation f of the vocab and adds beta * E[t]/||E[t]|| to
+    lm_head row f(t), so the model's argmax continuation of t is f(t) with a
+    margin set by beta. Returns (new_weights, f as int32 tensor).
+    """
+    g = _gen(seed)
+    V = cfg.vocab
+    f = torch.randperm(V, generator=g).to(torch.int64)
+    E = weights["embed"].to(torch.float32)
+    En = E / E.norm(dim=1, keepdim=True)
+    lm = weights["lm_head"].to(torch.float32).clone()
+    lm[f] += beta * En
+    w = dict(weights)
+    w["lm_head"] = lm.to(torch.bfloat16)
+    return w, f.to(torch.int32)
+
+
+def as_f64(t):
+    """bf16/fp32 torch tensor -> numpy fp64 (exact)."""
+    return t.detach().to("cpu").to(torch.float64).numpy()
