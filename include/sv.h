@@ -1,0 +1,241 @@
+/*
+ * sv.h — C ABI of the B200-native speculative-verify hot path (libsv.so).
+ *
+ * What this library computes: one decode lane of StreamServe (arXiv 2604.09562)
+ * — the batched, variable-depth speculative VERIFY step that the paper's
+ * PipeServe-Engine decode worker runs ("Adapt spec depth via SpecuStream;
+ * out <- llm_D.generate(req)", Alg. 3; "D_i: decode with
+ * SpecuStream, report metrics", Alg. 1), plus the KV
+ * concatenation it relies on (eq:kv_concatenation) and the
+ * prefill->decode KV transfer. The paper never
+ * defines the verification procedure; the one implemented here
+ * is Leviathan rejection sampling with a bonus token / greedy prefix match
+ * (PAPER.md:37, 65), fixed step by step in DESIGN.md "Readings" and
+ * SURVEY.md §8(c). The model is one (or more) Llama-shaped decoder layer(s) +
+ * lm-head with bf16 operands and fp32 accumulation.
+ *
+ * Conventions
+ *  - Every pointer is a DEVICE pointer unless its comment says (host).
+ *  - All device memory is allocated by the caller (PyTorch) and BORROWED; it
+ *    must outlive the context. The library never calls cudaMalloc.
+ *  - Every call enqueues work on the context's stream (given at sv_create)
+ *    and returns without synchronising, except where it says "syncs".
+ *    Device outputs are valid in stream order; device inputs must stay
+ *    unmodified until the stream has consumed them.
+ *  - Host-checkable misuse returns an error synchronously and enqueues
+ *    nothing. Device-detected problems set a sticky device error word that
+ *    is reported by the next sv_stats / sv_commit (see sv_status).
+ *  - A context is one decode lane on one GPU; it is not thread-safe.
+ *
+ * Sequence convention (SURVEY.md §8 "Verify rows"): a request with n
+ * committed tokens has cache length L = n - 1; its "pending" token (index L)
+ * has no KV yet. A verify of depth k evaluates the chain
+ * [pending, d_1..d_k] at absolute positions L..L+k (k + 1 query rows).
+ *
+ * Weight layout (all bf16, row-major [out][in], layer-stacked, BORROWED):
+ *   embed      [V][D]            attn_norm [n_layers][D]
+ *   wqkv       [n_layers][(Hq + 2 Hkv) d_h][D]   rows: q heads | k heads | v heads
+ *   wo         [n_layers][D][Hq d_h]
+ *   ffn_norm   [n_layers][D]     w_gate_up [n_layers][2F][D]  rows: gate F | up F
+ *   w_down     [n_layers][D][F]  final_norm [D]   lm_head [V][D]
+ * Every weight pointer must be 16-byte aligned.
+ *
+ * KV pool layout (bf16, BORROWED, size from sv_query_sizes):
+ *   [n_layers][n_pages][2 (K,V)][H_kv][page_size][d_h], keys stored post-RoPE.
+ */
+#ifndef SV_H_
+#define SV_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* sv_stream_t; /* == cudaStream_t */
+typedef struct sv_ctx sv_ctx;
+
+typedef enum {
+  SV_OK = 0,
+  SV_EINVAL = 1,   /* bad argument (null pointer, size out of range, duplicate slot, ...) */
+  SV_ESTATE = 2,   /* call not allowed in the slot's / context's current state */
+  SV_ENOKV = 3,    /* device free list ran out of KV pages (sticky, device-detected) */
+  SV_ECUDA = 4,    /* a CUDA runtime / driver call failed */
+  SV_ENCCL = 5,    /* an NCCL call failed */
+  SV_EDEVICE = 6   /* other device-detected error (bad token id, bad n_keep; sticky) */
+} sv_status;
+
+typedef enum { SV_GREEDY = 0, SV_SAMPLE = 1 } sv_mode;
+
+/* Device error word bits (sv_lane_stats.device_error). */
+#define SV_DERR_BAD_TOKEN 1   /* a draft / pending token outside [0, V) */
+#define SV_DERR_NO_PAGES 2    /* free list exhausted during append / commit */
+#define SV_DERR_BAD_KEEP 4    /* n_keep < 1 */
+
+typedef struct { /* (host) model + lane configuration */
+  int32_t n_layers, d_model, n_q_heads, n_kv_heads, head_dim, vocab;
+  int32_t ffn_dim;           /* 0 = no MLP (attention-only layer) */
+  float rope_theta, norm_eps;
+  int32_t page_size;         /* tokens per KV page: 64 */
+  int32_t n_pages;           /* pages in the pool (shared by all slots) */
+  int32_t max_slots;         /* request slots in this lane */
+  int32_t max_batch;         /* requests per sv_verify call */
+  int32_t max_depth;         /* k_i <= max_depth <= 32 */
+  int32_t max_pos;           /* RoPE table length >= max context + max_depth + 1 */
+} sv_config;
+
+typedef struct { /* device pointers, bf16, layouts above; BORROWED */
+  const void *embed, *attn_norm, *wqkv, *wo, *ffn_norm, *w_gate_up, *w_down, *final_norm, *lm_head;
+} sv_weights;
+
+typedef struct { /* (host) lane acceptance counters — SURVEY.md §8(a) a7; a_t = accepted / drafted */
+  uint64_t steps;                 /* sv_verify calls */
+  uint64_t rows;                  /* sum (k_i + 1) */
+  uint64_t drafted;               /* sum k_i */
+  uint64_t accepted;              /* sum a_i (prefix-stopped) */
+  uint64_t emitted;               /* sum (a_i + 1) */
+  uint64_t accepted_independent;  /* sum_j [u_j < r_j] over all j <= k_i (greedy: d_j == argmax) */
+  uint64_t hist_accepted[33];     /* count of requests with a_i = m */
+  uint64_t drafted_by_k[33];      /* sum k_i over requests with k_i = k */
+  uint64_t accepted_by_k[33];     /* sum a_i over requests with k_i = k */
+  int32_t device_error;           /* sticky SV_DERR_* bits */
+  int32_t _pad;
+} sv_lane_stats;
+
+/* Library version string, e.g. "sv 0.1 sm_100a". */
+const char* sv_version(void);
+/* Static message for a status code. */
+const char* sv_strerror(sv_status s);
+
+/* Bytes the caller must allocate for the KV pool and the workspace for cfg.
+ * Both buffers must be 1024-byte aligned. EINVAL on an invalid cfg
+ * (non-positive sizes, n_q_heads % n_kv_heads != 0, head_dim not in {64,128},
+ * d_model % 64 != 0, max_depth > 32, (max_depth + 1) * group > 64). */
+sv_status sv_query_sizes(const sv_config* cfg, size_t* kv_pool_bytes, size_t* workspace_bytes);
+
+/* Create a lane on the current CUDA device. Builds the fp32 RoPE table
+ * (fp64 angles, SURVEY.md §8(c) "Model details"), the device free list and the
+ * TMA descriptors, on `stream`; the kv_pool contents are not read.
+ * Syncs `stream` once before returning. */
+sv_status sv_create(const sv_config* cfg, const sv_weights* w, void* kv_pool, void* workspace,
+                    sv_stream_t stream, sv_ctx** out);
+/* Destroy the context (syncs its stream). Borrowed memory is not freed. */
+sv_status sv_destroy(sv_ctx* ctx);
+
+/* Append n_tokens of context KV to `slot` (eq:kv_concatenation):
+ * k, v: [n_layers][n_tokens][H_kv][d_h] bf16, post-RoPE (read in stream order).
+ * An EMPTY slot becomes ACTIVE and is bound to request_id (the Philox key of
+ * all its draws, so outputs never depend on slot or lane); on an ACTIVE slot
+ * request_id must match. Pages are popped from the device free list
+ * (SV_DERR_NO_PAGES if it runs out). pending_token becomes the chain head of
+ * the next verify. ESTATE on a PENDING slot (verified, not committed).
+ * n_tokens may be 0 (only sets the pending token). */
+sv_status sv_append_kv(sv_ctx* ctx, int32_t slot, uint64_t request_id, const void* k, const void* v,
+                       int32_t n_tokens, int32_t pending_token);
+
+/* The verify step. For each request b < batch:
+ *   slots[b]  (host) distinct ACTIVE slots;  depths[b] (host) k_b in [0, max_depth]
+ *   draft_tokens [sum k] int32, request-major (the drafter's tokens)
+ *   draft_probs  [sum k][V] fp32 rows q_j (the drafter's distributions) or NULL = one-hot drafts
+ *   seed: Philox key; mode: SV_GREEDY (argmax prefix match; seed, temperature and
+ *   draft_probs ignored) or SV_SAMPLE (Leviathan: accept iff u < p/q, residual /
+ *   bonus exponential race); temperature > 0 in SAMPLE (p = softmax(l / T)).
+ * Outputs (device, written in stream order):
+ *   accepted_len [batch] int32 a_b in [0, k_b] (-1 if the request hit a device error)
+ *   out_tokens   [batch][max_depth + 1] int32: d_1..d_a, y, then -1 padding
+ *   logits_out   NULL or [sum (k + 1)][V] fp32 copy of the target logits (pre-temperature)
+ * Lane counters are updated on the device. The call has no effect on the KV
+ * cache or slot lengths: the slots become PENDING until sv_commit.
+ * EINVAL: batch < 1 or > max_batch, bad depth, duplicate/out-of-range slot,
+ * null pointers, temperature <= 0 in SAMPLE. ESTATE: a slot not ACTIVE. */
+sv_status sv_verify(sv_ctx* ctx, int32_t batch, const int32_t* slots, const int32_t* depths,
+                    const int32_t* draft_tokens, const float* draft_probs, uint64_t seed,
+                    sv_mode mode, float temperature, int32_t* accepted_len, int32_t* out_tokens,
+                    float* logits_out);
+
+/* Decision-only verify (a6 + a7) on caller-provided logits [sum (k + 1)][V] fp32
+ * (rows in request-major chain order). Same RNG keying as sv_verify (the slot's
+ * request_id, positions from the slot's length). Runs no model and produces no
+ * chain KV: slots stay ACTIVE and the call is not committable. */
+sv_status sv_verify_logits(sv_ctx* ctx, int32_t batch, const int32_t* slots, const int32_t* depths,
+                           const int32_t* draft_tokens, const float* draft_probs, const float* logits,
+                           uint64_t seed, sv_mode mode, float temperature, int32_t* accepted_len,
+                           int32_t* out_tokens);
+
+/* Commit the last sv_verify (eq:kv_concatenation): for each
+ * request copy chain K/V rows 0..n-1 (n = a_b + 1, or min(n_keep[b], a_b + 1))
+ * into pages at positions L..L+n-1, popping pages at page boundaries; then
+ * L += n and pending <- the n-th emitted token. Rejected rows are dropped
+ * (rollback). n_keep: NULL or DEVICE int32 [batch] (values >= 1).
+ * ESTATE if there is no uncommitted verify. Returns the sticky device error
+ * observed so far WITHOUT syncing (i.e. from earlier sv_stats), else SV_OK. */
+sv_status sv_commit(sv_ctx* ctx, const int32_t* n_keep);
+
+/* Return the slot's pages to the free list; the slot becomes EMPTY. ESTATE if PENDING. */
+sv_status sv_release(sv_ctx* ctx, int32_t slot);
+
+/* Copy the lane counters to *out (host). Syncs the stream. reset != 0 zeroes
+ * the counters (not the error word). Returns SV_ENOKV / SV_EDEVICE if the
+ * sticky device error word is set. */
+sv_status sv_stats(sv_ctx* ctx, sv_lane_stats* out, int reset);
+
+/* Test hooks (teacher-forced parity). Buffers of the
+ * last sv_verify, valid in stream order until the next sv_verify. Names:
+ *   "h0" [T][D] f32 embed   "a" [T][D] bf16 attn-norm   "q" [T][Hq][d_h] bf16
+ *   "kc","vc" [n_layers][T][Hkv][d_h] bf16 chain K/V   "o" [T][Hq d_h] bf16
+ *   "h1" [T][D] f32   "b" [T][D] bf16   "u" [T][F] bf16   "h2" [T][D] f32
+ *   "z" [T][D] bf16   "logits" [T][V] f32   "tile_max","tile_sum" [T][nt] f32
+ *   "tile_arg" [T][nt] i32 (nt = ceil(V / 256))   "row_off" [batch+1] i32
+ *   "rope_cos","rope_sin" [max_pos][d_h/2] f32   "len","pending" [max_slots] i32
+ *   "page_table" [max_slots][max_pages_per_slot] i32   "free_top" [1] i32
+ * (the "last layer" values when n_layers > 1). sv_set_taps is accepted for
+ * ABI compatibility; buffers are always retained. */
+sv_status sv_set_taps(sv_ctx* ctx, int enable);
+sv_status sv_get_tap(sv_ctx* ctx, const char* name, void** dev_ptr, size_t* bytes);
+
+/* Test hook: u[i] = U(seed, rid, z, purpose, x0 + i) for i < n, computed by the
+ * same device Philox the verifier uses (fp32 out; purpose 0 ACCEPT, 1 RACE). */
+sv_status sv_debug_uniforms(sv_ctx* ctx, uint64_t seed, uint64_t rid, uint32_t z, int32_t purpose,
+                            int32_t x0, int32_t n, float* u);
+
+/* Bench fixture (planted-successor drafter, SURVEY.md §8(d) "Acceptance control"):
+ * for each request b (slots/depths (host) as in sv_verify), d_1 = succ[pending_b],
+ * d_j = succ[d_{j-1}], except where dev_mask[row] != 0 the token is dev_tok[row]
+ * (rows request-major, sum k). Writes draft_tokens [sum k] int32. One launch. */
+sv_status sv_draft_planted(sv_ctx* ctx, int32_t batch, const int32_t* slots, const int32_t* depths,
+                           const int32_t* succ, const uint8_t* dev_mask, const int32_t* dev_tok,
+                           int32_t* draft_tokens);
+
+/* ---------------- prefill -> decode KV hand-off ----------------
+ * NCCL point-to-point over NVLink ("NIXL" replaced by
+ * ncclSend/ncclRecv). Communicators are created by the library; the 128-byte
+ * unique id travels through the caller's process group (torch.distributed store). */
+sv_status sv_nccl_unique_id(uint8_t id[128]);
+sv_status sv_nccl_comm_init(int nranks, const uint8_t id[128], int rank, void** comm);
+sv_status sv_nccl_comm_destroy(void* comm);
+
+/* Prefill side: send n_tokens of packed KV [n_layers][n_tokens][2][H_kv][d_h] bf16
+ * followed by a 16-byte trailer {int32 pending_token, 3 x int32 reserved}
+ * (kv_packed must be contiguous, 16-byte aligned) to `peer` on `stream`. */
+sv_status sv_kv_send(const void* kv_packed, int32_t n_layers, int32_t n_kv_heads, int32_t head_dim,
+                     int32_t n_tokens, int peer, void* nccl_comm, sv_stream_t stream);
+
+/* Decode side: receive that message into the lane's staging buffer and append
+ * it to `slot` (sv_append_kv semantics; the pending token comes from the
+ * trailer on the device). staging: DEVICE buffer of at least
+ * sv_kv_packed_bytes(cfg, n_tokens) bytes, owned by the caller. */
+sv_status sv_kv_recv_append(sv_ctx* ctx, int32_t slot, uint64_t request_id, int32_t n_tokens,
+                            void* staging, int peer, void* nccl_comm);
+size_t sv_kv_packed_bytes(const sv_config* cfg, int32_t n_tokens);
+
+/* Pack context K/V [n_layers][n][H_kv][d_h] (two tensors) + pending into the
+ * hand-off wire format on `stream` (used by the prefill side). */
+sv_status sv_kv_pack(const void* k, const void* v, int32_t n_layers, int32_t n_kv_heads,
+                     int32_t head_dim, int32_t n_tokens, int32_t pending_token, void* kv_packed,
+                     sv_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SV_H_ */

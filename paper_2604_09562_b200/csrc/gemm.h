@@ -1,0 +1,24 @@
+// GEMM front-end used by the verify sequence: C = A[M][K] * B[N][K]^T with a fused
+// epilogue per call site.
+#pragma once
+#include "lane.h"
+
+namespace sv {
+
+enum GemmEpiKind { EPI_NONE = 0, EPI_QKV_ROPE = 1, EPI_RESIDUAL = 2, EPI_SWIGLU = 3, EPI_LOGITS = 4 };
+
+struct GemmEpi {
+  int layer;               // QKV: which layer's chain K/V scratch to write
+  const float* resid_in;   // RESIDUAL: h_in  (fp32 [M][N])
+  float* resid_out;        // RESIDUAL: h_out (fp32 [M][N]); may alias resid_in
+  float inv_temp;          // LOGITS: statistics are of l * inv_temp
+};
+
+struct GemmPlan;
+size_t gemm_workspace_bytes();
+GemmPlan* gemm_plan_create(const LaneDev& d, void* ws, cudaStream_t s);
+void gemm_plan_destroy(GemmPlan* p);
+cudaError_t gemm_run(GemmPlan* p, const bf16* A, const bf16* B, float* C, int M, int N, int K, int epi,
+                     const GemmEpi& e, cudaStream_t s);
+
+}  // namespace sv

@@ -1,0 +1,166 @@
+// a3: paged, GQA, chain-causal verify attention — first (SIMT, fp32 FMA) implementation
+// with split-KV partials and a combine pass. The tensor-core version replaces the main
+// kernel; the work list, partial layout and combine are shared.
+//
+// Semantics: for request b with cache length L and chain
+// rows j = 0..k, query (j, q head hq) attends cache keys 0..L-1 (pages) and chain keys
+// 0..j (scratch kc/vc), kv head hq / G, scale 1/sqrt(d_h), softmax.
+#include "common.cuh"
+#include "lane.h"
+
+namespace sv {
+
+constexpr int AS_KC = 32;   // keys per chunk
+
+__global__ void __launch_bounds__(128) attn_simt_kernel(LaneDev d, int layer) {
+  extern __shared__ float smem[];
+  const int dh = d.dh, G = d.Hq / d.Hkv;
+  float* Qs = smem;                              // [64][dh]
+  float* Ks = Qs + kAttnRows * dh;               // [dh][AS_KC + 1] (transposed)
+  float* Vs = Ks + dh * (AS_KC + 1);             // [AS_KC][dh]
+  float* Ps = Vs + AS_KC * dh;                   // [64][AS_KC]
+  float* Ms = Ps + kAttnRows * AS_KC;            // [64] running max
+  float* Ls = Ms + kAttnRows;                    // [64] running sum
+  float* Cs = Ls + kAttnRows;                    // [64] correction
+  const float scale = 1.0f / sqrtf(float(dh));
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int n_items = *d.n_items;
+  const size_t nkv = (size_t)d.Hkv * dh;
+
+  for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+    const int4 item = d.items[it];
+    const int b = item.x, h = item.y, split = item.z;
+    const int slot = d.slots[b], R = d.depths[b] + 1, L = d.len[slot];
+    const int row0 = d.row_off[b];
+    const int nr = R * G;
+    const int t0 = split * kSplitKeys;
+    const int t1 = min(t0 + kSplitKeys, L + R);
+    __syncthreads();
+    for (int i = tid; i < nr * dh; i += 128) {
+      const int rl = i / dh, dd = i % dh, j = rl / G, g = rl % G;
+      Qs[i] = bf2f(d.q[((size_t)(row0 + j) * d.Hq + h * G + g) * dh + dd]);
+    }
+    for (int r = tid; r < kAttnRows; r += 128) { Ms[r] = -INFINITY; Ls[r] = 0.f; }
+    const int groups = 128 / dh;                 // 1 (dh=128) or 2 (dh=64)
+    const int dd_own = tid % dh, rg = tid / dh;
+    float acc[kAttnRows];
+#pragma unroll
+    for (int i = 0; i < kAttnRows; ++i) acc[i] = 0.f;
+
+    for (int c0 = t0; c0 < t1; c0 += AS_KC) {
+      __syncthreads();
+      // load K (transposed) and V for keys c0 .. c0+31
+      for (int i = tid; i < AS_KC * dh; i += 128) {
+        const int kt = i / dh, dd = i % dh, t = c0 + kt;
+        float kv = 0.f, vv = 0.f;
+        if (t < t1) {
+          if (t < L) {
+            const int page = d.page_table[slot * d.max_pages_per_slot + t / d.page];
+            const size_t base = (((size_t)layer * d.n_pages + page) * 2) * d.Hkv;
+            const size_t off = (size_t)(t % d.page) * dh + dd;
+            kv = bf2f(d.pool[((base + h) * d.page) * dh + off]);
+            vv = bf2f(d.pool[((base + d.Hkv + h) * d.page) * dh + off]);
+          } else {
+            const size_t crow = (size_t)layer * d.Tmax + row0 + (t - L);
+            kv = bf2f(d.kc[crow * nkv + (size_t)h * dh + dd]);
+            vv = bf2f(d.vc[crow * nkv + (size_t)h * dh + dd]);
+          }
+        }
+        Ks[dd * (AS_KC + 1) + kt] = kv;
+        Vs[kt * dh + dd] = vv;
+      }
+      __syncthreads();
+      // scores S[rl][kt]
+      for (int p = tid; p < nr * AS_KC; p += 128) {
+        const int rl = p / AS_KC, kt = p % AS_KC, t = c0 + kt, j = rl / G;
+        float s = -INFINITY;
+        if (t < t1 && t <= L + j) {
+          float dot = 0.f;
+          const float* qr = Qs + rl * dh;
+          for (int dd = 0; dd < dh; ++dd) dot = fmaf(qr[dd], Ks[dd * (AS_KC + 1) + kt], dot);
+          s = dot * scale;
+        }
+        Ps[rl * AS_KC + kt] = s;
+      }
+      __syncthreads();
+      // online softmax, one warp per row
+      for (int rl = warp; rl < nr; rl += 4) {
+        const float s = Ps[rl * AS_KC + lane];
+        const float m_old = Ms[rl];
+        const float m_new = fmaxf(m_old, warp_max(s));
+        const float p = m_new == -INFINITY ? 0.f : expf(s - m_new);
+        const float corr = m_new == -INFINITY ? 1.f : expf(m_old - m_new);
+        const float ps = warp_sum(p);
+        Ps[rl * AS_KC + lane] = p;
+        if (lane == 0) { Ms[rl] = m_new; Ls[rl] = Ls[rl] * corr + ps; Cs[rl] = corr; }
+      }
+      __syncthreads();
+      // O[rl][dd] = O * corr + sum_t P V
+#pragma unroll
+      for (int i = 0; i < kAttnRows; ++i) {
+        const int rl = rg + i * groups;
+        if (i * groups < kAttnRows && rl < nr) {
+          float o = acc[i] * Cs[rl];
+#pragma unroll 8
+          for (int kt = 0; kt < AS_KC; ++kt) o = fmaf(Ps[rl * AS_KC + kt], Vs[kt * dh + dd_own], o);
+          acc[i] = o;
+        }
+      }
+    }
+    __syncthreads();
+    float* po = d.part_o + (size_t)it * kAttnRows * dh;
+#pragma unroll
+    for (int i = 0; i < kAttnRows; ++i) {
+      const int rl = rg + i * groups;
+      if (i * groups < kAttnRows && rl < nr) po[rl * dh + dd_own] = acc[i];
+    }
+    for (int rl = tid; rl < nr; rl += 128) {
+      d.part_ml[((size_t)it * kAttnRows + rl) * 2 + 0] = Ms[rl];
+      d.part_ml[((size_t)it * kAttnRows + rl) * 2 + 1] = Ls[rl];
+    }
+  }
+}
+
+cudaError_t launch_attention(const LaneDev& d, int layer, int batch, cudaStream_t s) {
+  const size_t smem = sizeof(float) * ((size_t)kAttnRows * d.dh + (size_t)d.dh * (AS_KC + 1) +
+                                       (size_t)AS_KC * d.dh + kAttnRows * AS_KC + 3 * kAttnRows);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(attn_simt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+    attr = true;
+  }
+  attn_simt_kernel<<<148 * 4, 128, smem, s>>>(d, layer);
+  return cudaGetLastError();
+}
+
+// combine split-KV partials: one CTA per chain row, threads over (q head, dim)
+__global__ void attn_combine_kernel(LaneDev d) {
+  const int r = blockIdx.x;
+  const int b = d.row_req[r], j = r - d.row_off[b];
+  const int G = d.Hq / d.Hkv, dh = d.dh;
+  const int slot = d.slots[b], R = d.depths[b] + 1, L = d.len[slot];
+  const int ns = (L + R + kSplitKeys - 1) / kSplitKeys;
+  for (int i = threadIdx.x; i < d.Hq * dh; i += blockDim.x) {
+    const int hq = i / dh, dd = i % dh, h = hq / G, g = hq % G, rl = j * G + g;
+    const int base = d.item_start[b] + h * ns;
+    float M = -INFINITY;
+    for (int s = 0; s < ns; ++s) M = fmaxf(M, d.part_ml[((size_t)(base + s) * kAttnRows + rl) * 2]);
+    float l = 0.f, o = 0.f;
+    for (int s = 0; s < ns; ++s) {
+      const size_t it = base + s;
+      const float ms = d.part_ml[(it * kAttnRows + rl) * 2];
+      if (ms == -INFINITY) continue;
+      const float w = expf(ms - M);
+      l += d.part_ml[(it * kAttnRows + rl) * 2 + 1] * w;
+      o += d.part_o[(it * kAttnRows + rl) * dh + dd] * w;
+    }
+    d.o[(size_t)r * d.Hq * dh + i] = f2bf(o / l);
+  }
+}
+
+cudaError_t launch_attn_combine(const LaneDev& d, int T, cudaStream_t s) {
+  attn_combine_kernel<<<T, 256, 0, s>>>(d);
+  return cudaGetLastError();
+}
+
+}  // namespace sv

@@ -1,0 +1,180 @@
+// KV-cache state kernels:
+//   a8  commit / rollback compaction (eq:kv_concatenation): chain rows
+//       0..n-1 of kc/vc -> pages at positions L..L+n-1, pages popped from the device free list
+//   a9  append (sv_append_kv / hand-off receive): context K/V -> newly popped pages
+//   release: pages back to the free list; hand-off wire packing.
+// Device free list: a stack free_list[0 .. top-1]; pops take [top-n, top) with one
+// atomicSub per request, pushes append with one atomicAdd (stream-ordered, never concurrent).
+#include "common.cuh"
+#include "lane.h"
+#include "../../include/sv.h"
+
+namespace sv {
+
+SV_DEV size_t pool_row(const LaneDev& d, int layer, int page, int kv, int h, int off) {
+  return ((((size_t)layer * d.n_pages + page) * 2 + kv) * d.Hkv + h) * d.page + off;
+}
+
+// pop `n` pages for `slot` whose first new page index is `first`; returns false on exhaustion
+SV_DEV bool pop_pages(const LaneDev& d, int slot, int first, int n) {
+  if (n <= 0) return true;
+  const int old = atomicSub(d.free_top, n);
+  if (old - n < 0) {
+    atomicOr(d.err, SV_DERR_NO_PAGES);
+    return false;
+  }
+  for (int i = 0; i < n; ++i) d.page_table[slot * d.max_pages_per_slot + first + i] = d.free_list[old - n + i];
+  return true;
+}
+
+// ------------------------------------------------------------------ a8 commit
+__global__ void __launch_bounds__(256) commit_kernel(LaneDev d, const int* __restrict__ n_keep) {
+  __shared__ int s_n, s_ok;
+  const int b = blockIdx.x;
+  const int slot = d.slots[b], L = d.len[slot];
+  if (threadIdx.x == 0) {
+    int n = d.acc_int[b] + 1;                    // acc_int = -1 on error -> n = 0
+    if (n > 0 && n_keep) {
+      const int nk = n_keep[b];
+      if (nk < 1) { atomicOr(d.err, SV_DERR_BAD_KEEP); n = 0; }
+      else if (nk < n) n = nk;
+    }
+    int ok = n > 0;
+    if (ok) {
+      const int have = (L + d.page - 1) / d.page, need = (L + n + d.page - 1) / d.page;
+      ok = pop_pages(d, slot, have, need - have);
+    }
+    s_n = n;
+    s_ok = ok;
+  }
+  __syncthreads();
+  if (!s_ok) return;
+  const int n = s_n, row0 = d.row_off[b];
+  const int vec_per_row = d.dh / 8;              // 16-byte vectors per (token, kv head)
+  const int per_tok = 2 * d.Hkv * vec_per_row;
+  const size_t nkv = (size_t)d.Hkv * d.dh;
+  for (int layer = 0; layer < d.n_layers; ++layer) {
+    for (int i = threadIdx.x; i < n * per_tok; i += blockDim.x) {
+      const int c = i / per_tok, rem = i % per_tok;
+      const int kv = rem / (d.Hkv * vec_per_row), h = (rem / vec_per_row) % d.Hkv, v8 = rem % vec_per_row;
+      const int t = L + c;
+      const int page = d.page_table[slot * d.max_pages_per_slot + t / d.page];
+      const bf16* src = (kv ? d.vc : d.kc) + ((size_t)layer * d.Tmax + row0 + c) * nkv + (size_t)h * d.dh + v8 * 8;
+      bf16* dst = d.pool + pool_row(d, layer, page, kv, h, t % d.page) * d.dh + v8 * 8;
+      *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(src);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    d.len[slot] = L + n;
+    d.pending[slot] = d.tok_int[(size_t)b * (d.max_depth + 1) + n - 1];
+  }
+}
+
+cudaError_t launch_commit(const LaneDev& d, const int* n_keep, int batch, cudaStream_t s) {
+  commit_kernel<<<batch, 256, 0, s>>>(d, n_keep);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ append (alloc + copy)
+// scratch int: d.batch_n is reused? no — a dedicated word: item_start[kMaxBatch] region is per
+// verify; append keeps its old length in n_items[1] (workspace word reserved for it).
+__global__ void append_alloc_kernel(LaneDev d, int slot, unsigned long long rid, int n, int pending,
+                                    const int* pending_dev, int* scratch) {
+  const int L = d.len[slot];
+  const int have = (L + d.page - 1) / d.page, need = (L + n + d.page - 1) / d.page;
+  int ok = 1;
+  if (need > d.max_pages_per_slot) { atomicOr(d.err, SV_DERR_NO_PAGES); ok = 0; }
+  if (ok) ok = pop_pages(d, slot, have, need - have);
+  int pend = pending_dev ? *pending_dev : pending;
+  if (pend < 0 || pend >= d.V) { atomicOr(d.err, SV_DERR_BAD_TOKEN); pend = 0; }
+  scratch[0] = L;
+  scratch[1] = ok;
+  if (ok) {
+    d.len[slot] = L + n;
+    d.pending[slot] = pend;
+    d.rid[slot] = rid;
+  }
+}
+
+// k, v: [n_layers][n][Hkv][dh] (packed = 0) or one buffer [n_layers][n][2][Hkv][dh] (packed = 1)
+__global__ void append_copy_kernel(LaneDev d, int slot, const bf16* __restrict__ k, const bf16* __restrict__ v,
+                                   int n, int packed, const int* __restrict__ scratch) {
+  if (!scratch[1]) return;
+  const int L = scratch[0];
+  const int vec_per_row = d.dh / 8;
+  const size_t per_tok = (size_t)2 * d.Hkv * vec_per_row;
+  const size_t total = (size_t)d.n_layers * n * per_tok;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+    const size_t lt = i / per_tok;
+    const int rem = int(i % per_tok);
+    const int layer = int(lt / n), c = int(lt % n);
+    const int kv = rem / (d.Hkv * vec_per_row), h = (rem / vec_per_row) % d.Hkv, v8 = rem % vec_per_row;
+    const bf16* src;
+    if (packed) src = k + ((((size_t)layer * n + c) * 2 + kv) * d.Hkv + h) * d.dh + v8 * 8;
+    else src = (kv ? v : k) + (((size_t)layer * n + c) * d.Hkv + h) * d.dh + v8 * 8;
+    const int t = L + c;
+    const int page = d.page_table[slot * d.max_pages_per_slot + t / d.page];
+    bf16* dst = d.pool + pool_row(d, layer, page, kv, h, t % d.page) * d.dh + v8 * 8;
+    *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(src);
+  }
+}
+
+cudaError_t launch_append(const LaneDev& d, int slot, unsigned long long rid, const bf16* k, const bf16* v, int n,
+                          int pending, const int* pending_dev, int packed, cudaStream_t s) {
+  int* scratch = d.n_items + 1;                  // two spare workspace words
+  append_alloc_kernel<<<1, 1, 0, s>>>(d, slot, rid, n, pending, pending_dev, scratch);
+  if (n > 0) {
+    const size_t total = (size_t)d.n_layers * n * 2 * d.Hkv * (d.dh / 8);
+    int grid = (int)((total + 255) / 256);
+    if (grid > 148 * 8) grid = 148 * 8;
+    append_copy_kernel<<<grid, 256, 0, s>>>(d, slot, k, v, n, packed, scratch);
+  }
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ release
+__global__ void release_kernel(LaneDev d, int slot) {
+  const int L = d.len[slot];
+  const int n = (L + d.page - 1) / d.page;
+  __shared__ int s_old;
+  if (threadIdx.x == 0) s_old = atomicAdd(d.free_top, n);
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x)
+    d.free_list[s_old + i] = d.page_table[slot * d.max_pages_per_slot + i];
+  __syncthreads();
+  if (threadIdx.x == 0) { d.len[slot] = 0; d.pending[slot] = 0; d.rid[slot] = 0ull; }
+}
+
+cudaError_t launch_release(const LaneDev& d, int slot, cudaStream_t s) {
+  release_kernel<<<1, 256, 0, s>>>(d, slot);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ hand-off packing
+__global__ void kv_pack_kernel(const bf16* __restrict__ k, const bf16* __restrict__ v, int n_layers, int Hkv, int dh,
+                               int n, int pending, bf16* __restrict__ out) {
+  const int vpr = dh / 8;
+  const size_t per_tok = (size_t)2 * Hkv * vpr;
+  const size_t total = (size_t)n_layers * n * per_tok;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+    const size_t lt = i / per_tok;
+    const int rem = int(i % per_tok);
+    const int kv = rem / (Hkv * vpr), h = (rem / vpr) % Hkv, v8 = rem % vpr;
+    const bf16* src = (kv ? v : k) + (lt * Hkv + h) * dh + v8 * 8;
+    *reinterpret_cast<uint4*>(out + i * 8) = *reinterpret_cast<const uint4*>(src);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    int* trailer = reinterpret_cast<int*>(out + total * 8);
+    trailer[0] = pending;
+    trailer[1] = trailer[2] = trailer[3] = 0;
+  }
+}
+
+cudaError_t launch_kv_pack(const bf16* k, const bf16* v, int n_layers, int Hkv, int dh, int n, int pending,
+                           void* packed, cudaStream_t s) {
+  kv_pack_kernel<<<148 * 2, 256, 0, s>>>(k, v, n_layers, Hkv, dh, n, pending, reinterpret_cast<bf16*>(packed));
+  return cudaGetLastError();
+}
+
+}  // namespace sv

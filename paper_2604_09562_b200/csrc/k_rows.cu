@@ -1,0 +1,300 @@
+// Row-wise kernels of the verify step:
+//   a1  plan: ragged batch assembly (row offsets, chain tokens, positions, attention work list)
+//   a2  embed + attn RMSNorm; generic RMSNorm; QKV RoPE epilogue
+//   a4  residual and SwiGLU epilogues
+//   a5  lm-head vocab-tile statistics (max, sum exp, lowest argmax)
+// plus test / fixture kernels (device Philox uniforms, planted drafter) and
+// lane-state initialisation.
+#include "common.cuh"
+#include "lane.h"
+#include "../../include/sv.h"
+
+namespace sv {
+
+// ------------------------------------------------------------------ a1: plan
+// One CTA. Serial prefix over <= 256 requests in thread 0, then parallel fills.
+__global__ void plan_kernel(LaneDev d, PlanArgs p, const int* __restrict__ draft_tokens, int attn) {
+  __shared__ int s_off[kMaxBatch + 1];
+  __shared__ int s_item[kMaxBatch + 1];
+  __shared__ int s_err[kMaxBatch];
+  const int B = p.batch;
+  if (threadIdx.x == 0) {
+    int o = 0, it = 0;
+    for (int b = 0; b < B; ++b) {
+      s_off[b] = o;
+      s_item[b] = it;
+      const int R = p.depths[b] + 1;
+      o += R;
+      if (attn) {
+        const int keys = d.len[p.slots[b]] + R;
+        it += ((keys + kSplitKeys - 1) / kSplitKeys) * d.Hkv;
+      }
+    }
+    s_off[B] = o;
+    s_item[B] = it;
+    *d.n_items = it;
+    *d.batch_n = B;
+  }
+  for (int b = threadIdx.x; b < B; b += blockDim.x) s_err[b] = 0;
+  __syncthreads();
+  for (int b = threadIdx.x; b <= B; b += blockDim.x) {
+    d.row_off[b] = s_off[b];
+    d.item_start[b] = s_item[b];
+    if (b < B) {
+      d.slots[b] = p.slots[b];
+      d.depths[b] = p.depths[b];
+    }
+  }
+  for (int r = threadIdx.x; r < p.T; r += blockDim.x) {
+    int lo = 0, hi = B - 1;                      // last b with s_off[b] <= r
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (s_off[mid] <= r) lo = mid; else hi = mid - 1;
+    }
+    const int b = lo, j = r - s_off[b], slot = p.slots[b];
+    int tok = j == 0 ? d.pending[slot] : draft_tokens[s_off[b] - b + j - 1];
+    if (tok < 0 || tok >= d.V) {
+      atomicOr(&s_err[b], 1);
+      tok = 0;
+    }
+    d.row_req[r] = b;
+    d.row_pos[r] = d.len[slot] + j;
+    d.chain_tok[r] = tok;
+  }
+  if (attn) {
+    const int n_items = s_item[B];
+    for (int it = threadIdx.x; it < n_items; it += blockDim.x) {
+      int lo = 0, hi = B - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (s_item[mid] <= it) lo = mid; else hi = mid - 1;
+      }
+      const int b = lo, rel = it - s_item[b];
+      const int keys = d.len[p.slots[b]] + p.depths[b] + 1;
+      const int ns = (keys + kSplitKeys - 1) / kSplitKeys;
+      d.items[it] = make_int4(b, rel / ns, rel % ns, ns);
+    }
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < B; b += blockDim.x) {
+    d.req_err[b] = s_err[b];
+    if (s_err[b]) atomicOr(d.err, SV_DERR_BAD_TOKEN);
+  }
+}
+
+cudaError_t launch_plan(const LaneDev& d, const PlanArgs& p, const int* draft_tokens, bool attn, cudaStream_t s) {
+  plan_kernel<<<1, 1024, 0, s>>>(d, p, draft_tokens, attn ? 1 : 0);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ a2: embed + RMSNorm
+// h0 = E[c]; a = bf16(RMSNorm(h0) * g), RMSNorm in fp32.
+template <int NT>
+__device__ float block_sum(float v) {
+  __shared__ float red[NT / 32];
+  v = warp_sum(v);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  float t = 0.f;
+#pragma unroll
+  for (int i = 0; i < NT / 32; ++i) t += red[i];
+  __syncthreads();
+  return t;
+}
+
+__global__ void __launch_bounds__(256) embed_norm_kernel(LaneDev d) {
+  const int r = blockIdx.x;
+  const int tok = d.chain_tok[r];
+  const bf16* e = d.embed + (size_t)tok * d.D;
+  float* h = d.h0 + (size_t)r * d.D;
+  float ss = 0.f;
+  for (int i = threadIdx.x; i < d.D; i += 256) {
+    const float x = bf2f(e[i]);
+    h[i] = x;
+    ss += x * x;
+  }
+  const float rstd = 1.0f / sqrtf(block_sum<256>(ss) / float(d.D) + d.eps);
+  for (int i = threadIdx.x; i < d.D; i += 256) d.a[(size_t)r * d.D + i] = f2bf(h[i] * rstd * bf2f(d.attn_norm[i]));
+}
+
+cudaError_t launch_embed_norm(const LaneDev& d, int T, cudaStream_t s) {
+  embed_norm_kernel<<<T, 256, 0, s>>>(d);
+  return cudaGetLastError();
+}
+
+__global__ void __launch_bounds__(256) rmsnorm_kernel(const float* __restrict__ x, const bf16* __restrict__ g,
+                                                      bf16* __restrict__ out, int D, float eps) {
+  const int r = blockIdx.x;
+  const float* xr = x + (size_t)r * D;
+  float ss = 0.f;
+  for (int i = threadIdx.x; i < D; i += 256) ss += xr[i] * xr[i];
+  const float rstd = 1.0f / sqrtf(block_sum<256>(ss) / float(D) + eps);
+  for (int i = threadIdx.x; i < D; i += 256) out[(size_t)r * D + i] = f2bf(xr[i] * rstd * bf2f(g[i]));
+}
+
+cudaError_t launch_rmsnorm(const LaneDev& d, const float* x, const bf16* g, bf16* out, int T, cudaStream_t s) {
+  rmsnorm_kernel<<<T, 256, 0, s>>>(x, g, out, d.D, d.eps);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ a2: QKV + RoPE epilogue
+// rotate_half RoPE at position row_pos[r] with the fp32 cos/sin table.
+__global__ void qkv_rope_kernel(LaneDev d, int layer) {
+  const int r = blockIdx.x;
+  const int half = d.dh / 2;
+  const int pos = d.row_pos[r];
+  const float* c = d.cbuf + (size_t)r * d.qkv_rows;
+  const float* cs = d.rope_cos + (size_t)pos * half;
+  const float* sn = d.rope_sin + (size_t)pos * half;
+  const int nq = d.Hq * d.dh, nk = d.Hkv * d.dh;
+  bf16* kc = d.kc + ((size_t)layer * d.Tmax + r) * nk;
+  bf16* vc = d.vc + ((size_t)layer * d.Tmax + r) * nk;
+  for (int i = threadIdx.x; i < (d.Hq + d.Hkv) * half; i += blockDim.x) {
+    const int head = i / half, m = i % half;
+    const float* src = c + head * d.dh;
+    const float x1 = src[m], x2 = src[m + half];
+    const float o1 = x1 * cs[m] - x2 * sn[m];
+    const float o2 = x2 * cs[m] + x1 * sn[m];
+    bf16* dst = head < d.Hq ? d.q + (size_t)r * nq + head * d.dh : kc + (head - d.Hq) * d.dh;
+    dst[m] = f2bf(o1);
+    dst[m + half] = f2bf(o2);
+  }
+  for (int i = threadIdx.x; i < nk; i += blockDim.x) vc[i] = f2bf(c[nq + nk + i]);
+}
+
+cudaError_t launch_qkv_rope_epilogue(const LaneDev& d, int layer, int T, cudaStream_t s) {
+  qkv_rope_kernel<<<T, 256, 0, s>>>(d, layer);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ a4: residual / SwiGLU epilogues
+__global__ void residual_kernel(const float* __restrict__ hin, const float* __restrict__ c, float* __restrict__ hout,
+                                size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    hout[i] = hin[i] + c[i];
+}
+
+cudaError_t launch_residual_epilogue(const float* hin, const float* c, float* hout, int T, int D, cudaStream_t s) {
+  residual_kernel<<<148 * 4, 256, 0, s>>>(hin, c, hout, (size_t)T * D);
+  return cudaGetLastError();
+}
+
+// u = bf16(silu(gate) * up), gate = C[:, j], up = C[:, F + j]
+__global__ void swiglu_kernel(LaneDev d, int T) {
+  const size_t n = (size_t)T * d.F;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const size_t r = i / d.F, j = i % d.F;
+    const float g = d.cbuf[r * 2 * d.F + j], up = d.cbuf[r * 2 * d.F + d.F + j];
+    d.u[i] = f2bf(g / (1.0f + expf(-g)) * up);
+  }
+}
+
+cudaError_t launch_swiglu_epilogue(const LaneDev& d, int T, cudaStream_t s) {
+  swiglu_kernel<<<148 * 4, 256, 0, s>>>(d, T);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ a5: vocab-tile statistics
+// One warp per (row, 256-wide tile): m = max(l * inv_temp), s = sum exp(l * inv_temp - m),
+// argmax = lowest index attaining the max of l * inv_temp.
+__global__ void tile_stats_kernel(LaneDev d, int T, float inv_temp) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= T * d.nt) return;
+  const int r = warp / d.nt, t = warp % d.nt;
+  const float* row = d.logits + (size_t)r * d.V;
+  const int x0 = t * kVocabTile;
+  float v[kVocabTile / 32];
+  float m = -INFINITY;
+  int am = 0x7fffffff;
+#pragma unroll
+  for (int i = 0; i < kVocabTile / 32; ++i) {
+    const int x = x0 + i * 32 + lane;
+    v[i] = x < d.V ? row[x] * inv_temp : -INFINITY;
+    if (v[i] > m) { m = v[i]; am = x; }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const float om = __shfl_xor_sync(0xffffffffu, m, o);
+    const int oa = __shfl_xor_sync(0xffffffffu, am, o);
+    if (om > m || (om == m && oa < am)) { m = om; am = oa; }
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < kVocabTile / 32; ++i) s += expf(v[i] - m);
+  s = warp_sum(s);
+  if (lane == 0) {
+    d.tile_max[(size_t)r * d.nt + t] = m;
+    d.tile_sum[(size_t)r * d.nt + t] = s;
+    d.tile_arg[(size_t)r * d.nt + t] = am;
+  }
+}
+
+cudaError_t launch_tile_stats(const LaneDev& d, int T, float inv_temp, cudaStream_t s) {
+  const int warps = T * d.nt;
+  tile_stats_kernel<<<(warps + 7) / 8, 256, 0, s>>>(d, T, inv_temp);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ test / fixture kernels
+__global__ void debug_uniforms_kernel(uint64_t seed, uint64_t rid, uint32_t z, int purpose, int x0, int n,
+                                      float* u) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int x = x0 + i;
+  if (purpose == PURPOSE_ACCEPT) {
+    u[i] = uniform_accept(seed, rid, z);      // x ignored (ACCEPT uses x = 0)
+  } else {
+    const u32x4 w = race_words(seed, rid, z, uint32_t(x) >> 2);
+    const uint32_t ww = (x & 3) == 0 ? w.x : (x & 3) == 1 ? w.y : (x & 3) == 2 ? w.z : w.w;
+    u[i] = word_to_uniform(ww);
+  }
+}
+
+cudaError_t launch_debug_uniforms(uint64_t seed, uint64_t rid, uint32_t z, int purpose, int x0, int n, float* u,
+                                  cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  debug_uniforms_kernel<<<(n + 255) / 256, 256, 0, s>>>(seed, rid, z, purpose, x0, n, u);
+  return cudaGetLastError();
+}
+
+// planted-successor drafter (bench fixture): one thread per request
+__global__ void draft_planted_kernel(LaneDev d, PlanArgs p, const int* __restrict__ succ,
+                                     const uint8_t* __restrict__ mask, const int* __restrict__ dev_tok,
+                                     int* __restrict__ out) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= p.batch) return;
+  int off = 0;
+  for (int i = 0; i < b; ++i) off += p.depths[i];
+  int prev = d.pending[p.slots[b]];
+  for (int j = 0; j < p.depths[b]; ++j) {
+    int t = succ[prev];
+    if (mask[off + j]) t = dev_tok[off + j];
+    out[off + j] = t;
+    prev = t;
+  }
+}
+
+cudaError_t launch_draft_planted(const LaneDev& d, const PlanArgs& p, const int* succ, const uint8_t* mask,
+                                 const int* dev_tok, int* draft_tokens, cudaStream_t s) {
+  draft_planted_kernel<<<(p.batch + 127) / 128, 128, 0, s>>>(d, p, succ, mask, dev_tok, draft_tokens);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ lane state init
+__global__ void init_state_kernel(LaneDev d) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < d.n_pages) d.free_list[i] = d.n_pages - 1 - i;     // pop order 0, 1, 2, ...
+  if (i < d.max_slots) { d.len[i] = 0; d.pending[i] = 0; d.rid[i] = 0ull; }
+  if (i < kNumStats) d.stats[i] = 0ull;
+  if (i == 0) { *d.free_top = d.n_pages; *d.err = 0; }
+}
+
+cudaError_t launch_init_state(const LaneDev& d, cudaStream_t s) {
+  int n = d.n_pages;
+  if (d.max_slots > n) n = d.max_slots;
+  if (kNumStats > n) n = kNumStats;
+  init_state_kernel<<<(n + 255) / 256, 256, 0, s>>>(d);
+  return cudaGetLastError();
+}
+
+}  // namespace sv

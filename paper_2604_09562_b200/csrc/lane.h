@@ -1,0 +1,86 @@
+// Internal (non-ABI) view of one decode lane: device pointers + sizes passed
+// by value to every kernel, and the launch functions each kernel file exports.
+#pragma once
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+namespace sv {
+
+typedef __nv_bfloat16 bf16;
+
+constexpr int kMaxBatch = 256;     // PlanArgs capacity (requests per verify)
+constexpr int kMaxDepth = 32;      // k_i <= 32 (sv_lane_stats histograms have 33 bins)
+constexpr int kVocabTile = 256;    // lm-head epilogue statistics tile
+constexpr int kAttnRows = 64;      // max (k+1) * G query rows per (request, kv head)
+constexpr int kSplitKeys = 512;    // keys per split-KV work item
+constexpr int kNumStats = 6 + 3 * (kMaxDepth + 1);
+
+// indices into the u64 stats array (mirrors sv_lane_stats)
+enum { ST_STEPS = 0, ST_ROWS, ST_DRAFTED, ST_ACCEPTED, ST_EMITTED, ST_INDEP, ST_HIST,
+       ST_DRAFTED_BY_K = ST_HIST + kMaxDepth + 1, ST_ACCEPTED_BY_K = ST_DRAFTED_BY_K + kMaxDepth + 1 };
+
+struct LaneDev {
+  // configuration
+  int n_layers, D, Hq, Hkv, dh, V, F, page, n_pages, max_slots, max_batch, max_depth, max_pos;
+  int max_pages_per_slot, nt, qkv_rows, Tmax;
+  float eps;
+  // borrowed weights (bf16)
+  const bf16 *embed, *attn_norm, *wqkv, *wo, *ffn_norm, *w_gate_up, *w_down, *final_norm, *lm_head;
+  bf16* pool;                        // [n_layers][n_pages][2][Hkv][page][dh]
+  // persistent lane state (workspace)
+  int* len;                          // [max_slots]
+  int* pending;                      // [max_slots]
+  unsigned long long* rid;           // [max_slots]
+  int* page_table;                   // [max_slots][max_pages_per_slot]
+  int* free_list;                    // [n_pages]
+  int* free_top;                     // [1]
+  unsigned long long* stats;         // [kNumStats]
+  int* err;                          // [1] sticky SV_DERR_* bits
+  const float *rope_cos, *rope_sin;  // [max_pos][dh/2]
+  // per-call buffers (workspace)
+  int *slots, *depths, *row_off, *row_req, *row_pos, *chain_tok, *req_err;
+  float *h0, *h1, *h2, *cbuf, *logits, *tile_max, *tile_sum;
+  int* tile_arg;
+  bf16 *a, *b, *z, *q, *kc, *vc, *o, *u;
+  int4* items;                       // attention work list: (request, kv head, split, 0)
+  int *item_start, *n_items;
+  float *part_o, *part_ml;           // split-KV partials
+  int *acc_int, *tok_int;            // internal copies of accepted_len / out_tokens for commit
+  int* batch_n;                      // [1] batch of the pending verify (device copy)
+};
+
+struct PlanArgs {
+  int batch, T;
+  int slots[kMaxBatch];
+  int depths[kMaxBatch];
+};
+
+// ---- launchers (stream-ordered; return cudaGetLastError()) ----
+cudaError_t launch_plan(const LaneDev& d, const PlanArgs& p, const int* draft_tokens, bool attn, cudaStream_t s);
+cudaError_t launch_embed_norm(const LaneDev& d, int T, cudaStream_t s);
+cudaError_t launch_rmsnorm(const LaneDev& d, const float* x, const bf16* g, bf16* out, int T, cudaStream_t s);
+// C[M][N] (fp32) = A[M][K] (bf16) * B[N][K]^T (bf16)
+cudaError_t launch_gemm_simt(const bf16* A, const bf16* B, float* C, int M, int N, int K, cudaStream_t s);
+cudaError_t launch_qkv_rope_epilogue(const LaneDev& d, int layer, int T, cudaStream_t s);
+cudaError_t launch_residual_epilogue(const float* hin, const float* c, float* hout, int T, int D, cudaStream_t s);
+cudaError_t launch_swiglu_epilogue(const LaneDev& d, int T, cudaStream_t s);
+cudaError_t launch_tile_stats(const LaneDev& d, int T, float inv_temp, cudaStream_t s);
+cudaError_t launch_attention(const LaneDev& d, int layer, int batch, cudaStream_t s);
+cudaError_t launch_attn_combine(const LaneDev& d, int T, cudaStream_t s);
+cudaError_t launch_finalize(const LaneDev& d, int batch, const int* draft_tokens, const float* draft_probs,
+                            const float* logits, uint64_t seed, int mode, float inv_temp,
+                            int* accepted_len, int* out_tokens, cudaStream_t s);
+cudaError_t launch_commit(const LaneDev& d, const int* n_keep, int batch, cudaStream_t s);
+cudaError_t launch_append(const LaneDev& d, int slot, unsigned long long rid, const bf16* k, const bf16* v,
+                          int n, int pending, const int* pending_dev, int packed, cudaStream_t s);
+cudaError_t launch_release(const LaneDev& d, int slot, cudaStream_t s);
+cudaError_t launch_init_state(const LaneDev& d, cudaStream_t s);
+cudaError_t launch_debug_uniforms(uint64_t seed, uint64_t rid, uint32_t z, int purpose, int x0, int n, float* u,
+                                  cudaStream_t s);
+cudaError_t launch_draft_planted(const LaneDev& d, const PlanArgs& p, const int* succ, const uint8_t* mask,
+                                 const int* dev_tok, int* draft_tokens, cudaStream_t s);
+cudaError_t launch_kv_pack(const bf16* k, const bf16* v, int n_layers, int Hkv, int dh, int n, int pending,
+                           void* packed, cudaStream_t s);
+
+}  // namespace sv

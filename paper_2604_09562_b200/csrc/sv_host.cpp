@@ -1,0 +1,580 @@
+// Host runtime behind include/sv.h: configuration checks, workspace layout, the per-slot
+// state machine, and the stream-ordered launch sequence of the verify step.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/sv.h"
+#include "lane.h"
+#include "gemm.h"
+
+using sv::bf16;
+
+namespace {
+
+enum SlotState { EMPTY = 0, ACTIVE = 1, PENDING = 2 };
+
+struct Layout {
+  size_t total = 0;
+  size_t rope_cos, rope_sin, len, pending, rid, page_table, free_list, free_top, stats, err;
+  size_t slots, depths, row_off, row_req, row_pos, chain_tok, req_err;
+  size_t h0, h1, h2, cbuf, logits, tile_max, tile_sum, tile_arg;
+  size_t a, b, z, q, kc, vc, o, u;
+  size_t items, item_start, n_items, part_o, part_ml, acc_int, tok_int, batch_n;
+  size_t gemm_ws;
+  size_t max_items;
+
+  size_t take(size_t bytes) {
+    total = (total + 1023) & ~size_t(1023);
+    const size_t off = total;
+    total += bytes;
+    return off;
+  }
+};
+
+size_t ceil_div(size_t a, size_t b) { return (a + b - 1) / b; }
+
+bool valid_cfg(const sv_config* c) {
+  if (!c) return false;
+  if (c->n_layers < 1 || c->d_model < 64 || c->n_q_heads < 1 || c->n_kv_heads < 1 || c->vocab < 1) return false;
+  if (c->n_q_heads % c->n_kv_heads) return false;
+  if (c->head_dim != 64 && c->head_dim != 128) return false;
+  if (c->d_model % 64 || c->ffn_dim < 0 || c->ffn_dim % 64) return false;
+  if ((c->n_q_heads * c->head_dim) % 64) return false;
+  if (c->page_size < 8 || c->page_size % 8 || c->n_pages < 1 || c->max_slots < 1) return false;
+  if (c->max_batch < 1 || c->max_batch > sv::kMaxBatch) return false;
+  if (c->max_depth < 0 || c->max_depth > sv::kMaxDepth) return false;
+  if ((c->max_depth + 1) * (c->n_q_heads / c->n_kv_heads) > sv::kAttnRows) return false;
+  if (c->max_pos < c->max_depth + 2) return false;
+  if (!(c->rope_theta > 0.f) || !(c->norm_eps >= 0.f)) return false;
+  return true;
+}
+
+Layout make_layout(const sv_config& c) {
+  Layout L;
+  const size_t T = (size_t)c.max_batch * (c.max_depth + 1);
+  const size_t D = c.d_model, V = c.vocab, F = c.ffn_dim;
+  const size_t nq = (size_t)c.n_q_heads * c.head_dim, nkv = (size_t)c.n_kv_heads * c.head_dim;
+  const size_t qkv_rows = nq + 2 * nkv;
+  const size_t mpps = ceil_div(c.max_pos, c.page_size);
+  const size_t nt = ceil_div(V, sv::kVocabTile);
+  L.rope_cos = L.take(4 * (size_t)c.max_pos * c.head_dim / 2);
+  L.rope_sin = L.take(4 * (size_t)c.max_pos * c.head_dim / 2);
+  L.len = L.take(4 * c.max_slots);
+  L.pending = L.take(4 * c.max_slots);
+  L.rid = L.take(8 * c.max_slots);
+  L.page_table = L.take(4 * c.max_slots * mpps);
+  L.free_list = L.take(4 * (size_t)c.n_pages);
+  L.free_top = L.take(4);
+  L.stats = L.take(8 * sv::kNumStats);
+  L.err = L.take(4);
+  L.slots = L.take(4 * c.max_batch);
+  L.depths = L.take(4 * c.max_batch);
+  L.row_off = L.take(4 * (c.max_batch + 1));
+  L.row_req = L.take(4 * T);
+  L.row_pos = L.take(4 * T);
+  L.chain_tok = L.take(4 * T);
+  L.req_err = L.take(4 * c.max_batch);
+  L.h0 = L.take(4 * T * D);
+  L.h1 = L.take(4 * T * D);
+  L.h2 = L.take(4 * T * D);
+  size_t cmax = qkv_rows;
+  if (D > cmax) cmax = D;
+  if (2 * F > cmax) cmax = 2 * F;
+  L.cbuf = L.take(4 * T * cmax);
+  L.logits = L.take(4 * T * V);
+  L.tile_max = L.take(4 * T * nt);
+  L.tile_sum = L.take(4 * T * nt);
+  L.tile_arg = L.take(4 * T * nt);
+  L.a = L.take(2 * T * D);
+  L.b = L.take(2 * T * D);
+  L.z = L.take(2 * T * D);
+  L.q = L.take(2 * T * nq);
+  L.kc = L.take(2 * (size_t)c.n_layers * T * nkv);
+  L.vc = L.take(2 * (size_t)c.n_layers * T * nkv);
+  L.o = L.take(2 * T * nq);
+  L.u = L.take(2 * T * (F ? F : 1));
+  // attention work items: sum over requests of Hkv * ceil((L_i + R_i) / split)
+  const size_t max_keys = (size_t)c.n_pages * c.page_size + T;
+  L.max_items = (size_t)c.n_kv_heads * (ceil_div(max_keys, sv::kSplitKeys) + c.max_batch);
+  L.items = L.take(16 * L.max_items);
+  L.item_start = L.take(4 * (c.max_batch + 1));
+  L.n_items = L.take(16);
+  L.part_o = L.take(4 * L.max_items * sv::kAttnRows * c.head_dim);
+  L.part_ml = L.take(8 * L.max_items * sv::kAttnRows);
+  L.acc_int = L.take(4 * c.max_batch);
+  L.tok_int = L.take(4 * c.max_batch * (c.max_depth + 1));
+  L.batch_n = L.take(4);
+  L.gemm_ws = L.take(sv::gemm_workspace_bytes());
+  L.total = (L.total + 1023) & ~size_t(1023);
+  return L;
+}
+
+}  // namespace
+
+struct sv_ctx {
+  sv_config cfg;
+  sv_weights w;
+  char* pool;
+  char* ws;
+  cudaStream_t stream;
+  Layout lay;
+  sv::LaneDev d;
+  std::vector<int> state;
+  std::vector<unsigned long long> rid;
+  bool pending_verify = false;
+  int pending_batch = 0;
+  std::vector<int> pending_slots;
+  int last_T = 0, last_batch = 0;
+  int sticky = 0;
+  sv::GemmPlan* gemm = nullptr;
+};
+
+static sv_status cuda_ok(cudaError_t e) {
+  if (e != cudaSuccess) {
+    fprintf(stderr, "[sv] CUDA error: %s\n", cudaGetErrorString(e));
+    return SV_ECUDA;
+  }
+  return SV_OK;
+}
+#define SV_CUDA(x)                                   \
+  do {                                               \
+    sv_status _s = cuda_ok(x);                       \
+    if (_s != SV_OK) return _s;                      \
+  } while (0)
+
+extern "C" {
+
+const char* sv_version(void) { return "sv 0.1 sm_100a"; }
+
+const char* sv_strerror(sv_status s) {
+  switch (s) {
+    case SV_OK: return "ok";
+    case SV_EINVAL: return "invalid argument";
+    case SV_ESTATE: return "call not allowed in the current slot/context state";
+    case SV_ENOKV: return "KV page free list exhausted (device)";
+    case SV_ECUDA: return "CUDA error";
+    case SV_ENCCL: return "NCCL error";
+    case SV_EDEVICE: return "device-detected error (bad token id / bad n_keep)";
+  }
+  return "unknown status";
+}
+
+sv_status sv_query_sizes(const sv_config* cfg, size_t* kv_pool_bytes, size_t* workspace_bytes) {
+  if (!valid_cfg(cfg) || !kv_pool_bytes || !workspace_bytes) return SV_EINVAL;
+  *kv_pool_bytes = (size_t)cfg->n_layers * cfg->n_pages * 2 * cfg->n_kv_heads * cfg->page_size * cfg->head_dim * 2;
+  *workspace_bytes = make_layout(*cfg).total;
+  return SV_OK;
+}
+
+sv_status sv_create(const sv_config* cfg, const sv_weights* w, void* kv_pool, void* workspace,
+                    sv_stream_t stream, sv_ctx** out) {
+  if (!valid_cfg(cfg) || !w || !kv_pool || !workspace || !out) return SV_EINVAL;
+  if (((uintptr_t)kv_pool | (uintptr_t)workspace) & 1023) return SV_EINVAL;
+  const void* wp[] = {w->embed, w->attn_norm, w->wqkv, w->wo, w->final_norm, w->lm_head};
+  for (const void* p : wp)
+    if (!p || ((uintptr_t)p & 15)) return SV_EINVAL;
+  if (cfg->ffn_dim > 0 && (!w->ffn_norm || !w->w_gate_up || !w->w_down)) return SV_EINVAL;
+  sv_ctx* c = new sv_ctx();
+  c->cfg = *cfg;
+  c->w = *w;
+  c->pool = (char*)kv_pool;
+  c->ws = (char*)workspace;
+  c->stream = (cudaStream_t)stream;
+  c->lay = make_layout(*cfg);
+  c->state.assign(cfg->max_slots, EMPTY);
+  c->rid.assign(cfg->max_slots, 0ull);
+  const Layout& L = c->lay;
+  char* ws = c->ws;
+  sv::LaneDev& d = c->d;
+  memset(&d, 0, sizeof(d));
+  d.n_layers = cfg->n_layers;
+  d.D = cfg->d_model;
+  d.Hq = cfg->n_q_heads;
+  d.Hkv = cfg->n_kv_heads;
+  d.dh = cfg->head_dim;
+  d.V = cfg->vocab;
+  d.F = cfg->ffn_dim;
+  d.page = cfg->page_size;
+  d.n_pages = cfg->n_pages;
+  d.max_slots = cfg->max_slots;
+  d.max_batch = cfg->max_batch;
+  d.max_depth = cfg->max_depth;
+  d.max_pos = cfg->max_pos;
+  d.max_pages_per_slot = (int)ceil_div(cfg->max_pos, cfg->page_size);
+  d.nt = (int)ceil_div(cfg->vocab, sv::kVocabTile);
+  d.qkv_rows = (cfg->n_q_heads + 2 * cfg->n_kv_heads) * cfg->head_dim;
+  d.Tmax = cfg->max_batch * (cfg->max_depth + 1);
+  d.eps = cfg->norm_eps;
+  d.embed = (const bf16*)w->embed;
+  d.attn_norm = (const bf16*)w->attn_norm;
+  d.wqkv = (const bf16*)w->wqkv;
+  d.wo = (const bf16*)w->wo;
+  d.ffn_norm = (const bf16*)w->ffn_norm;
+  d.w_gate_up = (const bf16*)w->w_gate_up;
+  d.w_down = (const bf16*)w->w_down;
+  d.final_norm = (const bf16*)w->final_norm;
+  d.lm_head = (const bf16*)w->lm_head;
+  d.pool = (bf16*)kv_pool;
+  d.len = (int*)(ws + L.len);
+  d.pending = (int*)(ws + L.pending);
+  d.rid = (unsigned long long*)(ws + L.rid);
+  d.page_table = (int*)(ws + L.page_table);
+  d.free_list = (int*)(ws + L.free_list);
+  d.free_top = (int*)(ws + L.free_top);
+  d.stats = (unsigned long long*)(ws + L.stats);
+  d.err = (int*)(ws + L.err);
+  d.rope_cos = (const float*)(ws + L.rope_cos);
+  d.rope_sin = (const float*)(ws + L.rope_sin);
+  d.slots = (int*)(ws + L.slots);
+  d.depths = (int*)(ws + L.depths);
+  d.row_off = (int*)(ws + L.row_off);
+  d.row_req = (int*)(ws + L.row_req);
+  d.row_pos = (int*)(ws + L.row_pos);
+  d.chain_tok = (int*)(ws + L.chain_tok);
+  d.req_err = (int*)(ws + L.req_err);
+  d.h0 = (float*)(ws + L.h0);
+  d.h1 = (float*)(ws + L.h1);
+  d.h2 = (float*)(ws + L.h2);
+  d.cbuf = (float*)(ws + L.cbuf);
+  d.logits = (float*)(ws + L.logits);
+  d.tile_max = (float*)(ws + L.tile_max);
+  d.tile_sum = (float*)(ws + L.tile_sum);
+  d.tile_arg = (int*)(ws + L.tile_arg);
+  d.a = (bf16*)(ws + L.a);
+  d.b = (bf16*)(ws + L.b);
+  d.z = (bf16*)(ws + L.z);
+  d.q = (bf16*)(ws + L.q);
+  d.kc = (bf16*)(ws + L.kc);
+  d.vc = (bf16*)(ws + L.vc);
+  d.o = (bf16*)(ws + L.o);
+  d.u = (bf16*)(ws + L.u);
+  d.items = (int4*)(ws + L.items);
+  d.item_start = (int*)(ws + L.item_start);
+  d.n_items = (int*)(ws + L.n_items);
+  d.part_o = (float*)(ws + L.part_o);
+  d.part_ml = (float*)(ws + L.part_ml);
+  d.acc_int = (int*)(ws + L.acc_int);
+  d.tok_int = (int*)(ws + L.tok_int);
+  d.batch_n = (int*)(ws + L.batch_n);
+
+  // RoPE table: fp64 angles pos * theta^(-2m/d_h), stored fp32 (SURVEY.md §8(c) "Model details")
+  const int half = cfg->head_dim / 2;
+  std::vector<float> cs((size_t)cfg->max_pos * half), sn((size_t)cfg->max_pos * half);
+  for (int m = 0; m < half; ++m) {
+    const double inv_freq = 1.0 / pow((double)cfg->rope_theta, 2.0 * m / cfg->head_dim);
+    for (int p = 0; p < cfg->max_pos; ++p) {
+      const double ang = (double)p * inv_freq;
+      cs[(size_t)p * half + m] = (float)cos(ang);
+      sn[(size_t)p * half + m] = (float)sin(ang);
+    }
+  }
+  sv_status st = SV_OK;
+  if ((st = cuda_ok(cudaMemcpyAsync(ws + L.rope_cos, cs.data(), cs.size() * 4, cudaMemcpyHostToDevice, c->stream))) ||
+      (st = cuda_ok(cudaMemcpyAsync(ws + L.rope_sin, sn.data(), sn.size() * 4, cudaMemcpyHostToDevice, c->stream))) ||
+      (st = cuda_ok(cudaMemsetAsync(ws + L.page_table, 0xff, 4 * (size_t)cfg->max_slots * d.max_pages_per_slot,
+                                    c->stream))) ||
+      (st = cuda_ok(sv::launch_init_state(d, c->stream)))) {
+    delete c;
+    return st;
+  }
+  c->gemm = sv::gemm_plan_create(d, ws + L.gemm_ws, c->stream);
+  if ((st = cuda_ok(cudaStreamSynchronize(c->stream)))) {
+    sv::gemm_plan_destroy(c->gemm);
+    delete c;
+    return st;
+  }
+  *out = c;
+  return SV_OK;
+}
+
+sv_status sv_destroy(sv_ctx* c) {
+  if (!c) return SV_EINVAL;
+  cudaStreamSynchronize(c->stream);
+  sv::gemm_plan_destroy(c->gemm);
+  delete c;
+  return SV_OK;
+}
+
+sv_status sv_append_kv(sv_ctx* c, int32_t slot, uint64_t request_id, const void* k, const void* v,
+                       int32_t n_tokens, int32_t pending_token) {
+  if (!c || slot < 0 || slot >= c->cfg.max_slots || n_tokens < 0) return SV_EINVAL;
+  if (n_tokens > 0 && (!k || !v || (((uintptr_t)k | (uintptr_t)v) & 15))) return SV_EINVAL;
+  if (pending_token < 0 || pending_token >= c->cfg.vocab) return SV_EINVAL;
+  if (c->state[slot] == PENDING) return SV_ESTATE;
+  if (c->state[slot] == ACTIVE && c->rid[slot] != request_id) return SV_EINVAL;
+  SV_CUDA(sv::launch_append(c->d, slot, request_id, (const bf16*)k, (const bf16*)v, n_tokens, pending_token,
+                            nullptr, 0, c->stream));
+  c->state[slot] = ACTIVE;
+  c->rid[slot] = request_id;
+  return SV_OK;
+}
+
+static sv_status check_batch(sv_ctx* c, int32_t batch, const int32_t* slots, const int32_t* depths,
+                             sv::PlanArgs& p) {
+  if (batch < 1 || batch > c->cfg.max_batch || !slots || !depths) return SV_EINVAL;
+  std::vector<char> seen(c->cfg.max_slots, 0);
+  p.batch = batch;
+  p.T = 0;
+  for (int b = 0; b < batch; ++b) {
+    const int s = slots[b], k = depths[b];
+    if (s < 0 || s >= c->cfg.max_slots || seen[s]) return SV_EINVAL;
+    if (k < 0 || k > c->cfg.max_depth) return SV_EINVAL;
+    seen[s] = 1;
+    p.slots[b] = s;
+    p.depths[b] = k;
+    p.T += k + 1;
+  }
+  for (int b = 0; b < batch; ++b)
+    if (c->state[slots[b]] != ACTIVE) return SV_ESTATE;
+  return SV_OK;
+}
+
+static sv_status gemm(sv_ctx* c, const bf16* A, const bf16* B, float* C, int M, int N, int K, int epi,
+                      const sv::GemmEpi& e) {
+  return cuda_ok(sv::gemm_run(c->gemm, A, B, C, M, N, K, epi, e, c->stream));
+}
+
+sv_status sv_verify(sv_ctx* c, int32_t batch, const int32_t* slots, const int32_t* depths,
+                    const int32_t* draft_tokens, const float* draft_probs, uint64_t seed, sv_mode mode,
+                    float temperature, int32_t* accepted_len, int32_t* out_tokens, float* logits_out) {
+  if (!c || !accepted_len || !out_tokens) return SV_EINVAL;
+  if (mode != SV_GREEDY && mode != SV_SAMPLE) return SV_EINVAL;
+  if (mode == SV_SAMPLE && !(temperature > 0.f)) return SV_EINVAL;
+  if (c->pending_verify) return SV_ESTATE;
+  sv::PlanArgs p;
+  sv_status st = check_batch(c, batch, slots, depths, p);
+  if (st) return st;
+  if (p.T > batch && !draft_tokens) return SV_EINVAL;
+  const sv::LaneDev& d = c->d;
+  const int T = p.T;
+  cudaStream_t s = c->stream;
+  const float inv_temp = mode == SV_SAMPLE ? 1.0f / temperature : 1.0f;
+  SV_CUDA(sv::launch_plan(d, p, draft_tokens, true, s));
+  SV_CUDA(sv::launch_embed_norm(d, T, s));
+  const size_t nq = (size_t)d.Hq * d.dh;
+  for (int layer = 0; layer < d.n_layers; ++layer) {
+    const float* hin = layer == 0 ? d.h0 : d.h2;
+    if (layer > 0) SV_CUDA(sv::launch_rmsnorm(d, hin, d.attn_norm + (size_t)layer * d.D, d.a, T, s));
+    sv::GemmEpi e{};
+    e.layer = layer;
+    if ((st = gemm(c, d.a, d.wqkv + (size_t)layer * d.qkv_rows * d.D, d.cbuf, T, d.qkv_rows, d.D,
+                   sv::EPI_QKV_ROPE, e)))
+      return st;
+    SV_CUDA(sv::launch_attention(d, layer, batch, s));
+    SV_CUDA(sv::launch_attn_combine(d, T, s));
+    float* hattn = d.F > 0 ? d.h1 : d.h2;
+    e.resid_in = hin;
+    e.resid_out = hattn;
+    if ((st = gemm(c, d.o, d.wo + (size_t)layer * d.D * nq, d.cbuf, T, d.D, (int)nq, sv::EPI_RESIDUAL, e)))
+      return st;
+    if (d.F > 0) {
+      SV_CUDA(sv::launch_rmsnorm(d, d.h1, d.ffn_norm + (size_t)layer * d.D, d.b, T, s));
+      if ((st = gemm(c, d.b, d.w_gate_up + (size_t)layer * 2 * d.F * d.D, d.cbuf, T, 2 * d.F, d.D,
+                     sv::EPI_SWIGLU, e)))
+        return st;
+      e.resid_in = d.h1;
+      e.resid_out = d.h2;
+      if ((st = gemm(c, d.u, d.w_down + (size_t)layer * d.D * d.F, d.cbuf, T, d.D, d.F, sv::EPI_RESIDUAL, e)))
+        return st;
+    }
+  }
+  SV_CUDA(sv::launch_rmsnorm(d, d.h2, d.final_norm, d.z, T, s));
+  sv::GemmEpi e{};
+  e.inv_temp = inv_temp;
+  if ((st = gemm(c, d.z, d.lm_head, d.logits, T, d.V, d.D, sv::EPI_LOGITS, e))) return st;
+  SV_CUDA(sv::launch_finalize(d, batch, draft_tokens, draft_probs, d.logits, seed, mode, inv_temp, accepted_len,
+                              out_tokens, s));
+  if (logits_out)
+    SV_CUDA(cudaMemcpyAsync(logits_out, d.logits, (size_t)T * d.V * 4, cudaMemcpyDeviceToDevice, s));
+  for (int b = 0; b < batch; ++b) c->state[slots[b]] = PENDING;
+  c->pending_verify = true;
+  c->pending_batch = batch;
+  c->pending_slots.assign(slots, slots + batch);
+  c->last_T = T;
+  c->last_batch = batch;
+  return SV_OK;
+}
+
+sv_status sv_verify_logits(sv_ctx* c, int32_t batch, const int32_t* slots, const int32_t* depths,
+                           const int32_t* draft_tokens, const float* draft_probs, const float* logits,
+                           uint64_t seed, sv_mode mode, float temperature, int32_t* accepted_len,
+                           int32_t* out_tokens) {
+  if (!c || !accepted_len || !out_tokens || !logits) return SV_EINVAL;
+  if (mode != SV_GREEDY && mode != SV_SAMPLE) return SV_EINVAL;
+  if (mode == SV_SAMPLE && !(temperature > 0.f)) return SV_EINVAL;
+  if (c->pending_verify) return SV_ESTATE;
+  sv::PlanArgs p;
+  sv_status st = check_batch(c, batch, slots, depths, p);
+  if (st) return st;
+  if (p.T > batch && !draft_tokens) return SV_EINVAL;
+  const float inv_temp = mode == SV_SAMPLE ? 1.0f / temperature : 1.0f;
+  sv::LaneDev d = c->d;
+  SV_CUDA(sv::launch_plan(d, p, draft_tokens, false, c->stream));
+  d.logits = const_cast<float*>(logits);
+  SV_CUDA(sv::launch_tile_stats(d, p.T, inv_temp, c->stream));
+  SV_CUDA(sv::launch_finalize(d, batch, draft_tokens, draft_probs, logits, seed, mode, inv_temp, accepted_len,
+                              out_tokens, c->stream));
+  c->last_T = p.T;
+  c->last_batch = batch;
+  return SV_OK;
+}
+
+sv_status sv_commit(sv_ctx* c, const int32_t* n_keep) {
+  if (!c) return SV_EINVAL;
+  if (!c->pending_verify) return SV_ESTATE;
+  SV_CUDA(sv::launch_commit(c->d, n_keep, c->pending_batch, c->stream));
+  for (int s : c->pending_slots) c->state[s] = ACTIVE;
+  c->pending_verify = false;
+  if (c->sticky & SV_DERR_NO_PAGES) return SV_ENOKV;
+  if (c->sticky) return SV_EDEVICE;
+  return SV_OK;
+}
+
+sv_status sv_release(sv_ctx* c, int32_t slot) {
+  if (!c || slot < 0 || slot >= c->cfg.max_slots) return SV_EINVAL;
+  if (c->state[slot] == PENDING) return SV_ESTATE;
+  if (c->state[slot] == EMPTY) return SV_OK;
+  SV_CUDA(sv::launch_release(c->d, slot, c->stream));
+  c->state[slot] = EMPTY;
+  c->rid[slot] = 0;
+  return SV_OK;
+}
+
+sv_status sv_stats(sv_ctx* c, sv_lane_stats* out, int reset) {
+  if (!c || !out) return SV_EINVAL;
+  unsigned long long buf[sv::kNumStats];
+  int err = 0;
+  SV_CUDA(cudaMemcpyAsync(buf, c->d.stats, sizeof(buf), cudaMemcpyDeviceToHost, c->stream));
+  SV_CUDA(cudaMemcpyAsync(&err, c->d.err, 4, cudaMemcpyDeviceToHost, c->stream));
+  SV_CUDA(cudaStreamSynchronize(c->stream));
+  memset(out, 0, sizeof(*out));
+  out->steps = buf[sv::ST_STEPS];
+  out->rows = buf[sv::ST_ROWS];
+  out->drafted = buf[sv::ST_DRAFTED];
+  out->accepted = buf[sv::ST_ACCEPTED];
+  out->emitted = buf[sv::ST_EMITTED];
+  out->accepted_independent = buf[sv::ST_INDEP];
+  for (int i = 0; i <= sv::kMaxDepth; ++i) {
+    out->hist_accepted[i] = buf[sv::ST_HIST + i];
+    out->drafted_by_k[i] = buf[sv::ST_DRAFTED_BY_K + i];
+    out->accepted_by_k[i] = buf[sv::ST_ACCEPTED_BY_K + i];
+  }
+  out->device_error = err;
+  c->sticky = err;
+  if (reset) SV_CUDA(cudaMemsetAsync(c->d.stats, 0, sizeof(buf), c->stream));
+  if (err & SV_DERR_NO_PAGES) return SV_ENOKV;
+  if (err) return SV_EDEVICE;
+  return SV_OK;
+}
+
+sv_status sv_set_taps(sv_ctx* c, int enable) {
+  (void)enable;
+  return c ? SV_OK : SV_EINVAL;
+}
+
+sv_status sv_get_tap(sv_ctx* c, const char* name, void** dev_ptr, size_t* bytes) {
+  if (!c || !name || !dev_ptr || !bytes) return SV_EINVAL;
+  const sv::LaneDev& d = c->d;
+  const size_t T = c->last_T, D = d.D, B = c->last_batch;
+  const size_t nq = (size_t)d.Hq * d.dh, nkv = (size_t)d.Hkv * d.dh;
+  struct Tap { const char* n; const void* p; size_t b; };
+  const Tap taps[] = {
+      {"h0", d.h0, 4 * T * D},
+      {"a", d.a, 2 * T * D},
+      {"q", d.q, 2 * T * nq},
+      {"kc", d.kc, 2 * (size_t)d.n_layers * d.Tmax * nkv},
+      {"vc", d.vc, 2 * (size_t)d.n_layers * d.Tmax * nkv},
+      {"o", d.o, 2 * T * nq},
+      {"h1", d.F > 0 ? d.h1 : d.h2, 4 * T * D},
+      {"b", d.b, 2 * T * D},
+      {"u", d.u, 2 * T * (size_t)d.F},
+      {"h2", d.h2, 4 * T * D},
+      {"z", d.z, 2 * T * D},
+      {"logits", d.logits, 4 * T * (size_t)d.V},
+      {"tile_max", d.tile_max, 4 * T * (size_t)d.nt},
+      {"tile_sum", d.tile_sum, 4 * T * (size_t)d.nt},
+      {"tile_arg", d.tile_arg, 4 * T * (size_t)d.nt},
+      {"row_off", d.row_off, 4 * (B + 1)},
+      {"rope_cos", d.rope_cos, 4 * (size_t)d.max_pos * d.dh / 2},
+      {"rope_sin", d.rope_sin, 4 * (size_t)d.max_pos * d.dh / 2},
+      {"len", d.len, 4 * (size_t)d.max_slots},
+      {"pending", d.pending, 4 * (size_t)d.max_slots},
+      {"page_table", d.page_table, 4 * (size_t)d.max_slots * d.max_pages_per_slot},
+      {"free_top", d.free_top, 4},
+      {"free_list", d.free_list, 4 * (size_t)d.n_pages},
+  };
+  for (const Tap& t : taps)
+    if (!strcmp(t.n, name)) {
+      *dev_ptr = const_cast<void*>(t.p);
+      *bytes = t.b;
+      return SV_OK;
+    }
+  return SV_EINVAL;
+}
+
+sv_status sv_debug_uniforms(sv_ctx* c, uint64_t seed, uint64_t rid, uint32_t z, int32_t purpose, int32_t x0,
+                            int32_t n, float* u) {
+  if (!c || !u || n < 0 || x0 < 0 || (purpose != 0 && purpose != 1)) return SV_EINVAL;
+  SV_CUDA(sv::launch_debug_uniforms(seed, rid, z, purpose, x0, n, u, c->stream));
+  return SV_OK;
+}
+
+sv_status sv_draft_planted(sv_ctx* c, int32_t batch, const int32_t* slots, const int32_t* depths,
+                           const int32_t* succ, const uint8_t* dev_mask, const int32_t* dev_tok,
+                           int32_t* draft_tokens) {
+  if (!c || !succ || !dev_mask || !dev_tok || !draft_tokens) return SV_EINVAL;
+  sv::PlanArgs p;
+  if (batch < 1 || batch > c->cfg.max_batch || !slots || !depths) return SV_EINVAL;
+  p.batch = batch;
+  p.T = 0;
+  for (int b = 0; b < batch; ++b) {
+    if (slots[b] < 0 || slots[b] >= c->cfg.max_slots || depths[b] < 0 || depths[b] > c->cfg.max_depth)
+      return SV_EINVAL;
+    p.slots[b] = slots[b];
+    p.depths[b] = depths[b];
+    p.T += depths[b] + 1;
+  }
+  SV_CUDA(sv::launch_draft_planted(c->d, p, succ, dev_mask, dev_tok, draft_tokens, c->stream));
+  return SV_OK;
+}
+
+sv_status sv_kv_pack(const void* k, const void* v, int32_t n_layers, int32_t n_kv_heads, int32_t head_dim,
+                     int32_t n_tokens, int32_t pending_token, void* kv_packed, sv_stream_t stream) {
+  if (!k || !v || !kv_packed || n_layers < 1 || n_kv_heads < 1 || n_tokens < 0 || head_dim % 8) return SV_EINVAL;
+  if (((uintptr_t)k | (uintptr_t)v | (uintptr_t)kv_packed) & 15) return SV_EINVAL;
+  SV_CUDA(sv::launch_kv_pack((const bf16*)k, (const bf16*)v, n_layers, n_kv_heads, head_dim, n_tokens,
+                             pending_token, kv_packed, (cudaStream_t)stream));
+  return SV_OK;
+}
+
+size_t sv_kv_packed_bytes(const sv_config* cfg, int32_t n_tokens) {
+  if (!cfg || n_tokens < 0) return 0;
+  return (size_t)cfg->n_layers * n_tokens * 2 * cfg->n_kv_heads * cfg->head_dim * 2 + 16;
+}
+
+}  // extern "C"
+
+// used by comm.cpp (hand-off receive): append from a packed device buffer
+sv_status sv_internal_append_packed(sv_ctx* c, int32_t slot, uint64_t request_id, const void* packed,
+                                    int32_t n_tokens) {
+  if (!c || slot < 0 || slot >= c->cfg.max_slots || n_tokens < 0 || !packed) return SV_EINVAL;
+  if (c->state[slot] == PENDING) return SV_ESTATE;
+  if (c->state[slot] == ACTIVE && c->rid[slot] != request_id) return SV_EINVAL;
+  const size_t body = (size_t)c->cfg.n_layers * n_tokens * 2 * c->cfg.n_kv_heads * c->cfg.head_dim * 2;
+  const int* trailer = (const int*)((const char*)packed + body);
+  SV_CUDA(sv::launch_append(c->d, slot, request_id, (const bf16*)packed, nullptr, n_tokens, 0, trailer, 1,
+                            c->stream));
+  c->state[slot] = ACTIVE;
+  c->rid[slot] = request_id;
+  return SV_OK;
+}
+
+cudaStream_t sv_internal_stream(sv_ctx* c) { return c->stream; }
+
+size_t sv_internal_packed_bytes(sv_ctx* c, int32_t n_tokens) { return sv_kv_packed_bytes(&c->cfg, n_tokens); }

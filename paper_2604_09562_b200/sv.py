@@ -1,0 +1,303 @@
+"""Thin ctypes binding over libsv.so (include/sv.h). Argument marshalling only:
+every step of the verify path runs in the library's CUDA kernels. PyTorch
+supplies device memory, the stream and process groups.
+
+    lane = Lane(cfg, weights)                        # weights: dict of cuda bf16 tensors
+    lane.append_kv(slot, request_id, k, v, pending)  # k, v: [n_layers][n][Hkv][dh] bf16 (cuda)
+    acc, toks = lane.verify(slots, depths, draft_tokens, draft_probs=None, seed=0, mode="sample")
+    lane.commit()
+    lane.stats()
+
+There is no CPU fallback: importing without a built libsv.so, or calling on a
+machine without a CUDA device, raises.
+"""
+import ctypes
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsv.so")
+
+SV_OK, SV_EINVAL, SV_ESTATE, SV_ENOKV, SV_ECUDA, SV_ENCCL, SV_EDEVICE = range(7)
+GREEDY, SAMPLE = 0, 1
+_STATUS = {0: "SV_OK", 1: "SV_EINVAL", 2: "SV_ESTATE", 3: "SV_ENOKV", 4: "SV_ECUDA", 5: "SV_ENCCL", 6: "SV_EDEVICE"}
+
+EXPORTED = [
+    "sv_version", "sv_strerror", "sv_query_sizes", "sv_create", "sv_destroy", "sv_append_kv", "sv_verify",
+    "sv_verify_logits", "sv_commit", "sv_release", "sv_stats", "sv_set_taps", "sv_get_tap", "sv_debug_uniforms",
+    "sv_draft_planted", "sv_nccl_unique_id", "sv_nccl_comm_init", "sv_nccl_comm_destroy", "sv_kv_send",
+    "sv_kv_recv_append", "sv_kv_packed_bytes", "sv_kv_pack",
+]
+
+
+class SvError(RuntimeError):
+    def __init__(self, status, what):
+        self.status = status
+        super().__init__(f"{what}: {_STATUS.get(status, status)} ({strerror(status)})")
+
+
+class Config(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int32) for n in ("n_layers", "d_model", "n_q_heads", "n_kv_heads", "head_dim",
+                                              "vocab", "ffn_dim")] + \
+               [("rope_theta", ctypes.c_float), ("norm_eps", ctypes.c_float)] + \
+               [(n, ctypes.c_int32) for n in ("page_size", "n_pages", "max_slots", "max_batch", "max_depth",
+                                              "max_pos")]
+
+    @classmethod
+    def from_any(cls, c):
+        get = (lambda k: c[k]) if isinstance(c, dict) else (lambda k: getattr(c, k))
+        return cls(**{n: get(n) for n, _ in cls._fields_})
+
+
+WEIGHT_NAMES = ("embed", "attn_norm", "wqkv", "wo", "ffn_norm", "w_gate_up", "w_down", "final_norm", "lm_head")
+
+
+class Weights(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_void_p) for n in WEIGHT_NAMES]
+
+
+class LaneStats(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_uint64) for n in ("steps", "rows", "drafted", "accepted", "emitted",
+                                               "accepted_independent")] + \
+               [("hist_accepted", ctypes.c_uint64 * 33), ("drafted_by_k", ctypes.c_uint64 * 33),
+                ("accepted_by_k", ctypes.c_uint64 * 33), ("device_error", ctypes.c_int32),
+                ("_pad", ctypes.c_int32)]
+
+    def as_dict(self):
+        d = {n: int(getattr(self, n)) for n in ("steps", "rows", "drafted", "accepted", "emitted",
+                                               "accepted_independent", "device_error")}
+        for n in ("hist_accepted", "drafted_by_k", "accepted_by_k"):
+            d[n] = [int(x) for x in getattr(self, n)]
+        return d
+
+
+_lib = None
+
+
+def load():
+    """Load libsv.so (raises if it has not been built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} not built; run `python -m paper_2604_09562_b200.build`")
+    lib = ctypes.CDLL(LIB_PATH)
+    vp, i32, u64, sz = ctypes.c_void_p, ctypes.c_int32, ctypes.c_uint64, ctypes.c_size_t
+    P = ctypes.POINTER
+    sig = {
+        "sv_version": ([], ctypes.c_char_p),
+        "sv_strerror": ([ctypes.c_int], ctypes.c_char_p),
+        "sv_query_sizes": ([P(Config), P(sz), P(sz)], ctypes.c_int),
+        "sv_create": ([P(Config), P(Weights), vp, vp, vp, P(vp)], ctypes.c_int),
+        "sv_destroy": ([vp], ctypes.c_int),
+        "sv_append_kv": ([vp, i32, u64, vp, vp, i32, i32], ctypes.c_int),
+        "sv_verify": ([vp, i32, P(i32), P(i32), vp, vp, u64, ctypes.c_int, ctypes.c_float, vp, vp, vp],
+                      ctypes.c_int),
+        "sv_verify_logits": ([vp, i32, P(i32), P(i32), vp, vp, vp, u64, ctypes.c_int, ctypes.c_float, vp, vp],
+                             ctypes.c_int),
+        "sv_commit": ([vp, vp], ctypes.c_int),
+        "sv_release": ([vp, i32], ctypes.c_int),
+        "sv_stats": ([vp, P(LaneStats), ctypes.c_int], ctypes.c_int),
+        "sv_set_taps": ([vp, ctypes.c_int], ctypes.c_int),
+        "sv_get_tap": ([vp, ctypes.c_char_p, P(vp), P(sz)], ctypes.c_int),
+        "sv_debug_uniforms": ([vp, u64, u64, ctypes.c_uint32, i32, i32, i32, vp], ctypes.c_int),
+        "sv_draft_planted": ([vp, i32, P(i32), P(i32), vp, vp, vp, vp], ctypes.c_int),
+        "sv_nccl_unique_id": ([ctypes.c_char_p], ctypes.c_int),
+        "sv_nccl_comm_init": ([ctypes.c_int, ctypes.c_char_p, ctypes.c_int, P(vp)], ctypes.c_int),
+        "sv_nccl_comm_destroy": ([vp], ctypes.c_int),
+        "sv_kv_send": ([vp, i32, i32, i32, i32, ctypes.c_int, vp, vp], ctypes.c_int),
+        "sv_kv_recv_append": ([vp, i32, u64, i32, vp, ctypes.c_int, vp], ctypes.c_int),
+        "sv_kv_packed_bytes": ([P(Config), i32], sz),
+        "sv_kv_pack": ([vp, vp, i32, i32, i32, i32, i32, vp, vp], ctypes.c_int),
+    }
+    for name, (args, res) in sig.items():
+        f = getattr(lib, name)
+        f.argtypes = args
+        f.restype = res
+    _lib = lib
+    return lib
+
+
+def strerror(status):
+    try:
+        return load().sv_strerror(status).decode()
+    except ImportError:
+        return "?"
+
+
+def _check(status, what):
+    if status != SV_OK:
+        raise SvError(status, what)
+
+
+def _i32_array(xs):
+    xs = [int(x) for x in xs]
+    return (ctypes.c_int32 * max(1, len(xs)))(*xs), len(xs)
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _aligned_empty(nbytes, device, align=1024):
+    buf = torch.empty(nbytes + align, dtype=torch.uint8, device=device)
+    off = (-buf.data_ptr()) % align
+    return buf, buf[off:off + nbytes]
+
+
+class Lane:
+    """One decode lane (one sv_ctx) on the current CUDA device and stream."""
+
+    def __init__(self, cfg, weights, stream=None, device=None):
+        if not torch.cuda.is_available():
+            raise RuntimeError("sv.Lane needs a CUDA device (no CPU fallback)")
+        self.lib = load()
+        self.cfg = Config.from_any(cfg)
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
+        kvb, wsb = ctypes.c_size_t(), ctypes.c_size_t()
+        _check(self.lib.sv_query_sizes(ctypes.byref(self.cfg), ctypes.byref(kvb), ctypes.byref(wsb)),
+               "sv_query_sizes")
+        self._pool_raw, self.kv_pool = _aligned_empty(kvb.value, self.device)
+        self._ws_raw, self.workspace = _aligned_empty(wsb.value, self.device)
+        self.weights = {}
+        w = Weights()
+        for n in WEIGHT_NAMES:
+            t = weights[n]
+            if t.dtype != torch.bfloat16 or t.device.type != "cuda" or not t.is_contiguous():
+                raise ValueError(f"weight {n} must be a contiguous cuda bf16 tensor")
+            self.weights[n] = t
+            setattr(w, n, t.data_ptr() if t.numel() else None)
+        self._w = w
+        ctx = ctypes.c_void_p()
+        _check(self.lib.sv_create(ctypes.byref(self.cfg), ctypes.byref(w), _ptr(self.kv_pool), _ptr(self.workspace),
+                                  ctypes.c_void_p(self.stream.cuda_stream), ctypes.byref(ctx)), "sv_create")
+        self.ctx = ctx
+        K1 = self.cfg.max_depth + 1
+        self._acc = torch.empty(self.cfg.max_batch, dtype=torch.int32, device=self.device)
+        self._tok = torch.empty(self.cfg.max_batch, K1, dtype=torch.int32, device=self.device)
+
+    def close(self):
+        if getattr(self, "ctx", None):
+            self.lib.sv_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ------------------------------------------------------------------ calls
+    def append_kv(self, slot, request_id, k, v, pending_token):
+        n = 0 if k is None else int(k.shape[1])
+        _check(self.lib.sv_append_kv(self.ctx, slot, request_id, _ptr(k), _ptr(v), n, int(pending_token)),
+               "sv_append_kv")
+
+    def verify(self, slots, depths, draft_tokens, draft_probs=None, seed=0, mode="greedy", temperature=1.0,
+               logits_out=None, out=None):
+        """Returns (accepted_len [B] int32, out_tokens [B][max_depth+1] int32) device tensors."""
+        s, B = _i32_array(slots)
+        dpt, _ = _i32_array(depths)
+        acc, tok = (self._acc[:B], self._tok[:B]) if out is None else out
+        m = GREEDY if mode in ("greedy", GREEDY) else SAMPLE
+        _check(self.lib.sv_verify(self.ctx, B, s, dpt, _ptr(draft_tokens), _ptr(draft_probs), seed, m,
+                                  float(temperature), _ptr(acc), _ptr(tok), _ptr(logits_out)), "sv_verify")
+        return acc, tok
+
+    def verify_logits(self, slots, depths, draft_tokens, logits, draft_probs=None, seed=0, mode="greedy",
+                      temperature=1.0):
+        s, B = _i32_array(slots)
+        dpt, _ = _i32_array(depths)
+        acc, tok = self._acc[:B], self._tok[:B]
+        m = GREEDY if mode in ("greedy", GREEDY) else SAMPLE
+        _check(self.lib.sv_verify_logits(self.ctx, B, s, dpt, _ptr(draft_tokens), _ptr(draft_probs), _ptr(logits),
+                                         seed, m, float(temperature), _ptr(acc), _ptr(tok)), "sv_verify_logits")
+        return acc, tok
+
+    def commit(self, n_keep=None):
+        _check(self.lib.sv_commit(self.ctx, _ptr(n_keep)), "sv_commit")
+
+    def release(self, slot):
+        _check(self.lib.sv_release(self.ctx, slot), "sv_release")
+
+    def stats(self, reset=False, check=True):
+        st = LaneStats()
+        r = self.lib.sv_stats(self.ctx, ctypes.byref(st), 1 if reset else 0)
+        if check:
+            _check(r, "sv_stats")
+        return st.as_dict()
+
+    def tap(self, name, dtype, shape=None):
+        """Device tensor viewing the library's buffer `name` (valid until the next verify)."""
+        p, nb = ctypes.c_void_p(), ctypes.c_size_t()
+        _check(self.lib.sv_get_tap(self.ctx, name.encode(), ctypes.byref(p), ctypes.byref(nb)), "sv_get_tap")
+        off = p.value - self.workspace.data_ptr()
+        if not (0 <= off and off + nb.value <= self.workspace.numel()):
+            raise RuntimeError(f"tap {name} outside the workspace")
+        t = self.workspace[off:off + nb.value].view(dtype)
+        return t if shape is None else t[: _numel(shape)].view(*shape)
+
+    def debug_uniforms(self, seed, rid, z, purpose, x0, n):
+        u = torch.empty(n, dtype=torch.float32, device=self.device)
+        _check(self.lib.sv_debug_uniforms(self.ctx, seed, rid, z, purpose, x0, n, _ptr(u)), "sv_debug_uniforms")
+        return u
+
+    def draft_planted(self, slots, depths, succ, dev_mask, dev_tok, out):
+        s, B = _i32_array(slots)
+        dpt, _ = _i32_array(depths)
+        _check(self.lib.sv_draft_planted(self.ctx, B, s, dpt, _ptr(succ), _ptr(dev_mask), _ptr(dev_tok), _ptr(out)),
+               "sv_draft_planted")
+        return out
+
+    # ------------------------------------------------------------------ hand-off
+    def kv_recv_append(self, slot, request_id, n_tokens, staging, peer, comm):
+        _check(self.lib.sv_kv_recv_append(self.ctx, slot, request_id, n_tokens, _ptr(staging), peer, comm),
+               "sv_kv_recv_append")
+
+    def packed_bytes(self, n_tokens):
+        return int(self.lib.sv_kv_packed_bytes(ctypes.byref(self.cfg), n_tokens))
+
+
+def _numel(shape):
+    n = 1
+    for s in shape:
+        n *= int(s)
+    return n
+
+
+# ---------------------------------------------------------------------- NCCL hand-off helpers
+def nccl_unique_id():
+    buf = ctypes.create_string_buffer(128)
+    _check(load().sv_nccl_unique_id(buf), "sv_nccl_unique_id")
+    return bytes(buf.raw)
+
+
+def nccl_comm_init(nranks, uid, rank):
+    comm = ctypes.c_void_p()
+    _check(load().sv_nccl_comm_init(nranks, uid, rank, ctypes.byref(comm)), "sv_nccl_comm_init")
+    return comm
+
+
+def nccl_comm_destroy(comm):
+    _check(load().sv_nccl_comm_destroy(comm), "sv_nccl_comm_destroy")
+
+
+def kv_pack(k, v, pending_token, out, stream=None):
+    L, n, H, dh = k.shape
+    st = stream if stream is not None else torch.cuda.current_stream(k.device)
+    _check(load().sv_kv_pack(_ptr(k), _ptr(v), L, H, dh, n, int(pending_token), _ptr(out),
+                             ctypes.c_void_p(st.cuda_stream)), "sv_kv_pack")
+    return out
+
+
+def kv_send(packed, n_layers, n_kv_heads, head_dim, n_tokens, peer, comm, stream=None):
+    st = stream if stream is not None else torch.cuda.current_stream(packed.device)
+    _check(load().sv_kv_send(_ptr(packed), n_layers, n_kv_heads, head_dim, n_tokens, peer, comm,
+                             ctypes.c_void_p(st.cuda_stream)), "sv_kv_send")
+
+
+def packed_bytes(cfg, n_tokens):
+    c = Config.from_any(cfg)
+    return int(load().sv_kv_packed_bytes(ctypes.byref(c), n_tokens))

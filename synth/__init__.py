@@ -46,8 +46,8 @@ class ModelConfig:
 
 # BASELINE.json configs[0]: toy verify (1 layer, 2 q / 2 kv heads x 64, vocab 512)
 TOY = ModelConfig(n_layers=1, d_model=128, n_q_heads=2, n_kv_heads=2, head_dim=64,
-                  vocab=512, ffn_dim=0, n_pages=64, max_slots=8, max_batch=8,
-                  max_depth=8, max_pos=512)
+                  vocab=512, ffn_dim=0, n_pages=128, max_slots=8, max_batch=8,
+                  max_depth=8, max_pos=2048)
 # coverage variant with the MLP on (SURVEY.md §8 "toy+mlp")
 TOY_MLP = TOY.with_(ffn_dim=256)
 # BASELINE.json configs[1] (and north-star): Llama-3-8B-shaped single layer + lm-head
