@@ -1,0 +1,425 @@
+#!/usr/bin/env python
+"""Benchmark of the speculative-verify hot path (BASELINE.json metric):
+accepted tokens/s of the verify step, verify-step us, % of the HBM / tensor roofline.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload ns|c2|c3|c4|toy]
+    python bench.py --impl reference ...        # the fp64 CPU oracle arm
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+A step = one planted-drafter launch (bench fixture) + sv_verify + sv_commit on one
+decode lane holding `batch` requests. Weak scaling: every
+rank runs its own lane (own requests, no collective on the data path). Inputs
+(weights, KV) live in HBM before the timed region and exceed L2 (126 MB).
+Prints ONE JSON line on rank 0.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import synth  # noqa: E402
+
+METRIC = "accepted tokens/s (verify step)"
+UNIT = "tokens/s"
+PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
+
+
+def peaks():
+    try:
+        p = json.load(open(PEAKS_FILE))
+        return dict(hbm=p["hbm_gbs"], bf16=p["bf16_tflops"], bf16_sus=p.get("bf16_tflops_sustained", p["bf16_tflops"]),
+                    src="measured")
+    except Exception:
+        return dict(hbm=6650.0, bf16=1590.0, bf16_sus=1400.0, src="fallback")
+
+
+# ------------------------------------------------------------------ clocks sampler
+class Clocks:
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.Q,
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            f = [x.strip() for x in line.split(",")]
+            if len(f) == 6:
+                self.rows.append(f)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------------ workload setup
+def planted_weights(wl):
+    w = synth.model_weights(wl.cfg, seed=0, embed_std=wl.embed_std)
+    if wl.beta > 0:
+        return synth.planted_successor(wl.cfg, w, seed=1, beta=wl.beta)
+    return w, torch.randperm(wl.cfg.vocab, generator=torch.Generator().manual_seed(1)).to(torch.int32)
+
+
+def build_lane(wl, rank, dev):
+    from paper_2604_09562_b200 import sv
+    cfg = wl.cfg
+    w, succ = planted_weights(wl)
+    wd = {k: v.to(dev) for k, v in w.items()}
+    lane = sv.Lane(cfg, wd)
+    ctx = synth.ctx_lengths(wl, seed=100 + rank)
+    reqs = []
+    for i, n in enumerate(ctx):
+        k, v = synth.context_kv(cfg, n, seed=10_000 * (rank + 1) + i)
+        pend = int(synth.random_tokens(1, cfg.vocab, seed=20_000 * (rank + 1) + i)[0])
+        rid = (rank << 32) | (i + 1)
+        lane.append_kv(i, rid, k.to(dev), v.to(dev), pend)
+        reqs.append(dict(L=n, rid=rid, pending=pend, k=k, v=v))
+    torch.cuda.synchronize(dev)
+    return lane, w, succ, reqs
+
+
+def depths_for(wl, n_steps, seed):
+    g = torch.Generator().manual_seed(seed)
+    return torch.randint(wl.kmin, wl.kmax + 1, (n_steps, wl.batch), generator=g).tolist()
+
+
+def algorithmic(wl, ctx_lens, depths):
+    """Algorithmic bytes / flops per launch of the two roofline kernels."""
+    cfg = wl.cfg
+    T = sum(k + 1 for k in depths)
+    kv_tok = 2 * cfg.n_kv_heads * cfg.head_dim * 2                       # 4096 B / token / layer
+    attn_bytes = sum(L * kv_tok for L in ctx_lens) + T * kv_tok + T * 2 * cfg.n_q_heads * cfg.head_dim * 2
+    lm_flops = 2.0 * T * cfg.d_model * cfg.vocab
+    return dict(T=T, attn_bytes=attn_bytes * cfg.n_layers, lm_flops=lm_flops)
+
+
+def run_gpu(args, wl, rank, world, dev):
+    from paper_2604_09562_b200 import sv
+    import torch.distributed as dist
+    lane, w, succ, reqs = build_lane(wl, rank, dev)
+    cfg = wl.cfg
+    B = wl.batch
+    total = args.warmup + args.steps
+    depths = depths_for(wl, total + args.e2e_steps, seed=7 + rank)
+    kmax_rows = B * wl.kmax
+    masks, devtok = synth.planted_masks(total + args.e2e_steps, kmax_rows, wl.alpha, cfg.vocab, seed=9 + rank)
+    masks_d, devtok_d, succ_d = masks.to(dev), devtok.to(dev), succ.to(dev)
+    drafts = torch.empty(kmax_rows, dtype=torch.int32, device=dev)
+    acc = torch.empty(B, dtype=torch.int32, device=dev)
+    tok = torch.empty(B, cfg.max_depth + 1, dtype=torch.int32, device=dev)
+    slots = list(range(B))
+    mode = wl.mode
+
+    def step(i):
+        lane.draft_planted(slots, depths[i], succ_d, masks_d[i], devtok_d[i], drafts)
+        lane.verify(slots, depths[i], drafts, None, seed=1234 + i, mode=mode, temperature=wl.temperature,
+                    out=(acc, tok))
+        lane.commit()
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize(dev)
+    lane.stats(reset=True)
+    # context lengths at the start of the timed region (for the algorithmic attention bytes)
+    ln = lane.tap("len", torch.int32, (cfg.max_slots,))[:B].cpu().tolist()
+    lane.profile(True)
+    lane.profile_read(reset=True)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    stream = torch.cuda.current_stream(dev)
+    launches0 = sv.launch_count()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    with Clocks(dev.index) as clk:
+        ev[0].record(stream)
+        for i in range(args.steps):
+            step(args.warmup + i)
+            ev[i + 1].record(stream)
+        torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    launches = sv.launch_count() - launches0
+    elapsed_ms = ev[0].elapsed_time(ev[-1])
+    per_step = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]
+    prof = lane.profile_read(reset=True)
+    lane.profile(False)
+    st = lane.stats()
+    tokens = st["emitted"]
+    # ----- roofline of the dominant kernels (live CUDA-event durations, averaged per launch)
+    pk = peaks()
+    alg = algorithmic(wl, ln, depths[args.warmup])
+    kern = {}
+    for name, (ms, n) in prof.items():
+        if n:
+            kern[name] = dict(ms_per_launch=ms / n, launches=n, share=ms / max(1e-9, sum(v[0] for v in prof.values())))
+    lm = kern.get("lm_head")
+    at = kern.get("attention")
+    roof = {}
+    if lm:
+        ach = alg["lm_flops"] / (lm["ms_per_launch"] * 1e-3) / 1e12
+        roof["lm_head"] = {"bound": "tensor", "achieved": round(ach, 2), "peak": pk["bf16_sus"], "unit": "TFLOP/s",
+                           "frac": round(ach / pk["bf16_sus"], 4), "traffic": None,
+                           "flops_per_launch": alg["lm_flops"], "us_per_launch": round(lm["ms_per_launch"] * 1e3, 2)}
+    if at:
+        ach = alg["attn_bytes"] / (at["ms_per_launch"] * 1e-3) / 1e9
+        roof["attention"] = {"bound": "hbm", "achieved": round(ach, 1), "peak": pk["hbm"], "unit": "GB/s",
+                             "frac": round(ach / pk["hbm"], 4), "frac_of_8tbs": round(ach / 8000.0, 4),
+                             "traffic": None, "bytes_per_launch": alg["attn_bytes"],
+                             "us_per_launch": round(at["ms_per_launch"] * 1e3, 2)}
+    dominant = max(kern.items(), key=lambda kv: kv[1]["ms_per_launch"] * kv[1]["launches"])[0] if kern else None
+    # ----- e2e through host buffers (host drafter, pinned H2D drafts, D2H results each step)
+    e2e = run_e2e(args, wl, lane, succ, depths, masks, devtok, dev, total) if args.e2e_steps > 0 else None
+    return dict(elapsed_ms=elapsed_ms, tokens=tokens, per_step=per_step, prof=kern, roof=roof, dominant=dominant,
+                launches=launches, clocks=clk.summary(), stats=st, e2e=e2e, w=w, succ=succ, reqs=reqs,
+                depths=depths, masks=masks, devtok=devtok, alg=alg)
+
+
+def run_e2e(args, wl, lane, succ, depths, masks, devtok, dev, start):
+    cfg = wl.cfg
+    B = wl.batch
+    slots = list(range(B))
+    succ_h = succ.numpy()
+    pend = lane.tap("pending", torch.int32, (cfg.max_slots,))[:B].cpu().numpy().copy()
+    h_drafts = torch.empty(B * wl.kmax, dtype=torch.int32).pin_memory()
+    h_acc = torch.empty(B, dtype=torch.int32).pin_memory()
+    h_tok = torch.empty(B, cfg.max_depth + 1, dtype=torch.int32).pin_memory()
+    d_drafts = torch.empty(B * wl.kmax, dtype=torch.int32, device=dev)
+    acc = torch.empty(B, dtype=torch.int32, device=dev)
+    tok = torch.empty(B, cfg.max_depth + 1, dtype=torch.int32, device=dev)
+    lane.stats(reset=True)
+    torch.cuda.synchronize(dev)
+    h2d = d2h = 0
+    t0 = time.perf_counter()
+    for s in range(args.e2e_steps):
+        i = start + s
+        ks = depths[i]
+        m, dt = masks[i].numpy(), devtok[i].numpy()
+        out, off = h_drafts.numpy(), 0
+        for b in range(B):               # host planted drafter on the last emitted token
+            prev = int(pend[b])
+            for j in range(ks[b]):
+                t = int(dt[off + j]) if m[off + j] else int(succ_h[prev])
+                out[off + j] = t
+                prev = t
+            off += ks[b]
+        n = off
+        d_drafts[:n].copy_(h_drafts[:n], non_blocking=True)
+        lane.verify(slots, ks, d_drafts, None, seed=99 + i, mode=wl.mode, temperature=wl.temperature, out=(acc, tok))
+        lane.commit()
+        h_acc.copy_(acc, non_blocking=True)
+        h_tok.copy_(tok, non_blocking=True)
+        torch.cuda.current_stream(dev).synchronize()
+        a, tk = h_acc.numpy(), h_tok.numpy()
+        pend = tk[np.arange(B), a]
+        h2d += n * 4
+        d2h += B * 4 + B * (cfg.max_depth + 1) * 4
+    el = time.perf_counter() - t0
+    st = lane.stats(reset=True)
+    return {"value": st["emitted"] / el, "unit": UNIT, "h2d_bytes_per_step": h2d // args.e2e_steps,
+            "d2h_bytes_per_step": d2h // args.e2e_steps, "steps": args.e2e_steps,
+            "ms_per_step": 1e3 * el / args.e2e_steps}
+
+
+# ------------------------------------------------------------------ CPU oracle (baseline / reference arm)
+def oracle_lane_for(wl, w, reqs, n_req):
+    from oracle.lane import OracleLane
+    wn = {k: v.to(torch.float32).numpy() for k, v in w.items()}
+    lane = OracleLane(wl.cfg, wn)
+    for i in range(n_req):
+        r = reqs[i]
+        lane.append_kv(i, r["rid"], r["k"].to(torch.float32).numpy(), r["v"].to(torch.float32).numpy(), r["pending"])
+    return lane
+
+
+def oracle_steps(wl, lane, n_req, succ, depths, masks, devtok, step_ids):
+    """Run verify+commit of the first n_req requests on the oracle; returns (tokens, seconds)."""
+    from oracle import verify as ov
+    succ_h = succ.numpy()
+    tokens, secs = 0, 0.0
+    for i in step_ids:
+        ks = depths[i][:n_req]
+        m, dt = masks[i].numpy(), devtok[i].numpy()
+        drafts, off = [], 0
+        for b in range(n_req):
+            prev = lane.slots[b]["pending"]
+            for j in range(ks[b]):
+                t = int(dt[off + j]) if m[off + j] else int(succ_h[prev])
+                drafts.append(t)
+                prev = t
+            off += ks[b]
+        mode = ov.GREEDY if wl.mode == "greedy" else ov.SAMPLE
+        t0 = time.perf_counter()
+        acc, em, _ = lane.verify(list(range(n_req)), ks, drafts, None, 1234 + i, mode, wl.temperature)
+        lane.commit()
+        secs += time.perf_counter() - t0
+        tokens += sum(a + 1 for a in acc)
+    return tokens, secs
+
+
+def blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        return max([i.get("num_threads", 1) for i in threadpool_info() if i.get("user_api") == "blas"] or [1])
+    except Exception:
+        return os.cpu_count()
+
+
+def cpu_baseline(wl, res, budget_s=20.0):
+    n_req = 1
+    lane = oracle_lane_for(wl, res["w"], res["reqs"], n_req)
+    tokens, secs, steps = 0, 0.0, 0
+    while secs < budget_s and steps < 8:
+        t, s = oracle_steps(wl, lane, n_req, res["succ"], res["depths"], res["masks"], res["devtok"], [steps])
+        tokens, secs, steps = tokens + t, secs + s, steps + 1
+    return {"value": round(tokens / secs, 3), "unit": UNIT, "cores": blas_threads(), "kind": "oracle",
+            "sample": f"{steps} verify+commit step(s) of request 0 of the {wl.name} workload (fp64 numpy oracle, "
+                      f"same weights/KV/drafts as the GPU lane); host os.cpu_count()={os.cpu_count()}",
+            "seconds": round(secs, 2), "tokens": tokens}
+
+
+def run_reference(args, wl):
+    """--impl reference: the fp64 CPU oracle, as it stands, on a bounded sample of the same workload."""
+    w, succ = planted_weights(wl)
+    ctx = synth.ctx_lengths(wl, seed=100)
+    reqs = []
+    for i in range(1):
+        k, v = synth.context_kv(wl.cfg, ctx[i], seed=10_000 + i)
+        pend = int(synth.random_tokens(1, wl.cfg.vocab, seed=20_000 + i)[0])
+        reqs.append(dict(L=ctx[i], rid=(0 << 32) | (i + 1), pending=pend, k=k, v=v))
+    total = args.warmup + args.steps
+    depths = depths_for(wl, total, seed=7)
+    masks, devtok = synth.planted_masks(total, wl.batch * wl.kmax, wl.alpha, wl.cfg.vocab, seed=9)
+    lane = oracle_lane_for(wl, w, reqs, 1)
+    oracle_steps(wl, lane, 1, succ, depths, masks, devtok, range(args.warmup))
+    tokens, secs = oracle_steps(wl, lane, 1, succ, depths, masks, devtok, range(args.warmup, total))
+    v = tokens / secs
+    line = {"impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * secs / args.steps, 2),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": wl.name, "sample": "request 0 of the workload per step"},
+            "cpu_baseline": {"value": round(v, 3), "unit": UNIT, "cores": blas_threads(), "kind": "oracle",
+                             "sample": f"request 0 of the {wl.name} workload, {args.steps} verify+commit steps"},
+            "e2e": {"value": round(v, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--workload", default="ns")
+    ap.add_argument("--impl", default="sv", choices=["sv", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--detail", action="store_true", help="add per-stage breakdown to the JSON line")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    wl = synth.workload(args.workload, steps_budget=args.warmup + args.steps + args.e2e_steps + 8)
+
+    if args.impl == "reference":
+        if rank == 0:
+            run_reference(args, wl)
+        return
+
+    import torch.distributed as dist
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    res = run_gpu(args, wl, rank, world, dev)
+    elapsed, tokens = res["elapsed_ms"], res["tokens"]
+    if world > 1:
+        t = torch.tensor([elapsed], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        n = torch.tensor([tokens], dtype=torch.float64, device=dev)
+        dist.all_reduce(n, op=dist.ReduceOp.SUM)
+        e2 = torch.tensor([res["e2e"]["value"] if res["e2e"] else 0.0], dtype=torch.float64, device=dev)
+        dist.all_reduce(e2, op=dist.ReduceOp.SUM)
+        elapsed, tokens = float(t.item()), float(n.item())
+        if res["e2e"]:
+            res["e2e"]["value"] = float(e2.item())
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    cfg = wl.cfg
+    value = tokens / (elapsed * 1e-3)
+    ps = sorted(res["per_step"])
+    st = res["stats"]
+    dom = res["dominant"]
+    roof = res["roof"].get(dom) or res["roof"].get("lm_head") or {}
+    line = {
+        "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(elapsed / args.steps, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": wl.name, "model": "Llama-3-8B-shaped 1 layer + lm-head (random init, planted successor)"
+                   if cfg.d_model == 4096 else "toy", "batch_per_gpu": wl.batch, "depth": [wl.kmin, wl.kmax],
+                   "ctx": list(wl.ctx), "mode": wl.mode, "parallelism": f"dp{world} (independent decode lanes)",
+                   "l2": "inputs > L2 (weights 1.5 GB + KV >= 1 GB per step)", "drafter": f"planted alpha={wl.alpha}"},
+        "verify_step_us": {"median": round(1e3 * statistics.median(ps), 1), "p10": round(1e3 * ps[len(ps) // 10], 1),
+                           "p90": round(1e3 * ps[(9 * len(ps)) // 10], 1)},
+        "acceptance": {"a_t": round(st["accepted"] / max(1, st["drafted"]), 4),
+                       "tokens_per_request_step": round(st["emitted"] / max(1, args.steps * wl.batch), 3)},
+        "roofline": {k: v for k, v in roof.items() if k in ("bound", "achieved", "peak", "unit", "frac", "traffic")}
+        | {"kernel": dom},
+        "kernels": res["roof"],
+        "gpu_launches": res["launches"],
+        "launches_per_step": round(res["launches"] / args.steps, 2),
+        "clocks": res["clocks"],
+        "e2e": res["e2e"],
+        "peaks": peaks()["src"],
+    }
+    if args.detail:
+        line["stages"] = {k: {"us": round(v["ms_per_launch"] * 1e3, 1), "share": round(v["share"], 4)}
+                          for k, v in res["prof"].items()}
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(wl, res)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

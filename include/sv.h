@@ -207,6 +207,18 @@ sv_status sv_draft_planted(sv_ctx* ctx, int32_t batch, const int32_t* slots, con
                            const int32_t* succ, const uint8_t* dev_mask, const int32_t* dev_tok,
                            int32_t* draft_tokens);
 
+/* Measurement hooks (bench.py): per-stage CUDA-event timing on the lane's stream.
+ * sv_profile_enable(ctx, 1) brackets every stage of sv_verify / sv_commit /
+ * sv_draft_planted with cudaEventRecord; sv_profile_read (syncs) returns, for each
+ * of sv_profile_num_stages() stages (names from sv_profile_stage_name), the summed
+ * device milliseconds and launch count since the last reset. sv_launch_count()
+ * is the number of CUDA kernels this library has launched in the process. */
+sv_status sv_profile_enable(sv_ctx* ctx, int on);
+int32_t sv_profile_num_stages(void);
+const char* sv_profile_stage_name(int32_t i);
+sv_status sv_profile_read(sv_ctx* ctx, double* ms_total, int64_t* count, int32_t n, int reset);
+uint64_t sv_launch_count(void);
+
 /* ---------------- prefill -> decode KV hand-off ----------------
  * NCCL point-to-point over NVLink ("NIXL" replaced by
  * ncclSend/ncclRecv). Communicators are created by the library; the 128-byte

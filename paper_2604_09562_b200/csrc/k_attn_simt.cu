@@ -129,6 +129,7 @@ cudaError_t launch_attention(const LaneDev& d, int layer, int batch, cudaStream_
     cudaFuncSetAttribute(attn_simt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
     attr = true;
   }
+  SV_COUNT_LAUNCH();
   attn_simt_kernel<<<148 * 4, 128, smem, s>>>(d, layer);
   return cudaGetLastError();
 }
@@ -159,6 +160,7 @@ __global__ void attn_combine_kernel(LaneDev d) {
 }
 
 cudaError_t launch_attn_combine(const LaneDev& d, int T, cudaStream_t s) {
+  SV_COUNT_LAUNCH();
   attn_combine_kernel<<<T, 256, 0, s>>>(d);
   return cudaGetLastError();
 }

@@ -171,6 +171,7 @@ __global__ void __launch_bounds__(FIN_THREADS) finalize_kernel(LaneDev d, const 
 cudaError_t launch_finalize(const LaneDev& d, int batch, const int* draft_tokens, const float* draft_probs,
                             const float* logits, uint64_t seed, int mode, float inv_temp, int* accepted_len,
                             int* out_tokens, cudaStream_t s) {
+  SV_COUNT_LAUNCH();
   finalize_kernel<<<batch, FIN_THREADS, 0, s>>>(d, draft_tokens, draft_probs, logits, seed, mode, inv_temp,
                                                 accepted_len, out_tokens);
   return cudaGetLastError();

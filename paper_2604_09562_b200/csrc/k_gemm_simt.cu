@@ -69,6 +69,7 @@ cudaError_t launch_gemm_simt(const bf16* A, const bf16* B, float* C, int M, int 
   if (M <= 0 || N <= 0) return cudaSuccess;
   if (K % SG_BK) return cudaErrorInvalidValue;
   dim3 grid((N + SG_BN - 1) / SG_BN, (M + SG_BM - 1) / SG_BM);
+  SV_COUNT_LAUNCH();
   gemm_simt_kernel<<<grid, 256, 0, s>>>(A, B, C, M, N, K);
   return cudaGetLastError();
 }

@@ -72,6 +72,7 @@ __global__ void __launch_bounds__(256) commit_kernel(LaneDev d, const int* __res
 }
 
 cudaError_t launch_commit(const LaneDev& d, const int* n_keep, int batch, cudaStream_t s) {
+  SV_COUNT_LAUNCH();
   commit_kernel<<<batch, 256, 0, s>>>(d, n_keep);
   return cudaGetLastError();
 }
@@ -123,11 +124,13 @@ __global__ void append_copy_kernel(LaneDev d, int slot, const bf16* __restrict__
 cudaError_t launch_append(const LaneDev& d, int slot, unsigned long long rid, const bf16* k, const bf16* v, int n,
                           int pending, const int* pending_dev, int packed, cudaStream_t s) {
   int* scratch = d.n_items + 1;                  // two spare workspace words
+  SV_COUNT_LAUNCH();
   append_alloc_kernel<<<1, 1, 0, s>>>(d, slot, rid, n, pending, pending_dev, scratch);
   if (n > 0) {
     const size_t total = (size_t)d.n_layers * n * 2 * d.Hkv * (d.dh / 8);
     int grid = (int)((total + 255) / 256);
     if (grid > 148 * 8) grid = 148 * 8;
+    SV_COUNT_LAUNCH();
     append_copy_kernel<<<grid, 256, 0, s>>>(d, slot, k, v, n, packed, scratch);
   }
   return cudaGetLastError();
@@ -147,6 +150,7 @@ __global__ void release_kernel(LaneDev d, int slot) {
 }
 
 cudaError_t launch_release(const LaneDev& d, int slot, cudaStream_t s) {
+  SV_COUNT_LAUNCH();
   release_kernel<<<1, 256, 0, s>>>(d, slot);
   return cudaGetLastError();
 }
@@ -173,6 +177,7 @@ __global__ void kv_pack_kernel(const bf16* __restrict__ k, const bf16* __restric
 
 cudaError_t launch_kv_pack(const bf16* k, const bf16* v, int n_layers, int Hkv, int dh, int n, int pending,
                            void* packed, cudaStream_t s) {
+  SV_COUNT_LAUNCH();
   kv_pack_kernel<<<148 * 2, 256, 0, s>>>(k, v, n_layers, Hkv, dh, n, pending, reinterpret_cast<bf16*>(packed));
   return cudaGetLastError();
 }

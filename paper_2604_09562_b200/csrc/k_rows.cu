@@ -11,6 +11,8 @@
 
 namespace sv {
 
+unsigned long long g_launch_count = 0;
+
 // ------------------------------------------------------------------ a1: plan
 // One CTA. Serial prefix over <= 256 requests in thread 0, then parallel fills.
 __global__ void plan_kernel(LaneDev d, PlanArgs p, const int* __restrict__ draft_tokens, int attn) {
@@ -83,6 +85,7 @@ __global__ void plan_kernel(LaneDev d, PlanArgs p, const int* __restrict__ draft
 }
 
 cudaError_t launch_plan(const LaneDev& d, const PlanArgs& p, const int* draft_tokens, bool attn, cudaStream_t s) {
+  SV_COUNT_LAUNCH();
   plan_kernel<<<1, 1024, 0, s>>>(d, p, draft_tokens, attn ? 1 : 0);
   return cudaGetLastError();
 }
@@ -118,6 +121,7 @@ __global__ void __launch_bounds__(256) embed_norm_kernel(LaneDev d) {
 }
 
 cudaError_t launch_embed_norm(const LaneDev& d, int T, cudaStream_t s) {
+  SV_COUNT_LAUNCH();
   embed_norm_kernel<<<T, 256, 0, s>>>(d);
   return cudaGetLastError();
 }
@@ -133,6 +137,7 @@ __global__ void __launch_bounds__(256) rmsnorm_kernel(const float* __restrict__ 
 }
 
 cudaError_t launch_rmsnorm(const LaneDev& d, const float* x, const bf16* g, bf16* out, int T, cudaStream_t s) {
+  SV_COUNT_LAUNCH();
   rmsnorm_kernel<<<T, 256, 0, s>>>(x, g, out, d.D, d.eps);
   return cudaGetLastError();
 }
@@ -163,6 +168,7 @@ __global__ void qkv_rope_kernel(LaneDev d, int layer) {
 }
 
 cudaError_t launch_qkv_rope_epilogue(const LaneDev& d, int layer, int T, cudaStream_t s) {
+  SV_COUNT_LAUNCH();
   qkv_rope_kernel<<<T, 256, 0, s>>>(d, layer);
   return cudaGetLastError();
 }
@@ -175,6 +181,7 @@ __global__ void residual_kernel(const float* __restrict__ hin, const float* __re
 }
 
 cudaError_t launch_residual_epilogue(const float* hin, const float* c, float* hout, int T, int D, cudaStream_t s) {
+  SV_COUNT_LAUNCH();
   residual_kernel<<<148 * 4, 256, 0, s>>>(hin, c, hout, (size_t)T * D);
   return cudaGetLastError();
 }
@@ -190,6 +197,7 @@ __global__ void swiglu_kernel(LaneDev d, int T) {
 }
 
 cudaError_t launch_swiglu_epilogue(const LaneDev& d, int T, cudaStream_t s) {
+  SV_COUNT_LAUNCH();
   swiglu_kernel<<<148 * 4, 256, 0, s>>>(d, T);
   return cudaGetLastError();
 }
@@ -231,6 +239,7 @@ __global__ void tile_stats_kernel(LaneDev d, int T, float inv_temp) {
 
 cudaError_t launch_tile_stats(const LaneDev& d, int T, float inv_temp, cudaStream_t s) {
   const int warps = T * d.nt;
+  SV_COUNT_LAUNCH();
   tile_stats_kernel<<<(warps + 7) / 8, 256, 0, s>>>(d, T, inv_temp);
   return cudaGetLastError();
 }
@@ -253,6 +262,7 @@ __global__ void debug_uniforms_kernel(uint64_t seed, uint64_t rid, uint32_t z, i
 cudaError_t launch_debug_uniforms(uint64_t seed, uint64_t rid, uint32_t z, int purpose, int x0, int n, float* u,
                                   cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
+  SV_COUNT_LAUNCH();
   debug_uniforms_kernel<<<(n + 255) / 256, 256, 0, s>>>(seed, rid, z, purpose, x0, n, u);
   return cudaGetLastError();
 }
@@ -276,6 +286,7 @@ __global__ void draft_planted_kernel(LaneDev d, PlanArgs p, const int* __restric
 
 cudaError_t launch_draft_planted(const LaneDev& d, const PlanArgs& p, const int* succ, const uint8_t* mask,
                                  const int* dev_tok, int* draft_tokens, cudaStream_t s) {
+  SV_COUNT_LAUNCH();
   draft_planted_kernel<<<(p.batch + 127) / 128, 128, 0, s>>>(d, p, succ, mask, dev_tok, draft_tokens);
   return cudaGetLastError();
 }
@@ -293,6 +304,7 @@ cudaError_t launch_init_state(const LaneDev& d, cudaStream_t s) {
   int n = d.n_pages;
   if (d.max_slots > n) n = d.max_slots;
   if (kNumStats > n) n = kNumStats;
+  SV_COUNT_LAUNCH();
   init_state_kernel<<<(n + 255) / 256, 256, 0, s>>>(d);
   return cudaGetLastError();
 }

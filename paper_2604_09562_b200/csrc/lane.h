@@ -50,6 +50,10 @@ struct LaneDev {
   int* batch_n;                      // [1] batch of the pending verify (device copy)
 };
 
+// kernels launched by the library so far (measurement hook, sv_launch_count)
+extern unsigned long long g_launch_count;
+#define SV_COUNT_LAUNCH() (++::sv::g_launch_count)
+
 struct PlanArgs {
   int batch, T;
   int slots[kMaxBatch];

@@ -117,6 +117,32 @@ Layout make_layout(const sv_config& c) {
 
 }  // namespace
 
+// live per-stage timing with CUDA events on the lane's stream (sv_profile_*)
+enum Stage { ST_PLAN = 0, ST_EMBED, ST_QKV, ST_ATTN, ST_COMBINE, ST_OPROJ, ST_FFN_NORM, ST_GATE_UP, ST_DOWN,
+             ST_FINAL_NORM, ST_LM_HEAD, ST_FINALIZE, ST_COMMIT, ST_DRAFT, ST_ATTN_NORM, ST_NUM };
+static const char* kStageNames[ST_NUM] = {"plan", "embed_norm", "qkv_rope", "attention", "attn_combine", "o_proj",
+                                          "ffn_norm", "gate_up_swiglu", "down", "final_norm", "lm_head",
+                                          "finalize", "commit", "draft", "attn_norm"};
+
+struct Prof {
+  bool on = false;
+  std::vector<cudaEvent_t> free_ev;
+  struct Rec { int stage; cudaEvent_t a, b; };
+  std::vector<Rec> recs;
+  double ms[ST_NUM] = {};
+  long long n[ST_NUM] = {};
+  cudaEvent_t get() {
+    if (free_ev.empty()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      return e;
+    }
+    cudaEvent_t e = free_ev.back();
+    free_ev.pop_back();
+    return e;
+  }
+};
+
 struct sv_ctx {
   sv_config cfg;
   sv_weights w;
@@ -133,7 +159,43 @@ struct sv_ctx {
   int last_T = 0, last_batch = 0;
   int sticky = 0;
   sv::GemmPlan* gemm = nullptr;
+  Prof prof;
 };
+
+static cudaEvent_t prof_begin(sv_ctx* c) {
+  if (!c->prof.on) return nullptr;
+  cudaEvent_t e = c->prof.get();
+  cudaEventRecord(e, c->stream);
+  return e;
+}
+static void prof_end(sv_ctx* c, int stage, cudaEvent_t a) {
+  if (!a) return;
+  cudaEvent_t b = c->prof.get();
+  cudaEventRecord(b, c->stream);
+  c->prof.recs.push_back({stage, a, b});
+  if (c->prof.recs.size() > 4096) {          // fold old records to bound memory
+    cudaEventSynchronize(b);
+    for (auto& r : c->prof.recs) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, r.a, r.b);
+      c->prof.ms[r.stage] += ms;
+      c->prof.n[r.stage] += 1;
+      c->prof.free_ev.push_back(r.a);
+      c->prof.free_ev.push_back(r.b);
+    }
+    c->prof.recs.clear();
+  }
+}
+// run `expr` (returning sv_status or cudaError_t) as timed stage `id`
+#define STAGE(c, id, expr)                    \
+  do {                                        \
+    cudaEvent_t _pe = prof_begin(c);          \
+    auto _r = (expr);                         \
+    prof_end(c, id, _pe);                     \
+    if (_r) return stage_status(_r);          \
+  } while (0)
+static sv_status stage_status(cudaError_t e);
+static sv_status stage_status(sv_status s) { return s; }
 
 static sv_status cuda_ok(cudaError_t e) {
   if (e != cudaSuccess) {
@@ -142,6 +204,7 @@ static sv_status cuda_ok(cudaError_t e) {
   }
   return SV_OK;
 }
+static sv_status stage_status(cudaError_t e) { return cuda_ok(e); }
 #define SV_CUDA(x)                                   \
   do {                                               \
     sv_status _s = cuda_ok(x);                       \
@@ -355,41 +418,37 @@ sv_status sv_verify(sv_ctx* c, int32_t batch, const int32_t* slots, const int32_
   const int T = p.T;
   cudaStream_t s = c->stream;
   const float inv_temp = mode == SV_SAMPLE ? 1.0f / temperature : 1.0f;
-  SV_CUDA(sv::launch_plan(d, p, draft_tokens, true, s));
-  SV_CUDA(sv::launch_embed_norm(d, T, s));
+  STAGE(c, ST_PLAN, sv::launch_plan(d, p, draft_tokens, true, s));
+  STAGE(c, ST_EMBED, sv::launch_embed_norm(d, T, s));
   const size_t nq = (size_t)d.Hq * d.dh;
   for (int layer = 0; layer < d.n_layers; ++layer) {
     const float* hin = layer == 0 ? d.h0 : d.h2;
-    if (layer > 0) SV_CUDA(sv::launch_rmsnorm(d, hin, d.attn_norm + (size_t)layer * d.D, d.a, T, s));
+    if (layer > 0) STAGE(c, ST_ATTN_NORM, sv::launch_rmsnorm(d, hin, d.attn_norm + (size_t)layer * d.D, d.a, T, s));
     sv::GemmEpi e{};
     e.layer = layer;
-    if ((st = gemm(c, d.a, d.wqkv + (size_t)layer * d.qkv_rows * d.D, d.cbuf, T, d.qkv_rows, d.D,
-                   sv::EPI_QKV_ROPE, e)))
-      return st;
-    SV_CUDA(sv::launch_attention(d, layer, batch, s));
-    SV_CUDA(sv::launch_attn_combine(d, T, s));
+    STAGE(c, ST_QKV, gemm(c, d.a, d.wqkv + (size_t)layer * d.qkv_rows * d.D, d.cbuf, T, d.qkv_rows, d.D,
+                          sv::EPI_QKV_ROPE, e));
+    STAGE(c, ST_ATTN, sv::launch_attention(d, layer, batch, s));
+    STAGE(c, ST_COMBINE, sv::launch_attn_combine(d, T, s));
     float* hattn = d.F > 0 ? d.h1 : d.h2;
     e.resid_in = hin;
     e.resid_out = hattn;
-    if ((st = gemm(c, d.o, d.wo + (size_t)layer * d.D * nq, d.cbuf, T, d.D, (int)nq, sv::EPI_RESIDUAL, e)))
-      return st;
+    STAGE(c, ST_OPROJ, gemm(c, d.o, d.wo + (size_t)layer * d.D * nq, d.cbuf, T, d.D, (int)nq, sv::EPI_RESIDUAL, e));
     if (d.F > 0) {
-      SV_CUDA(sv::launch_rmsnorm(d, d.h1, d.ffn_norm + (size_t)layer * d.D, d.b, T, s));
-      if ((st = gemm(c, d.b, d.w_gate_up + (size_t)layer * 2 * d.F * d.D, d.cbuf, T, 2 * d.F, d.D,
-                     sv::EPI_SWIGLU, e)))
-        return st;
+      STAGE(c, ST_FFN_NORM, sv::launch_rmsnorm(d, d.h1, d.ffn_norm + (size_t)layer * d.D, d.b, T, s));
+      STAGE(c, ST_GATE_UP, gemm(c, d.b, d.w_gate_up + (size_t)layer * 2 * d.F * d.D, d.cbuf, T, 2 * d.F, d.D,
+                                sv::EPI_SWIGLU, e));
       e.resid_in = d.h1;
       e.resid_out = d.h2;
-      if ((st = gemm(c, d.u, d.w_down + (size_t)layer * d.D * d.F, d.cbuf, T, d.D, d.F, sv::EPI_RESIDUAL, e)))
-        return st;
+      STAGE(c, ST_DOWN, gemm(c, d.u, d.w_down + (size_t)layer * d.D * d.F, d.cbuf, T, d.D, d.F, sv::EPI_RESIDUAL, e));
     }
   }
-  SV_CUDA(sv::launch_rmsnorm(d, d.h2, d.final_norm, d.z, T, s));
+  STAGE(c, ST_FINAL_NORM, sv::launch_rmsnorm(d, d.h2, d.final_norm, d.z, T, s));
   sv::GemmEpi e{};
   e.inv_temp = inv_temp;
-  if ((st = gemm(c, d.z, d.lm_head, d.logits, T, d.V, d.D, sv::EPI_LOGITS, e))) return st;
-  SV_CUDA(sv::launch_finalize(d, batch, draft_tokens, draft_probs, d.logits, seed, mode, inv_temp, accepted_len,
-                              out_tokens, s));
+  STAGE(c, ST_LM_HEAD, gemm(c, d.z, d.lm_head, d.logits, T, d.V, d.D, sv::EPI_LOGITS, e));
+  STAGE(c, ST_FINALIZE, sv::launch_finalize(d, batch, draft_tokens, draft_probs, d.logits, seed, mode, inv_temp,
+                                            accepted_len, out_tokens, s));
   if (logits_out)
     SV_CUDA(cudaMemcpyAsync(logits_out, d.logits, (size_t)T * d.V * 4, cudaMemcpyDeviceToDevice, s));
   for (int b = 0; b < batch; ++b) c->state[slots[b]] = PENDING;
@@ -428,7 +487,7 @@ sv_status sv_verify_logits(sv_ctx* c, int32_t batch, const int32_t* slots, const
 sv_status sv_commit(sv_ctx* c, const int32_t* n_keep) {
   if (!c) return SV_EINVAL;
   if (!c->pending_verify) return SV_ESTATE;
-  SV_CUDA(sv::launch_commit(c->d, n_keep, c->pending_batch, c->stream));
+  STAGE(c, ST_COMMIT, sv::launch_commit(c->d, n_keep, c->pending_batch, c->stream));
   for (int s : c->pending_slots) c->state[s] = ACTIVE;
   c->pending_verify = false;
   if (c->sticky & SV_DERR_NO_PAGES) return SV_ENOKV;
@@ -540,7 +599,7 @@ sv_status sv_draft_planted(sv_ctx* c, int32_t batch, const int32_t* slots, const
     p.depths[b] = depths[b];
     p.T += depths[b] + 1;
   }
-  SV_CUDA(sv::launch_draft_planted(c->d, p, succ, dev_mask, dev_tok, draft_tokens, c->stream));
+  STAGE(c, ST_DRAFT, sv::launch_draft_planted(c->d, p, succ, dev_mask, dev_tok, draft_tokens, c->stream));
   return SV_OK;
 }
 
@@ -557,6 +616,41 @@ size_t sv_kv_packed_bytes(const sv_config* cfg, int32_t n_tokens) {
   if (!cfg || n_tokens < 0) return 0;
   return (size_t)cfg->n_layers * n_tokens * 2 * cfg->n_kv_heads * cfg->head_dim * 2 + 16;
 }
+
+sv_status sv_profile_enable(sv_ctx* c, int on) {
+  if (!c) return SV_EINVAL;
+  c->prof.on = on != 0;
+  return SV_OK;
+}
+
+int32_t sv_profile_num_stages(void) { return ST_NUM; }
+
+const char* sv_profile_stage_name(int32_t i) { return (i >= 0 && i < ST_NUM) ? kStageNames[i] : nullptr; }
+
+sv_status sv_profile_read(sv_ctx* c, double* ms_total, int64_t* count, int32_t n, int reset) {
+  if (!c || !ms_total || !count || n < ST_NUM) return SV_EINVAL;
+  SV_CUDA(cudaStreamSynchronize(c->stream));
+  for (auto& r : c->prof.recs) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, r.a, r.b);
+    c->prof.ms[r.stage] += ms;
+    c->prof.n[r.stage] += 1;
+    c->prof.free_ev.push_back(r.a);
+    c->prof.free_ev.push_back(r.b);
+  }
+  c->prof.recs.clear();
+  for (int i = 0; i < ST_NUM; ++i) {
+    ms_total[i] = c->prof.ms[i];
+    count[i] = c->prof.n[i];
+    if (reset) {
+      c->prof.ms[i] = 0;
+      c->prof.n[i] = 0;
+    }
+  }
+  return SV_OK;
+}
+
+uint64_t sv_launch_count(void) { return sv::g_launch_count; }
 
 }  // extern "C"
 

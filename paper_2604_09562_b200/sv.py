@@ -27,7 +27,8 @@ EXPORTED = [
     "sv_version", "sv_strerror", "sv_query_sizes", "sv_create", "sv_destroy", "sv_append_kv", "sv_verify",
     "sv_verify_logits", "sv_commit", "sv_release", "sv_stats", "sv_set_taps", "sv_get_tap", "sv_debug_uniforms",
     "sv_draft_planted", "sv_nccl_unique_id", "sv_nccl_comm_init", "sv_nccl_comm_destroy", "sv_kv_send",
-    "sv_kv_recv_append", "sv_kv_packed_bytes", "sv_kv_pack",
+    "sv_kv_recv_append", "sv_kv_packed_bytes", "sv_kv_pack", "sv_profile_enable", "sv_profile_num_stages",
+    "sv_profile_stage_name", "sv_profile_read", "sv_launch_count",
 ]
 
 
@@ -110,6 +111,11 @@ def load():
         "sv_kv_recv_append": ([vp, i32, u64, i32, vp, ctypes.c_int, vp], ctypes.c_int),
         "sv_kv_packed_bytes": ([P(Config), i32], sz),
         "sv_kv_pack": ([vp, vp, i32, i32, i32, i32, i32, vp, vp], ctypes.c_int),
+        "sv_profile_enable": ([vp, ctypes.c_int], ctypes.c_int),
+        "sv_profile_num_stages": ([], i32),
+        "sv_profile_stage_name": ([i32], ctypes.c_char_p),
+        "sv_profile_read": ([vp, P(ctypes.c_double), P(ctypes.c_int64), i32, ctypes.c_int], ctypes.c_int),
+        "sv_launch_count": ([], u64),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -251,6 +257,18 @@ class Lane:
                "sv_draft_planted")
         return out
 
+    # ------------------------------------------------------------------ measurement hooks
+    def profile(self, on=True):
+        _check(self.lib.sv_profile_enable(self.ctx, 1 if on else 0), "sv_profile_enable")
+
+    def profile_read(self, reset=True):
+        """{stage: (total_ms, launches)} since the last reset (syncs the stream)."""
+        n = self.lib.sv_profile_num_stages()
+        ms = (ctypes.c_double * n)()
+        cnt = (ctypes.c_int64 * n)()
+        _check(self.lib.sv_profile_read(self.ctx, ms, cnt, n, 1 if reset else 0), "sv_profile_read")
+        return {self.lib.sv_profile_stage_name(i).decode(): (ms[i], cnt[i]) for i in range(n)}
+
     # ------------------------------------------------------------------ hand-off
     def kv_recv_append(self, slot, request_id, n_tokens, staging, peer, comm):
         _check(self.lib.sv_kv_recv_append(self.ctx, slot, request_id, n_tokens, _ptr(staging), peer, comm),
@@ -268,6 +286,11 @@ def _numel(shape):
 
 
 # ---------------------------------------------------------------------- NCCL hand-off helpers
+def launch_count():
+    """Kernels launched by libsv.so in this process."""
+    return int(load().sv_launch_count())
+
+
 def nccl_unique_id():
     buf = ctypes.create_string_buffer(128)
     _check(load().sv_nccl_unique_id(buf), "sv_nccl_unique_id")

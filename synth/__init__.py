@@ -158,6 +158,64 @@ def planted_successor(cfg, weights, seed, beta):
     return w, f.to(torch.int32)
 
 
+@dataclass(frozen=True)
+class Workload:
+    """A bench / parity workload."""
+    name: str
+    cfg: ModelConfig
+    batch: int
+    ctx: tuple            # (min, max) context length at start, uniform
+    kmin: int
+    kmax: int
+    mode: str             # "greedy" | "sample"
+    alpha: float          # planted drafter: probability each draft follows the planted successor
+    embed_std: float = 8.0
+    beta: float = 0.3     # planted-successor strength (logit margin ~ beta * sqrt(D))
+    temperature: float = 1.0
+
+
+def workload(name, steps_budget=64):
+    """Named workloads. `steps_budget` sizes the page pool for that many verify steps."""
+    def pool(batch, ctx_max, kmax, page=64):
+        per_req = (ctx_max + (kmax + 1) * steps_budget + page - 1) // page + 1
+        return batch * per_req, ctx_max + (kmax + 1) * steps_budget + 64
+    if name == "ns":          # north-star: bs64, k = 8, 4k context (BASELINE metric's verify-step config)
+        n_pages, max_pos = pool(64, 4096, 8)
+        cfg = LLAMA.with_(n_pages=n_pages, max_slots=64, max_batch=64, max_pos=max_pos)
+        return Workload("ns", cfg, 64, (4096, 4096), 8, 8, "greedy", 0.8)
+    if name == "c2":          # BASELINE configs[1]: bs64, adaptive k 1-8, ALPACA-like 256-token prompts
+        n_pages, max_pos = pool(64, 256, 8)
+        cfg = LLAMA.with_(n_pages=n_pages, max_slots=64, max_batch=64, max_pos=max_pos)
+        return Workload("c2", cfg, 64, (256, 256), 1, 8, "sample", 0.75)
+    if name == "c3":          # BASELINE configs[2]: bs128, context 1k-2k, sampled
+        n_pages, max_pos = pool(128, 2048, 8)
+        cfg = LLAMA.with_(n_pages=n_pages, max_slots=128, max_batch=128, max_pos=max_pos)
+        return Workload("c3", cfg, 128, (1024, 2048), 5, 8, "sample", 0.72)
+    if name == "c4":          # BASELINE configs[3] decode lane: bs32, 8k prompts
+        n_pages, max_pos = pool(32, 8192, 8)
+        cfg = LLAMA.with_(n_pages=n_pages, max_slots=32, max_batch=32, max_pos=max_pos)
+        return Workload("c4", cfg, 32, (8192, 8192), 8, 8, "greedy", 0.85)
+    if name == "toy":         # BASELINE configs[0]
+        n_pages, max_pos = pool(4, 128, 4)
+        cfg = TOY.with_(n_pages=n_pages, max_slots=4, max_batch=4, max_pos=max_pos)
+        return Workload("toy", cfg, 4, (128, 128), 1, 4, "sample", 0.7, embed_std=1.0, beta=0.0)
+    raise KeyError(name)
+
+
+def ctx_lengths(wl, seed):
+    g = _gen(seed)
+    lo, hi = wl.ctx
+    return [int(x) for x in torch.randint(lo, hi + 1, (wl.batch,), generator=g)]
+
+
+def planted_masks(n_steps, rows, alpha, vocab, seed):
+    """Per-step deviation masks (1 with probability 1 - alpha) and replacement tokens."""
+    g = _gen(seed)
+    m = (torch.rand(n_steps, rows, generator=g) >= alpha).to(torch.uint8)
+    t = torch.randint(0, vocab, (n_steps, rows), generator=g, dtype=torch.int32)
+    return m, t
+
+
 def as_f64(t):
     """bf16/fp32 torch tensor -> numpy fp64 (exact)."""
     return t.detach().to("cpu").to(torch.float64).numpy()
