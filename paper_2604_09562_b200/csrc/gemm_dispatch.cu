@@ -1,30 +1,83 @@
-// GEMM dispatch: the SIMT path (GEMM into fp32 scratch, then a separate epilogue
-// kernel). The tcgen05 path with fused epilogues plugs in here.
+// GEMM dispatch. Default: the tcgen05 kernel with fused epilogues (k_gemm_tc.cu).
+// SV_GEMM=simt selects the SIMT reference path (GEMM into fp32 scratch + separate
+// epilogue kernels), kept as an in-library cross-check.
+#include <cudaTypedefs.h>
+#include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
 
+#include <map>
+#include <tuple>
+
 #include "gemm.h"
+#include "gemm_tc.h"
 
 namespace sv {
 
 struct GemmPlan {
   LaneDev d;
+  bool use_tc = true;
+  int num_sms = 148;
+  PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  std::map<std::tuple<const void*, uint64_t, uint64_t>, CUtensorMap> maps;
 };
 
 size_t gemm_workspace_bytes() { return 4096; }
+
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+      q != cudaDriverEntryPointSuccess)
+    return nullptr;
+  return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+}
+
+// bf16 row-major [rows][cols] tensor, box 64 (cols, 128 B) x 128 rows, 128-byte swizzle
+static const CUtensorMap* get_map(GemmPlan* p, const void* base, uint64_t rows, uint64_t cols) {
+  auto key = std::make_tuple(base, rows, cols);
+  auto it = p->maps.find(key);
+  if (it != p->maps.end()) return &it->second;
+  CUtensorMap m;
+  memset(&m, 0, sizeof(m));
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 2};
+  cuuint32_t box[2] = {64, 128};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = p->encode(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    fprintf(stderr, "[sv] cuTensorMapEncodeTiled failed (%d)\n", (int)r);
+    return nullptr;
+  }
+  return &(p->maps[key] = m);
+}
 
 GemmPlan* gemm_plan_create(const LaneDev& d, void* ws, cudaStream_t s) {
   (void)ws;
   (void)s;
   GemmPlan* p = new GemmPlan();
   p->d = d;
+  const char* env = getenv("SV_GEMM");
+  p->use_tc = !(env && !strcmp(env, "simt"));
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, dev);
+  if (p->use_tc) {
+    p->encode = get_encode();
+    if (!p->encode) {
+      fprintf(stderr, "[sv] cuTensorMapEncodeTiled unavailable\n");
+      p->use_tc = false;
+    }
+  }
   return p;
 }
 
 void gemm_plan_destroy(GemmPlan* p) { delete p; }
 
-cudaError_t gemm_run(GemmPlan* p, const bf16* A, const bf16* B, float* C, int M, int N, int K, int epi,
-                     const GemmEpi& e, cudaStream_t s) {
+static cudaError_t gemm_simt(GemmPlan* p, const bf16* A, const bf16* B, float* C, int M, int N, int K, int epi,
+                             const GemmEpi& e, cudaStream_t s) {
   cudaError_t err = launch_gemm_simt(A, B, C, M, N, K, s);
   if (err != cudaSuccess) return err;
   switch (epi) {
@@ -34,6 +87,62 @@ cudaError_t gemm_run(GemmPlan* p, const bf16* A, const bf16* B, float* C, int M,
     case EPI_LOGITS: return launch_tile_stats(p->d, M, e.inv_temp, s);
     default: return cudaSuccess;
   }
+}
+
+cudaError_t gemm_run(GemmPlan* p, const bf16* A, const bf16* B, float* C, int M, int N, int K, int epi,
+                     const GemmEpi& e, cudaStream_t s) {
+  if (!p->use_tc || (K % 64)) return gemm_simt(p, A, B, C, M, N, K, epi, e, s);
+  const LaneDev& d = p->d;
+  const CUtensorMap* ma = get_map(p, A, (uint64_t)d.Tmax, (uint64_t)K);
+  const CUtensorMap* mb = get_map(p, B, (uint64_t)N, (uint64_t)K);
+  if (!ma || !mb) return cudaErrorInvalidValue;
+  GemmTcArgs g;
+  memset(&g, 0, sizeof(g));
+  g.M = M;
+  g.N = N;
+  g.K = K;
+  g.n_tiles = (N + 255) / 256;
+  g.out = C;
+  g.ldo = N;
+  switch (epi) {
+    case EPI_QKV_ROPE: {
+      g.kind = GEMM_EPI_QKV_ROPE;
+      const size_t nkv = (size_t)d.Hkv * d.dh;
+      g.q = d.q;
+      g.kc = d.kc + (size_t)e.layer * d.Tmax * nkv;
+      g.vc = d.vc + (size_t)e.layer * d.Tmax * nkv;
+      g.row_pos = d.row_pos;
+      g.rope_cos = d.rope_cos;
+      g.rope_sin = d.rope_sin;
+      g.Hq = d.Hq;
+      g.Hkv = d.Hkv;
+      g.dh = d.dh;
+      break;
+    }
+    case EPI_RESIDUAL:
+      g.kind = GEMM_EPI_RESIDUAL;
+      g.resid_in = e.resid_in;
+      g.resid_out = e.resid_out;
+      break;
+    case EPI_SWIGLU:
+      if ((N / 2) % 128) return gemm_simt(p, A, B, C, M, N, K, epi, e, s);
+      g.kind = GEMM_EPI_SWIGLU;
+      g.u = d.u;
+      g.F = N / 2;
+      g.n_tiles = (N / 2) / 128;
+      break;
+    case EPI_LOGITS:
+      g.kind = GEMM_EPI_LOGITS;
+      g.tmax = d.tile_max;
+      g.tsum = d.tile_sum;
+      g.targ = d.tile_arg;
+      g.nt = d.nt;
+      g.inv_temp = e.inv_temp;
+      break;
+    default:
+      g.kind = GEMM_EPI_NONE;
+  }
+  return launch_gemm_tc(*ma, *mb, g, p->num_sms, s);
 }
 
 }  // namespace sv

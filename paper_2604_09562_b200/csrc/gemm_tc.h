@@ -1,0 +1,39 @@
+// Arguments of the tcgen05 GEMM kernel (k_gemm_tc.cu) and its fused epilogues.
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+namespace sv {
+
+enum GemmTcEpi { GEMM_EPI_NONE = 0, GEMM_EPI_QKV_ROPE = 1, GEMM_EPI_RESIDUAL = 2, GEMM_EPI_SWIGLU = 3,
+                 GEMM_EPI_LOGITS = 4 };
+
+struct GemmTcArgs {
+  int kind;
+  int M, N, K;            // logical problem (N = 2F for SWIGLU)
+  int n_tiles;            // output tiles along N
+  float* out;             // NONE / LOGITS: fp32 [M][ldo]
+  int ldo;
+  const float* resid_in;  // RESIDUAL: out = resid_in + acc, fp32 [M][ldo]
+  float* resid_out;
+  // QKV_ROPE
+  __nv_bfloat16 *q, *kc, *vc;
+  const int* row_pos;
+  const float *rope_cos, *rope_sin;
+  int Hq, Hkv, dh;
+  // SWIGLU
+  __nv_bfloat16* u;
+  int F;
+  // LOGITS statistics [M][nt]
+  float *tmax, *tsum;
+  int* targ;
+  int nt;
+  float inv_temp;
+};
+
+int gemm_tc_smem_bytes();
+cudaError_t launch_gemm_tc(const CUtensorMap& map_a, const CUtensorMap& map_b, const GemmTcArgs& g, int num_sms,
+                           cudaStream_t s);
+
+}  // namespace sv
