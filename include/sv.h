@@ -116,7 +116,8 @@ sv_status sv_query_sizes(const sv_config* cfg, size_t* kv_pool_bytes, size_t* wo
 
 /* Create a lane on the current CUDA device. Builds the fp32 RoPE table
  * (fp64 angles, SURVEY.md §8(c) "Model details"), the device free list and the
- * TMA descriptors, on `stream`; the kv_pool contents are not read.
+ * TMA descriptors, on `stream`; the kv_pool is zero-filled (attention reads whole
+ * pages; zero rows beyond a slot's length keep masked keys finite).
  * Syncs `stream` once before returning. */
 sv_status sv_create(const sv_config* cfg, const sv_weights* w, void* kv_pool, void* workspace,
                     sv_stream_t stream, sv_ctx** out);

@@ -18,6 +18,8 @@ struct GemmPlan;
 size_t gemm_workspace_bytes();
 GemmPlan* gemm_plan_create(const LaneDev& d, void* ws, cudaStream_t s);
 void gemm_plan_destroy(GemmPlan* p);
+// a3 verify attention: tcgen05 kernel when the shape allows (page 64, d_h 64/128), else SIMT
+cudaError_t attn_run(GemmPlan* p, int layer, int batch, cudaStream_t s);
 cudaError_t gemm_run(GemmPlan* p, const bf16* A, const bf16* B, float* C, int M, int N, int K, int epi,
                      const GemmEpi& e, cudaStream_t s);
 

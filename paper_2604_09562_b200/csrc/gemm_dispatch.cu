@@ -9,6 +9,7 @@
 #include <map>
 #include <tuple>
 
+#include "attn_tc.h"
 #include "gemm.h"
 #include "gemm_tc.h"
 
@@ -20,9 +21,14 @@ struct GemmPlan {
   int num_sms = 148;
   PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
   std::map<std::tuple<const void*, uint64_t, uint64_t>, CUtensorMap> maps;
+  bool use_tc_attn = true;
+  bool attn_maps_ok = false;
+  CUtensorMap map_q, map_kv;
 };
 
 size_t gemm_workspace_bytes() { return 4096; }
+
+static bool encode_attn_maps(GemmPlan* p);
 
 static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   void* fn = nullptr;
@@ -64,17 +70,51 @@ GemmPlan* gemm_plan_create(const LaneDev& d, void* ws, cudaStream_t s) {
   int dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, dev);
-  if (p->use_tc) {
-    p->encode = get_encode();
-    if (!p->encode) {
-      fprintf(stderr, "[sv] cuTensorMapEncodeTiled unavailable\n");
-      p->use_tc = false;
-    }
+  p->encode = get_encode();
+  if (!p->encode) {
+    fprintf(stderr, "[sv] cuTensorMapEncodeTiled unavailable\n");
+    p->use_tc = false;
   }
+  const char* aenv = getenv("SV_ATTN");
+  const int G = d.Hq / d.Hkv;
+  p->use_tc_attn = p->encode && !(aenv && !strcmp(aenv, "simt")) && d.page == 64 && (d.dh == 64 || d.dh == 128) &&
+                   (64 % G) == 0;
+  if (p->use_tc_attn) p->attn_maps_ok = encode_attn_maps(p);
   return p;
 }
 
 void gemm_plan_destroy(GemmPlan* p) { delete p; }
+
+static bool encode_attn_maps(GemmPlan* p) {
+  const LaneDev& d = p->d;
+  const int G = d.Hq / d.Hkv;
+  // Q: 3-D (d_h, Hq, Tmax) bf16, box (64, G, 64 / G) -> 64 query rows (token-major, head-minor)
+  cuuint64_t qdims[3] = {(cuuint64_t)d.dh, (cuuint64_t)d.Hq, (cuuint64_t)d.Tmax};
+  cuuint64_t qstr[2] = {(cuuint64_t)d.dh * 2, (cuuint64_t)d.Hq * d.dh * 2};
+  cuuint32_t qbox[3] = {64, (cuuint32_t)G, (cuuint32_t)(64 / G)};
+  cuuint32_t es3[3] = {1, 1, 1};
+  if (p->encode(&p->map_q, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, d.q, qdims, qstr, qbox, es3,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return false;
+  // KV pool: 2-D (d_h, n_layers * n_pages * 2 * Hkv * page) bf16, box (64, 64) = one page of one head
+  cuuint64_t kdims[2] = {(cuuint64_t)d.dh, (cuuint64_t)d.n_layers * d.n_pages * 2 * d.Hkv * d.page};
+  cuuint64_t kstr[1] = {(cuuint64_t)d.dh * 2};
+  cuuint32_t kbox[2] = {64, 64};
+  cuuint32_t es2[2] = {1, 1};
+  if (p->encode(&p->map_kv, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, d.pool, kdims, kstr, kbox, es2,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return false;
+  return true;
+}
+
+cudaError_t attn_run(GemmPlan* p, int layer, int batch, cudaStream_t s) {
+  const LaneDev& d = p->d;
+  if (p->use_tc_attn && p->attn_maps_ok)
+    return launch_attention_tc(p->map_q, p->map_kv, d, layer, p->num_sms, s);
+  return launch_attention(d, layer, batch, s);
+}
 
 static cudaError_t gemm_simt(GemmPlan* p, const bf16* A, const bf16* B, float* C, int M, int N, int K, int epi,
                              const GemmEpi& e, cudaStream_t s) {

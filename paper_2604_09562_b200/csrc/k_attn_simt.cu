@@ -33,8 +33,8 @@ __global__ void __launch_bounds__(128) attn_simt_kernel(LaneDev d, int layer) {
     const int slot = d.slots[b], R = d.depths[b] + 1, L = d.len[slot];
     const int row0 = d.row_off[b];
     const int nr = R * G;
-    const int t0 = split * kSplitKeys;
-    const int t1 = min(t0 + kSplitKeys, L + R);
+    const int t0 = split_t0(split);
+    const int t1 = split_t1(split, item.w, L, R);
     __syncthreads();
     for (int i = tid; i < nr * dh; i += 128) {
       const int rl = i / dh, dd = i % dh, j = rl / G, g = rl % G;
@@ -140,7 +140,8 @@ __global__ void attn_combine_kernel(LaneDev d) {
   const int b = d.row_req[r], j = r - d.row_off[b];
   const int G = d.Hq / d.Hkv, dh = d.dh;
   const int slot = d.slots[b], R = d.depths[b] + 1, L = d.len[slot];
-  const int ns = (L + R + kSplitKeys - 1) / kSplitKeys;
+  (void)R;
+  const int ns = num_splits(L);
   for (int i = threadIdx.x; i < d.Hq * dh; i += blockDim.x) {
     const int hq = i / dh, dd = i % dh, h = hq / G, g = hq % G, rl = j * G + g;
     const int base = d.item_start[b] + h * ns;

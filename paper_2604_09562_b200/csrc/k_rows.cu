@@ -27,10 +27,7 @@ __global__ void plan_kernel(LaneDev d, PlanArgs p, const int* __restrict__ draft
       s_item[b] = it;
       const int R = p.depths[b] + 1;
       o += R;
-      if (attn) {
-        const int keys = d.len[p.slots[b]] + R;
-        it += ((keys + kSplitKeys - 1) / kSplitKeys) * d.Hkv;
-      }
+      if (attn) it += num_splits(d.len[p.slots[b]]) * d.Hkv;
     }
     s_off[B] = o;
     s_item[B] = it;
@@ -72,8 +69,7 @@ __global__ void plan_kernel(LaneDev d, PlanArgs p, const int* __restrict__ draft
         if (s_item[mid] <= it) lo = mid; else hi = mid - 1;
       }
       const int b = lo, rel = it - s_item[b];
-      const int keys = d.len[p.slots[b]] + p.depths[b] + 1;
-      const int ns = (keys + kSplitKeys - 1) / kSplitKeys;
+      const int ns = num_splits(d.len[p.slots[b]]);
       d.items[it] = make_int4(b, rel / ns, rel % ns, ns);
     }
   }

@@ -50,6 +50,15 @@ struct LaneDev {
   int* batch_n;                      // [1] batch of the pending verify (device copy)
 };
 
+// Split-KV work items: request b (cache length L, R = k + 1 chain rows) is split over its
+// page keys [0, L) into ceil(L / kSplitKeys) items (at least one); the chain keys L..L+R-1
+// always belong to the last item. Item s covers keys [split_t0, split_t1).
+__host__ __device__ inline int num_splits(int L) { return L <= 0 ? 1 : (L + kSplitKeys - 1) / kSplitKeys; }
+__host__ __device__ inline int split_t0(int s) { return s * kSplitKeys; }
+__host__ __device__ inline int split_t1(int s, int ns, int L, int R) {
+  return s == ns - 1 ? L + R : (s + 1) * kSplitKeys;
+}
+
 // kernels launched by the library so far (measurement hook, sv_launch_count)
 extern unsigned long long g_launch_count;
 #define SV_COUNT_LAUNCH() (++::sv::g_launch_count)

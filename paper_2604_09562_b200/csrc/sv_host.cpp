@@ -100,7 +100,7 @@ Layout make_layout(const sv_config& c) {
   L.o = L.take(2 * T * nq);
   L.u = L.take(2 * T * (F ? F : 1));
   // attention work items: sum over requests of Hkv * ceil((L_i + R_i) / split)
-  const size_t max_keys = (size_t)c.n_pages * c.page_size + T;
+  const size_t max_keys = (size_t)c.n_pages * c.page_size;
   L.max_items = (size_t)c.n_kv_heads * (ceil_div(max_keys, sv::kSplitKeys) + c.max_batch);
   L.items = L.take(16 * L.max_items);
   L.item_start = L.take(4 * (c.max_batch + 1));
@@ -340,6 +340,8 @@ sv_status sv_create(const sv_config* cfg, const sv_weights* w, void* kv_pool, vo
   sv_status st = SV_OK;
   if ((st = cuda_ok(cudaMemcpyAsync(ws + L.rope_cos, cs.data(), cs.size() * 4, cudaMemcpyHostToDevice, c->stream))) ||
       (st = cuda_ok(cudaMemcpyAsync(ws + L.rope_sin, sn.data(), sn.size() * 4, cudaMemcpyHostToDevice, c->stream))) ||
+      (st = cuda_ok(cudaMemsetAsync(kv_pool, 0, (size_t)cfg->n_layers * cfg->n_pages * 2 * cfg->n_kv_heads *
+                                                    cfg->page_size * cfg->head_dim * 2, c->stream))) ||
       (st = cuda_ok(cudaMemsetAsync(ws + L.page_table, 0xff, 4 * (size_t)cfg->max_slots * d.max_pages_per_slot,
                                     c->stream))) ||
       (st = cuda_ok(sv::launch_init_state(d, c->stream)))) {
@@ -428,7 +430,7 @@ sv_status sv_verify(sv_ctx* c, int32_t batch, const int32_t* slots, const int32_
     e.layer = layer;
     STAGE(c, ST_QKV, gemm(c, d.a, d.wqkv + (size_t)layer * d.qkv_rows * d.D, d.cbuf, T, d.qkv_rows, d.D,
                           sv::EPI_QKV_ROPE, e));
-    STAGE(c, ST_ATTN, sv::launch_attention(d, layer, batch, s));
+    STAGE(c, ST_ATTN, sv::attn_run(c->gemm, layer, batch, s));
     STAGE(c, ST_COMBINE, sv::launch_attn_combine(d, T, s));
     float* hattn = d.F > 0 ? d.h1 : d.h2;
     e.resid_in = hin;

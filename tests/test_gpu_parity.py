@@ -80,21 +80,23 @@ def run_and_check(S, slots, depths, drafts, mode, seed=1234, temperature=1.0, pr
     # a3: attention, fed the GPU's q and chain k/v
     go = S.tap("o", torch.bfloat16, (T, Hq * dh))
     if check_attention:
-        worst = 0.0
+        worst, worst_sig = 0.0, 0.0
         r0 = 0
         for s, kk in zip(slots, depths):
             c = S.ctx[s]
             R = kk + 1
-            ref = model.verify_attention(f64(gq[r0:r0 + R]), f64(c["k"][0]), f64(c["v"][0]),
-                                         f64(gk[r0:r0 + R]), f64(gv[r0:r0 + R]))
+            q_, ck, cv = f64(gq[r0:r0 + R]), f64(c["k"][0]), f64(c["v"][0])
+            kc_, vc_ = f64(gk[r0:r0 + R]), f64(gv[r0:r0 + R])
+            ref = model.verify_attention(q_, ck, cv, kc_, vc_).reshape(R, Hq, dh)
             g = f64(go[r0:r0 + R]).reshape(R, Hq, dh)
-            ref = ref.reshape(R, Hq, dh)
+            err = np.abs(g - ref)
             rms = np.sqrt((ref ** 2).mean(axis=2))
-            err = np.abs(g - ref).max(axis=2) / np.maximum(rms, 1e-30)
-            worst = max(worst, float(err.max()))
+            worst = max(worst, float((err.max(axis=2) / np.maximum(rms, 1e-30)).max()))
+            tol = attention_tolerance(q_, ck, cv, kc_, vc_)
+            worst_sig = max(worst_sig, float((err / tol).max()))
             r0 += R
-        report["o"] = dict(max_rel=worst)
-        assert worst <= ATTN_REL, worst
+        report["o"] = dict(max_rel=worst, max_err_over_tol=worst_sig)
+        assert worst_sig <= 1.0, (worst_sig, worst)
     # a4: O-proj + residual, MLP
     h1 = S.tap("h1", torch.float32, (T, D))
     ref_h1 = model.attn_out(f64(h0), f64(go), W["wo"][0])
@@ -136,6 +138,32 @@ def run_and_check(S, slots, depths, drafts, mode, seed=1234, temperature=1.0, pr
         assert all(t == -1 for t in tok[b][acc[b] + 1:])
     report["borderline"] = borderline
     return report, acc, tok
+
+
+def attention_tolerance(q, ck, cv, kc, vc):
+    """Per-element tolerance of the GPU attention output (a3).
+
+    The GPU rounds the softmax weights P to bf16 (8 significant bits) before the P.V
+    tensor-core product: relative error |dw_i / w_i| <= 2^-8, ~uniform. With w the exact
+    weights and O the exact output, that perturbs O_d by sum_i dw_i (v_id - O_d) / sum w, a
+    zero-mean sum with std sigma_d <= 2^-8/sqrt(3) * sqrt(sum_i w_i^2 (v_id - O_d)^2). Both
+    sides then round O to bf16 (<= 2^-8 |O_d| each). Tolerance = 6 sigma_d + 2^-7 |O_d|
+    (+ fp32 slack)."""
+    R, Hq, dh = q.shape
+    Hkv = kc.shape[1]
+    G = Hq // Hkv
+    L = ck.shape[0]
+    tol = np.zeros((R, Hq, dh))
+    for j in range(R):
+        keys = np.concatenate([ck[:L], kc[: j + 1]])
+        vals = np.concatenate([cv[:L], vc[: j + 1]])
+        for hq in range(Hq):
+            w = model.softmax(keys[:, hq // G, :] @ q[j, hq] / np.sqrt(dh))
+            v = vals[:, hq // G, :]
+            o = w @ v
+            sig = 2.0 ** -8 / np.sqrt(3.0) * np.sqrt((w[:, None] ** 2 * (v - o[None]) ** 2).sum(axis=0))
+            tol[j, hq] = 6 * sig + 2.0 ** -7 * np.abs(o) + 1e-6 * np.abs(v).max()
+    return tol
 
 
 def _cmp_resid(name, g, ref, report):
