@@ -7,8 +7,9 @@
 
 namespace sv {
 int attn_tc_smem_bytes(int dh);
-// map_q: 3-D (d_h, Hq, Tmax) over the Q buffer, box (64, G, 64 / G); map_kv: 2-D (d_h, pool rows),
-// box (64, 64); both bf16 with 128-byte swizzle.
+// map_q: 3-D (d_h, Hq, Tmax) over the Q buffer, box (64, 1, q_box_tokens) = one q head's chain rows;
+// map_kv: 2-D (d_h, pool rows), box (64, 64) = one page of one kv head; both bf16, 128-byte swizzle.
+// Requires page_size 64, d_h in {64, 128}, G = Hq / Hkv <= 4 and max_depth + 1 <= q_box_tokens <= 32.
 cudaError_t launch_attention_tc(const CUtensorMap& map_q, const CUtensorMap& map_kv, const LaneDev& d, int layer,
-                                int num_sms, cudaStream_t s);
+                                int num_sms, int q_box_tokens, cudaStream_t s);
 }  // namespace sv

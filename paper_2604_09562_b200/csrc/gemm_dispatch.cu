@@ -24,6 +24,7 @@ struct GemmPlan {
   bool use_tc_attn = true;
   bool attn_maps_ok = false;
   CUtensorMap map_q, map_kv;
+  int q_box_tokens = 16;
 };
 
 size_t gemm_workspace_bytes() { return 4096; }
@@ -78,7 +79,7 @@ GemmPlan* gemm_plan_create(const LaneDev& d, void* ws, cudaStream_t s) {
   const char* aenv = getenv("SV_ATTN");
   const int G = d.Hq / d.Hkv;
   p->use_tc_attn = p->encode && !(aenv && !strcmp(aenv, "simt")) && d.page == 64 && (d.dh == 64 || d.dh == 128) &&
-                   (64 % G) == 0;
+                   G <= 4 && d.max_depth + 1 <= 32;
   if (p->use_tc_attn) p->attn_maps_ok = encode_attn_maps(p);
   return p;
 }
@@ -88,10 +89,12 @@ void gemm_plan_destroy(GemmPlan* p) { delete p; }
 static bool encode_attn_maps(GemmPlan* p) {
   const LaneDev& d = p->d;
   const int G = d.Hq / d.Hkv;
-  // Q: 3-D (d_h, Hq, Tmax) bf16, box (64, G, 64 / G) -> 64 query rows (token-major, head-minor)
+  // Q: 3-D (d_h, Hq, Tmax) bf16, box (64, 1, q_box_tokens) = the chain rows of one q head
+  (void)G;
+  p->q_box_tokens = d.max_depth + 1 <= 8 ? 8 : (d.max_depth + 1 <= 16 ? 16 : 32);
   cuuint64_t qdims[3] = {(cuuint64_t)d.dh, (cuuint64_t)d.Hq, (cuuint64_t)d.Tmax};
   cuuint64_t qstr[2] = {(cuuint64_t)d.dh * 2, (cuuint64_t)d.Hq * d.dh * 2};
-  cuuint32_t qbox[3] = {64, (cuuint32_t)G, (cuuint32_t)(64 / G)};
+  cuuint32_t qbox[3] = {64, 1, (cuuint32_t)p->q_box_tokens};
   cuuint32_t es3[3] = {1, 1, 1};
   if (p->encode(&p->map_q, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, d.q, qdims, qstr, qbox, es3,
                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
@@ -112,7 +115,7 @@ static bool encode_attn_maps(GemmPlan* p) {
 cudaError_t attn_run(GemmPlan* p, int layer, int batch, cudaStream_t s) {
   const LaneDev& d = p->d;
   if (p->use_tc_attn && p->attn_maps_ok)
-    return launch_attention_tc(p->map_q, p->map_kv, d, layer, p->num_sms, s);
+    return launch_attention_tc(p->map_q, p->map_kv, d, layer, p->num_sms, p->q_box_tokens, s);
   return launch_attention(d, layer, batch, s);
 }
 
