@@ -12,4 +12,9 @@ int attn_tc_smem_bytes(int dh);
 // Requires page_size 64, d_h in {64, 128}, G = Hq / Hkv <= 4 and max_depth + 1 <= q_box_tokens <= 32.
 cudaError_t launch_attention_tc(const CUtensorMap& map_q, const CUtensorMap& map_kv, const LaneDev& d, int layer,
                                 int num_sms, int q_box_tokens, cudaStream_t s);
+// keys-on-lanes variant (k_attn_tc2.cu), d_h = 128 only. map_q: 3-D (d_h, Hq, Tmax), box (64, G, 64 / G)
+// = the 64 query slots j*G + g of one kv head; map_kv as above. Requires (max_depth + 1) * G <= 64.
+int attn_tc2_smem_bytes();
+cudaError_t launch_attention_tc2(const CUtensorMap& map_q, const CUtensorMap& map_kv, const LaneDev& d, int layer,
+                                 int num_sms, cudaStream_t s);
 }  // namespace sv

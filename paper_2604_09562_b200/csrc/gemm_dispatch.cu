@@ -22,8 +22,9 @@ struct GemmPlan {
   PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
   std::map<std::tuple<const void*, uint64_t, uint64_t>, CUtensorMap> maps;
   bool use_tc_attn = true;
+  bool use_tc2_attn = false;       // keys-on-lanes kernel (d_h = 128)
   bool attn_maps_ok = false;
-  CUtensorMap map_q, map_kv;
+  CUtensorMap map_q, map_q2, map_kv;
   int q_box_tokens = 16;
 };
 
@@ -80,6 +81,8 @@ GemmPlan* gemm_plan_create(const LaneDev& d, void* ws, cudaStream_t s) {
   const int G = d.Hq / d.Hkv;
   p->use_tc_attn = p->encode && !(aenv && !strcmp(aenv, "simt")) && d.page == 64 && (d.dh == 64 || d.dh == 128) &&
                    G <= 4 && d.max_depth + 1 <= 32;
+  p->use_tc2_attn = p->use_tc_attn && d.dh == 128 && (d.max_depth + 1) * G <= 64 && (64 % G) == 0 &&
+                    !(aenv && !strcmp(aenv, "tc1"));
   if (p->use_tc_attn) p->attn_maps_ok = encode_attn_maps(p);
   return p;
 }
@@ -90,7 +93,6 @@ static bool encode_attn_maps(GemmPlan* p) {
   const LaneDev& d = p->d;
   const int G = d.Hq / d.Hkv;
   // Q: 3-D (d_h, Hq, Tmax) bf16, box (64, 1, q_box_tokens) = the chain rows of one q head
-  (void)G;
   p->q_box_tokens = d.max_depth + 1 <= 8 ? 8 : (d.max_depth + 1 <= 16 ? 16 : 32);
   cuuint64_t qdims[3] = {(cuuint64_t)d.dh, (cuuint64_t)d.Hq, (cuuint64_t)d.Tmax};
   cuuint64_t qstr[2] = {(cuuint64_t)d.dh * 2, (cuuint64_t)d.Hq * d.dh * 2};
@@ -100,6 +102,14 @@ static bool encode_attn_maps(GemmPlan* p) {
                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return false;
+  // Q for the keys-on-lanes kernel: box (64, G, 64 / G) = slots j*G + g of one kv head
+  if (p->use_tc2_attn) {
+    cuuint32_t qbox2[3] = {64, (cuuint32_t)G, (cuuint32_t)(64 / G)};
+    if (p->encode(&p->map_q2, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, d.q, qdims, qstr, qbox2, es3,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return false;
+  }
   // KV pool: 2-D (d_h, n_layers * n_pages * 2 * Hkv * page) bf16, box (64, 64) = one page of one head
   cuuint64_t kdims[2] = {(cuuint64_t)d.dh, (cuuint64_t)d.n_layers * d.n_pages * 2 * d.Hkv * d.page};
   cuuint64_t kstr[1] = {(cuuint64_t)d.dh * 2};
@@ -114,6 +124,8 @@ static bool encode_attn_maps(GemmPlan* p) {
 
 cudaError_t attn_run(GemmPlan* p, int layer, int batch, cudaStream_t s) {
   const LaneDev& d = p->d;
+  if (p->use_tc2_attn && p->attn_maps_ok)
+    return launch_attention_tc2(p->map_q2, p->map_kv, d, layer, p->num_sms, s);
   if (p->use_tc_attn && p->attn_maps_ok)
     return launch_attention_tc(p->map_q, p->map_kv, d, layer, p->num_sms, p->q_box_tokens, s);
   return launch_attention(d, layer, batch, s);

@@ -134,35 +134,49 @@ cudaError_t launch_attention(const LaneDev& d, int layer, int batch, cudaStream_
   return cudaGetLastError();
 }
 
-// combine split-KV partials: one CTA per chain row, threads over (q head, dim)
-__global__ void attn_combine_kernel(LaneDev d) {
-  const int r = blockIdx.x;
+// combine split-KV partials: one warp per (chain row, q head); lanes over d_h (float4 each
+// for d_h = 128, float2 for 64). O = sum_s e^(m_s - M) O_s / sum_s e^(m_s - M) l_s, M = max m_s.
+template <int DH>
+__global__ void __launch_bounds__(256) attn_combine_kernel(LaneDev d, int T) {
+  constexpr int V = DH / 32;                       // floats per lane
+  const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (wid >= T * d.Hq) return;
+  const int r = wid / d.Hq, hq = wid % d.Hq;
   const int b = d.row_req[r], j = r - d.row_off[b];
-  const int G = d.Hq / d.Hkv, dh = d.dh;
-  const int slot = d.slots[b], R = d.depths[b] + 1, L = d.len[slot];
-  (void)R;
-  const int ns = num_splits(L);
-  for (int i = threadIdx.x; i < d.Hq * dh; i += blockDim.x) {
-    const int hq = i / dh, dd = i % dh, h = hq / G, g = hq % G, rl = j * G + g;
-    const int base = d.item_start[b] + h * ns;
-    float M = -INFINITY;
-    for (int s = 0; s < ns; ++s) M = fmaxf(M, d.part_ml[((size_t)(base + s) * kAttnRows + rl) * 2]);
-    float l = 0.f, o = 0.f;
-    for (int s = 0; s < ns; ++s) {
-      const size_t it = base + s;
-      const float ms = d.part_ml[(it * kAttnRows + rl) * 2];
-      if (ms == -INFINITY) continue;
-      const float w = expf(ms - M);
-      l += d.part_ml[(it * kAttnRows + rl) * 2 + 1] * w;
-      o += d.part_o[(it * kAttnRows + rl) * dh + dd] * w;
+  const int G = d.Hq / d.Hkv, h = hq / G, g = hq % G, rl = j * G + g;
+  const int ns = num_splits(d.len[d.slots[b]]);
+  const int base = d.item_start[b] + h * ns;
+  float M = -INFINITY;
+  for (int s = 0; s < ns; ++s) M = fmaxf(M, d.part_ml[((size_t)(base + s) * kAttnRows + rl) * 2]);
+  float l = 0.f, o[V];
+#pragma unroll
+  for (int i = 0; i < V; ++i) o[i] = 0.f;
+  for (int s = 0; s < ns; ++s) {
+    const size_t it = base + s;
+    const float2 ml = *reinterpret_cast<const float2*>(d.part_ml + (it * kAttnRows + rl) * 2);
+    if (ml.x == -INFINITY) continue;
+    const float w = expf(ml.x - M);
+    l += ml.y * w;
+    const float* src = d.part_o + (it * kAttnRows + rl) * DH + lane * V;
+    if constexpr (V == 4) {
+      const float4 v = *reinterpret_cast<const float4*>(src);
+      o[0] += v.x * w; o[1] += v.y * w; o[2] += v.z * w; o[3] += v.w * w;
+    } else {
+      const float2 v = *reinterpret_cast<const float2*>(src);
+      o[0] += v.x * w; o[1] += v.y * w;
     }
-    d.o[(size_t)r * d.Hq * dh + i] = f2bf(o / l);
   }
+  const float inv = 1.0f / l;
+  bf16* dst = d.o + (size_t)r * d.Hq * DH + (size_t)hq * DH + lane * V;
+#pragma unroll
+  for (int i = 0; i < V; i += 2) *reinterpret_cast<__nv_bfloat162*>(dst + i) = __floats2bfloat162_rn(o[i] * inv, o[i + 1] * inv);
 }
 
 cudaError_t launch_attn_combine(const LaneDev& d, int T, cudaStream_t s) {
+  const int warps = T * d.Hq;
   SV_COUNT_LAUNCH();
-  attn_combine_kernel<<<T, 256, 0, s>>>(d);
+  if (d.dh == 128) attn_combine_kernel<128><<<(warps + 7) / 8, 256, 0, s>>>(d, T);
+  else attn_combine_kernel<64><<<(warps + 7) / 8, 256, 0, s>>>(d, T);
   return cudaGetLastError();
 }
 

@@ -33,6 +33,12 @@
 
 namespace sv {
 
+// debug timeline of CTA 0 (LaneDev::trace, enabled by SV_TRACE=1): event e, tile / item i
+#define SV_TR(e, i)                                                          \
+  do {                                                                       \
+    if (d.trace && blockIdx.x == 0 && (i) < 256) d.trace[(e)*256 + (i)] = clock64(); \
+  } while (0)
+
 namespace {
 constexpr int KT = 64;                     // keys per tile (= page size)
 constexpr int ST = 4;                      // K/V ring stages
@@ -144,6 +150,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     int stage = 0;
     uint32_t phase = 0;
     int iter = 0;
+    uint32_t ptile = 0;
     for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++iter) {
       const ItemInfo I = item_info(d, it);
       const int qb = iter & 1;
@@ -157,6 +164,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
       for (int t = 0; t < I.n_tiles; ++t) {
         if (lane == 0) tc::mbar_wait(&kv_empty[stage], phase ^ 1);
+        if (lane == 0) SV_TR(0, ptile);
         __syncwarp();
         uint8_t* sk = sKV + stage * C::STAGE_BYTES;
         uint8_t* sv_ = sk + C::KV_BYTES;
@@ -170,6 +178,7 @@ __global__ void __launch_bounds__(THREADS, 1)
               tc::tma_load_2d_hint(sk + hf * (KT * 128), &map_kv, &kv_full[stage], hf * 64, rk, pol);
               tc::tma_load_2d_hint(sv_ + hf * (KT * 128), &map_kv, &kv_full[stage], hf * 64, rv, pol);
             }
+            SV_TR(1, ptile);
           }
         } else {
           // chain tile: keys L + c, c < R, from the chain scratch; zero rows beyond R
@@ -192,8 +201,10 @@ __global__ void __launch_bounds__(THREADS, 1)
           tc::fence_proxy_async();
           __syncwarp();
           if (lane == 0) tc::mbar_arrive(&kv_full[stage]);
+          if (lane == 0) SV_TR(1, ptile);
         }
         if (++stage == ST) { stage = 0; phase ^= 1; }
+        ++ptile;
       }
     }
   } else if (warp == 1) {
@@ -218,7 +229,9 @@ __global__ void __launch_bounds__(THREADS, 1)
             // ---- S(t) = Q K^T into S[g & 1]
             const int sb = g & 1;
             tc::mbar_wait(&kv_full[stage], phase);
+            SV_TR(2, g);
             tc::mbar_wait(&s_free[sb], ((g >> 1) & 1) ^ 1);
+            SV_TR(3, g);
             tc::fence_after();
             const uint32_t sk = tc::smem_u32(sKV + stage * C::STAGE_BYTES);
 #pragma unroll
@@ -234,6 +247,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             // ---- O += P(t-1) V(t-1)
             const int pb = prev_g & 1;
             tc::mbar_wait(&p_full[pb], (prev_g >> 1) & 1);
+            SV_TR(4, prev_g);
             tc::fence_after();
             const uint32_t sv_ = tc::smem_u32(sKV + prev_stage * C::STAGE_BYTES + C::KV_BYTES);
 #pragma unroll
@@ -276,6 +290,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       for (int t = 0; t < I.n_tiles; ++t, ++g) {
         const int sb = g & 1;
         tc::mbar_wait(&s_full[sb], (g >> 1) & 1);
+        if (warp == 4 && lane == 0) SV_TR(5, g);
         tc::fence_after();
         if (quad_active) {
           uint32_t sv[32];
@@ -347,6 +362,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           tc::tmem_st_wait();
         }
         tc::fence_before();
+        if (warp == 4 && lane == 0) SV_TR(6, g);
         tc::mbar_arrive(&p_full[sb]);
       }
       // ---- item epilogue: unnormalised O, m (natural-log units), l -> split-KV partials
@@ -379,6 +395,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
       tc::fence_before();
       tc::mbar_arrive(&o_empty[ob]);
+      if (warp == 4 && lane == 0) SV_TR(7, iter);
     }
   }
   tc::fence_before();

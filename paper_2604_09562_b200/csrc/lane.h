@@ -48,6 +48,7 @@ struct LaneDev {
   float *part_o, *part_ml;           // split-KV partials
   int *acc_int, *tok_int;            // internal copies of accepted_len / out_tokens for commit
   int* batch_n;                      // [1] batch of the pending verify (device copy)
+  unsigned long long* trace;         // [16][256] clock64 trace of CTA 0 (SV_TRACE=1) or nullptr
 };
 
 // Split-KV work items: request b (cache length L, R = k + 1 chain rows) is split over its

@@ -26,7 +26,7 @@ struct Layout {
   size_t h0, h1, h2, cbuf, logits, tile_max, tile_sum, tile_arg;
   size_t a, b, z, q, kc, vc, o, u;
   size_t items, item_start, n_items, part_o, part_ml, acc_int, tok_int, batch_n;
-  size_t gemm_ws;
+  size_t gemm_ws, trace;
   size_t max_items;
 
   size_t take(size_t bytes) {
@@ -111,6 +111,7 @@ Layout make_layout(const sv_config& c) {
   L.tok_int = L.take(4 * c.max_batch * (c.max_depth + 1));
   L.batch_n = L.take(4);
   L.gemm_ws = L.take(sv::gemm_workspace_bytes());
+  L.trace = L.take(8 * 16 * 256);
   L.total = (L.total + 1023) & ~size_t(1023);
   return L;
 }
@@ -325,6 +326,7 @@ sv_status sv_create(const sv_config* cfg, const sv_weights* w, void* kv_pool, vo
   d.acc_int = (int*)(ws + L.acc_int);
   d.tok_int = (int*)(ws + L.tok_int);
   d.batch_n = (int*)(ws + L.batch_n);
+  d.trace = getenv("SV_TRACE") ? (unsigned long long*)(ws + L.trace) : nullptr;
 
   // RoPE table: fp64 angles pos * theta^(-2m/d_h), stored fp32 (SURVEY.md §8(c) "Model details")
   const int half = cfg->head_dim / 2;
@@ -569,6 +571,7 @@ sv_status sv_get_tap(sv_ctx* c, const char* name, void** dev_ptr, size_t* bytes)
       {"page_table", d.page_table, 4 * (size_t)d.max_slots * d.max_pages_per_slot},
       {"free_top", d.free_top, 4},
       {"free_list", d.free_list, 4 * (size_t)d.n_pages},
+      {"trace", d.trace ? (const void*)d.trace : (const void*)(c->ws + c->lay.trace), 8 * 16 * 256},
   };
   for (const Tap& t : taps)
     if (!strcmp(t.n, name)) {
