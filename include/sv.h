@@ -200,6 +200,12 @@ sv_status sv_get_tap(sv_ctx* ctx, const char* name, void** dev_ptr, size_t* byte
 sv_status sv_debug_uniforms(sv_ctx* ctx, uint64_t seed, uint64_t rid, uint32_t z, int32_t purpose,
                             int32_t x0, int32_t n, float* u);
 
+/* Test hook: C[M][N] fp32 = A[M][K] * B[N][K]^T (bf16, row-major, 16-byte aligned) with the
+ * lane's GEMM path (tcgen05 unless SV_GEMM=simt). M <= max_batch * (max_depth + 1), K % 64 == 0.
+ * `variant`: 0 = the lane's default kernel, 1 = 1-SM tcgen05, 2 = 2-SM tcgen05, 3 = SIMT. */
+sv_status sv_debug_gemm(sv_ctx* ctx, const void* A, const void* B, float* C, int32_t M, int32_t N, int32_t K,
+                        int32_t variant);
+
 /* Bench fixture (planted-successor drafter, SURVEY.md §8(d) "Acceptance control"):
  * for each request b (slots/depths (host) as in sv_verify), d_1 = succ[pending_b],
  * d_j = succ[d_{j-1}], except where dev_mask[row] != 0 the token is dev_tok[row]

@@ -26,9 +26,20 @@ struct GemmPlan {
   bool attn_maps_ok = false;
   CUtensorMap map_q, map_q2, map_kv;
   int q_box_tokens = 16;
+  int* sk_counters = nullptr;
+  float* partials = nullptr;
+  bool use_streamk = false;
+  bool use_2sm = false;
 };
 
-size_t gemm_workspace_bytes() { return 4096; }
+static size_t counter_bytes(int Tmax, int max_n) {
+  const size_t n = (size_t)((Tmax + 127) / 128) * ((max_n + 255) / 256);
+  return (n * 4 + 1023) & ~size_t(1023);
+}
+
+size_t gemm_workspace_bytes(int Tmax, int max_n) {
+  return counter_bytes(Tmax, max_n) + gemm_tc_partial_bytes(kGemmMaxSms);
+}
 
 static bool encode_attn_maps(GemmPlan* p);
 
@@ -63,8 +74,6 @@ static const CUtensorMap* get_map(GemmPlan* p, const void* base, uint64_t rows, 
 }
 
 GemmPlan* gemm_plan_create(const LaneDev& d, void* ws, cudaStream_t s) {
-  (void)ws;
-  (void)s;
   GemmPlan* p = new GemmPlan();
   p->d = d;
   const char* env = getenv("SV_GEMM");
@@ -72,6 +81,18 @@ GemmPlan* gemm_plan_create(const LaneDev& d, void* ws, cudaStream_t s) {
   int dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, dev);
+  if (p->num_sms > kGemmMaxSms) p->num_sms = kGemmMaxSms;
+  // stream-K scratch: counters first (zeroed here; the kernel re-zeroes each tile it completes)
+  int max_n = d.qkv_rows;
+  if (d.D > max_n) max_n = d.D;
+  if (2 * d.F > max_n) max_n = 2 * d.F;
+  const size_t cb = counter_bytes(d.Tmax, max_n);
+  p->sk_counters = reinterpret_cast<int*>(ws);
+  p->partials = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + cb);
+  cudaMemsetAsync(ws, 0, cb, s);
+  const char* skenv = getenv("SV_STREAMK");
+  p->use_streamk = skenv && !strcmp(skenv, "1");     // measured slower than whole tiles: opt-in
+  p->use_2sm = env && !strcmp(env, "tc2");
   p->encode = get_encode();
   if (!p->encode) {
     fprintf(stderr, "[sv] cuTensorMapEncodeTiled unavailable\n");
@@ -159,6 +180,10 @@ cudaError_t gemm_run(GemmPlan* p, const bf16* A, const bf16* B, float* C, int M,
   g.n_tiles = (N + 255) / 256;
   g.out = C;
   g.ldo = N;
+  if (p->use_streamk) {
+    g.partials = p->partials;
+    g.sk_counters = p->sk_counters;
+  }
   switch (epi) {
     case EPI_QKV_ROPE: {
       g.kind = GEMM_EPI_QKV_ROPE;
@@ -197,7 +222,31 @@ cudaError_t gemm_run(GemmPlan* p, const bf16* A, const bf16* B, float* C, int M,
     default:
       g.kind = GEMM_EPI_NONE;
   }
+  if (p->use_2sm && !g.partials) return launch_gemm_tc2(*ma, *mb, g, p->num_sms, s);
   return launch_gemm_tc(*ma, *mb, g, p->num_sms, s);
+}
+
+}  // namespace sv
+
+namespace sv {
+
+cudaError_t gemm_debug(GemmPlan* p, const bf16* A, const bf16* B, float* C, int M, int N, int K, int variant,
+                       cudaStream_t s) {
+  if (variant == 3 || (variant == 0 && !p->use_tc) || !p->encode) return launch_gemm_simt(A, B, C, M, N, K, s);
+  const CUtensorMap* ma = get_map(p, A, (uint64_t)M, (uint64_t)K);
+  const CUtensorMap* mb = get_map(p, B, (uint64_t)N, (uint64_t)K);
+  if (!ma || !mb) return cudaErrorInvalidValue;
+  GemmTcArgs g;
+  memset(&g, 0, sizeof(g));
+  g.kind = GEMM_EPI_NONE;
+  g.M = M;
+  g.N = N;
+  g.K = K;
+  g.n_tiles = (N + 255) / 256;
+  g.out = C;
+  g.ldo = N;
+  const bool two = variant == 2 || (variant == 0 && p->use_2sm);
+  return two ? launch_gemm_tc2(*ma, *mb, g, p->num_sms, s) : launch_gemm_tc(*ma, *mb, g, p->num_sms, s);
 }
 
 }  // namespace sv

@@ -30,9 +30,19 @@ struct GemmTcArgs {
   int* targ;
   int nt;
   float inv_temp;
+  // stream-K (decided at launch): partial-tile buffers [grid][2][128 x 256] fp32 and per-tile
+  // arrival counters (zero between launches)
+  int streamk, sk_w;
+  float* partials;
+  int* sk_counters;
 };
 
+constexpr int kGemmMaxSms = 160;
 int gemm_tc_smem_bytes();
+size_t gemm_tc_partial_bytes(int num_sms);
+// 2-SM (cta_group::2) variant: 256 x 256 tiles per CTA pair (see k_gemm_tc.cu)
+cudaError_t launch_gemm_tc2(const CUtensorMap& map_a, const CUtensorMap& map_b, const GemmTcArgs& g, int num_sms,
+                            cudaStream_t s);
 cudaError_t launch_gemm_tc(const CUtensorMap& map_a, const CUtensorMap& map_b, const GemmTcArgs& g, int num_sms,
                            cudaStream_t s);
 

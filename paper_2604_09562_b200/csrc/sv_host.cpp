@@ -110,7 +110,7 @@ Layout make_layout(const sv_config& c) {
   L.acc_int = L.take(4 * c.max_batch);
   L.tok_int = L.take(4 * c.max_batch * (c.max_depth + 1));
   L.batch_n = L.take(4);
-  L.gemm_ws = L.take(sv::gemm_workspace_bytes());
+  L.gemm_ws = L.take(sv::gemm_workspace_bytes((int)T, (int)cmax));
   L.trace = L.take(8 * 16 * 256);
   L.total = (L.total + 1023) & ~size_t(1023);
   return L;
@@ -586,6 +586,14 @@ sv_status sv_debug_uniforms(sv_ctx* c, uint64_t seed, uint64_t rid, uint32_t z, 
                             int32_t n, float* u) {
   if (!c || !u || n < 0 || x0 < 0 || (purpose != 0 && purpose != 1)) return SV_EINVAL;
   SV_CUDA(sv::launch_debug_uniforms(seed, rid, z, purpose, x0, n, u, c->stream));
+  return SV_OK;
+}
+
+sv_status sv_debug_gemm(sv_ctx* c, const void* A, const void* B, float* C, int32_t M, int32_t N, int32_t K,
+                        int32_t variant) {
+  if (!c || !A || !B || !C || M < 1 || N < 1 || K < 64 || K % 64 || M > c->d.Tmax) return SV_EINVAL;
+  if (((uintptr_t)A | (uintptr_t)B | (uintptr_t)C) & 15) return SV_EINVAL;
+  SV_CUDA(sv::gemm_debug(c->gemm, (const bf16*)A, (const bf16*)B, C, M, N, K, variant, c->stream));
   return SV_OK;
 }
 

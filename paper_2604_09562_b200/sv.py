@@ -28,7 +28,7 @@ EXPORTED = [
     "sv_verify_logits", "sv_commit", "sv_release", "sv_stats", "sv_set_taps", "sv_get_tap", "sv_debug_uniforms",
     "sv_draft_planted", "sv_nccl_unique_id", "sv_nccl_comm_init", "sv_nccl_comm_destroy", "sv_kv_send",
     "sv_kv_recv_append", "sv_kv_packed_bytes", "sv_kv_pack", "sv_profile_enable", "sv_profile_num_stages",
-    "sv_profile_stage_name", "sv_profile_read", "sv_launch_count",
+    "sv_profile_stage_name", "sv_profile_read", "sv_launch_count", "sv_debug_gemm",
 ]
 
 
@@ -116,6 +116,7 @@ def load():
         "sv_profile_stage_name": ([i32], ctypes.c_char_p),
         "sv_profile_read": ([vp, P(ctypes.c_double), P(ctypes.c_int64), i32, ctypes.c_int], ctypes.c_int),
         "sv_launch_count": ([], u64),
+        "sv_debug_gemm": ([vp, vp, vp, vp, i32, i32, i32, i32], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -249,6 +250,13 @@ class Lane:
         u = torch.empty(n, dtype=torch.float32, device=self.device)
         _check(self.lib.sv_debug_uniforms(self.ctx, seed, rid, z, purpose, x0, n, _ptr(u)), "sv_debug_uniforms")
         return u
+
+    def debug_gemm(self, A, B, C, variant=0):
+        """C = A B^T through the library's GEMM kernels (test hook)."""
+        M, K = A.shape
+        N = B.shape[0]
+        _check(self.lib.sv_debug_gemm(self.ctx, _ptr(A), _ptr(B), _ptr(C), M, N, K, variant), "sv_debug_gemm")
+        return C
 
     def draft_planted(self, slots, depths, succ, dev_mask, dev_tok, out):
         s, B = _i32_array(slots)
