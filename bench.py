@@ -163,7 +163,9 @@ def run_gpu(args, wl, rank, world, dev):
     lane.stats(reset=True)
     # context lengths at the start of the timed region (for the algorithmic attention bytes)
     ln = lane.tap("len", torch.int32, (cfg.max_slots,))[:B].cpu().tolist()
-    lane.profile(True)
+    # only the roofline kernels are bracketed by events in the timed region (every record is a
+    # host call and a stream dependency); --detail times every stage and says so in the line
+    lane.profile(True if args.detail else ["lm_head", "attention"])
     lane.profile_read(reset=True)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     stream = torch.cuda.current_stream(dev)

@@ -72,6 +72,7 @@ typedef enum { SV_GREEDY = 0, SV_SAMPLE = 1 } sv_mode;
 #define SV_DERR_BAD_TOKEN 1   /* a draft / pending token outside [0, V) */
 #define SV_DERR_NO_PAGES 2    /* free list exhausted during append / commit */
 #define SV_DERR_BAD_KEEP 4    /* n_keep < 1 */
+#define SV_DERR_MAX_POS 8     /* a chain or commit would pass max_pos; that request is not committed */
 
 typedef struct { /* (host) model + lane configuration */
   int32_t n_layers, d_model, n_q_heads, n_kv_heads, head_dim, vocab;
@@ -202,7 +203,10 @@ sv_status sv_debug_uniforms(sv_ctx* ctx, uint64_t seed, uint64_t rid, uint32_t z
 
 /* Test hook: C[M][N] fp32 = A[M][K] * B[N][K]^T (bf16, row-major, 16-byte aligned) with the
  * lane's GEMM path (tcgen05 unless SV_GEMM=simt). M <= max_batch * (max_depth + 1), K % 64 == 0.
- * `variant`: 0 = the lane's default kernel, 1 = 1-SM tcgen05, 2 = 2-SM tcgen05, 3 = SIMT. */
+ * `variant`: 0 = the lane's default kernel, 1 = 1-SM tcgen05, 2 = 2-SM tcgen05, 3 = SIMT,
+ *   4 = 1-SM tcgen05 with operand loads skipped after the pipeline fill (timing diagnostic only:
+ *   the result is meaningless), 5 = weight-major 2-SM tcgen05 (the default), 6 / 7 / 8 = variant 5
+ *   with loads skipped / epilogue skipped / both (timing diagnostics). */
 sv_status sv_debug_gemm(sv_ctx* ctx, const void* A, const void* B, float* C, int32_t M, int32_t N, int32_t K,
                         int32_t variant);
 
@@ -215,12 +219,14 @@ sv_status sv_draft_planted(sv_ctx* ctx, int32_t batch, const int32_t* slots, con
                            int32_t* draft_tokens);
 
 /* Measurement hooks (bench.py): per-stage CUDA-event timing on the lane's stream.
- * sv_profile_enable(ctx, 1) brackets every stage of sv_verify / sv_commit /
- * sv_draft_planted with cudaEventRecord; sv_profile_read (syncs) returns, for each
+ * sv_profile_enable(ctx, mask) brackets stage i of sv_verify / sv_commit /
+ * sv_draft_planted with cudaEventRecord when bit i of mask is set (-1 = all
+ * stages, 0 = off; each record costs host time and a stream dependency, so a
+ * timed run enables only the stages it reports). sv_profile_read (syncs) returns, for each
  * of sv_profile_num_stages() stages (names from sv_profile_stage_name), the summed
  * device milliseconds and launch count since the last reset. sv_launch_count()
  * is the number of CUDA kernels this library has launched in the process. */
-sv_status sv_profile_enable(sv_ctx* ctx, int on);
+sv_status sv_profile_enable(sv_ctx* ctx, int32_t stage_mask);
 int32_t sv_profile_num_stages(void);
 const char* sv_profile_stage_name(int32_t i);
 sv_status sv_profile_read(sv_ctx* ctx, double* ms_total, int64_t* count, int32_t n, int reset);

@@ -20,7 +20,7 @@ struct GemmPlan {
   bool use_tc = true;
   int num_sms = 148;
   PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
-  std::map<std::tuple<const void*, uint64_t, uint64_t>, CUtensorMap> maps;
+  std::map<std::tuple<const void*, uint64_t, uint64_t, uint32_t>, CUtensorMap> maps;
   bool use_tc_attn = true;
   bool use_tc2_attn = false;       // keys-on-lanes kernel (d_h = 128)
   bool attn_maps_ok = false;
@@ -29,7 +29,8 @@ struct GemmPlan {
   int* sk_counters = nullptr;
   float* partials = nullptr;
   bool use_streamk = false;
-  bool use_2sm = false;
+  bool use_2sm = false;            // token-major 2-SM kernel (SV_GEMM=tc2)
+  bool use_1sm = false;            // token-major 1-SM kernel (SV_GEMM=tc1)
 };
 
 static size_t counter_bytes(int Tmax, int max_n) {
@@ -52,16 +53,17 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
 }
 
-// bf16 row-major [rows][cols] tensor, box 64 (cols, 128 B) x 128 rows, 128-byte swizzle
-static const CUtensorMap* get_map(GemmPlan* p, const void* base, uint64_t rows, uint64_t cols) {
-  auto key = std::make_tuple(base, rows, cols);
+// bf16 row-major [rows][cols] tensor, box 64 (cols, 128 B) x box_rows, 128-byte swizzle
+static const CUtensorMap* get_map(GemmPlan* p, const void* base, uint64_t rows, uint64_t cols,
+                                  uint32_t box_rows = 128) {
+  auto key = std::make_tuple(base, rows, cols, box_rows);
   auto it = p->maps.find(key);
   if (it != p->maps.end()) return &it->second;
   CUtensorMap m;
   memset(&m, 0, sizeof(m));
   cuuint64_t dims[2] = {cols, rows};
   cuuint64_t strides[1] = {cols * 2};
-  cuuint32_t box[2] = {64, 128};
+  cuuint32_t box[2] = {64, box_rows};
   cuuint32_t es[2] = {1, 1};
   CUresult r = p->encode(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -93,6 +95,7 @@ GemmPlan* gemm_plan_create(const LaneDev& d, void* ws, cudaStream_t s) {
   const char* skenv = getenv("SV_STREAMK");
   p->use_streamk = skenv && !strcmp(skenv, "1");     // measured slower than whole tiles: opt-in
   p->use_2sm = env && !strcmp(env, "tc2");
+  p->use_1sm = env && !strcmp(env, "tc1");
   p->encode = get_encode();
   if (!p->encode) {
     fprintf(stderr, "[sv] cuTensorMapEncodeTiled unavailable\n");
@@ -165,6 +168,20 @@ static cudaError_t gemm_simt(GemmPlan* p, const bf16* A, const bf16* B, float* C
   }
 }
 
+// weight-major 2-SM kernel: weights (B) on the MMA's M side, the M tokens of A on its N side
+static cudaError_t gemm_sw(GemmPlan* p, const bf16* A, const bf16* B, int M, int K, GemmTcArgs& g, cudaStream_t s) {
+  const bool swiglu = g.kind == GEMM_EPI_SWIGLU;
+  const int num_mp = swiglu ? g.F / 128 : (g.N + 255) / 256;
+  g.nt_tok = gemm_sw_choose_nt(M, num_mp, p->num_sms / 2);
+  if (const char* nt = getenv("SV_SW_NT")) g.nt_tok = atoi(nt);   // experiment override
+  if (const char* dg = getenv("SV_SW_DIAG")) g.diag = atoi(dg);    // experiment: 1 no loads, 2 no epilogue
+  if (g.kind == GEMM_EPI_LOGITS) g.trace = p->d.trace;                // lm-head tile timeline (SV_TRACE)
+  const CUtensorMap* mw = get_map(p, B, (uint64_t)g.N, (uint64_t)K, swiglu ? 64 : 128);
+  const CUtensorMap* mx = get_map(p, A, (uint64_t)M, (uint64_t)K, (uint32_t)(g.nt_tok / 2));  // rows >= M: zero
+  if (!mw || !mx) return cudaErrorInvalidValue;
+  return launch_gemm_sw(*mw, *mx, g, p->num_sms, s);
+}
+
 cudaError_t gemm_run(GemmPlan* p, const bf16* A, const bf16* B, float* C, int M, int N, int K, int epi,
                      const GemmEpi& e, cudaStream_t s) {
   if (!p->use_tc || (K % 64)) return gemm_simt(p, A, B, C, M, N, K, epi, e, s);
@@ -223,7 +240,8 @@ cudaError_t gemm_run(GemmPlan* p, const bf16* A, const bf16* B, float* C, int M,
       g.kind = GEMM_EPI_NONE;
   }
   if (p->use_2sm && !g.partials) return launch_gemm_tc2(*ma, *mb, g, p->num_sms, s);
-  return launch_gemm_tc(*ma, *mb, g, p->num_sms, s);
+  if (p->use_1sm || g.partials) return launch_gemm_tc(*ma, *mb, g, p->num_sms, s);
+  return gemm_sw(p, A, B, M, K, g, s);
 }
 
 }  // namespace sv
@@ -245,6 +263,12 @@ cudaError_t gemm_debug(GemmPlan* p, const bf16* A, const bf16* B, float* C, int 
   g.n_tiles = (N + 255) / 256;
   g.out = C;
   g.ldo = N;
+  g.diag = variant == 4 ? 1 : 0;
+  if (variant >= 6) {                                  // weight-major diagnostics (timing only)
+    g.diag = variant == 6 ? 1 : variant == 7 ? 2 : variant == 8 ? 3 : 5;  // 6: MMA only, 7: no epilogue,
+                                                                          // 8: both, 9: MMA only with A in TMEM
+  }
+  if (variant >= 5 || (variant == 0 && !p->use_2sm && !p->use_1sm)) return gemm_sw(p, A, B, M, K, g, s);
   const bool two = variant == 2 || (variant == 0 && p->use_2sm);
   return two ? launch_gemm_tc2(*ma, *mb, g, p->num_sms, s) : launch_gemm_tc(*ma, *mb, g, p->num_sms, s);
 }

@@ -33,6 +33,9 @@ struct GemmTcArgs {
   // stream-K (decided at launch): partial-tile buffers [grid][2][128 x 256] fp32 and per-tile
   // arrival counters (zero between launches)
   int streamk, sk_w;
+  int nt_tok;  // weight-major kernel: token tile width (N of the MMA), multiple of 16, <= 256
+  unsigned long long* trace;  // weight-major kernel: per-tile clock64 trace of CTA 0 (SV_TRACE)
+  int diag;  // 1: skip TMA after the first STAGES k-blocks (measures the MMA/epilogue-only time)
   float* partials;
   int* sk_counters;
 };
@@ -43,6 +46,12 @@ size_t gemm_tc_partial_bytes(int num_sms);
 // 2-SM (cta_group::2) variant: 256 x 256 tiles per CTA pair (see k_gemm_tc.cu)
 cudaError_t launch_gemm_tc2(const CUtensorMap& map_a, const CUtensorMap& map_b, const GemmTcArgs& g, int num_sms,
                             cudaStream_t s);
+// weight-major 2-SM variant (k_gemm_sw.cu): map_w = weights [N][K] box (64, 128) (box rows 64 for
+// SWIGLU), map_x = tokens [>= M][K] box (64, nt_tok / 2)
+int gemm_sw_choose_nt(int T, int num_mp, int n_pairs);
+int gemm_sw_smem_bytes();
+cudaError_t launch_gemm_sw(const CUtensorMap& map_w, const CUtensorMap& map_x, const GemmTcArgs& g, int num_sms,
+                           cudaStream_t s);
 cudaError_t launch_gemm_tc(const CUtensorMap& map_a, const CUtensorMap& map_b, const GemmTcArgs& g, int num_sms,
                            cudaStream_t s);
 

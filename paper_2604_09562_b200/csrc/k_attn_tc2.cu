@@ -239,8 +239,9 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    // ======================= MMA issuer
-    if (lane == 0) {
+    // ======================= MMA issuer: the whole warp runs the loop (warp-uniform state, so
+    // ptxas keeps descriptors in uniform registers); one elected lane issues
+    {
       int ks = 0, vs = 0;
       uint32_t kph = 0, vph = 0;
       uint32_t g = 0;
@@ -261,46 +262,52 @@ __global__ void __launch_bounds__(THREADS, 1)
           if (t < I.n_tiles) {
             const int sb = g & 1;
             tc::mbar_wait(&k_full[ks], kph);
-            SV_TR2(2, g);
+            if (lane == 0) SV_TR2(2, g);
             tc::mbar_wait(&s_free[sb], ((g >> 1) & 1) ^ 1);
-            SV_TR2(3, g);
+            if (lane == 0) SV_TR2(3, g);
             tc::fence_after();
             const uint32_t sk = tc::smem_u32(sK + ks * KV_BYTES);
+            if (tc::elect_one()) {
 #pragma unroll
-            for (int kk = 0; kk < DH / 16; ++kk) {
-              const uint32_t koff = (kk % 4) * 32;
-              const uint64_t da = tc::sdesc_sw128(sk + (kk / 4) * (KT * 128) + koff, 16, 1024);
-              const uint64_t db = tc::sdesc_sw128(sq + (kk / 4) * (NQ * 128) + koff, 16, 1024);
-              tc::umma_bf16(tmem + S_COL + sb * NQ, da, db, IDESC_QK, kk > 0);
+              for (int kk = 0; kk < DH / 16; ++kk) {
+                const uint32_t koff = (kk % 4) * 32;
+                const uint64_t da = tc::sdesc_sw128(sk + (kk / 4) * (KT * 128) + koff, 16, 1024);
+                const uint64_t db = tc::sdesc_sw128(sq + (kk / 4) * (NQ * 128) + koff, 16, 1024);
+                tc::umma_bf16(tmem + S_COL + sb * NQ, da, db, IDESC_QK, kk > 0);
+              }
+              tc::umma_commit(&s_full[sb]);
+              tc::umma_commit(&k_empty[ks]);                      // K tile no longer needed
+              if (t == I.n_tiles - 1) tc::umma_commit(q_empty);   // last read of Q for this item
             }
-            tc::umma_commit(&s_full[sb]);
-            tc::umma_commit(&k_empty[ks]);                      // K tile no longer needed
-            if (t == I.n_tiles - 1) tc::umma_commit(q_empty);   // last read of Q for this item
+            __syncwarp();
           }
           if (t > 0) {
             const int pb = prev_g & 1;
             tc::mbar_wait(&p_full[pb], (prev_g >> 1) & 1);
             tc::mbar_wait(&v_full[prev_vs], prev_vph);
-            SV_TR2(4, prev_g);
+            if (lane == 0) SV_TR2(4, prev_g);
             tc::fence_after();
             const uint32_t sv_ = tc::smem_u32(sV + prev_vs * KV_BYTES);
             const uint32_t sp = sp0 + pb * P_BYTES;
+            if (tc::elect_one()) {
 #pragma unroll
-            for (int kk = 0; kk < KT / 16; ++kk) {
-              // A = V^T: d_h contiguous (MN-major), LBO = next 64-wide d_h atom (128 keys * 128 B),
-              // SBO = next 8 keys; B = P^T: slots contiguous (MN-major), SBO = next 8 keys
-              const uint64_t da = tc::sdesc_sw128(sv_ + kk * 2048, KT * 128, 1024);
-              const uint64_t db = tc::sdesc_sw128(sp + kk * 2048, 8192, 1024);
-              tc::umma_bf16(o_tm, da, db, IDESC_PV, (t > 1) || (kk > 0));
-            }
-            // column sums of the bf16 P^T actually used: L^T += ones(128 x keys) . P^T
+              for (int kk = 0; kk < KT / 16; ++kk) {
+                // A = V^T: d_h contiguous (MN-major), LBO = next 64-wide d_h atom (128 keys * 128 B),
+                // SBO = next 8 keys; B = P^T: slots contiguous (MN-major), SBO = next 8 keys
+                const uint64_t da = tc::sdesc_sw128(sv_ + kk * 2048, KT * 128, 1024);
+                const uint64_t db = tc::sdesc_sw128(sp + kk * 2048, 8192, 1024);
+                tc::umma_bf16(o_tm, da, db, IDESC_PV, (t > 1) || (kk > 0));
+              }
+              // column sums of the bf16 P^T actually used: L^T += ones(128 x keys) . P^T
 #pragma unroll
-            for (int kk = 0; kk < KT / 16; ++kk) {
-              const uint64_t db = tc::sdesc_sw128(sp + kk * 2048, 8192, 1024);
-              tc::umma_bf16_ts(l_tm, tmem + ONE_COL + kk * 8, db, IDESC_L, (t > 1) || (kk > 0));
+              for (int kk = 0; kk < KT / 16; ++kk) {
+                const uint64_t db = tc::sdesc_sw128(sp + kk * 2048, 8192, 1024);
+                tc::umma_bf16_ts(l_tm, tmem + ONE_COL + kk * 8, db, IDESC_L, (t > 1) || (kk > 0));
+              }
+              tc::umma_commit(&v_empty[prev_vs]);
+              tc::umma_commit(&s_free[pb]);
             }
-            tc::umma_commit(&v_empty[prev_vs]);
-            tc::umma_commit(&s_free[pb]);
+            __syncwarp();
           }
           if (t < I.n_tiles) {
             prev_vs = vs;
@@ -311,7 +318,8 @@ __global__ void __launch_bounds__(THREADS, 1)
             if (++vs == VST) { vs = 0; vph ^= 1; }
           }
         }
-        tc::umma_commit(&o_full[ob]);
+        if (tc::elect_one()) tc::umma_commit(&o_full[ob]);
+        __syncwarp();
       }
     }
   } else if (warp >= 3) {

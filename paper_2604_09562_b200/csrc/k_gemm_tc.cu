@@ -34,7 +34,8 @@ constexpr int B_BYTES = BN * BK * 2;             // 32 KB
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;   // 48 KB
 constexpr int THREADS = 256;
 constexpr uint32_t IDESC = tc::idesc_bf16(BM, BN);
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int STG_BYTES = 4 * 4096;              // epilogue staging, 4 KB per epilogue warp
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + STG_BYTES;
 constexpr int EPI_BAR = 1;                       // named barrier of the 4 epilogue warps
 }  // namespace
 
@@ -125,51 +126,103 @@ struct PartialSrc {
   }
 };
 
-// ------------------------------------------------------------------ epilogues
-// Each epilogue thread owns one accumulator row (TMEM lane) and walks its 256 columns
-// in 8 chunks of 32.
-template <class Src>
-__device__ __forceinline__ void epi_store_f32(const GemmTcArgs& g, int row, int n0, const Src& src) {
-  uint32_t r[32];
-  for (int c = 0; c < BN / 32; ++c) {
-    src.get(c * 32, r);
-    if (row >= g.M) continue;
-    const int n = n0 + c * 32;
-    float* dst = g.out + (size_t)row * g.ldo + n;
-    if (g.kind == GEMM_EPI_RESIDUAL) {
-      const float* in = g.resid_in + (size_t)row * g.ldo + n;
-      float* o = g.resid_out + (size_t)row * g.ldo + n;
-      if (n + 32 <= g.N) {
+// ------------------------------------------------------------------ coalesced stores
+// An epilogue thread holds 32 consecutive values of ITS row (TMEM lane = row). Stored
+// directly, every warp instruction would touch 32 rows = 32 partial sectors. Instead the warp
+// transposes its 32 x 32 block through a 4 KB staging buffer (16-byte chunks XOR-swizzled by
+// row, so both phases are bank-conflict free) and writes whole row segments: 8 lanes x 16 B
+// per fp32 row (4 rows per instruction), 4 lanes x 16 B per bf16 row (8 rows per instruction).
+struct Stage32 {
+  uint4* s;     // this warp's staging buffer (256 x 16 B)
+  int lane;
+  int row0;     // global row of lane 0
+};
+
+__device__ __forceinline__ void stage_put_f32(const Stage32& st, const uint32_t (&r)[32]) {
+  uint4* p = st.s + st.lane * 8;
 #pragma unroll
-        for (int i = 0; i < 32; i += 4) {
-          const float4 h = *reinterpret_cast<const float4*>(in + i);
-          *reinterpret_cast<float4*>(o + i) =
-              make_float4(h.x + u2f(r[i]), h.y + u2f(r[i + 1]), h.z + u2f(r[i + 2]), h.w + u2f(r[i + 3]));
+  for (int j = 0; j < 8; ++j) p[j ^ (st.lane & 7)] = make_uint4(r[4 * j], r[4 * j + 1], r[4 * j + 2], r[4 * j + 3]);
+  __syncwarp();
+}
+
+// out[row][n + i] = staged (+ in[row][n + i] when in != nullptr) for rows < M, columns < N.
+// in may alias out (each element is read and written by the same lane).
+__device__ __forceinline__ void stage_write_f32(const Stage32& st, float* out, const float* in, size_t ld, int M,
+                                                int n, int N) {
+  const int rs = st.lane >> 3, ch = st.lane & 7;
+  const int col = n + ch * 4;
+  const bool vec = col + 4 <= N && (ld & 3) == 0;
+#pragma unroll
+  for (int it = 0; it < 8; ++it) {
+    const int r = it * 4 + rs, row = st.row0 + r;
+    const uint4 u = st.s[r * 8 + (ch ^ (r & 7))];
+    float v[4] = {u2f(u.x), u2f(u.y), u2f(u.z), u2f(u.w)};
+    if (row < M) {
+      const size_t o = (size_t)row * ld + col;
+      if (vec) {
+        if (in) {
+          const float4 h = *reinterpret_cast<const float4*>(in + o);
+          v[0] += h.x;
+          v[1] += h.y;
+          v[2] += h.z;
+          v[3] += h.w;
         }
+        *reinterpret_cast<float4*>(out + o) = make_float4(v[0], v[1], v[2], v[3]);
       } else {
-        for (int i = 0; i < 32 && n + i < g.N; ++i) o[i] = in[i] + u2f(r[i]);
-      }
-    } else {
-      if (n + 32 <= g.N) {
-#pragma unroll
-        for (int i = 0; i < 32; i += 4)
-          *reinterpret_cast<float4*>(dst + i) = make_float4(u2f(r[i]), u2f(r[i + 1]), u2f(r[i + 2]), u2f(r[i + 3]));
-      } else {
-        for (int i = 0; i < 32 && n + i < g.N; ++i) dst[i] = u2f(r[i]);
+        for (int i = 0; i < 4 && col + i < N; ++i) out[o + i] = in ? in[o + i] + v[i] : v[i];
       }
     }
   }
+  __syncwarp();
 }
 
-// a5: fp32 logits + per-(row, 256-col tile) max / sum exp / lowest argmax of l * inv_temp
+__device__ __forceinline__ void stage_put_bf16(const Stage32& st, const __nv_bfloat16 (&o)[32]) {
+  uint4* p = st.s + st.lane * 4;
+  const int f = (st.lane >> 1) & 3;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) p[j ^ f] = *reinterpret_cast<const uint4*>(&o[8 * j]);
+  __syncwarp();
+}
+
+// out0 = address of (row0, first column); rows r < rows_valid get their 32 staged values
+__device__ __forceinline__ void stage_write_bf16(const Stage32& st, __nv_bfloat16* out0, size_t ld, int rows_valid) {
+  const int rs = st.lane >> 2, ch = st.lane & 3;
+#pragma unroll
+  for (int it = 0; it < 4; ++it) {
+    const int r = it * 8 + rs;
+    const uint4 v = st.s[r * 4 + (ch ^ ((r >> 1) & 3))];
+    if (r < rows_valid) *reinterpret_cast<uint4*>(out0 + (size_t)r * ld + ch * 8) = v;
+  }
+  __syncwarp();
+}
+
+// ------------------------------------------------------------------ epilogues
+// Each epilogue thread owns one accumulator row (TMEM lane) and walks its 256 columns
+// in 8 chunks of 32; all lanes of the warp take part in every chunk (warp-collective
+// tcgen05.ld and staging), rows >= M are masked at the global store.
 template <class Src>
-__device__ __forceinline__ void epi_logits(const GemmTcArgs& g, int row, int n0, int n_blk, const Src& src) {
+__device__ __forceinline__ void epi_store_f32(const GemmTcArgs& g, const Stage32& st, int n0, const Src& src) {
+  uint32_t r[32];
+  const bool resid = g.kind == GEMM_EPI_RESIDUAL;
+  for (int c = 0; c < BN / 32; ++c) {
+    src.get(c * 32, r);
+    stage_put_f32(st, r);
+    stage_write_f32(st, resid ? g.resid_out : g.out, resid ? g.resid_in : nullptr, g.ldo, g.M, n0 + c * 32, g.N);
+  }
+}
+
+// a5: fp32 logits + per-(row, 128-col vocab tile) max / sum exp / lowest argmax of l * inv_temp
+template <class Src>
+__device__ __forceinline__ void epi_logits(const GemmTcArgs& g, const Stage32& st, int n0, int n_blk,
+                                           const Src& src) {
+  const int row = st.row0 + st.lane;
   uint32_t r[32];
   float m = -INFINITY, s = 0.f;
   int am = 0x7fffffff;
   for (int c = 0; c < BN / 32; ++c) {
     src.get(c * 32, r);
     const int n = n0 + c * 32;
+    stage_put_f32(st, r);
     float cm = -INFINITY;
     int ca = 0x7fffffff;
 #pragma unroll
@@ -187,32 +240,31 @@ __device__ __forceinline__ void epi_logits(const GemmTcArgs& g, int row, int n0,
     s = (m == -INFINITY ? 0.f : s * expf(m - mn)) + cs;
     if (cm > m) am = ca;
     m = mn;
-    if (row < g.M) {
-      float* dst = g.out + (size_t)row * g.ldo + n;
-      if (n + 32 <= g.N) {
-#pragma unroll
-        for (int i = 0; i < 32; i += 4)
-          *reinterpret_cast<float4*>(dst + i) = make_float4(u2f(r[i]), u2f(r[i + 1]), u2f(r[i + 2]), u2f(r[i + 3]));
-      } else {
-        for (int i = 0; i < 32 && n + i < g.N; ++i) dst[i] = u2f(r[i]);
+    stage_write_f32(st, g.out, nullptr, g.ldo, g.M, n, g.N);
+    if ((c & 3) == 3) {                            // statistics per 128-column vocab tile
+      const int tile = n_blk * 2 + (c >> 2);
+      if (row < g.M && tile < g.nt) {
+        const size_t o = (size_t)row * g.nt + tile;
+        g.tmax[o] = m;
+        g.tsum[o] = s;
+        g.targ[o] = am;
       }
+      m = -INFINITY;
+      s = 0.f;
+      am = 0x7fffffff;
     }
-  }
-  if (row < g.M) {
-    const size_t o = (size_t)row * g.nt + n_blk;
-    g.tmax[o] = m;
-    g.tsum[o] = s;
-    g.targ[o] = am;
   }
 }
 
 // a2: q/k RoPE (rotate_half, fp32 table) + bf16 store to Q / chain K; v plain bf16 store
 template <class Src>
-__device__ __forceinline__ void epi_qkv(const GemmTcArgs& g, int row, int n0, const Src& src) {
+__device__ __forceinline__ void epi_qkv(const GemmTcArgs& g, const Stage32& st, int n0, const Src& src) {
+  const int row = st.row0 + st.lane;
   const int dh = g.dh, half = dh / 2;
   const int heads_per_tile = BN / dh;
   const int nkv = g.Hkv * dh;
   const int pos = row < g.M ? g.row_pos[row] : 0;
+  const int rows_valid = g.M - st.row0;
   uint32_t x1[32], x2[32];
   for (int hh = 0; hh < heads_per_tile; ++hh) {
     const int head = n0 / dh + hh;
@@ -220,7 +272,7 @@ __device__ __forceinline__ void epi_qkv(const GemmTcArgs& g, int row, int n0, co
     for (int c = 0; c < half / 32; ++c) {
       src.get(cbase + c * 32, x1);
       src.get(cbase + half + c * 32, x2);
-      if (row >= g.M || head >= g.Hq + 2 * g.Hkv) continue;
+      if (head >= g.Hq + 2 * g.Hkv) continue;        // warp-uniform
       __nv_bfloat16 o1[32], o2[32];
       if (head < g.Hq + g.Hkv) {
         const float* cs = g.rope_cos + (size_t)pos * half + c * 32;
@@ -239,45 +291,51 @@ __device__ __forceinline__ void epi_qkv(const GemmTcArgs& g, int row, int n0, co
         }
       }
       __nv_bfloat16* dst;
-      if (head < g.Hq) dst = g.q + (size_t)row * g.Hq * dh + (size_t)head * dh;
-      else if (head < g.Hq + g.Hkv) dst = g.kc + (size_t)row * nkv + (size_t)(head - g.Hq) * dh;
-      else dst = g.vc + (size_t)row * nkv + (size_t)(head - g.Hq - g.Hkv) * dh;
-#pragma unroll
-      for (int i = 0; i < 32; i += 8) {
-        *reinterpret_cast<uint4*>(dst + c * 32 + i) = *reinterpret_cast<const uint4*>(&o1[i]);
-        *reinterpret_cast<uint4*>(dst + half + c * 32 + i) = *reinterpret_cast<const uint4*>(&o2[i]);
+      size_t ld;
+      if (head < g.Hq) {
+        dst = g.q + (size_t)st.row0 * g.Hq * dh + (size_t)head * dh;
+        ld = (size_t)g.Hq * dh;
+      } else if (head < g.Hq + g.Hkv) {
+        dst = g.kc + (size_t)st.row0 * nkv + (size_t)(head - g.Hq) * dh;
+        ld = nkv;
+      } else {
+        dst = g.vc + (size_t)st.row0 * nkv + (size_t)(head - g.Hq - g.Hkv) * dh;
+        ld = nkv;
       }
+      stage_put_bf16(st, o1);
+      stage_write_bf16(st, dst + c * 32, ld, rows_valid);
+      stage_put_bf16(st, o2);
+      stage_write_bf16(st, dst + half + c * 32, ld, rows_valid);
     }
   }
 }
 
 // a4: u = bf16(silu(gate) * up); tile columns 0..127 are gate rows, 128..255 the matching up rows
 template <class Src>
-__device__ __forceinline__ void epi_swiglu(const GemmTcArgs& g, int row, int n_blk, const Src& src) {
+__device__ __forceinline__ void epi_swiglu(const GemmTcArgs& g, const Stage32& st, int n_blk, const Src& src) {
   uint32_t gt[32], up[32];
   for (int c = 0; c < 4; ++c) {
     src.get(c * 32, gt);
     src.get(128 + c * 32, up);
-    if (row >= g.M) continue;
     __nv_bfloat16 o[32];
 #pragma unroll
     for (int i = 0; i < 32; ++i) {
       const float x = u2f(gt[i]);
       o[i] = f2bf(x / (1.0f + expf(-x)) * u2f(up[i]));
     }
-    __nv_bfloat16* dst = g.u + (size_t)row * g.F + n_blk * 128 + c * 32;
-#pragma unroll
-    for (int i = 0; i < 32; i += 8) *reinterpret_cast<uint4*>(dst + i) = *reinterpret_cast<const uint4*>(&o[i]);
+    stage_put_bf16(st, o);
+    stage_write_bf16(st, g.u + (size_t)st.row0 * g.F + n_blk * 128 + c * 32, g.F, g.M - st.row0);
   }
 }
 
 template <class Src>
-__device__ __forceinline__ void run_epilogue(const GemmTcArgs& g, const TileCoord& tcd, int row, const Src& src) {
+__device__ __forceinline__ void run_epilogue(const GemmTcArgs& g, const TileCoord& tcd, const Stage32& st,
+                                             const Src& src) {
   switch (g.kind) {
-    case GEMM_EPI_LOGITS: epi_logits(g, row, tcd.n_blk * BN, tcd.n_blk, src); break;
-    case GEMM_EPI_QKV_ROPE: epi_qkv(g, row, tcd.n_blk * BN, src); break;
-    case GEMM_EPI_SWIGLU: epi_swiglu(g, row, tcd.n_blk, src); break;
-    default: epi_store_f32(g, row, tcd.n_blk * BN, src); break;
+    case GEMM_EPI_LOGITS: epi_logits(g, st, tcd.n_blk * BN, tcd.n_blk, src); break;
+    case GEMM_EPI_QKV_ROPE: epi_qkv(g, st, tcd.n_blk * BN, src); break;
+    case GEMM_EPI_SWIGLU: epi_swiglu(g, st, tcd.n_blk, src); break;
+    default: epi_store_f32(g, st, tcd.n_blk * BN, src); break;
   }
 }
 
@@ -346,6 +404,11 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         for (int kb = p.kb0; kb < p.kb1; ++kb) {
           tc::mbar_wait(&empty[stage], phase ^ 1);
+          if (g.diag == 1 && (kb >= STAGES || p.tile != blockIdx.x)) {  // diagnostic: MMA on stale smem
+            tc::mbar_arrive(&full[stage]);
+            if (++stage == STAGES) { stage = 0; phase ^= 1; }
+            continue;
+          }
           tc::mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
           tc::tma_load_2d(sA + stage * A_BYTES, &map_a, &full[stage], kb * BK, arow);
           uint8_t* b = sB + stage * B_BYTES;
@@ -387,6 +450,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     // ---------------- epilogue warps (TMEM lanes 32*(warp%4) ..)
     const int q = warp & 3;
     const int rl = q * 32 + lane;                   // row inside the tile
+    uint4* stg = reinterpret_cast<uint4*>(smem + STAGES * STAGE_BYTES + 256) + q * 256;
     int acc = 0;
     uint32_t acc_phase = 0;
     PieceIter pi(g, num_tiles, nk);
@@ -396,9 +460,9 @@ __global__ void __launch_bounds__(THREADS, 1)
       tc::mbar_wait(&tfull[acc], acc_phase);
       tc::fence_after();
       const TmemSrc tsrc{tmem_base + (uint32_t(q * 32) << 16) + acc * BN};
-      const int row = tcd.m_blk * BM + rl;
+      const Stage32 st{stg, lane, tcd.m_blk * BM + q * 32};
       if (p.kb0 == 0 && p.kb1 == nk) {
-        run_epilogue(g, tcd, row, tsrc);
+        run_epilogue(g, tcd, st, tsrc);
         tc::fence_before();
         tc::mbar_arrive(&tempty[acc]);
       } else {
@@ -430,7 +494,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (*sk_flag) {
           __threadfence();
           const PartialSrc psrc{&g, rl, c_lo, n, p.tile, nk};
-          run_epilogue(g, tcd, row, psrc);
+          run_epilogue(g, tcd, st, psrc);
         }
         tc::named_bar(EPI_BAR, 128);                  // sk_flag reused by the next piece
       }
@@ -493,46 +557,8 @@ constexpr int B2_BYTES = 128 * BK * 2;              // 16 KB: this CTA's half of
 constexpr int STAGE2_BYTES = A_BYTES + B2_BYTES;    // 32 KB
 constexpr int STAGES2 = 6;
 constexpr uint32_t IDESC2 = tc::idesc_bf16(PAIR_M, BN);
-constexpr int SMEM2_BYTES = STAGES2 * STAGE2_BYTES + 1024 + 256;
-constexpr uint32_t kPeerBitMask = 0xFEFFFFFFu;      // shared::cluster address of the rank-0 CTA
+constexpr int SMEM2_BYTES = STAGES2 * STAGE2_BYTES + 1024 + 256 + STG_BYTES;
 }  // namespace
-
-__device__ __forceinline__ uint32_t cluster_rank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ void cluster_sync_all() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-__device__ __forceinline__ void tma_load_2d_2sm(void* dst, const CUtensorMap* m, uint32_t bar_cluster, int x, int y,
-                                                uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
-      "[%0], [%1, {%3, %4}], [%2], %5;" ::"r"(tc::smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(m)), "r"(bar_cluster), "r"(x), "r"(y), "l"(policy)
-      : "memory");
-}
-__device__ __forceinline__ void umma_bf16_2sm(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
-  asm volatile(
-      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(
-          d),
-      "l"(a), "l"(b), "r"(idesc), "r"(acc)
-      : "memory");
-}
-// arrive on the barrier at this smem offset in every CTA of `mask` once the MMAs complete
-__device__ __forceinline__ void umma_commit_2sm(uint64_t* bar, uint16_t mask) {
-  asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
-                   tc::smem_u32(bar)),
-               "h"(mask)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_cta0(uint64_t* bar) {
-  asm volatile(
-      "{\n .reg .b32 ra;\n mapa.shared::cluster.u32 ra, %0, 0;\n mbarrier.arrive.release.cluster.shared::cluster.b64 "
-      "_, [ra];\n}\n" ::"r"(tc::smem_u32(bar))
-      : "memory");
-}
 
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
@@ -549,7 +575,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t rank = cluster_rank();
+  const uint32_t rank = tc::cluster_rank();
   const bool leader = rank == 0;
   const int num_pm = (g.M + PAIR_M - 1) / PAIR_M;
   const int num_tiles = num_pm * g.n_tiles;
@@ -576,7 +602,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
   tc::fence_before();
   __syncthreads();
-  cluster_sync_all();
+  tc::cluster_sync_all();
   tc::fence_after();
   const uint32_t tmem_base = *tmem_holder;
 
@@ -593,9 +619,9 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int kb = 0; kb < nk; ++kb) {
           tc::mbar_wait(&empty[stage], phase ^ 1);
           if (leader) tc::mbar_arrive_expect_tx(&full[stage], 2 * STAGE2_BYTES);
-          const uint32_t fb = tc::smem_u32(&full[stage]) & kPeerBitMask;
-          tma_load_2d_2sm(sA + stage * A_BYTES, &map_a, fb, kb * BK, arow, tc::policy_evict_last());
-          tma_load_2d_2sm(sB + stage * B2_BYTES, &map_b, fb, kb * BK, brow, pol_b);
+          const uint32_t fb = tc::smem_u32(&full[stage]) & tc::kPeerBitMask;
+          tc::tma_load_2d_2sm(sA + stage * A_BYTES, &map_a, fb, kb * BK, arow, tc::policy_evict_last());
+          tc::tma_load_2d_2sm(sB + stage * B2_BYTES, &map_b, fb, kb * BK, brow, pol_b);
           if (++stage == STAGES2) { stage = 0; phase ^= 1; }
         }
       }
@@ -618,17 +644,18 @@ __global__ void __launch_bounds__(THREADS, 1)
           const uint64_t db = tc::sdesc_sw128(tc::smem_u32(sB + stage * B2_BYTES), 16, 1024);
 #pragma unroll
           for (int kk = 0; kk < BK / 16; ++kk)
-            umma_bf16_2sm(d, da + 2 * kk, db + 2 * kk, IDESC2, (kb | kk) != 0);
-          umma_commit_2sm(&empty[stage], 0x3);
+            tc::umma_bf16_2sm(d, da + 2 * kk, db + 2 * kk, IDESC2, (kb | kk) != 0);
+          tc::umma_commit_2sm(&empty[stage], 0x3);
           if (++stage == STAGES2) { stage = 0; phase ^= 1; }
         }
-        umma_commit_2sm(&tfull[acc], 0x3);
+        tc::umma_commit_2sm(&tfull[acc], 0x3);
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
     }
   } else if (warp >= 4) {
     // ---------------- epilogue warps of both CTAs (own 128 rows of the pair tile)
     const int q = warp & 3;
+    uint4* stg = reinterpret_cast<uint4*>(smem + STAGES2 * STAGE2_BYTES + 256) + q * 256;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int t = cluster; t < num_tiles; t += n_clusters) {
@@ -636,17 +663,17 @@ __global__ void __launch_bounds__(THREADS, 1)
       tc::mbar_wait(&tfull[acc], acc_phase);
       tc::fence_after();
       const TmemSrc tsrc{tmem_base + (uint32_t(q * 32) << 16) + acc * BN};
-      const int row = m_pair * PAIR_M + (int)rank * 128 + q * 32 + lane;
-      run_epilogue(g, TileCoord{0, n_blk}, row, tsrc);
+      const Stage32 st{stg, lane, m_pair * PAIR_M + (int)rank * 128 + q * 32};
+      run_epilogue(g, TileCoord{0, n_blk}, st, tsrc);
       tc::fence_before();
       if (leader) tc::mbar_arrive(&tempty[acc]);
-      else mbar_arrive_cta0(&tempty[acc]);
+      else tc::mbar_arrive_cta0(&tempty[acc]);
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
   }
   tc::fence_before();
   __syncthreads();
-  cluster_sync_all();
+  tc::cluster_sync_all();
   if (warp == 2) {
     tc::fence_after();
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem_base) : "memory");

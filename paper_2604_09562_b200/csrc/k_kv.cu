@@ -20,6 +20,7 @@ SV_DEV bool pop_pages(const LaneDev& d, int slot, int first, int n) {
   if (n <= 0) return true;
   const int old = atomicSub(d.free_top, n);
   if (old - n < 0) {
+    atomicAdd(d.free_top, n);                    // undo: the pages were not taken
     atomicOr(d.err, SV_DERR_NO_PAGES);
     return false;
   }
@@ -42,7 +43,12 @@ __global__ void __launch_bounds__(256) commit_kernel(LaneDev d, const int* __res
     int ok = n > 0;
     if (ok) {
       const int have = (L + d.page - 1) / d.page, need = (L + n + d.page - 1) / d.page;
-      ok = pop_pages(d, slot, have, need - have);
+      if (L + n > d.max_pos || need > d.max_pages_per_slot) {
+        atomicOr(d.err, SV_DERR_MAX_POS);
+        ok = 0;
+      } else {
+        ok = pop_pages(d, slot, have, need - have);
+      }
     }
     s_n = n;
     s_ok = ok;
@@ -85,7 +91,7 @@ __global__ void append_alloc_kernel(LaneDev d, int slot, unsigned long long rid,
   const int L = d.len[slot];
   const int have = (L + d.page - 1) / d.page, need = (L + n + d.page - 1) / d.page;
   int ok = 1;
-  if (need > d.max_pages_per_slot) { atomicOr(d.err, SV_DERR_NO_PAGES); ok = 0; }
+  if (L + n > d.max_pos || need > d.max_pages_per_slot) { atomicOr(d.err, SV_DERR_MAX_POS); ok = 0; }
   if (ok) ok = pop_pages(d, slot, have, need - have);
   int pend = pending_dev ? *pending_dev : pending;
   if (pend < 0 || pend >= d.V) { atomicOr(d.err, SV_DERR_BAD_TOKEN); pend = 0; }

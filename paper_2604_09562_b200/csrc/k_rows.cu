@@ -56,8 +56,13 @@ __global__ void plan_kernel(LaneDev d, PlanArgs p, const int* __restrict__ draft
       atomicOr(&s_err[b], 1);
       tok = 0;
     }
+    int pos = d.len[slot] + j;
+    if (pos >= d.max_pos) {                      // chain would run past the position table
+      atomicOr(&s_err[b], 2);
+      pos = d.max_pos - 1;                       // keep every read in range; the request is not committed
+    }
     d.row_req[r] = b;
-    d.row_pos[r] = d.len[slot] + j;
+    d.row_pos[r] = pos;
     d.chain_tok[r] = tok;
   }
   if (attn) {
@@ -76,7 +81,8 @@ __global__ void plan_kernel(LaneDev d, PlanArgs p, const int* __restrict__ draft
   __syncthreads();
   for (int b = threadIdx.x; b < B; b += blockDim.x) {
     d.req_err[b] = s_err[b];
-    if (s_err[b]) atomicOr(d.err, SV_DERR_BAD_TOKEN);
+    if (s_err[b] & 1) atomicOr(d.err, SV_DERR_BAD_TOKEN);
+    if (s_err[b] & 2) atomicOr(d.err, SV_DERR_MAX_POS);
   }
 }
 
@@ -199,7 +205,7 @@ cudaError_t launch_swiglu_epilogue(const LaneDev& d, int T, cudaStream_t s) {
 }
 
 // ------------------------------------------------------------------ a5: vocab-tile statistics
-// One warp per (row, 256-wide tile): m = max(l * inv_temp), s = sum exp(l * inv_temp - m),
+// One warp per (row, kVocabTile-wide tile): m = max(l * inv_temp), s = sum exp(l * inv_temp - m),
 // argmax = lowest index attaining the max of l * inv_temp.
 __global__ void tile_stats_kernel(LaneDev d, int T, float inv_temp) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;

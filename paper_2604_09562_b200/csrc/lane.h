@@ -11,7 +11,7 @@ typedef __nv_bfloat16 bf16;
 
 constexpr int kMaxBatch = 256;     // PlanArgs capacity (requests per verify)
 constexpr int kMaxDepth = 32;      // k_i <= 32 (sv_lane_stats histograms have 33 bins)
-constexpr int kVocabTile = 256;    // lm-head epilogue statistics tile
+constexpr int kVocabTile = 128;    // lm-head epilogue statistics tile
 constexpr int kAttnRows = 64;      // max (k+1) * G query rows per (request, kv head)
 constexpr int kSplitKeys = 1024;   // page keys per split-KV work item
 constexpr int kNumStats = 6 + 3 * (kMaxDepth + 1);

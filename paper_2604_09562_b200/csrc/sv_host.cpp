@@ -126,7 +126,7 @@ static const char* kStageNames[ST_NUM] = {"plan", "embed_norm", "qkv_rope", "att
                                           "finalize", "commit", "draft", "attn_norm"};
 
 struct Prof {
-  bool on = false;
+  uint32_t mask = 0;                          // bit i: time stage i
   std::vector<cudaEvent_t> free_ev;
   struct Rec { int stage; cudaEvent_t a, b; };
   std::vector<Rec> recs;
@@ -163,34 +163,43 @@ struct sv_ctx {
   Prof prof;
 };
 
-static cudaEvent_t prof_begin(sv_ctx* c) {
-  if (!c->prof.on) return nullptr;
+static cudaEvent_t prof_begin(sv_ctx* c, int stage) {
+  if (!(c->prof.mask >> stage & 1u)) return nullptr;
   cudaEvent_t e = c->prof.get();
   cudaEventRecord(e, c->stream);
   return e;
+}
+// fold finished records into the totals; never blocks the host (a blocking fold would drain
+// the stream and put bubbles into the very region being timed)
+static void prof_fold(sv_ctx* c, bool wait) {
+  size_t keep = 0;
+  auto& recs = c->prof.recs;
+  for (size_t i = 0; i < recs.size(); ++i) {
+    auto& r = recs[i];
+    if (!wait && cudaEventQuery(r.b) != cudaSuccess) {
+      recs[keep++] = r;
+      continue;
+    }
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, r.a, r.b);
+    c->prof.ms[r.stage] += ms;
+    c->prof.n[r.stage] += 1;
+    c->prof.free_ev.push_back(r.a);
+    c->prof.free_ev.push_back(r.b);
+  }
+  recs.resize(keep);
 }
 static void prof_end(sv_ctx* c, int stage, cudaEvent_t a) {
   if (!a) return;
   cudaEvent_t b = c->prof.get();
   cudaEventRecord(b, c->stream);
   c->prof.recs.push_back({stage, a, b});
-  if (c->prof.recs.size() > 4096) {          // fold old records to bound memory
-    cudaEventSynchronize(b);
-    for (auto& r : c->prof.recs) {
-      float ms = 0.f;
-      cudaEventElapsedTime(&ms, r.a, r.b);
-      c->prof.ms[r.stage] += ms;
-      c->prof.n[r.stage] += 1;
-      c->prof.free_ev.push_back(r.a);
-      c->prof.free_ev.push_back(r.b);
-    }
-    c->prof.recs.clear();
-  }
+  if (c->prof.recs.size() >= 8192 && c->prof.recs.size() % 1024 == 0) prof_fold(c, false);
 }
 // run `expr` (returning sv_status or cudaError_t) as timed stage `id`
 #define STAGE(c, id, expr)                    \
   do {                                        \
-    cudaEvent_t _pe = prof_begin(c);          \
+    cudaEvent_t _pe = prof_begin(c, id);      \
     auto _r = (expr);                         \
     prof_end(c, id, _pe);                     \
     if (_r) return stage_status(_r);          \
@@ -364,6 +373,11 @@ sv_status sv_destroy(sv_ctx* c) {
   if (!c) return SV_EINVAL;
   cudaStreamSynchronize(c->stream);
   sv::gemm_plan_destroy(c->gemm);
+  for (auto e : c->prof.free_ev) cudaEventDestroy(e);
+  for (auto& r : c->prof.recs) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
   delete c;
   return SV_OK;
 }
@@ -630,9 +644,15 @@ size_t sv_kv_packed_bytes(const sv_config* cfg, int32_t n_tokens) {
   return (size_t)cfg->n_layers * n_tokens * 2 * cfg->n_kv_heads * cfg->head_dim * 2 + 16;
 }
 
-sv_status sv_profile_enable(sv_ctx* c, int on) {
+sv_status sv_profile_enable(sv_ctx* c, int32_t stage_mask) {
   if (!c) return SV_EINVAL;
-  c->prof.on = on != 0;
+  c->prof.mask = (uint32_t)stage_mask;
+  // create the events up front: cudaEventCreate inside a timed region costs host time
+  while (stage_mask && c->prof.free_ev.size() < 4096) {
+    cudaEvent_t e;
+    SV_CUDA(cudaEventCreate(&e));
+    c->prof.free_ev.push_back(e);
+  }
   return SV_OK;
 }
 
@@ -643,15 +663,7 @@ const char* sv_profile_stage_name(int32_t i) { return (i >= 0 && i < ST_NUM) ? k
 sv_status sv_profile_read(sv_ctx* c, double* ms_total, int64_t* count, int32_t n, int reset) {
   if (!c || !ms_total || !count || n < ST_NUM) return SV_EINVAL;
   SV_CUDA(cudaStreamSynchronize(c->stream));
-  for (auto& r : c->prof.recs) {
-    float ms = 0.f;
-    cudaEventElapsedTime(&ms, r.a, r.b);
-    c->prof.ms[r.stage] += ms;
-    c->prof.n[r.stage] += 1;
-    c->prof.free_ev.push_back(r.a);
-    c->prof.free_ev.push_back(r.b);
-  }
-  c->prof.recs.clear();
+  prof_fold(c, true);
   for (int i = 0; i < ST_NUM; ++i) {
     ms_total[i] = c->prof.ms[i];
     count[i] = c->prof.n[i];

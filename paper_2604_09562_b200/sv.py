@@ -111,7 +111,7 @@ def load():
         "sv_kv_recv_append": ([vp, i32, u64, i32, vp, ctypes.c_int, vp], ctypes.c_int),
         "sv_kv_packed_bytes": ([P(Config), i32], sz),
         "sv_kv_pack": ([vp, vp, i32, i32, i32, i32, i32, vp, vp], ctypes.c_int),
-        "sv_profile_enable": ([vp, ctypes.c_int], ctypes.c_int),
+        "sv_profile_enable": ([vp, ctypes.c_int32], ctypes.c_int),
         "sv_profile_num_stages": ([], i32),
         "sv_profile_stage_name": ([i32], ctypes.c_char_p),
         "sv_profile_read": ([vp, P(ctypes.c_double), P(ctypes.c_int64), i32, ctypes.c_int], ctypes.c_int),
@@ -267,7 +267,15 @@ class Lane:
 
     # ------------------------------------------------------------------ measurement hooks
     def profile(self, on=True):
-        _check(self.lib.sv_profile_enable(self.ctx, 1 if on else 0), "sv_profile_enable")
+        """on: True (all stages), False (off) or an iterable of stage names."""
+        if on is True or on is False:
+            mask = -1 if on else 0
+        else:
+            names = [self.lib.sv_profile_stage_name(i).decode() for i in range(self.lib.sv_profile_num_stages())]
+            mask = 0
+            for n in on:
+                mask |= 1 << names.index(n)
+        _check(self.lib.sv_profile_enable(self.ctx, mask), "sv_profile_enable")
 
     def profile_read(self, reset=True):
         """{stage: (total_ms, launches)} since the last reset (syncs the stream)."""

@@ -21,7 +21,7 @@ for name, (M, N, K) in shapes.items():
     c = torch.empty(M, N, device="cuda")
     ref = a.float() @ b.float().T
     res = {}
-    for var, label in ((1, "1sm"), (2, "2sm")):
+    for var, label in ((1, "1sm"), (2, "2sm"), (5, "wmaj"), (4, "mma-only"), (6, "w-mma"), (7, "w-noepi"), (8, "w-both")):
         lane.debug_gemm(a, b, c, var)
         torch.cuda.synchronize()
         err = ((c - ref).abs().max() / ref.abs().max()).item()
@@ -33,6 +33,8 @@ for name, (M, N, K) in shapes.items():
         torch.cuda.synchronize()
         us = e0.elapsed_time(e1) / 10 * 1e3
         res[label] = (us, 2 * M * N * K / us / 1e6, err)
+    torch.matmul(a, b.T)
+    torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(10):

@@ -1,4 +1,4 @@
-"""The library's GEMM kernels (tcgen05 1-SM, tcgen05 2-SM cluster pair, SIMT) through the
+"""The library's GEMM kernels (tcgen05 1-SM, tcgen05 2-SM cluster pair, weight-major 2-SM, SIMT) through the
 sv_debug_gemm test hook, against the plain definition C = A B^T evaluated in fp64 on the host.
 
 Inputs are bf16, so products are exact in fp32; only the fp32 accumulation rounds. The bound
@@ -21,7 +21,7 @@ def lane():
     return sv.Lane(cfg, {k: v.cuda() for k, v in w.items()})
 
 
-@pytest.mark.parametrize("variant", [1, 2, 3, 0])
+@pytest.mark.parametrize("variant", [1, 2, 3, 5, 0])
 @pytest.mark.parametrize("M,N,K", [(1, 300, 64), (200, 1000, 4096), (576, 6144, 4096),
                                    (130, 4096 + 64 + 7, 512), (576, 520, 14336)])
 def test_gemm_against_definition(lane, variant, M, N, K):

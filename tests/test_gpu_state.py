@@ -247,3 +247,20 @@ def test_free_list_exhaustion():
     with pytest.raises(sv.SvError) as e:
         S.lane.stats()
     assert e.value.status == sv.SV_ENOKV
+
+
+def test_chain_past_max_pos_is_refused_not_crashed():
+    """A chain that would run past the position table sets SV_DERR_MAX_POS, returns
+    accepted_len = -1 for that request and commits nothing for it; the others are unaffected."""
+    cfg = synth.TOY.with_(max_pos=256)
+    S = Setup(cfg, [253, 100], seed=15)             # chain positions 253..257 > 255
+    d = synth.random_tokens(8, cfg.vocab, seed=4).cuda()
+    acc, _ = S.lane.verify([0, 1], [4, 4], d)
+    S.lane.commit()
+    torch.cuda.synchronize()
+    assert int(acc[0]) == -1 and 0 <= int(acc[1]) <= 4
+    ln = S.lane.tap("len", torch.int32, (cfg.max_slots,)).cpu()
+    assert int(ln[0]) == 253 and int(ln[1]) == 100 + int(acc[1]) + 1
+    with pytest.raises(sv.SvError) as e:
+        S.lane.stats()
+    assert e.value.status == sv.SV_EDEVICE
