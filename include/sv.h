@@ -188,11 +188,13 @@ sv_status sv_stats(sv_ctx* ctx, sv_lane_stats* out, int reset);
  *   "kc","vc" [n_layers][T][Hkv][d_h] bf16 chain K/V   "o" [T][Hq d_h] bf16
  *   "h1" [T][D] f32   "b" [T][D] bf16   "u" [T][F] bf16   "h2" [T][D] f32
  *   "z" [T][D] bf16   "logits" [T][V] f32   "tile_max","tile_sum" [T][nt] f32
- *   "tile_arg" [T][nt] i32 (nt = ceil(V / 256))   "row_off" [batch+1] i32
+ *   "tile_arg" [T][nt] i32 (nt = ceil(V / 128))   "row_off" [batch+1] i32
  *   "rope_cos","rope_sin" [max_pos][d_h/2] f32   "len","pending" [max_slots] i32
  *   "page_table" [max_slots][max_pages_per_slot] i32   "free_top" [1] i32
- * (the "last layer" values when n_layers > 1). sv_set_taps is accepted for
- * ABI compatibility; buffers are always retained. */
+ * (the "last layer" values when n_layers > 1). Every buffer is retained, except
+ * that a greedy sv_verify skips storing "logits" (its decisions read only the
+ * vocab-tile statistics) unless sv_set_taps(ctx, 1) was called or logits_out is
+ * given; sv_set_taps(ctx, 0) (the default) restores that. */
 sv_status sv_set_taps(sv_ctx* ctx, int enable);
 sv_status sv_get_tap(sv_ctx* ctx, const char* name, void** dev_ptr, size_t* bytes);
 

@@ -12,6 +12,7 @@ struct GemmEpi {
   const float* resid_in;   // RESIDUAL: h_in  (fp32 [M][N])
   float* resid_out;        // RESIDUAL: h_out (fp32 [M][N]); may alias resid_in
   float inv_temp;          // LOGITS: statistics are of l * inv_temp
+  bool write_out;          // LOGITS: also store the fp32 logits (tensor-core paths; SIMT always does)
 };
 
 struct GemmPlan;

@@ -235,6 +235,7 @@ cudaError_t gemm_run(GemmPlan* p, const bf16* A, const bf16* B, float* C, int M,
       g.targ = d.tile_arg;
       g.nt = d.nt;
       g.inv_temp = e.inv_temp;
+      if (!e.write_out) g.out = nullptr;
       break;
     default:
       g.kind = GEMM_EPI_NONE;

@@ -146,7 +146,7 @@ __device__ __forceinline__ void sw_epi_logits(const SwEpi& e, const SwTile& tl) 
     for (int i = 0; i < 16; ++i) {
       const int t = t0 + c + i;
       const float l = sw_u2f(r[i]);
-      if (valid && t < g.M && !(g.diag & 8)) g.out[(size_t)t * g.ldo + f] = l;   // diag 8: no logits store
+      if (g.out && valid && t < g.M) g.out[(size_t)t * g.ldo + f] = l;
       x[i] = valid ? l * g.inv_temp : -INFINITY;
     }
     // column max over the warp's 32 rows: one redux per column, result in every lane;

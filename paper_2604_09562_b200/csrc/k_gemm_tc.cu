@@ -240,7 +240,7 @@ __device__ __forceinline__ void epi_logits(const GemmTcArgs& g, const Stage32& s
     s = (m == -INFINITY ? 0.f : s * expf(m - mn)) + cs;
     if (cm > m) am = ca;
     m = mn;
-    stage_write_f32(st, g.out, nullptr, g.ldo, g.M, n, g.N);
+    if (g.out) stage_write_f32(st, g.out, nullptr, g.ldo, g.M, n, g.N);
     if ((c & 3) == 3) {                            // statistics per 128-column vocab tile
       const int tile = n_blk * 2 + (c >> 2);
       if (row < g.M && tile < g.nt) {

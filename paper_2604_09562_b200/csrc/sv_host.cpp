@@ -159,6 +159,7 @@ struct sv_ctx {
   std::vector<int> pending_slots;
   int last_T = 0, last_batch = 0;
   int sticky = 0;
+  bool taps = false;                 // keep every intermediate (fp32 logits included) for sv_get_tap
   sv::GemmPlan* gemm = nullptr;
   Prof prof;
 };
@@ -464,6 +465,9 @@ sv_status sv_verify(sv_ctx* c, int32_t batch, const int32_t* slots, const int32_
   STAGE(c, ST_FINAL_NORM, sv::launch_rmsnorm(d, d.h2, d.final_norm, d.z, T, s));
   sv::GemmEpi e{};
   e.inv_temp = inv_temp;
+  // greedy decisions need only the vocab-tile statistics: the fp32 logits (T x V x 4 bytes)
+  // are stored only when something reads them
+  e.write_out = c->taps || mode != SV_GREEDY || logits_out != nullptr;
   STAGE(c, ST_LM_HEAD, gemm(c, d.z, d.lm_head, d.logits, T, d.V, d.D, sv::EPI_LOGITS, e));
   STAGE(c, ST_FINALIZE, sv::launch_finalize(d, batch, draft_tokens, draft_probs, d.logits, seed, mode, inv_temp,
                                             accepted_len, out_tokens, s));
@@ -551,8 +555,9 @@ sv_status sv_stats(sv_ctx* c, sv_lane_stats* out, int reset) {
 }
 
 sv_status sv_set_taps(sv_ctx* c, int enable) {
-  (void)enable;
-  return c ? SV_OK : SV_EINVAL;
+  if (!c) return SV_EINVAL;
+  c->taps = enable != 0;
+  return SV_OK;
 }
 
 sv_status sv_get_tap(sv_ctx* c, const char* name, void** dev_ptr, size_t* bytes) {

@@ -236,6 +236,10 @@ class Lane:
             _check(r, "sv_stats")
         return st.as_dict()
 
+    def set_taps(self, on=True):
+        """Keep every intermediate (incl. the fp32 logits a greedy verify would skip) for tap()."""
+        _check(self.lib.sv_set_taps(self.ctx, 1 if on else 0), "sv_set_taps")
+
     def tap(self, name, dtype, shape=None):
         """Device tensor viewing the library's buffer `name` (valid until the next verify)."""
         p, nb = ctypes.c_void_p(), ctypes.c_size_t()

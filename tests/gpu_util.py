@@ -33,6 +33,7 @@ class Setup:
                                                                           embed_std=embed_std, std=std)
         self.wd = {k: v.cuda() for k, v in self.w.items()}
         self.lane = sv.Lane(cfg, self.wd)
+        self.lane.set_taps(True)                    # the stage tests read every intermediate
         self.ctx = []
         for i, n in enumerate(ctx_lens):
             k, v = synth.context_kv(cfg, n, seed=1000 + 17 * seed + i)

@@ -264,3 +264,26 @@ def test_chain_past_max_pos_is_refused_not_crashed():
     with pytest.raises(sv.SvError) as e:
         S.lane.stats()
     assert e.value.status == sv.SV_EDEVICE
+
+
+def test_greedy_without_taps_skips_logits_but_decides_the_same():
+    """A greedy verify with taps off does not store the fp32 logits (its decisions read only the
+    vocab-tile statistics); decisions must equal those of a lane that keeps every tap."""
+    cfg = synth.LLAMA.with_(n_layers=1, n_pages=64, max_slots=4, max_batch=4, max_pos=1024)
+    d = synth.random_tokens(4 * 6, cfg.vocab, seed=21).cuda()
+    d2 = synth.random_tokens(4 * 6, cfg.vocab, seed=23).cuda()
+    out = []
+    for taps in (True, False):
+        S = Setup(cfg, [100, 300, 64, 700], seed=22)
+        S.lane.set_taps(taps)
+        acc, tok = S.lane.verify([0, 1, 2, 3], [6, 6, 6, 6], d)
+        a1, t1 = acc.cpu().clone(), tok.cpu().clone()
+        S.lane.commit()
+        lg = S.lane.tap("logits", torch.float32, (4 * 7, cfg.vocab))   # device view (sized by the last T)
+        lg.fill_(float("nan"))
+        acc, tok = S.lane.verify([0, 1, 2, 3], [6, 6, 6, 6], d2)
+        torch.cuda.synchronize()
+        out.append((a1, t1, acc.cpu().clone(), tok.cpu().clone(), bool(torch.isnan(lg).all())))
+    for i in range(4):
+        assert torch.equal(out[0][i], out[1][i])
+    assert not out[0][4] and out[1][4]          # taps on: logits stored; off: untouched
