@@ -43,6 +43,22 @@ def peaks():
         return dict(hbm=6650.0, bf16=1590.0, bf16_sus=1400.0, src="fallback")
 
 
+def ncu_traffic():
+    """DRAM bytes (read + write) per launch of each roofline kernel from the committed
+    `ncu --set full` capture (profiles/<round>_ncu_full.json, newest round), or {}."""
+    import glob
+    files = sorted(glob.glob(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "*_ncu_full.json")))
+    if not files:
+        return {}
+    try:
+        rows = json.load(open(files[-1]))
+    except Exception:
+        return {}
+    names = {"gemm_sw_kernel": "lm_head", "attn_tc2_kernel": "attention"}
+    return {names[r["kernel"]]: {"bytes": int(r["dram_bytes"]), "src": os.path.basename(files[-1])}
+            for r in rows if r.get("kernel") in names}
+
+
 # ------------------------------------------------------------------ clocks sampler
 class Clocks:
     """Samples SM clock and clock-event (throttle) reasons through NVML every 2 ms while the
@@ -190,6 +206,7 @@ def run_gpu(args, wl, rank, world, dev):
     tokens = st["emitted"]
     # ----- roofline of the dominant kernels (live CUDA-event durations, averaged per launch)
     pk = peaks()
+    traffic = ncu_traffic()
     alg = algorithmic(wl, ln, depths[args.warmup])
     kern = {}
     for name, (ms, n) in prof.items():
@@ -201,13 +218,15 @@ def run_gpu(args, wl, rank, world, dev):
     if lm:
         ach = alg["lm_flops"] / (lm["ms_per_launch"] * 1e-3) / 1e12
         roof["lm_head"] = {"bound": "tensor", "achieved": round(ach, 2), "peak": pk["bf16_sus"], "unit": "TFLOP/s",
-                           "frac": round(ach / pk["bf16_sus"], 4), "traffic": None,
+                           "frac": round(ach / pk["bf16_sus"], 4), "traffic": traffic.get("lm_head", {}).get("bytes"),
+                           "traffic_src": traffic.get("lm_head", {}).get("src"),
                            "flops_per_launch": alg["lm_flops"], "us_per_launch": round(lm["ms_per_launch"] * 1e3, 2)}
     if at:
         ach = alg["attn_bytes"] / (at["ms_per_launch"] * 1e-3) / 1e9
         roof["attention"] = {"bound": "hbm", "achieved": round(ach, 1), "peak": pk["hbm"], "unit": "GB/s",
                              "frac": round(ach / pk["hbm"], 4), "frac_of_8tbs": round(ach / 8000.0, 4),
-                             "traffic": None, "bytes_per_launch": alg["attn_bytes"],
+                             "traffic": traffic.get("attention", {}).get("bytes"), "bytes_per_launch": alg["attn_bytes"],
+                             "traffic_src": traffic.get("attention", {}).get("src"),
                              "us_per_launch": round(at["ms_per_launch"] * 1e3, 2)}
     dominant = max(kern.items(), key=lambda kv: kv[1]["ms_per_launch"] * kv[1]["launches"])[0] if kern else None
     # ----- e2e through host buffers (host drafter, pinned H2D drafts, D2H results each step)
