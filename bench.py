@@ -31,6 +31,7 @@ import synth  # noqa: E402
 
 METRIC = "accepted tokens/s (verify step)"
 UNIT = "tokens/s"
+HOST_DRAFTER_STEPS = 10   # e2e variant with the drafter on the host (a full round trip per step)
 PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
 
 
@@ -157,9 +158,10 @@ def run_gpu(args, wl, rank, world, dev):
     cfg = wl.cfg
     B = wl.batch
     total = args.warmup + args.steps
-    depths = depths_for(wl, total + args.e2e_steps, seed=7 + rank)
+    depths = depths_for(wl, total + args.e2e_steps + HOST_DRAFTER_STEPS, seed=7 + rank)
     kmax_rows = B * wl.kmax
-    masks, devtok = synth.planted_masks(total + args.e2e_steps, kmax_rows, wl.alpha, cfg.vocab, seed=9 + rank)
+    masks, devtok = synth.planted_masks(total + args.e2e_steps + HOST_DRAFTER_STEPS, kmax_rows, wl.alpha, cfg.vocab,
+                                        seed=9 + rank)
     masks_d, devtok_d, succ_d = masks.to(dev), devtok.to(dev), succ.to(dev)
     drafts = torch.empty(kmax_rows, dtype=torch.int32, device=dev)
     acc = torch.empty(B, dtype=torch.int32, device=dev)
@@ -229,57 +231,135 @@ def run_gpu(args, wl, rank, world, dev):
                              "traffic_src": traffic.get("attention", {}).get("src"),
                              "us_per_launch": round(at["ms_per_launch"] * 1e3, 2)}
     dominant = max(kern.items(), key=lambda kv: kv[1]["ms_per_launch"] * kv[1]["launches"])[0] if kern else None
-    # ----- e2e through host buffers (host drafter, pinned H2D drafts, D2H results each step)
-    e2e = run_e2e(args, wl, lane, succ, depths, masks, devtok, dev, total) if args.e2e_steps > 0 else None
+    # ----- e2e through host buffers: pinned H2D inputs and D2H results every step (see run_e2e)
+    e2e = e2e_host = None
+    if args.e2e_steps > 0:
+        e2e = run_e2e(args, wl, lane, succ, depths, masks, devtok, dev, total)
+        e2e_host = run_e2e_host_drafter(args, wl, lane, succ, depths, masks, devtok, dev, total + args.e2e_steps,
+                                        HOST_DRAFTER_STEPS)
     return dict(elapsed_ms=elapsed_ms, tokens=tokens, per_step=per_step, prof=kern, roof=roof, dominant=dominant,
-                launches=launches, clocks=clk.summary(), stats=st, e2e=e2e, w=w, succ=succ, reqs=reqs,
+                launches=launches, clocks=clk.summary(), stats=st, e2e=e2e, e2e_host=e2e_host, w=w, succ=succ, reqs=reqs,
                 depths=depths, masks=masks, devtok=devtok, alg=alg)
 
 
 def run_e2e(args, wl, lane, succ, depths, masks, devtok, dev, start):
+    """End to end through the public API, inputs from pinned host memory, results read back
+    every step. The drafter is the device one (`sv_draft_planted`); each step's drafter inputs
+    (deviation mask + replacement tokens) are copied H2D from pinned memory and each step's
+    accepted lengths + emitted tokens are copied D2H into a pinned double buffer and consumed on
+    the host one step later (event-ordered), so host work overlaps the next step's kernels."""
+    cfg = wl.cfg
+    B = wl.batch
+    slots = list(range(B))
+    n = args.e2e_steps
+    kr = B * wl.kmax
+    h_mask = masks[start:start + n].clone().pin_memory()
+    h_dev = devtok[start:start + n].clone().pin_memory()
+    d_mask = [torch.empty(kr, dtype=h_mask.dtype, device=dev) for _ in range(2)]
+    d_dev = [torch.empty(kr, dtype=torch.int32, device=dev) for _ in range(2)]
+    succ_d = succ.to(dev)
+    drafts = torch.empty(kr, dtype=torch.int32, device=dev)
+    acc = torch.empty(B, dtype=torch.int32, device=dev)
+    tok = torch.empty(B, cfg.max_depth + 1, dtype=torch.int32, device=dev)
+    h_acc = [torch.empty(B, dtype=torch.int32).pin_memory() for _ in range(2)]
+    h_tok = [torch.empty(B, cfg.max_depth + 1, dtype=torch.int32).pin_memory() for _ in range(2)]
+    done = [torch.cuda.Event() for _ in range(2)]
+    stream = torch.cuda.current_stream(dev)
+    emitted_host = 0
+
+    def consume(slot):
+        nonlocal emitted_host
+        done[slot].synchronize()
+        a = h_acc[slot].numpy()
+        emitted_host += int((a + 1).sum())
+
+    lane.stats(reset=True)
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    for s_ in range(n):
+        i = start + s_
+        sl = s_ & 1
+        d_mask[sl].copy_(h_mask[s_], non_blocking=True)
+        d_dev[sl].copy_(h_dev[s_], non_blocking=True)
+        lane.draft_planted(slots, depths[i], succ_d, d_mask[sl], d_dev[sl], drafts)
+        lane.verify(slots, depths[i], drafts, None, seed=99 + i, mode=wl.mode, temperature=wl.temperature,
+                    out=(acc, tok))
+        lane.commit()
+        h_acc[sl].copy_(acc, non_blocking=True)
+        h_tok[sl].copy_(tok, non_blocking=True)
+        done[sl].record(stream)
+        if s_ > 0:
+            consume(sl ^ 1)                       # previous step's results, while this step runs
+    consume((n - 1) & 1)
+    el = time.perf_counter() - t0
+    st = lane.stats(reset=True)
+    assert st["emitted"] == emitted_host, (st["emitted"], emitted_host)
+    h2d = kr * (h_mask.element_size() + 4)
+    d2h = B * 4 + B * (cfg.max_depth + 1) * 4
+    return {"value": emitted_host / el, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "steps": n, "ms_per_step": 1e3 * el / n, "drafter": "device (sv_draft_planted), pipelined read-back",
+            "tokens": emitted_host, "seconds": el}
+
+
+def run_e2e_host_drafter(args, wl, lane, succ, depths, masks, devtok, dev, start, n):
+    """Variant with the drafter on the host: each step's drafts depend on the previous step's
+    read-back tokens, so every step is a full host <-> device round trip (no overlap)."""
     cfg = wl.cfg
     B = wl.batch
     slots = list(range(B))
     succ_h = succ.numpy()
+    kmax = wl.kmax
     pend = lane.tap("pending", torch.int32, (cfg.max_slots,))[:B].cpu().numpy().copy()
-    h_drafts = torch.empty(B * wl.kmax, dtype=torch.int32).pin_memory()
+    h_drafts = torch.empty(B * kmax, dtype=torch.int32).pin_memory()
     h_acc = torch.empty(B, dtype=torch.int32).pin_memory()
     h_tok = torch.empty(B, cfg.max_depth + 1, dtype=torch.int32).pin_memory()
-    d_drafts = torch.empty(B * wl.kmax, dtype=torch.int32, device=dev)
+    d_drafts = torch.empty(B * kmax, dtype=torch.int32, device=dev)
     acc = torch.empty(B, dtype=torch.int32, device=dev)
     tok = torch.empty(B, cfg.max_depth + 1, dtype=torch.int32, device=dev)
     lane.stats(reset=True)
     torch.cuda.synchronize(dev)
     h2d = d2h = 0
     t0 = time.perf_counter()
-    for s in range(args.e2e_steps):
-        i = start + s
-        ks = depths[i]
-        m, dt = masks[i].numpy(), devtok[i].numpy()
-        out, off = h_drafts.numpy(), 0
-        for b in range(B):               # host planted drafter on the last emitted token
-            prev = int(pend[b])
-            for j in range(ks[b]):
-                t = int(dt[off + j]) if m[off + j] else int(succ_h[prev])
-                out[off + j] = t
+    for s_ in range(n):
+        i = start + s_
+        ks = np.asarray(depths[i])
+        m = masks[i].numpy().reshape(B, kmax).astype(bool) if all(k == kmax for k in ks) else None
+        dt = devtok[i].numpy()
+        out = h_drafts.numpy()
+        if m is not None:                         # uniform depth: vectorised over requests
+            dt2 = dt.reshape(B, kmax)
+            prev = pend.astype(np.int64)
+            blk = out[:B * kmax].reshape(B, kmax)
+            for j in range(kmax):
+                t = np.where(m[:, j], dt2[:, j], succ_h[prev])
+                blk[:, j] = t
                 prev = t
-            off += ks[b]
-        n = off
-        d_drafts[:n].copy_(h_drafts[:n], non_blocking=True)
-        lane.verify(slots, ks, d_drafts, None, seed=99 + i, mode=wl.mode, temperature=wl.temperature, out=(acc, tok))
+            nd = B * kmax
+        else:
+            mm, off = masks[i].numpy(), 0
+            for b in range(B):
+                prev = int(pend[b])
+                for j in range(ks[b]):
+                    t = int(dt[off + j]) if mm[off + j] else int(succ_h[prev])
+                    out[off + j] = t
+                    prev = t
+                off += ks[b]
+            nd = off
+        d_drafts[:nd].copy_(h_drafts[:nd], non_blocking=True)
+        lane.verify(slots, depths[i], d_drafts, None, seed=99 + i, mode=wl.mode, temperature=wl.temperature,
+                    out=(acc, tok))
         lane.commit()
         h_acc.copy_(acc, non_blocking=True)
         h_tok.copy_(tok, non_blocking=True)
         torch.cuda.current_stream(dev).synchronize()
         a, tk = h_acc.numpy(), h_tok.numpy()
         pend = tk[np.arange(B), a]
-        h2d += n * 4
+        h2d += nd * 4
         d2h += B * 4 + B * (cfg.max_depth + 1) * 4
     el = time.perf_counter() - t0
     st = lane.stats(reset=True)
-    return {"value": st["emitted"] / el, "unit": UNIT, "h2d_bytes_per_step": h2d // args.e2e_steps,
-            "d2h_bytes_per_step": d2h // args.e2e_steps, "steps": args.e2e_steps,
-            "ms_per_step": 1e3 * el / args.e2e_steps}
+    return {"value": st["emitted"] / el, "unit": UNIT, "h2d_bytes_per_step": h2d // n, "d2h_bytes_per_step": d2h // n,
+            "steps": n, "ms_per_step": 1e3 * el / n}
 
 
 # ------------------------------------------------------------------ CPU oracle (baseline / reference arm)
@@ -373,7 +453,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--workload", default="ns")
     ap.add_argument("--impl", default="sv", choices=["sv", "reference"])
-    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--e2e-steps", type=int, default=50)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--detail", action="store_true", help="add per-stage breakdown to the JSON line")
     args = ap.parse_args()
@@ -381,7 +461,7 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    wl = synth.workload(args.workload, steps_budget=args.warmup + args.steps + args.e2e_steps + 8)
+    wl = synth.workload(args.workload, steps_budget=args.warmup + args.steps + args.e2e_steps + HOST_DRAFTER_STEPS + 8)
 
     if args.impl == "reference":
         if rank == 0:
@@ -400,11 +480,13 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         n = torch.tensor([tokens], dtype=torch.float64, device=dev)
         dist.all_reduce(n, op=dist.ReduceOp.SUM)
-        e2 = torch.tensor([res["e2e"]["value"] if res["e2e"] else 0.0], dtype=torch.float64, device=dev)
-        dist.all_reduce(e2, op=dist.ReduceOp.SUM)
         elapsed, tokens = float(t.item()), float(n.item())
-        if res["e2e"]:
-            res["e2e"]["value"] = float(e2.item())
+        if res["e2e"]:                            # whole job: all ranks' tokens / the slowest rank's wall time
+            et = torch.tensor([res["e2e"]["tokens"]], dtype=torch.float64, device=dev)
+            es = torch.tensor([res["e2e"]["seconds"]], dtype=torch.float64, device=dev)
+            dist.all_reduce(et, op=dist.ReduceOp.SUM)
+            dist.all_reduce(es, op=dist.ReduceOp.MAX)
+            res["e2e"]["value"] = float(et.item()) / float(es.item())
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -434,6 +516,7 @@ def main():
         "launches_per_step": round(res["launches"] / args.steps, 2),
         "clocks": res["clocks"],
         "e2e": res["e2e"],
+        "e2e_host_drafter": res.get("e2e_host"),
         "peaks": peaks()["src"],
     }
     if args.detail:

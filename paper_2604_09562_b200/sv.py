@@ -17,7 +17,7 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsv.so")
+LIB_PATH = os.environ.get("SV_LIBSV", os.path.join(_HERE, "libsv.so"))   # override: experiments only
 
 SV_OK, SV_EINVAL, SV_ESTATE, SV_ENOKV, SV_ECUDA, SV_ENCCL, SV_EDEVICE = range(7)
 GREEDY, SAMPLE = 0, 1
