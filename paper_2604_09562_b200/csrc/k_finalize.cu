@@ -47,26 +47,48 @@ __global__ void __launch_bounds__(FIN_THREADS) finalize_kernel(LaneDev d, const 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = FIN_THREADS / 32;
   const size_t V = d.V;
 
-  // 1. combine the vocab-tile statistics of each chain row (warp per row)
+  // 1. combine the vocab-tile statistics of each chain row (warp per row): one online pass,
+  //    loads batched 8 deep per lane so the memory round trips overlap
   for (int j = warp; j <= k; j += nw) {
     const float* tm = d.tile_max + (size_t)(r0 + j) * d.nt;
     const float* ts = d.tile_sum + (size_t)(r0 + j) * d.nt;
     const int* ta = d.tile_arg + (size_t)(r0 + j) * d.nt;
-    float m = -INFINITY;
+    float m = -INFINITY, S = 0.f;
     int am = 0x7fffffff;
-    for (int t = lane; t < d.nt; t += 32) {
-      const float v = tm[t];
-      if (v > m) { m = v; am = ta[t]; }          // t increasing per lane: strict > keeps lowest
+    constexpr int U = 8;
+    for (int t0 = lane; t0 < d.nt; t0 += 32 * U) {
+      float vm[U], vs[U];
+      int va[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int t = t0 + 32 * u;
+        const bool ok = t < d.nt;
+        vm[u] = ok ? tm[t] : -INFINITY;
+        vs[u] = ok ? ts[t] : 0.f;
+        va[u] = ok ? ta[t] : 0x7fffffff;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {                 // t increasing per lane: strict > keeps lowest
+        if (vm[u] > m) {
+          S = (m == -INFINITY ? 0.f : S * expf(m - vm[u])) + vs[u];
+          m = vm[u];
+          am = va[u];
+        } else if (vm[u] != -INFINITY) {
+          S += vs[u] * expf(vm[u] - m);
+        }
+      }
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
       const float om = __shfl_xor_sync(0xffffffffu, m, o);
+      const float oS = __shfl_xor_sync(0xffffffffu, S, o);
       const int oa = __shfl_xor_sync(0xffffffffu, am, o);
-      if (om > m || (om == m && oa < am)) { m = om; am = oa; }
+      const float mn = fmaxf(m, om);
+      const float Sn = (m == -INFINITY ? 0.f : S * expf(m - mn)) + (om == -INFINITY ? 0.f : oS * expf(om - mn));
+      if (om > m || (om == m && oa < am)) am = oa;
+      m = mn;
+      S = Sn;
     }
-    float S = 0.f;
-    for (int t = lane; t < d.nt; t += 32) S += ts[t] * expf(tm[t] - m);
-    S = warp_sum(S);
     if (lane == 0) { s_m[j] = m; s_S[j] = S; s_top[j] = am; }
   }
   __syncthreads();

@@ -122,9 +122,103 @@ __global__ void __launch_bounds__(256) embed_norm_kernel(LaneDev d) {
   for (int i = threadIdx.x; i < d.D; i += 256) d.a[(size_t)r * d.D + i] = f2bf(h[i] * rstd * bf2f(d.attn_norm[i]));
 }
 
+// Vectorised forms (D <= 8192, 16-byte aligned rows): each thread keeps its <= 4 eight-element
+// vectors in registers between the sum of squares and the scaled store (one read of the input).
+__device__ __forceinline__ void bf16x8_to_f32(const uint4& u, float (&x)[8]) {
+  const __nv_bfloat162* p = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 f = __bfloat1622float2(p[i]);
+    x[2 * i] = f.x;
+    x[2 * i + 1] = f.y;
+  }
+}
+__device__ __forceinline__ uint4 f32x8_to_bf16(const float (&x)[8]) {
+  uint4 u;
+  __nv_bfloat162* p = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) p[i] = __floats2bfloat162_rn(x[2 * i], x[2 * i + 1]);
+  return u;
+}
+
+constexpr int kNormMaxVec = 4;   // 4 x 8 elements x 256 threads: D <= 8192
+
+__global__ void __launch_bounds__(256) embed_norm_vec_kernel(LaneDev d) {
+  const int r = blockIdx.x;
+  const int nv = d.D / 8;
+  const uint4* e = reinterpret_cast<const uint4*>(d.embed + (size_t)d.chain_tok[r] * d.D);
+  float4* h = reinterpret_cast<float4*>(d.h0 + (size_t)r * d.D);
+  float x[kNormMaxVec][8];
+  float ss = 0.f;
+#pragma unroll
+  for (int k = 0; k < kNormMaxVec; ++k) {
+    const int v = threadIdx.x + k * 256;
+    if (v < nv) {
+      bf16x8_to_f32(e[v], x[k]);
+      h[2 * v] = make_float4(x[k][0], x[k][1], x[k][2], x[k][3]);
+      h[2 * v + 1] = make_float4(x[k][4], x[k][5], x[k][6], x[k][7]);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) ss += x[k][i] * x[k][i];
+    }
+  }
+  const float rstd = 1.0f / sqrtf(block_sum<256>(ss) / float(d.D) + d.eps);
+  const uint4* gw = reinterpret_cast<const uint4*>(d.attn_norm);
+  uint4* out = reinterpret_cast<uint4*>(d.a + (size_t)r * d.D);
+#pragma unroll
+  for (int k = 0; k < kNormMaxVec; ++k) {
+    const int v = threadIdx.x + k * 256;
+    if (v < nv) {
+      float g[8], y[8];
+      bf16x8_to_f32(gw[v], g);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) y[i] = x[k][i] * rstd * g[i];
+      out[v] = f32x8_to_bf16(y);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) rmsnorm_vec_kernel(const float* __restrict__ x, const bf16* __restrict__ g,
+                                                          bf16* __restrict__ out, int D, float eps) {
+  const int r = blockIdx.x;
+  const int nv = D / 8;
+  const float4* xr = reinterpret_cast<const float4*>(x + (size_t)r * D);
+  float v8[kNormMaxVec][8];
+  float ss = 0.f;
+#pragma unroll
+  for (int k = 0; k < kNormMaxVec; ++k) {
+    const int v = threadIdx.x + k * 256;
+    if (v < nv) {
+      const float4 a = xr[2 * v], b = xr[2 * v + 1];
+      v8[k][0] = a.x; v8[k][1] = a.y; v8[k][2] = a.z; v8[k][3] = a.w;
+      v8[k][4] = b.x; v8[k][5] = b.y; v8[k][6] = b.z; v8[k][7] = b.w;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) ss += v8[k][i] * v8[k][i];
+    }
+  }
+  const float rstd = 1.0f / sqrtf(block_sum<256>(ss) / float(D) + eps);
+  const uint4* gw = reinterpret_cast<const uint4*>(g);
+  uint4* o = reinterpret_cast<uint4*>(out + (size_t)r * D);
+#pragma unroll
+  for (int k = 0; k < kNormMaxVec; ++k) {
+    const int v = threadIdx.x + k * 256;
+    if (v < nv) {
+      float gg[8], y[8];
+      bf16x8_to_f32(gw[v], gg);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) y[i] = v8[k][i] * rstd * gg[i];
+      o[v] = f32x8_to_bf16(y);
+    }
+  }
+}
+
+static bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
+
 cudaError_t launch_embed_norm(const LaneDev& d, int T, cudaStream_t s) {
   SV_COUNT_LAUNCH();
-  embed_norm_kernel<<<T, 256, 0, s>>>(d);
+  if (d.D <= 256 * 8 * kNormMaxVec && aligned16(d.embed) && aligned16(d.attn_norm))
+    embed_norm_vec_kernel<<<T, 256, 0, s>>>(d);
+  else
+    embed_norm_kernel<<<T, 256, 0, s>>>(d);
   return cudaGetLastError();
 }
 
@@ -140,7 +234,10 @@ __global__ void __launch_bounds__(256) rmsnorm_kernel(const float* __restrict__ 
 
 cudaError_t launch_rmsnorm(const LaneDev& d, const float* x, const bf16* g, bf16* out, int T, cudaStream_t s) {
   SV_COUNT_LAUNCH();
-  rmsnorm_kernel<<<T, 256, 0, s>>>(x, g, out, d.D, d.eps);
+  if (d.D <= 256 * 8 * kNormMaxVec && aligned16(g))
+    rmsnorm_vec_kernel<<<T, 256, 0, s>>>(x, g, out, d.D, d.eps);
+  else
+    rmsnorm_kernel<<<T, 256, 0, s>>>(x, g, out, d.D, d.eps);
   return cudaGetLastError();
 }
 
