@@ -136,9 +136,12 @@ cudaError_t launch_attention(const LaneDev& d, int layer, int batch, cudaStream_
 
 // combine split-KV partials: one warp per (chain row, q head); lanes over d_h (float4 each
 // for d_h = 128, float2 for 64). O = sum_s e^(m_s - M) O_s / sum_s e^(m_s - M) l_s, M = max m_s.
+// The loads of up to 8 splits are issued together (one memory round trip per 8 splits), with an
+// online rescale between chunks.
 template <int DH>
 __global__ void __launch_bounds__(256) attn_combine_kernel(LaneDev d, int T) {
   constexpr int V = DH / 32;                       // floats per lane
+  constexpr int MS = 8;
   const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (wid >= T * d.Hq) return;
   const int r = wid / d.Hq, hq = wid % d.Hq;
@@ -146,25 +149,42 @@ __global__ void __launch_bounds__(256) attn_combine_kernel(LaneDev d, int T) {
   const int G = d.Hq / d.Hkv, h = hq / G, g = hq % G, rl = j * G + g;
   const int ns = num_splits(d.len[d.slots[b]]);
   const int base = d.item_start[b] + h * ns;
-  float M = -INFINITY;
-  for (int s = 0; s < ns; ++s) M = fmaxf(M, d.part_ml[((size_t)(base + s) * kAttnRows + rl) * 2]);
-  float l = 0.f, o[V];
+  float M = -INFINITY, l = 0.f, o[V];
 #pragma unroll
   for (int i = 0; i < V; ++i) o[i] = 0.f;
-  for (int s = 0; s < ns; ++s) {
-    const size_t it = base + s;
-    const float2 ml = *reinterpret_cast<const float2*>(d.part_ml + (it * kAttnRows + rl) * 2);
-    if (ml.x == -INFINITY) continue;
-    const float w = expf(ml.x - M);
-    l += ml.y * w;
-    const float* src = d.part_o + (it * kAttnRows + rl) * DH + lane * V;
-    if constexpr (V == 4) {
-      const float4 v = *reinterpret_cast<const float4*>(src);
-      o[0] += v.x * w; o[1] += v.y * w; o[2] += v.z * w; o[3] += v.w * w;
-    } else {
-      const float2 v = *reinterpret_cast<const float2*>(src);
-      o[0] += v.x * w; o[1] += v.y * w;
+  for (int s0 = 0; s0 < ns; s0 += MS) {
+    float2 ml[MS];
+    float v[MS][V];
+#pragma unroll
+    for (int k = 0; k < MS; ++k) {
+      const int s = s0 + k;
+      const size_t it = (size_t)(base + s) * kAttnRows + rl;
+      ml[k] = s < ns ? *reinterpret_cast<const float2*>(d.part_ml + it * 2) : make_float2(-INFINITY, 0.f);
+      const float* src = d.part_o + it * DH + lane * V;
+      if constexpr (V == 4) {
+        const float4 x = s < ns ? *reinterpret_cast<const float4*>(src) : make_float4(0.f, 0.f, 0.f, 0.f);
+        v[k][0] = x.x; v[k][1] = x.y; v[k][2] = x.z; v[k][3] = x.w;
+      } else {
+        const float2 x = s < ns ? *reinterpret_cast<const float2*>(src) : make_float2(0.f, 0.f);
+        v[k][0] = x.x; v[k][1] = x.y;
+      }
     }
+    float Mn = M;
+#pragma unroll
+    for (int k = 0; k < MS; ++k) Mn = fmaxf(Mn, ml[k].x);
+    if (Mn == -INFINITY) continue;
+    const float sc = M == -INFINITY ? 0.f : expf(M - Mn);
+    l *= sc;
+#pragma unroll
+    for (int i = 0; i < V; ++i) o[i] *= sc;
+#pragma unroll
+    for (int k = 0; k < MS; ++k) {
+      const float w = ml[k].x == -INFINITY ? 0.f : expf(ml[k].x - Mn);
+      l += ml[k].y * w;
+#pragma unroll
+      for (int i = 0; i < V; ++i) o[i] += v[k][i] * w;
+    }
+    M = Mn;
   }
   const float inv = 1.0f / l;
   bf16* dst = d.o + (size_t)r * d.Hq * DH + (size_t)hq * DH + lane * V;

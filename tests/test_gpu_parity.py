@@ -239,7 +239,14 @@ def test_llama_shape_stages():
     drafts = synth.random_tokens(sum(depths), cfg.vocab, seed=10)
     rep, _, _ = run_and_check(S, slots, depths, drafts, "greedy")
     print("llama greedy", rep)
-    S.lane.commit()
-    # second step, sampled with dense q, on the committed state (cache lengths advanced)
-    for b, s_ in enumerate(slots):
-        pass
+
+
+def test_llama_long_contexts_split_kv():
+    """Contexts of 1..5 split-KV work items (1024 page keys each) per (request, kv head): the
+    keys-on-lanes kernel merges the splits' partials in-kernel (last split to finish)."""
+    cfg = synth.LLAMA.with_(n_pages=256, max_slots=4, max_batch=4, max_pos=6144)
+    S = Setup(cfg, [2100, 4200, 1030, 3000], seed=11)
+    slots, depths = [0, 1, 2, 3], [8, 3, 5, 0]
+    drafts = synth.random_tokens(sum(depths), cfg.vocab, seed=12)
+    rep, _, _ = run_and_check(S, slots, depths, drafts, "greedy")
+    print("llama long contexts", rep)
