@@ -28,6 +28,7 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 import synth  # noqa: E402
+from paper_2604_09562_b200 import dist as svdist  # noqa: E402
 
 METRIC = "accepted tokens/s (verify step)"
 UNIT = "tokens/s"
@@ -129,7 +130,7 @@ def build_lane(wl, rank, dev):
     for i, n in enumerate(ctx):
         k, v = synth.context_kv(cfg, n, seed=10_000 * (rank + 1) + i)
         pend = int(synth.random_tokens(1, cfg.vocab, seed=20_000 * (rank + 1) + i)[0])
-        rid = (rank << 32) | (i + 1)
+        rid = svdist.request_id(rank, i)
         lane.append_kv(i, rid, k.to(dev), v.to(dev), pend)
         reqs.append(dict(L=n, rid=rid, pending=pend, k=k, v=v))
     torch.cuda.synchronize(dev)
@@ -475,18 +476,11 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
     res = run_gpu(args, wl, rank, world, dev)
     elapsed, tokens = res["elapsed_ms"], res["tokens"]
-    if world > 1:
-        t = torch.tensor([elapsed], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        n = torch.tensor([tokens], dtype=torch.float64, device=dev)
-        dist.all_reduce(n, op=dist.ReduceOp.SUM)
-        elapsed, tokens = float(t.item()), float(n.item())
-        if res["e2e"]:                            # whole job: all ranks' tokens / the slowest rank's wall time
-            et = torch.tensor([res["e2e"]["tokens"]], dtype=torch.float64, device=dev)
-            es = torch.tensor([res["e2e"]["seconds"]], dtype=torch.float64, device=dev)
-            dist.all_reduce(et, op=dist.ReduceOp.SUM)
-            dist.all_reduce(es, op=dist.ReduceOp.MAX)
-            res["e2e"]["value"] = float(et.item()) / float(es.item())
+    if world > 1:                                 # whole job: all ranks' tokens / the slowest rank's time
+        elapsed, tokens = svdist.reduce_region(elapsed, tokens, device=dev)
+        if res["e2e"]:
+            es, et = svdist.reduce_region(res["e2e"]["seconds"], res["e2e"]["tokens"], device=dev)
+            res["e2e"]["value"] = et / es
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()

@@ -256,6 +256,18 @@ sv_status sv_kv_recv_append(sv_ctx* ctx, int32_t slot, uint64_t request_id, int3
                             void* staging, int peer, void* nccl_comm);
 size_t sv_kv_packed_bytes(const sv_config* cfg, int32_t n_tokens);
 
+/* Append a hand-off message that is already in device memory (same-GPU prefill, or a
+ * caller-side transport): kv_packed in the wire format above, n_tokens entries, the
+ * pending token from its trailer. sv_append_kv semantics and errors. */
+sv_status sv_kv_append_packed(sv_ctx* ctx, int32_t slot, uint64_t request_id, int32_t n_tokens,
+                              const void* kv_packed);
+
+/* Transport self-test on one GPU: inside one NCCL group, send kv_packed to this rank
+ * and receive it into `staging`, then append it to `slot` (sv_kv_recv_append's path
+ * with peer = own rank). nccl_comm: a communicator in which this process is `rank`. */
+sv_status sv_kv_loopback_append(sv_ctx* ctx, int32_t slot, uint64_t request_id, int32_t n_tokens,
+                                const void* kv_packed, void* staging, int rank, void* nccl_comm);
+
 /* Pack context K/V [n_layers][n][H_kv][d_h] (two tensors) + pending into the
  * hand-off wire format on `stream` (used by the prefill side). */
 sv_status sv_kv_pack(const void* k, const void* v, int32_t n_layers, int32_t n_kv_heads,

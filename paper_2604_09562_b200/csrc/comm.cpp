@@ -75,4 +75,25 @@ sv_status sv_kv_recv_append(sv_ctx* ctx, int32_t slot, uint64_t request_id, int3
   return sv_internal_append_packed(ctx, slot, request_id, staging, n_tokens);
 }
 
+sv_status sv_kv_append_packed(sv_ctx* ctx, int32_t slot, uint64_t request_id, int32_t n_tokens,
+                              const void* kv_packed) {
+  if (!ctx || !kv_packed || n_tokens < 0 || ((uintptr_t)kv_packed & 15)) return SV_EINVAL;
+  return sv_internal_append_packed(ctx, slot, request_id, kv_packed, n_tokens);
+}
+
+sv_status sv_kv_loopback_append(sv_ctx* ctx, int32_t slot, uint64_t request_id, int32_t n_tokens,
+                                const void* kv_packed, void* staging, int rank, void* nccl_comm) {
+  if (!ctx || !kv_packed || !staging || !nccl_comm || n_tokens < 0 || rank < 0) return SV_EINVAL;
+  if (((uintptr_t)kv_packed | (uintptr_t)staging) & 15) return SV_EINVAL;
+  const size_t bytes = sv_internal_packed_bytes(ctx, n_tokens);
+  cudaStream_t st = sv_internal_stream(ctx);
+  sv_status s = nccl_ok(ncclGroupStart());
+  if (s) return s;
+  sv_status s1 = nccl_ok(ncclSend(kv_packed, bytes, ncclUint8, rank, (ncclComm_t)nccl_comm, st));
+  sv_status s2 = nccl_ok(ncclRecv(staging, bytes, ncclUint8, rank, (ncclComm_t)nccl_comm, st));
+  sv_status s3 = nccl_ok(ncclGroupEnd());
+  if (s1 || s2 || s3) return s1 ? s1 : (s2 ? s2 : s3);
+  return sv_internal_append_packed(ctx, slot, request_id, staging, n_tokens);
+}
+
 }  // extern "C"

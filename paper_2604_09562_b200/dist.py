@@ -1,0 +1,44 @@
+"""Host logic of the multi-lane (multi-GPU) path.
+
+Requests shard across decode lanes, one process per GPU, with no collective inside the verify
+step (outputs are lane-count invariant: every draw is keyed by the request id). The collectives
+here are all off the data path: the max-over-ranks timing / total-token reduction of a measured
+region, and the broadcast of the NCCL unique id that sets up a hand-off communicator (a9).
+Works with any torch.distributed backend (NCCL on the GPU box, gloo in the CPU tests).
+"""
+import torch
+import torch.distributed as dist
+
+
+def shard(n_global, rank, world):
+    """Contiguous block partition of n_global requests over `world` lanes; lane `rank`'s indices."""
+    base, extra = divmod(n_global, world)
+    lo = rank * base + min(rank, extra)
+    return list(range(lo, lo + base + (1 if rank < extra else 0)))
+
+
+def request_id(rank, i):
+    """Globally unique request id of the i-th request of lane `rank` (the Philox key)."""
+    return (int(rank) << 32) | (int(i) + 1)
+
+
+def reduce_region(elapsed, tokens, device=None, group=None):
+    """(max elapsed over ranks, total tokens over ranks) of a timed region; identity when not
+    initialised. elapsed in any time unit; the job's throughput is tokens / elapsed."""
+    if not (dist.is_available() and dist.is_initialized()):
+        return float(elapsed), float(tokens)
+    t = torch.tensor([float(elapsed)], dtype=torch.float64, device=device)
+    n = torch.tensor([float(tokens)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    dist.all_reduce(n, op=dist.ReduceOp.SUM, group=group)
+    return float(t.item()), float(n.item())
+
+
+def broadcast_bytes(payload, src, nbytes, device=None, group=None):
+    """Broadcast a fixed-size byte string (e.g. the 128-byte NCCL unique id) from rank `src`."""
+    buf = torch.zeros(nbytes, dtype=torch.uint8, device=device)
+    if dist.get_rank(group) == src:
+        assert payload is not None and len(payload) == nbytes
+        buf.copy_(torch.frombuffer(bytearray(payload), dtype=torch.uint8))
+    dist.broadcast(buf, src=src, group=group)
+    return bytes(buf.cpu().numpy().tobytes())

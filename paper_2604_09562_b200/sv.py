@@ -28,7 +28,8 @@ EXPORTED = [
     "sv_verify_logits", "sv_commit", "sv_release", "sv_stats", "sv_set_taps", "sv_get_tap", "sv_debug_uniforms",
     "sv_draft_planted", "sv_nccl_unique_id", "sv_nccl_comm_init", "sv_nccl_comm_destroy", "sv_kv_send",
     "sv_kv_recv_append", "sv_kv_packed_bytes", "sv_kv_pack", "sv_profile_enable", "sv_profile_num_stages",
-    "sv_profile_stage_name", "sv_profile_read", "sv_launch_count", "sv_debug_gemm",
+    "sv_profile_stage_name", "sv_profile_read", "sv_launch_count", "sv_debug_gemm", "sv_kv_append_packed",
+    "sv_kv_loopback_append",
 ]
 
 
@@ -109,6 +110,8 @@ def load():
         "sv_nccl_comm_destroy": ([vp], ctypes.c_int),
         "sv_kv_send": ([vp, i32, i32, i32, i32, ctypes.c_int, vp, vp], ctypes.c_int),
         "sv_kv_recv_append": ([vp, i32, u64, i32, vp, ctypes.c_int, vp], ctypes.c_int),
+        "sv_kv_append_packed": ([vp, i32, u64, i32, vp], ctypes.c_int),
+        "sv_kv_loopback_append": ([vp, i32, u64, i32, vp, vp, ctypes.c_int, vp], ctypes.c_int),
         "sv_kv_packed_bytes": ([P(Config), i32], sz),
         "sv_kv_pack": ([vp, vp, i32, i32, i32, i32, i32, vp, vp], ctypes.c_int),
         "sv_profile_enable": ([vp, ctypes.c_int32], ctypes.c_int),
@@ -293,6 +296,13 @@ class Lane:
     def kv_recv_append(self, slot, request_id, n_tokens, staging, peer, comm):
         _check(self.lib.sv_kv_recv_append(self.ctx, slot, request_id, n_tokens, _ptr(staging), peer, comm),
                "sv_kv_recv_append")
+
+    def kv_append_packed(self, slot, request_id, n_tokens, packed):
+        _check(self.lib.sv_kv_append_packed(self.ctx, slot, request_id, n_tokens, _ptr(packed)), "sv_kv_append_packed")
+
+    def kv_loopback_append(self, slot, request_id, n_tokens, packed, staging, rank, comm):
+        _check(self.lib.sv_kv_loopback_append(self.ctx, slot, request_id, n_tokens, _ptr(packed), _ptr(staging), rank,
+                                              comm), "sv_kv_loopback_append")
 
     def packed_bytes(self, n_tokens):
         return int(self.lib.sv_kv_packed_bytes(ctypes.byref(self.cfg), n_tokens))
