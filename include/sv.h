@@ -274,6 +274,49 @@ sv_status sv_kv_pack(const void* k, const void* v, int32_t n_layers, int32_t n_k
                      int32_t head_dim, int32_t n_tokens, int32_t pending_token, void* kv_packed,
                      sv_stream_t stream);
 
+/* ---------------- SpecuStream depth controller (NEXT-1; host code, no device work) ----------------
+ * PAPER.md §3.5, Alg. 4 "SpecuStream Adaptation", eq:acceptance_gradient ..
+ * eq_exponential_smoothing, readings DESIGN.md R21-R24. One sv_flow_state per
+ * decode lane; value-in / value-out (the input state is never modified). All structs are host. */
+#define SV_SPEC_MAX_H 64
+typedef struct {
+  double d_base;                 /* baseline depth (5) */
+  double gamma;                  /* amplification (5) */
+  double d_min, d_max;           /* clip range (2, 20) */
+  int32_t h;                     /* flow-vector length, 1..SV_SPEC_MAX_H (10) */
+  int32_t projection_source;     /* 0: t_proj from the measured t (Alg. 4); 1: from tau_recent */
+  double tau_target;             /* target throughput, tokens/s (400) */
+  double micro_batch_numerator;  /* 16 * 5 = 80 (eq:microbatch_size) */
+} sv_spec_config;
+typedef struct {
+  double f[SV_SPEC_MAX_H];       /* flow vector (first h entries used) */
+  int32_t idx;                   /* next write index, 0..h-1 */
+  int32_t _pad;
+  double tau_recent;             /* smoothed throughput, tokens/s */
+} sv_flow_state;
+typedef struct {
+  int32_t depth;                 /* d* = round-half-up(clip(d, d_min, d_max)) */
+  int32_t micro_batch;           /* max(1, floor(numerator / d*)) */
+  double projected;              /* t_proj */
+  double raw_depth, delta, mag, scale, adj;   /* intermediates (audit) */
+} sv_spec_plan;
+
+/* Paper defaults (d_base 5, gamma 5, d_min 2, d_max 20, h 10, tau_target 400, numerator 80). */
+void sv_spec_default_config(sv_spec_config* cfg);
+/* f = 0, idx = 0, tau_recent = tau_target. EINVAL on an invalid cfg
+ * (need 1 <= d_min <= d_base <= d_max, 1 <= h <= SV_SPEC_MAX_H, gamma >= 0, tau_target > 0). */
+sv_status sv_spec_reset(const sv_spec_config* cfg, sv_flow_state* state);
+/* One Alg. 4 step on (a, l, t): a acceptance in [0,1], l load in [0,1], t throughput >= 0.
+ * Writes *plan and *out (out may alias in). EINVAL on invalid cfg / state / inputs. */
+sv_status sv_spec_adapt(const sv_spec_config* cfg, const sv_flow_state* in, double a, double l, double t,
+                        sv_spec_plan* plan, sv_flow_state* out);
+/* The lane's control step (R24): from two sv_stats snapshots taken `seconds` apart,
+ * a = (accepted1 - accepted0) / (drafted1 - drafted0) (0 when nothing was drafted),
+ * t = (emitted1 - emitted0) / seconds, l = active / max_batch; then sv_spec_adapt. */
+sv_status sv_spec_step(const sv_spec_config* cfg, const sv_flow_state* in, const sv_lane_stats* s0,
+                       const sv_lane_stats* s1, double seconds, int32_t active, int32_t max_batch,
+                       sv_spec_plan* plan, sv_flow_state* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -29,7 +29,7 @@ EXPORTED = [
     "sv_draft_planted", "sv_nccl_unique_id", "sv_nccl_comm_init", "sv_nccl_comm_destroy", "sv_kv_send",
     "sv_kv_recv_append", "sv_kv_packed_bytes", "sv_kv_pack", "sv_profile_enable", "sv_profile_num_stages",
     "sv_profile_stage_name", "sv_profile_read", "sv_launch_count", "sv_debug_gemm", "sv_kv_append_packed",
-    "sv_kv_loopback_append",
+    "sv_kv_loopback_append", "sv_spec_default_config", "sv_spec_reset", "sv_spec_adapt", "sv_spec_step",
 ]
 
 
@@ -238,6 +238,12 @@ class Lane:
         if check:
             _check(r, "sv_stats")
         return st.as_dict()
+
+    def stats_raw(self, reset=False):
+        """The sv_lane_stats struct itself (for the SpecuStream controller's window deltas)."""
+        st = LaneStats()
+        _check(self.lib.sv_stats(self.ctx, ctypes.byref(st), 1 if reset else 0), "sv_stats")
+        return st
 
     def set_taps(self, on=True):
         """Keep every intermediate (incl. the fp32 logits a greedy verify would skip) for tap()."""
