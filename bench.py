@@ -36,6 +36,12 @@ HOST_DRAFTER_STEPS = 10   # e2e variant with the drafter on the host (a full rou
 PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
 
 
+def _json_default(o):
+    if hasattr(o, "item"):                            # numpy / torch scalars
+        return o.item()
+    raise TypeError(f"not JSON serializable: {type(o).__name__}")
+
+
 def peaks():
     try:
         p = json.load(open(PEAKS_FILE))
@@ -152,6 +158,52 @@ def algorithmic(wl, ctx_lens, depths):
     return dict(T=T, attn_bytes=attn_bytes * cfg.n_layers, lm_flops=lm_flops)
 
 
+class ControlledDepths:
+    """Depths from the SpecuStream controller (NEXT-1, R21-R24): every WINDOW steps the
+    lane's counters (sv_stats) give a = accepted / drafted, t = emitted / seconds and l = 1 (full
+    batch); Alg. 4 in the library returns d*, and all requests of the lane draft min(d*, kmax) tokens
+    until the next window. Per-request planted acceptance follows AR(1) around wl.alpha
+    (SPEC.md:360), so the controller's gradient tracking has a signal to follow."""
+    WINDOW = 8
+
+    def __init__(self, wl, n_steps, seed):
+        from paper_2604_09562_b200 import specustream as sps
+        self.wl, self.B, self.K = wl, wl.batch, wl.kmax
+        self.ctl = sps.Controller()
+        alphas = synth.ar1_alphas(n_steps, self.B, wl.alpha, wl.alpha_sigma, 0.9, seed)
+        self.mreq, self.treq = synth.planted_masks_req(n_steps, self.B, self.K, alphas, wl.cfg.vocab, seed + 1)
+        self.d = min(int(self.ctl.cfg.d_base), self.K)
+        self.depths = [[self.d] * self.B for _ in range(n_steps)]
+        self.masks = torch.zeros(n_steps, self.B * self.K, dtype=torch.uint8).pin_memory()
+        self.devtok = torch.zeros(n_steps, self.B * self.K, dtype=torch.int32).pin_memory()
+        self.trace, self.s0, self.t0 = [], None, 0.0
+
+    def prepare(self, i, masks_d=None, devtok_d=None):
+        """Lay out step i's drafter inputs for the current depth (ragged, request-major)."""
+        d, B = self.d, self.B
+        self.depths[i] = [d] * B
+        self.masks[i, :B * d] = self.mreq[i, :, :d].reshape(-1)
+        self.devtok[i, :B * d] = self.treq[i, :, :d].reshape(-1)
+        if masks_d is not None:
+            masks_d[i].copy_(self.masks[i], non_blocking=True)
+            devtok_d[i].copy_(self.devtok[i], non_blocking=True)
+
+    def restart(self, lane):
+        self.s0, self.t0 = lane.stats_raw(), time.perf_counter()
+
+    def tick(self, lane, i):
+        if (i + 1) % self.WINDOW:
+            return
+        s1, now = lane.stats_raw(), time.perf_counter()
+        if self.s0 is not None:
+            plan = self.ctl.step(self.s0, s1, max(now - self.t0, 1e-9), self.B, self.B)
+            self.d = max(1, min(plan.depth, self.K))
+            self.trace.append({"step": i + 1, "a": round((s1.accepted - self.s0.accepted) /
+                                                         max(1, s1.drafted - self.s0.drafted), 4),
+                               "depth": plan.depth, "raw": round(plan.raw_depth, 4), "mag": round(plan.mag, 5)})
+        self.s0, self.t0 = s1, now
+
+
 def run_gpu(args, wl, rank, world, dev):
     from paper_2604_09562_b200 import sv
     import torch.distributed as dist
@@ -163,6 +215,10 @@ def run_gpu(args, wl, rank, world, dev):
     kmax_rows = B * wl.kmax
     masks, devtok = synth.planted_masks(total + args.e2e_steps + HOST_DRAFTER_STEPS, kmax_rows, wl.alpha, cfg.vocab,
                                         seed=9 + rank)
+    ctl = None
+    if wl.controller:
+        ctl = ControlledDepths(wl, total + args.e2e_steps + HOST_DRAFTER_STEPS, seed=11 + rank)
+        depths, masks, devtok = ctl.depths, ctl.masks, ctl.devtok
     masks_d, devtok_d, succ_d = masks.to(dev), devtok.to(dev), succ.to(dev)
     drafts = torch.empty(kmax_rows, dtype=torch.int32, device=dev)
     acc = torch.empty(B, dtype=torch.int32, device=dev)
@@ -171,6 +227,8 @@ def run_gpu(args, wl, rank, world, dev):
     mode = wl.mode
 
     def step(i):
+        if ctl:
+            ctl.prepare(i, masks_d, devtok_d)
         lane.draft_planted(slots, depths[i], succ_d, masks_d[i], devtok_d[i], drafts)
         lane.verify(slots, depths[i], drafts, None, seed=1234 + i, mode=mode, temperature=wl.temperature,
                     out=(acc, tok))
@@ -178,8 +236,12 @@ def run_gpu(args, wl, rank, world, dev):
 
     for i in range(args.warmup):
         step(i)
+        if ctl:
+            ctl.tick(lane, i)
     torch.cuda.synchronize(dev)
     lane.stats(reset=True)
+    if ctl:
+        ctl.restart(lane)
     # context lengths at the start of the timed region (for the algorithmic attention bytes)
     ln = lane.tap("len", torch.int32, (cfg.max_slots,))[:B].cpu().tolist()
     # only the roofline kernels are bracketed by events in the timed region (every record is a
@@ -197,6 +259,8 @@ def run_gpu(args, wl, rank, world, dev):
         for i in range(args.steps):
             step(args.warmup + i)
             ev[i + 1].record(stream)
+            if ctl:                                   # the control loop reads the counters (syncs)
+                ctl.tick(lane, args.warmup + i)
         torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
@@ -210,7 +274,12 @@ def run_gpu(args, wl, rank, world, dev):
     # ----- roofline of the dominant kernels (live CUDA-event durations, averaged per launch)
     pk = peaks()
     traffic = ncu_traffic()
-    alg = algorithmic(wl, ln, depths[args.warmup])
+    # per-launch algorithmic work averaged over the timed region: mean T over its steps, context
+    # lengths at the region's midpoint (they grow by the emitted tokens)
+    ln1 = lane.tap("len", torch.int32, (cfg.max_slots,))[:B].cpu().tolist()
+    mid = [(x + y) / 2.0 for x, y in zip(ln, ln1)]
+    algs = [algorithmic(wl, mid, depths[args.warmup + i]) for i in range(args.steps)]
+    alg = {k: sum(a[k] for a in algs) / len(algs) for k in algs[0]}
     kern = {}
     for name, (ms, n) in prof.items():
         if n:
@@ -234,13 +303,18 @@ def run_gpu(args, wl, rank, world, dev):
     dominant = max(kern.items(), key=lambda kv: kv[1]["ms_per_launch"] * kv[1]["launches"])[0] if kern else None
     # ----- e2e through host buffers: pinned H2D inputs and D2H results every step (see run_e2e)
     e2e = e2e_host = None
+    if ctl:                                           # later regions draft at the controller's last depth
+        for i in range(total, total + args.e2e_steps + HOST_DRAFTER_STEPS):
+            ctl.prepare(i)
     if args.e2e_steps > 0:
         e2e = run_e2e(args, wl, lane, succ, depths, masks, devtok, dev, total)
         e2e_host = run_e2e_host_drafter(args, wl, lane, succ, depths, masks, devtok, dev, total + args.e2e_steps,
                                         HOST_DRAFTER_STEPS)
     return dict(elapsed_ms=elapsed_ms, tokens=tokens, per_step=per_step, prof=kern, roof=roof, dominant=dominant,
                 launches=launches, clocks=clk.summary(), stats=st, e2e=e2e, e2e_host=e2e_host, w=w, succ=succ, reqs=reqs,
-                depths=depths, masks=masks, devtok=devtok, alg=alg)
+                depths=depths, masks=masks, devtok=devtok, alg=alg,
+                controller=({"window_steps": ControlledDepths.WINDOW, "final_depth": ctl.d, "trace": ctl.trace[-6:]}
+                            if ctl else None))
 
 
 def run_e2e(args, wl, lane, succ, depths, masks, devtok, dev, start):
@@ -443,7 +517,7 @@ def run_reference(args, wl):
             "cpu_baseline": {"value": round(v, 3), "unit": UNIT, "cores": blas_threads(), "kind": "oracle",
                              "sample": f"request 0 of the {wl.name} workload, {args.steps} verify+commit steps"},
             "e2e": {"value": round(v, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    print(json.dumps(line, default=_json_default), flush=True)
 
 
 # ------------------------------------------------------------------ main
@@ -511,6 +585,7 @@ def main():
         "clocks": res["clocks"],
         "e2e": res["e2e"],
         "e2e_host_drafter": res.get("e2e_host"),
+        "controller": res.get("controller"),
         "peaks": peaks()["src"],
     }
     if args.detail:
@@ -518,7 +593,7 @@ def main():
                           for k, v in res["prof"].items()}
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(wl, res)
-    print(json.dumps(line), flush=True)
+    print(json.dumps(line, default=_json_default), flush=True)
     if world > 1:
         dist.destroy_process_group()
 

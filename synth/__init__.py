@@ -172,6 +172,8 @@ class Workload:
     embed_std: float = 8.0
     beta: float = 0.3     # planted-successor strength (logit margin ~ beta * sqrt(D))
     temperature: float = 1.0
+    controller: bool = False   # depths from the SpecuStream controller (NEXT-1) instead of U{kmin..kmax}
+    alpha_sigma: float = 0.0   # per-request acceptance follows AR(1) around alpha with this stationary std
 
 
 def workload(name, steps_budget=64):
@@ -190,7 +192,7 @@ def workload(name, steps_budget=64):
     if name == "c3":          # BASELINE configs[2]: bs128, context 1k-2k, sampled
         n_pages, max_pos = pool(128, 2048, 8)
         cfg = LLAMA.with_(n_pages=n_pages, max_slots=128, max_batch=128, max_pos=max_pos)
-        return Workload("c3", cfg, 128, (1024, 2048), 5, 8, "sample", 0.72)
+        return Workload("c3", cfg, 128, (1024, 2048), 5, 8, "sample", 0.72, controller=True, alpha_sigma=0.10)
     if name == "c4":          # BASELINE configs[3] decode lane: bs32, 8k prompts
         n_pages, max_pos = pool(32, 8192, 8)
         cfg = LLAMA.with_(n_pages=n_pages, max_slots=32, max_batch=32, max_pos=max_pos)
@@ -213,6 +215,30 @@ def planted_masks(n_steps, rows, alpha, vocab, seed):
     g = _gen(seed)
     m = (torch.rand(n_steps, rows, generator=g) >= alpha).to(torch.uint8)
     t = torch.randint(0, vocab, (n_steps, rows), generator=g, dtype=torch.int32)
+    return m, t
+
+
+def ar1_alphas(n_steps, batch, p0, sigma, rho, seed):
+    """Per-request planted acceptance probabilities [n_steps][batch]: AR(1) around p0 with
+    stationary std sigma and coefficient rho ("order-1 autoregressive process"),
+    clipped to [0, 1]."""
+    g = _gen(seed)
+    a = torch.empty(n_steps, batch, dtype=torch.float64)
+    x = p0 + sigma * torch.randn(batch, generator=g, dtype=torch.float64)
+    innov = sigma * (1.0 - rho * rho) ** 0.5
+    for i in range(n_steps):
+        a[i] = x.clamp(0.0, 1.0)
+        x = p0 + rho * (x - p0) + innov * torch.randn(batch, generator=g, dtype=torch.float64)
+    return a
+
+
+def planted_masks_req(n_steps, batch, kmax, alphas, vocab, seed):
+    """Per-step, per-request deviation masks [n_steps][batch][kmax] (1 with probability
+    1 - alphas[step][request]) and replacement tokens of the same shape."""
+    g = _gen(seed)
+    u = torch.rand(n_steps, batch, kmax, generator=g, dtype=torch.float64)
+    m = (u >= alphas[:, :, None]).to(torch.uint8)
+    t = torch.randint(0, vocab, (n_steps, batch, kmax), generator=g, dtype=torch.int32)
     return m, t
 
 
