@@ -8,6 +8,12 @@
 
 namespace sv {
 
+// ---------------------------------------------------------------- programmatic dependent launch
+// (lane.h launch_pdl): wait = every earlier kernel of the stream has finished and its writes are
+// visible; trigger = the next kernel may be scheduled now.
+SV_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+SV_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // ---------------------------------------------------------------- Philox4x32-10
 // Counter-based RNG (north_star "counter-based Philox RNG"); constants of
 // Random123 / cuRAND. Key = (seed_lo, seed_hi); counter =

@@ -142,6 +142,8 @@ template <int DH>
 __global__ void __launch_bounds__(256) attn_combine_kernel(LaneDev d, int T) {
   constexpr int V = DH / 32;                       // floats per lane
   constexpr int MS = 8;
+  pdl_trigger();
+  pdl_wait();
   const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (wid >= T * d.Hq) return;
   const int r = wid / d.Hq, hq = wid % d.Hq;
@@ -195,9 +197,8 @@ __global__ void __launch_bounds__(256) attn_combine_kernel(LaneDev d, int T) {
 cudaError_t launch_attn_combine(const LaneDev& d, int T, cudaStream_t s) {
   const int warps = T * d.Hq;
   SV_COUNT_LAUNCH();
-  if (d.dh == 128) attn_combine_kernel<128><<<(warps + 7) / 8, 256, 0, s>>>(d, T);
-  else attn_combine_kernel<64><<<(warps + 7) / 8, 256, 0, s>>>(d, T);
-  return cudaGetLastError();
+  if (d.dh == 128) return launch_pdl(attn_combine_kernel<128>, dim3((warps + 7) / 8), dim3(256), 0, s, 1, d, T);
+  return launch_pdl(attn_combine_kernel<64>, dim3((warps + 7) / 8), dim3(256), 0, s, 1, d, T);
 }
 
 }  // namespace sv

@@ -124,6 +124,8 @@ __global__ void __launch_bounds__(THREADS, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0 && ((raw_s & 1023) != 0)) __trap();   // SMEM budget has no alignment slack
+  pdl_trigger();
+  pdl_wait();                                           // n_items, Q, pages: written by earlier kernels
   const int n_items = *d.n_items;
   const int G = d.Hq / d.Hkv;
   const size_t nkv = (size_t)d.Hkv * DH;
@@ -520,8 +522,7 @@ cudaError_t launch_attention_tc2(const CUtensorMap& map_q, const CUtensorMap& ma
     attr = true;
   }
   SV_COUNT_LAUNCH();
-  attn_tc2_kernel<<<num_sms, THREADS, SMEM, s>>>(map_q, map_kv, d, layer);
-  return cudaGetLastError();
+  return launch_pdl(attn_tc2_kernel, dim3(num_sms), dim3(THREADS), SMEM, s, 1, map_q, map_kv, d, layer);
 }
 
 }  // namespace sv

@@ -39,6 +39,8 @@ __global__ void __launch_bounds__(FIN_THREADS) finalize_kernel(LaneDev d, const 
   __shared__ Best s_bestR[FIN_THREADS / 32], s_bestP[FIN_THREADS / 32];
   __shared__ float s_sumR[FIN_THREADS / 32];
 
+  pdl_trigger();
+  pdl_wait();
   const int b = blockIdx.x;
   const int k = d.depths[b], slot = d.slots[b], r0 = d.row_off[b], doff = r0 - b;
   const int L = d.len[slot];
@@ -194,9 +196,8 @@ cudaError_t launch_finalize(const LaneDev& d, int batch, const int* draft_tokens
                             const float* logits, uint64_t seed, int mode, float inv_temp, int* accepted_len,
                             int* out_tokens, cudaStream_t s) {
   SV_COUNT_LAUNCH();
-  finalize_kernel<<<batch, FIN_THREADS, 0, s>>>(d, draft_tokens, draft_probs, logits, seed, mode, inv_temp,
-                                                accepted_len, out_tokens);
-  return cudaGetLastError();
+  return launch_pdl(finalize_kernel, dim3(batch), dim3(FIN_THREADS), 0, s, 1, d, draft_tokens, draft_probs, logits,
+                    seed, mode, inv_temp, accepted_len, out_tokens);
 }
 
 }  // namespace sv

@@ -340,6 +340,12 @@ __global__ void __launch_bounds__(THREADS, 1)
   tc::cluster_sync_all();
   tc::fence_after();
   const uint32_t tmem_base = *tmem_holder;
+  // PDL: everything above overlaps the previous kernel's tail. Weights are never written by the
+  // step, so the producer also prefetches the first tile's weight stages before waiting; every other
+  // global access (tokens, residuals, outputs) comes after pdl_wait.
+  pdl_trigger();
+  const int npre = (g.diag & 1) || cluster >= num_tiles ? 0 : (nk < STAGES ? nk : STAGES);
+  if (warp != 0) pdl_wait();
   if (g.trace && threadIdx.x == 0 && blockIdx.x < 512) g.trace[10 * 256 + blockIdx.x / 2 + (rank ? 128 : 0)] = sw_gtimer();
 
   // Producer and MMA roles run as whole, converged warps with one elected lane issuing: the
@@ -352,26 +358,42 @@ __global__ void __launch_bounds__(THREADS, 1)
     const uint32_t tx = 2u * (A_BYTES + (NT / 2) * BK * 2);
     int stage = 0;
     uint32_t phase = 0;
+    auto load_w = [&](int st, int m_pair, int kb) {
+      const uint32_t fb = tc::smem_u32(&full[st]) & tc::kPeerBitMask;
+      uint8_t* a = sA + st * A_BYTES;
+      if (swiglu) {
+        const int j0 = m_pair * 128 + (int)rank * 64;
+        tc::tma_load_2d_2sm(a, &map_w, fb, kb * BK, j0, pol_w);
+        tc::tma_load_2d_2sm(a + A_BYTES / 2, &map_w, fb, kb * BK, g.F + j0, pol_w);
+      } else {
+        tc::tma_load_2d_2sm(a, &map_w, fb, kb * BK, m_pair * 256 + (int)rank * 128, pol_w);
+      }
+    };
+    // weight stages of the first tile, before the dependency wait (the ring starts empty)
+    if (tc::elect_one()) {
+      for (int kb = 0; kb < npre; ++kb) {
+        if (leader) tc::mbar_arrive_expect_tx(&full[kb], tx);
+        load_w(kb, cluster / n_tok, kb);
+      }
+    }
+    __syncwarp();
+    pdl_wait();
     for (int t = cluster; t < num_tiles; t += n_clusters) {
       const int n_blk = t % n_tok, m_pair = t / n_tok;    // token tiles of one weight tile run together
       const int xrow = n_blk * NT + (int)rank * (NT / 2);
       for (int kb = 0; kb < nk; ++kb) {
         tc::mbar_wait(&empty[stage], phase ^ 1);
         const bool skip = (g.diag & 1) && (kb >= STAGES || t != cluster);   // diagnostic: stale smem
+        const bool pre = t == cluster && kb < npre;       // weights already in flight
         if (tc::elect_one()) {
           if (skip) {
             if (leader) tc::mbar_arrive(&full[stage]);
           } else {
-            if (leader) tc::mbar_arrive_expect_tx(&full[stage], tx);
-            const uint32_t fb = tc::smem_u32(&full[stage]) & tc::kPeerBitMask;
-            uint8_t* a = sA + stage * A_BYTES;
-            if (swiglu) {
-              const int j0 = m_pair * 128 + (int)rank * 64;
-              tc::tma_load_2d_2sm(a, &map_w, fb, kb * BK, j0, pol_w);
-              tc::tma_load_2d_2sm(a + A_BYTES / 2, &map_w, fb, kb * BK, g.F + j0, pol_w);
-            } else {
-              tc::tma_load_2d_2sm(a, &map_w, fb, kb * BK, m_pair * 256 + (int)rank * 128, pol_w);
+            if (!pre) {
+              if (leader) tc::mbar_arrive_expect_tx(&full[stage], tx);
+              load_w(stage, m_pair, kb);
             }
+            const uint32_t fb = tc::smem_u32(&full[stage]) & tc::kPeerBitMask;
             tc::tma_load_2d_2sm(sB + stage * BX_BYTES, &map_x, fb, kb * BK, xrow, pol_x);
           }
         }
@@ -488,20 +510,8 @@ cudaError_t launch_gemm_sw(const CUtensorMap& map_w, const CUtensorMap& map_x, c
   const int num_mp = g.kind == GEMM_EPI_SWIGLU ? g.F / 128 : (g.N + 255) / 256;
   const int num_tiles = num_mp * ((g.M + g.nt_tok - 1) / g.nt_tok);
   const int clusters = num_tiles < num_sms / 2 ? num_tiles : num_sms / 2;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(2 * clusters);
-  cfg.blockDim = dim3(THREADS);
-  cfg.dynamicSmemBytes = SMEM_BYTES;
-  cfg.stream = s;
-  cudaLaunchAttribute attrs[1];
-  attrs[0].id = cudaLaunchAttributeClusterDimension;
-  attrs[0].val.clusterDim.x = 2;
-  attrs[0].val.clusterDim.y = 1;
-  attrs[0].val.clusterDim.z = 1;
-  cfg.attrs = attrs;
-  cfg.numAttrs = 1;
   SV_COUNT_LAUNCH();
-  return cudaLaunchKernelEx(&cfg, gemm_sw_kernel, map_w, map_x, g);
+  return launch_pdl(gemm_sw_kernel, dim3(2 * clusters), dim3(THREADS), SMEM_BYTES, s, 2, map_w, map_x, g);
 }
 
 }  // namespace sv

@@ -30,6 +30,8 @@ SV_DEV bool pop_pages(const LaneDev& d, int slot, int first, int n) {
 
 // ------------------------------------------------------------------ a8 commit
 __global__ void __launch_bounds__(256) commit_kernel(LaneDev d, const int* __restrict__ n_keep) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ int s_n, s_ok;
   const int b = blockIdx.x;
   const int slot = d.slots[b], L = d.len[slot];
@@ -79,8 +81,7 @@ __global__ void __launch_bounds__(256) commit_kernel(LaneDev d, const int* __res
 
 cudaError_t launch_commit(const LaneDev& d, const int* n_keep, int batch, cudaStream_t s) {
   SV_COUNT_LAUNCH();
-  commit_kernel<<<batch, 256, 0, s>>>(d, n_keep);
-  return cudaGetLastError();
+  return launch_pdl(commit_kernel, dim3(batch), dim3(256), 0, s, 1, d, n_keep);
 }
 
 // ------------------------------------------------------------------ append (alloc + copy)

@@ -5,6 +5,8 @@
 //   a5  lm-head vocab-tile statistics (max, sum exp, lowest argmax)
 // plus test / fixture kernels (device Philox uniforms, planted drafter) and
 // lane-state initialisation.
+#include <stdlib.h>
+
 #include "common.cuh"
 #include "lane.h"
 #include "../../include/sv.h"
@@ -13,9 +15,19 @@ namespace sv {
 
 unsigned long long g_launch_count = 0;
 
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("SV_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 // ------------------------------------------------------------------ a1: plan
 // One CTA. Serial prefix over <= 256 requests in thread 0, then parallel fills.
 __global__ void plan_kernel(LaneDev d, PlanArgs p, const int* __restrict__ draft_tokens, int attn) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ int s_off[kMaxBatch + 1];
   __shared__ int s_item[kMaxBatch + 1];
   __shared__ int s_err[kMaxBatch];
@@ -88,8 +100,7 @@ __global__ void plan_kernel(LaneDev d, PlanArgs p, const int* __restrict__ draft
 
 cudaError_t launch_plan(const LaneDev& d, const PlanArgs& p, const int* draft_tokens, bool attn, cudaStream_t s) {
   SV_COUNT_LAUNCH();
-  plan_kernel<<<1, 1024, 0, s>>>(d, p, draft_tokens, attn ? 1 : 0);
-  return cudaGetLastError();
+  return launch_pdl(plan_kernel, dim3(1), dim3(1024), 0, s, 1, d, p, draft_tokens, attn ? 1 : 0);
 }
 
 // ------------------------------------------------------------------ a2: embed + RMSNorm
@@ -108,6 +119,8 @@ __device__ float block_sum(float v) {
 }
 
 __global__ void __launch_bounds__(256) embed_norm_kernel(LaneDev d) {
+  pdl_trigger();
+  pdl_wait();
   const int r = blockIdx.x;
   const int tok = d.chain_tok[r];
   const bf16* e = d.embed + (size_t)tok * d.D;
@@ -144,6 +157,8 @@ __device__ __forceinline__ uint4 f32x8_to_bf16(const float (&x)[8]) {
 constexpr int kNormMaxVec = 4;   // 4 x 8 elements x 256 threads: D <= 8192
 
 __global__ void __launch_bounds__(256) embed_norm_vec_kernel(LaneDev d) {
+  pdl_trigger();
+  pdl_wait();
   const int r = blockIdx.x;
   const int nv = d.D / 8;
   const uint4* e = reinterpret_cast<const uint4*>(d.embed + (size_t)d.chain_tok[r] * d.D);
@@ -179,6 +194,8 @@ __global__ void __launch_bounds__(256) embed_norm_vec_kernel(LaneDev d) {
 
 __global__ void __launch_bounds__(256) rmsnorm_vec_kernel(const float* __restrict__ x, const bf16* __restrict__ g,
                                                           bf16* __restrict__ out, int D, float eps) {
+  pdl_trigger();
+  pdl_wait();
   const int r = blockIdx.x;
   const int nv = D / 8;
   const float4* xr = reinterpret_cast<const float4*>(x + (size_t)r * D);
@@ -216,14 +233,15 @@ static bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
 cudaError_t launch_embed_norm(const LaneDev& d, int T, cudaStream_t s) {
   SV_COUNT_LAUNCH();
   if (d.D <= 256 * 8 * kNormMaxVec && aligned16(d.embed) && aligned16(d.attn_norm))
-    embed_norm_vec_kernel<<<T, 256, 0, s>>>(d);
+    return launch_pdl(embed_norm_vec_kernel, dim3(T), dim3(256), 0, s, 1, d);
   else
-    embed_norm_kernel<<<T, 256, 0, s>>>(d);
-  return cudaGetLastError();
+    return launch_pdl(embed_norm_kernel, dim3(T), dim3(256), 0, s, 1, d);
 }
 
 __global__ void __launch_bounds__(256) rmsnorm_kernel(const float* __restrict__ x, const bf16* __restrict__ g,
                                                       bf16* __restrict__ out, int D, float eps) {
+  pdl_trigger();
+  pdl_wait();
   const int r = blockIdx.x;
   const float* xr = x + (size_t)r * D;
   float ss = 0.f;
@@ -235,10 +253,9 @@ __global__ void __launch_bounds__(256) rmsnorm_kernel(const float* __restrict__ 
 cudaError_t launch_rmsnorm(const LaneDev& d, const float* x, const bf16* g, bf16* out, int T, cudaStream_t s) {
   SV_COUNT_LAUNCH();
   if (d.D <= 256 * 8 * kNormMaxVec && aligned16(g))
-    rmsnorm_vec_kernel<<<T, 256, 0, s>>>(x, g, out, d.D, d.eps);
+    return launch_pdl(rmsnorm_vec_kernel, dim3(T), dim3(256), 0, s, 1, x, g, out, d.D, d.eps);
   else
-    rmsnorm_kernel<<<T, 256, 0, s>>>(x, g, out, d.D, d.eps);
-  return cudaGetLastError();
+    return launch_pdl(rmsnorm_kernel, dim3(T), dim3(256), 0, s, 1, x, g, out, d.D, d.eps);
 }
 
 // ------------------------------------------------------------------ a2: QKV + RoPE epilogue
@@ -370,6 +387,8 @@ cudaError_t launch_debug_uniforms(uint64_t seed, uint64_t rid, uint32_t z, int p
 __global__ void draft_planted_kernel(LaneDev d, PlanArgs p, const int* __restrict__ succ,
                                      const uint8_t* __restrict__ mask, const int* __restrict__ dev_tok,
                                      int* __restrict__ out) {
+  pdl_trigger();
+  pdl_wait();
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= p.batch) return;
   int off = 0;
@@ -386,8 +405,8 @@ __global__ void draft_planted_kernel(LaneDev d, PlanArgs p, const int* __restric
 cudaError_t launch_draft_planted(const LaneDev& d, const PlanArgs& p, const int* succ, const uint8_t* mask,
                                  const int* dev_tok, int* draft_tokens, cudaStream_t s) {
   SV_COUNT_LAUNCH();
-  draft_planted_kernel<<<(p.batch + 127) / 128, 128, 0, s>>>(d, p, succ, mask, dev_tok, draft_tokens);
-  return cudaGetLastError();
+  return launch_pdl(draft_planted_kernel, dim3((p.batch + 127) / 128), dim3(128), 0, s, 1, d, p, succ, mask, dev_tok,
+                    draft_tokens);
 }
 
 // ------------------------------------------------------------------ lane state init

@@ -64,6 +64,38 @@ __host__ __device__ inline int split_t1(int s, int ns, int L, int R) {
 extern unsigned long long g_launch_count;
 #define SV_COUNT_LAUNCH() (++::sv::g_launch_count)
 
+// Programmatic dependent launch (PDL) for the step's kernels: the next kernel in the stream may be
+// scheduled while this one finishes; every kernel calls pdl_wait() (griddepcontrol.wait) before it
+// touches anything an earlier kernel of the step writes, so only its prologue (barrier / TMEM
+// setup, weight prefetch) overlaps. SV_PDL=0 launches them normally.
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              int cluster_x, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  int n = 0;
+  if (pdl_enabled()) {
+    at[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[n].val.programmaticStreamSerializationAllowed = 1;
+    ++n;
+  }
+  if (cluster_x > 1) {
+    at[n].id = cudaLaunchAttributeClusterDimension;
+    at[n].val.clusterDim.x = cluster_x;
+    at[n].val.clusterDim.y = 1;
+    at[n].val.clusterDim.z = 1;
+    ++n;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = n;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 struct PlanArgs {
   int batch, T;
   int slots[kMaxBatch];
