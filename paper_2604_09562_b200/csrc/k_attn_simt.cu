@@ -134,71 +134,79 @@ cudaError_t launch_attention(const LaneDev& d, int layer, int batch, cudaStream_
   return cudaGetLastError();
 }
 
-// combine split-KV partials: one warp per (chain row, q head); lanes over d_h (float4 each
-// for d_h = 128, float2 for 64). O = sum_s e^(m_s - M) O_s / sum_s e^(m_s - M) l_s, M = max m_s.
-// The loads of up to 8 splits are issued together (one memory round trip per 8 splits), with an
-// online rescale between chunks.
+// combine split-KV partials. One CTA per chain row (the row's request, position and split count
+// are looked up once), each warp merges q heads w, w + 8, ...: lanes over d_h (float4 each for
+// d_h = 128, float2 for 64); the loads of up to 8 splits are issued together, with an online
+// rescale between chunks. O = sum_s e^(m_s - M) O_s / sum_s e^(m_s - M) l_s, M = max m_s.
 template <int DH>
 __global__ void __launch_bounds__(256) attn_combine_kernel(LaneDev d, int T) {
-  constexpr int V = DH / 32;                       // floats per lane
-  constexpr int MS = 8;
   pdl_trigger();
   pdl_wait();
-  const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (wid >= T * d.Hq) return;
-  const int r = wid / d.Hq, hq = wid % d.Hq;
-  const int b = d.row_req[r], j = r - d.row_off[b];
-  const int G = d.Hq / d.Hkv, h = hq / G, g = hq % G, rl = j * G + g;
-  const int ns = num_splits(d.len[d.slots[b]]);
-  const int base = d.item_start[b] + h * ns;
-  float M = -INFINITY, l = 0.f, o[V];
-#pragma unroll
-  for (int i = 0; i < V; ++i) o[i] = 0.f;
-  for (int s0 = 0; s0 < ns; s0 += MS) {
-    float2 ml[MS];
-    float v[MS][V];
-#pragma unroll
-    for (int k = 0; k < MS; ++k) {
-      const int s = s0 + k;
-      const size_t it = (size_t)(base + s) * kAttnRows + rl;
-      ml[k] = s < ns ? *reinterpret_cast<const float2*>(d.part_ml + it * 2) : make_float2(-INFINITY, 0.f);
-      const float* src = d.part_o + it * DH + lane * V;
-      if constexpr (V == 4) {
-        const float4 x = s < ns ? *reinterpret_cast<const float4*>(src) : make_float4(0.f, 0.f, 0.f, 0.f);
-        v[k][0] = x.x; v[k][1] = x.y; v[k][2] = x.z; v[k][3] = x.w;
-      } else {
-        const float2 x = s < ns ? *reinterpret_cast<const float2*>(src) : make_float2(0.f, 0.f);
-        v[k][0] = x.x; v[k][1] = x.y;
-      }
-    }
-    float Mn = M;
-#pragma unroll
-    for (int k = 0; k < MS; ++k) Mn = fmaxf(Mn, ml[k].x);
-    if (Mn == -INFINITY) continue;
-    const float sc = M == -INFINITY ? 0.f : expf(M - Mn);
-    l *= sc;
-#pragma unroll
-    for (int i = 0; i < V; ++i) o[i] *= sc;
-#pragma unroll
-    for (int k = 0; k < MS; ++k) {
-      const float w = ml[k].x == -INFINITY ? 0.f : expf(ml[k].x - Mn);
-      l += ml[k].y * w;
-#pragma unroll
-      for (int i = 0; i < V; ++i) o[i] += v[k][i] * w;
-    }
-    M = Mn;
+  constexpr int V = DH / 32;                       // floats per lane
+  constexpr int MS = 8;
+  __shared__ int s_j, s_ns, s_base;
+  const int r = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    const int b = d.row_req[r];
+    s_j = r - d.row_off[b];
+    s_ns = num_splits(d.len[d.slots[b]]);
+    s_base = d.item_start[b];
   }
-  const float inv = 1.0f / l;
-  bf16* dst = d.o + (size_t)r * d.Hq * DH + (size_t)hq * DH + lane * V;
+  __syncthreads();
+  const int j = s_j, ns = s_ns;
+  const int G = d.Hq / d.Hkv;
+  for (int hq = warp; hq < d.Hq; hq += 8) {
+    const int h = hq / G, g = hq % G, rl = j * G + g;
+    const int base = s_base + h * ns;
+    float M = -INFINITY, l = 0.f, o[V];
 #pragma unroll
-  for (int i = 0; i < V; i += 2) *reinterpret_cast<__nv_bfloat162*>(dst + i) = __floats2bfloat162_rn(o[i] * inv, o[i + 1] * inv);
+    for (int i = 0; i < V; ++i) o[i] = 0.f;
+    for (int s0 = 0; s0 < ns; s0 += MS) {
+      float2 ml[MS];
+      float v[MS][V];
+#pragma unroll
+      for (int k = 0; k < MS; ++k) {
+        const int s = s0 + k;
+        const size_t it = (size_t)(base + s) * kAttnRows + rl;
+        ml[k] = s < ns ? *reinterpret_cast<const float2*>(d.part_ml + it * 2) : make_float2(-INFINITY, 0.f);
+        const float* src = d.part_o + it * DH + lane * V;
+        if constexpr (V == 4) {
+          const float4 x = s < ns ? *reinterpret_cast<const float4*>(src) : make_float4(0.f, 0.f, 0.f, 0.f);
+          v[k][0] = x.x; v[k][1] = x.y; v[k][2] = x.z; v[k][3] = x.w;
+        } else {
+          const float2 x = s < ns ? *reinterpret_cast<const float2*>(src) : make_float2(0.f, 0.f);
+          v[k][0] = x.x; v[k][1] = x.y;
+        }
+      }
+      float Mn = M;
+#pragma unroll
+      for (int k = 0; k < MS; ++k) Mn = fmaxf(Mn, ml[k].x);
+      if (Mn == -INFINITY) continue;
+      const float sc = M == -INFINITY ? 0.f : expf(M - Mn);
+      l *= sc;
+#pragma unroll
+      for (int i = 0; i < V; ++i) o[i] *= sc;
+#pragma unroll
+      for (int k = 0; k < MS; ++k) {
+        const float w = ml[k].x == -INFINITY ? 0.f : expf(ml[k].x - Mn);
+        l += ml[k].y * w;
+#pragma unroll
+        for (int i = 0; i < V; ++i) o[i] += v[k][i] * w;
+      }
+      M = Mn;
+    }
+    const float inv = 1.0f / l;
+    bf16* dst = d.o + (size_t)r * d.Hq * DH + (size_t)hq * DH + lane * V;
+#pragma unroll
+    for (int i = 0; i < V; i += 2)
+      *reinterpret_cast<__nv_bfloat162*>(dst + i) = __floats2bfloat162_rn(o[i] * inv, o[i + 1] * inv);
+  }
 }
 
 cudaError_t launch_attn_combine(const LaneDev& d, int T, cudaStream_t s) {
-  const int warps = T * d.Hq;
   SV_COUNT_LAUNCH();
-  if (d.dh == 128) return launch_pdl(attn_combine_kernel<128>, dim3((warps + 7) / 8), dim3(256), 0, s, 1, d, T);
-  return launch_pdl(attn_combine_kernel<64>, dim3((warps + 7) / 8), dim3(256), 0, s, 1, d, T);
+  if (d.dh == 128) return launch_pdl(attn_combine_kernel<128>, dim3(T), dim3(256), 0, s, 1, d, T);
+  return launch_pdl(attn_combine_kernel<64>, dim3(T), dim3(256), 0, s, 1, d, T);
 }
 
 }  // namespace sv

@@ -58,19 +58,35 @@ __global__ void __launch_bounds__(256) commit_kernel(LaneDev d, const int* __res
   __syncthreads();
   if (!s_ok) return;
   const int n = s_n, row0 = d.row_off[b];
+  // the <= 6 pages covering tokens L .. L + n - 1 (n <= 33, page >= 8), staged once
+  __shared__ int s_pg[8];
+  const int pg0 = L / d.page, npg = (L + n - 1) / d.page - pg0 + 1;
+  if (threadIdx.x < npg) s_pg[threadIdx.x] = d.page_table[slot * d.max_pages_per_slot + pg0 + threadIdx.x];
+  __syncthreads();
   const int vec_per_row = d.dh / 8;              // 16-byte vectors per (token, kv head)
   const int per_tok = 2 * d.Hkv * vec_per_row;
   const size_t nkv = (size_t)d.Hkv * d.dh;
-  for (int layer = 0; layer < d.n_layers; ++layer) {
-    for (int i = threadIdx.x; i < n * per_tok; i += blockDim.x) {
-      const int c = i / per_tok, rem = i % per_tok;
+  const int total = d.n_layers * n * per_tok;
+  constexpr int U = 4;                           // loads of U vectors in flight before their stores
+  for (int i0 = threadIdx.x; i0 < total; i0 += U * blockDim.x) {
+    uint4 v[U];
+    bf16* dst[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = i0 + u * blockDim.x;
+      dst[u] = nullptr;
+      if (i >= total) continue;
+      const int layer = i / (n * per_tok), li = i % (n * per_tok);
+      const int c = li / per_tok, rem = li % per_tok;
       const int kv = rem / (d.Hkv * vec_per_row), h = (rem / vec_per_row) % d.Hkv, v8 = rem % vec_per_row;
       const int t = L + c;
-      const int page = d.page_table[slot * d.max_pages_per_slot + t / d.page];
       const bf16* src = (kv ? d.vc : d.kc) + ((size_t)layer * d.Tmax + row0 + c) * nkv + (size_t)h * d.dh + v8 * 8;
-      bf16* dst = d.pool + pool_row(d, layer, page, kv, h, t % d.page) * d.dh + v8 * 8;
-      *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(src);
+      v[u] = *reinterpret_cast<const uint4*>(src);
+      dst[u] = d.pool + pool_row(d, layer, s_pg[t / d.page - pg0], kv, h, t % d.page) * d.dh + v8 * 8;
     }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (dst[u]) *reinterpret_cast<uint4*>(dst[u]) = v[u];
   }
   __syncthreads();
   if (threadIdx.x == 0) {

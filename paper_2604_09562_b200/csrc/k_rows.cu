@@ -31,22 +31,26 @@ __global__ void plan_kernel(LaneDev d, PlanArgs p, const int* __restrict__ draft
   __shared__ int s_off[kMaxBatch + 1];
   __shared__ int s_item[kMaxBatch + 1];
   __shared__ int s_err[kMaxBatch];
+  __shared__ int s_len[kMaxBatch];
   const int B = p.batch;
-  if (threadIdx.x == 0) {
+  for (int b = threadIdx.x; b < B; b += blockDim.x) {   // the per-request loads, in parallel
+    s_len[b] = d.len[p.slots[b]];
+    s_err[b] = 0;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {                                // prefix sums over shared memory only
     int o = 0, it = 0;
     for (int b = 0; b < B; ++b) {
       s_off[b] = o;
       s_item[b] = it;
-      const int R = p.depths[b] + 1;
-      o += R;
-      if (attn) it += num_splits(d.len[p.slots[b]]) * d.Hkv;
+      o += p.depths[b] + 1;
+      if (attn) it += num_splits(s_len[b]) * d.Hkv;
     }
     s_off[B] = o;
     s_item[B] = it;
     *d.n_items = it;
     *d.batch_n = B;
   }
-  for (int b = threadIdx.x; b < B; b += blockDim.x) s_err[b] = 0;
   __syncthreads();
   for (int b = threadIdx.x; b <= B; b += blockDim.x) {
     d.row_off[b] = s_off[b];
@@ -68,7 +72,7 @@ __global__ void plan_kernel(LaneDev d, PlanArgs p, const int* __restrict__ draft
       atomicOr(&s_err[b], 1);
       tok = 0;
     }
-    int pos = d.len[slot] + j;
+    int pos = s_len[b] + j;
     if (pos >= d.max_pos) {                      // chain would run past the position table
       atomicOr(&s_err[b], 2);
       pos = d.max_pos - 1;                       // keep every read in range; the request is not committed
@@ -86,7 +90,7 @@ __global__ void plan_kernel(LaneDev d, PlanArgs p, const int* __restrict__ draft
         if (s_item[mid] <= it) lo = mid; else hi = mid - 1;
       }
       const int b = lo, rel = it - s_item[b];
-      const int ns = num_splits(d.len[p.slots[b]]);
+      const int ns = num_splits(s_len[b]);
       d.items[it] = make_int4(b, rel / ns, rel % ns, ns);
     }
   }
