@@ -177,6 +177,10 @@ sv_status sv_commit(sv_ctx* ctx, const int32_t* n_keep);
 /* Return the slot's pages to the free list; the slot becomes EMPTY. ESTATE if PENDING. */
 sv_status sv_release(sv_ctx* ctx, int32_t slot);
 
+/* Lane occupancy for the router (FlowGuard's M_w and L_w): slots that are not EMPTY, and pages
+ * left on the device free list. Syncs the lane's stream. */
+sv_status sv_lane_occupancy(sv_ctx* ctx, int32_t* active_slots, int32_t* free_pages);
+
 /* Copy the lane counters to *out (host). Syncs the stream. reset != 0 zeroes
  * the counters (not the error word). Returns SV_ENOKV / SV_EDEVICE if the
  * sticky device error word is set. */
@@ -316,6 +320,38 @@ sv_status sv_spec_adapt(const sv_spec_config* cfg, const sv_flow_state* in, doub
 sv_status sv_spec_step(const sv_spec_config* cfg, const sv_flow_state* in, const sv_lane_stats* s0,
                        const sv_lane_stats* s1, double seconds, int32_t active, int32_t max_batch,
                        sv_spec_plan* plan, sv_flow_state* out);
+
+/* ---------------- FlowGuard lane router (NEXT-2; host code, no device work) ----------------
+ * PAPER.md §3.3: eq:flowguard_score, eq:overload_detection / eq:overload_score,
+ * eq:fallback_selection and Alg. 2 "FlowGuard Worker Selection"; readings
+ * DESIGN.md R25-R28. Routes an incoming request to one of n decode lanes from their published
+ * metrics. Pure function of its inputs; all structs are host. */
+typedef struct {
+  double alpha[4];        /* weights of C, 1-M, 1-Q, 1-L (0.4, 0.1, 0.3, 0.2); >= 0, sum 1 within 1e-9 */
+  double tau;             /* overload threshold (0.85), > 0 */
+  double q_max;           /* queue-depth normaliser (100), >= 1 */
+  int64_t staleness_ms;   /* a snapshot older than this is stale (1000) */
+} sv_route_config;
+typedef struct {
+  int64_t timestamp_ms;   /* when the lane published it */
+  double cache_hit;       /* C_w in [0, 1] */
+  double mem_util;        /* M_w in [0, 1] */
+  double queue_depth;     /* Q_raw >= 0 */
+  double active_load;     /* L_w in [0, 1] */
+} sv_lane_metrics;
+#define SV_ROUTE_OVERLOADED 1
+#define SV_ROUTE_STALE 2
+
+/* Paper defaults. */
+void sv_route_default_config(sv_route_config* cfg);
+/* Alg. 2 over n >= 1 lanes at time now_ms. live_queue: NULL or n fresh queue depths that replace
+ * the snapshots' (Alg. 2 "load_i.qd <- Q_{P_i}.size()"). Writes *chosen; optional outputs:
+ * scores[n] (NaN for excluded lanes), flags[n] (SV_ROUTE_* bits), *used_fallback (1 when every
+ * lane was stale or overloaded and the argmin queue depth was taken). Ties: lowest index.
+ * EINVAL on invalid cfg / metrics (fractions outside [0,1], negative queue, n < 1, NULL). */
+sv_status sv_route_select(const sv_route_config* cfg, int32_t n, const sv_lane_metrics* metrics,
+                          const double* live_queue, int64_t now_ms, int32_t* chosen, double* scores,
+                          uint8_t* flags, int32_t* used_fallback);
 
 #ifdef __cplusplus
 }

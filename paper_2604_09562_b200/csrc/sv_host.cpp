@@ -527,6 +527,18 @@ sv_status sv_release(sv_ctx* c, int32_t slot) {
   return SV_OK;
 }
 
+sv_status sv_lane_occupancy(sv_ctx* c, int32_t* active_slots, int32_t* free_pages) {
+  if (!c || !active_slots || !free_pages) return SV_EINVAL;
+  int ft = 0;
+  SV_CUDA(cudaMemcpyAsync(&ft, c->d.free_top, 4, cudaMemcpyDeviceToHost, c->stream));
+  SV_CUDA(cudaStreamSynchronize(c->stream));
+  int n = 0;
+  for (int st : c->state) n += st != EMPTY;
+  *active_slots = n;
+  *free_pages = ft < 0 ? 0 : ft;
+  return SV_OK;
+}
+
 sv_status sv_stats(sv_ctx* c, sv_lane_stats* out, int reset) {
   if (!c || !out) return SV_EINVAL;
   unsigned long long buf[sv::kNumStats];

@@ -42,3 +42,33 @@ def broadcast_bytes(payload, src, nbytes, device=None, group=None):
         buf.copy_(torch.frombuffer(bytearray(payload), dtype=torch.uint8))
     dist.broadcast(buf, src=src, group=group)
     return bytes(buf.cpu().numpy().tobytes())
+
+
+# ---------------------------------------------------------------- FlowGuard routing across lanes
+def lane_metrics(lane, cfg, queue_depth, now_ms, cache_hit=0.0):
+    """A lane's published FlowGuard signals (Table 2 / eq:flowguard_score): memory
+    utilisation = KV pages in use / pool, load = occupied slots / slots, the lane's queue depth,
+    and the cache hit rate (0: no prefix-cache reuse in this system). Syncs the lane's stream."""
+    active, free = lane.occupancy()
+    return (int(now_ms), float(cache_hit), 1.0 - free / cfg.n_pages, float(queue_depth), active / cfg.max_slots)
+
+
+def gather_metrics(local, device=None, group=None):
+    """all_gather of every lane's 5-field metrics tuple (SURVEY.md §8(e) exchange 2, off the hot path)."""
+    t = torch.tensor([float(x) for x in local], dtype=torch.float64, device=device)
+    out = [torch.zeros_like(t) for _ in range(dist.get_world_size(group))]
+    dist.all_gather(out, t, group=group)
+    return [(int(o[0].item()), float(o[1]), float(o[2]), float(o[3]), float(o[4])) for o in out]
+
+
+def route_requests(n_requests, metrics, now_ms, cfg=None):
+    """Admission routing of n new requests with FlowGuard (Alg. 2, in libsv): each assignment adds
+    one to the chosen lane's live queue depth before the next request is routed."""
+    from . import flowguard
+    live = [m[3] for m in metrics]
+    out = []
+    for _ in range(n_requests):
+        chosen, _, _, _ = flowguard.select(metrics, live, now_ms, cfg)
+        out.append(chosen)
+        live[chosen] += 1
+    return out

@@ -30,6 +30,7 @@ EXPORTED = [
     "sv_kv_recv_append", "sv_kv_packed_bytes", "sv_kv_pack", "sv_profile_enable", "sv_profile_num_stages",
     "sv_profile_stage_name", "sv_profile_read", "sv_launch_count", "sv_debug_gemm", "sv_kv_append_packed",
     "sv_kv_loopback_append", "sv_spec_default_config", "sv_spec_reset", "sv_spec_adapt", "sv_spec_step",
+    "sv_route_default_config", "sv_route_select", "sv_lane_occupancy",
 ]
 
 
@@ -111,6 +112,7 @@ def load():
         "sv_kv_send": ([vp, i32, i32, i32, i32, ctypes.c_int, vp, vp], ctypes.c_int),
         "sv_kv_recv_append": ([vp, i32, u64, i32, vp, ctypes.c_int, vp], ctypes.c_int),
         "sv_kv_append_packed": ([vp, i32, u64, i32, vp], ctypes.c_int),
+        "sv_lane_occupancy": ([vp, P(i32), P(i32)], ctypes.c_int),
         "sv_kv_loopback_append": ([vp, i32, u64, i32, vp, vp, ctypes.c_int, vp], ctypes.c_int),
         "sv_kv_packed_bytes": ([P(Config), i32], sz),
         "sv_kv_pack": ([vp, vp, i32, i32, i32, i32, i32, vp, vp], ctypes.c_int),
@@ -238,6 +240,12 @@ class Lane:
         if check:
             _check(r, "sv_stats")
         return st.as_dict()
+
+    def occupancy(self):
+        """(active slots, free KV pages) — the router's L_w and M_w inputs."""
+        a, f = ctypes.c_int32(), ctypes.c_int32()
+        _check(self.lib.sv_lane_occupancy(self.ctx, ctypes.byref(a), ctypes.byref(f)), "sv_lane_occupancy")
+        return a.value, f.value
 
     def stats_raw(self, reset=False):
         """The sv_lane_stats struct itself (for the SpecuStream controller's window deltas)."""

@@ -28,6 +28,46 @@ def _free_port():
         return s.getsockname()[1]
 
 
+def _route_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        # lane r publishes (timestamp, C, M, Q, L); lane 1 is busier
+        local = (1000, 0.0, 0.3 + 0.4 * rank, 5.0 + 20.0 * rank, 0.5 + 0.3 * rank)
+        metrics = svdist.gather_metrics(local)
+        assign = svdist.route_requests(12, metrics, 1200) if rank == 0 else None
+        blob = svdist.broadcast_bytes(bytes(assign) if assign is not None else None, src=0, nbytes=12)
+        q.put((rank, metrics, list(blob)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(120)
+def test_gloo_world2_flowguard_admission_routing():
+    from oracle import flowguard as fg
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_route_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=100) for _ in range(world))
+    for p in procs:
+        p.join(timeout=30)
+        assert p.exitcode == 0
+    assert res[0][1] == res[1][1] and res[0][2] == res[1][2]        # every rank sees the same metrics / routes
+    metrics = [fg.WorkerMetrics(*m) for m in res[0][1]]
+    live, want = [m.queue_depth for m in metrics], []
+    for _ in range(12):                                               # oracle: Alg. 2 per admission
+        d = fg.select_worker(metrics, live, 1200, fg.RouteConfig())
+        want.append(d.chosen)
+        live[d.chosen] += 1
+    assert res[0][2] == want
+    assert 0 in want                                                  # the idle lane takes requests
+
+
 def _worker(rank, world, port, q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)

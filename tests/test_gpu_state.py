@@ -287,3 +287,12 @@ def test_greedy_without_taps_skips_logits_but_decides_the_same():
     for i in range(4):
         assert torch.equal(out[0][i], out[1][i])
     assert not out[0][4] and out[1][4]          # taps on: logits stored; off: untouched
+
+
+def test_lane_occupancy():
+    cfg = synth.TOY.with_(n_pages=32)
+    S = Setup(cfg, [100, 64, 1], seed=16)                          # 2 + 1 + 1 pages
+    active, free = S.lane.occupancy()
+    assert active == 3 and free == 32 - 4
+    S.lane.release(1)
+    assert S.lane.occupancy() == (2, 32 - 3)
