@@ -544,16 +544,23 @@ def main():
         return
 
     import torch.distributed as dist
-    dev = torch.device("cuda", local)
+    # SV_BENCH_SHARED_GPU=1 (validation only): several ranks on one GPU over gloo, to exercise the
+    # multi-rank flow on a single-GPU box; the driver's N-GPU runs use one GPU per rank and NCCL
+    shared = os.environ.get("SV_BENCH_SHARED_GPU") == "1"
+    dev = torch.device("cuda", local % torch.cuda.device_count() if shared else local)
     torch.cuda.set_device(dev)
+    red_dev = torch.device("cpu") if shared else dev
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     res = run_gpu(args, wl, rank, world, dev)
     elapsed, tokens = res["elapsed_ms"], res["tokens"]
     if world > 1:                                 # whole job: all ranks' tokens / the slowest rank's time
-        elapsed, tokens = svdist.reduce_region(elapsed, tokens, device=dev)
+        elapsed, tokens = svdist.reduce_region(elapsed, tokens, device=red_dev)
         if res["e2e"]:
-            es, et = svdist.reduce_region(res["e2e"]["seconds"], res["e2e"]["tokens"], device=dev)
+            es, et = svdist.reduce_region(res["e2e"]["seconds"], res["e2e"]["tokens"], device=red_dev)
             res["e2e"]["value"] = et / es
     if rank != 0:
         if world > 1:
