@@ -175,7 +175,10 @@ static cudaError_t gemm_sw(GemmPlan* p, const bf16* A, const bf16* B, int M, int
   g.nt_tok = gemm_sw_choose_nt(M, num_mp, p->num_sms / 2);
   if (const char* nt = getenv("SV_SW_NT")) g.nt_tok = atoi(nt);   // experiment override
   if (const char* dg = getenv("SV_SW_DIAG")) g.diag = atoi(dg);    // experiment: 1 no loads, 2 no epilogue
-  if (g.kind == GEMM_EPI_LOGITS) g.trace = p->d.trace;                // lm-head tile timeline (SV_TRACE)
+  {                                                                  // tile timeline (SV_TRACE): lm-head by
+    const char* tk = getenv("SV_TRACE_GEMM");                        // default, or the GEMM kind named here
+    if (g.kind == (tk ? atoi(tk) : (int)GEMM_EPI_LOGITS)) g.trace = p->d.trace;
+  }
   const CUtensorMap* mw = get_map(p, B, (uint64_t)g.N, (uint64_t)K, swiglu ? 64 : 128);
   const CUtensorMap* mx = get_map(p, A, (uint64_t)M, (uint64_t)K, (uint32_t)(g.nt_tok / 2));  // rows >= M: zero
   if (!mw || !mx) return cudaErrorInvalidValue;

@@ -40,7 +40,7 @@ constexpr int BK = 64, STAGES = 6, THREADS = 384;   // 4 role warps + 8 epilogue
 constexpr int A_BYTES = 128 * BK * 2;             // 16 KB: this CTA's 128 weight rows
 constexpr int BX_BYTES = 128 * BK * 2;            // 16 KB: room for NT/2 <= 128 token rows
 constexpr int STAGE_BYTES = A_BYTES + BX_BYTES;
-constexpr int XCH_BYTES = 2 * 2 * 4 * 16 * 32 * 4;  // 32 KB: partner-row exchange [parity][half][quadrant]
+constexpr int XCH_BYTES = 2 * 4 * 16 * 32 * 4;      // 16 KB: partner-row exchange / output staging [half][quadrant]
 constexpr int RED_BYTES = 3 * 4 * 256 * 4;        // 12 KB: per-warp column statistics
 constexpr int AUX_BYTES = XCH_BYTES > RED_BYTES ? XCH_BYTES : RED_BYTES;
 constexpr int POS_BYTES = 256 * 4;                 // QKV: positions of the tile's tokens
@@ -85,30 +85,57 @@ __device__ __forceinline__ void sw_ld16(uint32_t taddr, uint32_t (&r)[16]) {
 }
 
 // ---------------------------------------------------------------- fp32 stores (+ residual)
-// The residual input may alias the output, so the compiler cannot move a load above an earlier
-// store: the chunk's 16 loads are issued explicitly before any of its stores (otherwise every
-// column pays a full memory round trip in sequence).
+// The warp's own 2 KB slot of the AUX region (output staging)
+__device__ __forceinline__ float* sw_slot(const SwEpi& e) { return e.aux + (e.h * 4 + e.q) * (16 * 32); }
+
+// fp32 outputs (+ residual): the chunk's accumulators are transposed through the warp's slot so
+// every load / store is a 16-byte access of a 128-byte row segment (4 tokens per instruction);
+// the residual rows of the next chunk are loaded one chunk ahead. The residual input may alias
+// the output: each element is read before it is written, by the same lane.
 __device__ __forceinline__ void sw_epi_f32(const SwEpi& e, const SwTile& tl) {
   const GemmTcArgs& g = *e.g;
-  const int f = tl.m_pair * 256 + e.rank * 128 + e.q * 32 + e.lane;
+  const int f0 = tl.m_pair * 256 + e.rank * 128 + e.q * 32;   // first feature of this warp
   const bool resid = g.kind == GEMM_EPI_RESIDUAL;
   float* out = resid ? g.resid_out : g.out;
   const int t0 = tl.n_blk * e.NT;
-  const bool fok = f < g.N;
+  float* st = sw_slot(e);                                     // [16 tokens][32 features] fp32
+  // lane -> (token tok = it * 4 + lane / 8, 4 features at part * 4): whole 128-byte row segments
+  const int part = e.lane & 7, fcol = f0 + part * 4;
+  const bool vec = (g.ldo & 3) == 0 && fcol + 4 <= g.N;
+  auto load_in = [&](float4 (&h)[4], int c) {                 // residual rows of chunk c
+#pragma unroll
+    for (int it = 0; it < 4; ++it) {
+      const int t = t0 + c + it * 4 + (e.lane >> 3);
+      h[it] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (resid && vec && c < e.NT && t < g.M) h[it] = __ldcg(reinterpret_cast<const float4*>(g.resid_in + (size_t)t * g.ldo + fcol));
+    }
+  };
+  float4 hn[4];
+  load_in(hn, e.h * 16);
   for (int c = e.h * 16; c < e.NT; c += 32) {
+    float4 h[4];
+#pragma unroll
+    for (int it = 0; it < 4; ++it) h[it] = hn[it];
+    load_in(hn, c + 32);                                      // next chunk's rows in flight
     uint32_t r[16];
     sw_ld16(e.tbase + c, r);
-    float v[16];
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const int t = t0 + c + i;
-      v[i] = (resid && fok && t < g.M) ? __ldcg(g.resid_in + (size_t)t * g.ldo + f) : 0.f;
-    }
+    for (int i = 0; i < 16; ++i) st[i * 32 + e.lane] = sw_u2f(r[i]);
+    __syncwarp();
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const int t = t0 + c + i;
-      if (fok && t < g.M) out[(size_t)t * g.ldo + f] = v[i] + sw_u2f(r[i]);
+    for (int it = 0; it < 4; ++it) {
+      const int tok = it * 4 + (e.lane >> 3), t = t0 + c + tok;
+      if (t >= g.M) continue;
+      const float4 v = *reinterpret_cast<const float4*>(st + tok * 32 + part * 4);
+      const size_t o = (size_t)t * g.ldo + fcol;
+      if (vec) {
+        *reinterpret_cast<float4*>(out + o) = make_float4(v.x + h[it].x, v.y + h[it].y, v.z + h[it].z, v.w + h[it].w);
+      } else {                                                // ragged feature tail / unaligned rows
+        const float vv[4] = {v.x, v.y, v.z, v.w};
+        for (int k = 0; k < 4 && fcol + k < g.N; ++k) out[o + k] = resid ? g.resid_in[o + k] + vv[k] : vv[k];
+      }
     }
+    __syncwarp();
   }
 }
 
@@ -204,15 +231,34 @@ __device__ __forceinline__ void sw_epi_logits(const SwEpi& e, const SwTile& tl) 
 // ---------------------------------------------------------------- partner-row exchange
 // Publishes this warp's 16 values and returns the values of row (own row ^ pmask) for the
 // same columns. pmask = 32 or 64 (a partner in another warp of this CTA).
-__device__ __forceinline__ void sw_exchange(const SwEpi& e, int parity, int pmask, const uint32_t (&r)[16],
-                                            float (&p)[16]) {
-  float* buf = e.aux + (parity * 2 + e.h) * (4 * 16 * 32);
+__device__ __forceinline__ void sw_exchange(const SwEpi& e, int pmask, const uint32_t (&r)[16], float (&p)[16]) {
+  float* buf = e.aux + e.h * (4 * 16 * 32);
 #pragma unroll
   for (int i = 0; i < 16; ++i) buf[(e.q * 16 + i) * 32 + e.lane] = sw_u2f(r[i]);
   tc::named_bar(XCH_BAR + e.h, 128);
   const int pq = e.q ^ (pmask >> 5);
 #pragma unroll
   for (int i = 0; i < 16; ++i) p[i] = buf[(pq * 16 + i) * 32 + e.lane];
+  tc::named_bar(XCH_BAR + e.h, 128);                    // partner reads done: own slot reusable
+}
+
+
+// Store a 32-feature x 16-token bf16 block (lane = feature, y[i] = token i) with 16-byte stores:
+// transposed through the warp's slot, 4 lanes per token row, 8 tokens per instruction. out0 =
+// address of (first token, feature of lane 0); ld = row stride in elements; ntok = valid tokens.
+__device__ __forceinline__ void sw_store_bf16(const SwEpi& e, const __nv_bfloat16 (&y)[16], __nv_bfloat16* out0,
+                                              size_t ld, int ntok) {
+  __nv_bfloat16* st = reinterpret_cast<__nv_bfloat16*>(sw_slot(e));
+#pragma unroll
+  for (int i = 0; i < 16; ++i) st[i * 32 + e.lane] = y[i];
+  __syncwarp();
+#pragma unroll
+  for (int it = 0; it < 2; ++it) {
+    const int tok = it * 8 + (e.lane >> 2), part = e.lane & 3;
+    if (tok < ntok)
+      *reinterpret_cast<uint4*>(out0 + (size_t)tok * ld + part * 8) = *reinterpret_cast<const uint4*>(st + tok * 32 + part * 8);
+  }
+  __syncwarp();
 }
 
 // ---------------------------------------------------------------- a2 QKV + RoPE
@@ -226,17 +272,18 @@ __device__ __forceinline__ void sw_epi_qkv(const SwEpi& e, const SwTile& tl) {
   const bool rope = head < g.Hq + g.Hkv;
   const bool lo = d < half;
   const int dd = lo ? d : d - half;
+  const int d0 = d - e.lane;                              // first feature of this warp (32-aligned)
   __nv_bfloat16* dst;
   size_t ld;
   if (head < g.Hq) {
     ld = (size_t)g.Hq * dh;
-    dst = g.q + (size_t)head * dh + d;
+    dst = g.q + (size_t)head * dh + d0;
   } else if (head < g.Hq + g.Hkv) {
     ld = (size_t)g.Hkv * dh;
-    dst = g.kc + (size_t)(head - g.Hq) * dh + d;
+    dst = g.kc + (size_t)(head - g.Hq) * dh + d0;
   } else {
     ld = (size_t)g.Hkv * dh;
-    dst = g.vc + (size_t)(head - g.Hq - g.Hkv) * dh + d;
+    dst = g.vc + (size_t)(head - g.Hq - g.Hkv) * dh + d0;
   }
   const int t0 = tl.n_blk * e.NT;
   for (int col = e.tid; col < e.NT; col += EPI_THREADS) {     // the tile's token positions
@@ -244,27 +291,39 @@ __device__ __forceinline__ void sw_epi_qkv(const SwEpi& e, const SwTile& tl) {
     e.pos[col] = t < g.M ? g.row_pos[t] : 0;
   }
   tc::named_bar(EPI_BAR, EPI_THREADS);
-  int parity = 0;
-  for (int c = e.h * 16; c < e.NT; c += 32, parity ^= 1) {
+  // RoPE table values of the next chunk are loaded while this chunk's accumulators come out of
+  // TMEM and cross the partner exchange (software pipeline: a single-tile launch exposes the epilogue)
+  auto load_tab = [&](float (&cs)[16], float (&sn)[16], int c) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const bool ok = rope && head < nheads && c < e.NT;
+      const size_t o = ok ? (size_t)e.pos[c + i] * half + dd : 0;
+      cs[i] = ok ? __ldg(g.rope_cos + o) : 1.f;
+      sn[i] = ok ? __ldg(g.rope_sin + o) : 0.f;
+    }
+  };
+  float csn[16], snn[16];
+  load_tab(csn, snn, e.h * 16);
+  for (int c = e.h * 16; c < e.NT; c += 32) {
+    float cs[16], sn[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      cs[i] = csn[i];
+      sn[i] = snn[i];
+    }
+    load_tab(csn, snn, c + 32);
     uint32_t r[16];
     float p[16];
     sw_ld16(e.tbase + c, r);
-    sw_exchange(e, parity, half, r, p);                   // partner = d +- half, same head
-    if (head >= nheads) continue;
-    float cs[16], sn[16];
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {                        // all table loads before any store
-      const size_t o = (size_t)e.pos[c + i] * half + dd;
-      cs[i] = rope ? __ldg(g.rope_cos + o) : 1.f;
-      sn[i] = rope ? __ldg(g.rope_sin + o) : 0.f;
-    }
+    sw_exchange(e, half, r, p);                           // partner = d +- half, same head
+    if (head >= nheads) continue;                         // warp-uniform
+    __nv_bfloat16 y[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
-      const int t = t0 + c + i;
       const float x = sw_u2f(r[i]);
-      const float y = !rope ? x : lo ? x * cs[i] - p[i] * sn[i] : x * cs[i] + p[i] * sn[i];
-      if (t < g.M) dst[(size_t)t * ld] = f2bf(y);
+      y[i] = f2bf(!rope ? x : lo ? x * cs[i] - p[i] * sn[i] : x * cs[i] + p[i] * sn[i]);
     }
+    sw_store_bf16(e, y, dst + (size_t)(t0 + c) * ld, ld, min(16, g.M - (t0 + c)));
   }
   tc::named_bar(EPI_BAR, EPI_THREADS);                    // XCH / POS are reused by the next tile
 }
@@ -275,20 +334,21 @@ __device__ __forceinline__ void sw_epi_swiglu(const SwEpi& e, const SwTile& tl) 
   const int rho = e.q * 32 + e.lane;                      // < 64: gate row, >= 64: up row
   const int j = tl.m_pair * 128 + e.rank * 64 + (rho & 63);
   const int t0 = tl.n_blk * e.NT;
-  int parity = 0;
-  for (int c = e.h * 16; c < e.NT; c += 32, parity ^= 1) {
+  const int j0 = j - e.lane;                              // first feature of this warp (32-aligned)
+  for (int c = e.h * 16; c < e.NT; c += 32) {
     uint32_t r[16];
     float p[16];
     sw_ld16(e.tbase + c, r);
-    sw_exchange(e, parity, 64, r, p);
-    if (rho >= 64 || j >= g.F) continue;
+    sw_exchange(e, 64, r, p);
+    if (rho >= 64 || j0 >= g.F) continue;                 // warp-uniform (F % 128 == 0)
+    __nv_bfloat16 y[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
-      const int t = t0 + c + i;
-      if (t >= g.M) continue;
       const float x = sw_u2f(r[i]);
-      g.u[(size_t)t * g.F + j] = f2bf(__fdividef(x, 1.0f + __expf(-x)) * p[i]);
+      y[i] = f2bf(__fdividef(x, 1.0f + __expf(-x)) * p[i]);
     }
+    const int ntok = min(16, g.M - (t0 + c));
+    sw_store_bf16(e, y, g.u + (size_t)(t0 + c) * g.F + j0, g.F, ntok);
   }
   tc::named_bar(EPI_BAR, EPI_THREADS);                    // XCH / POS are reused by the next tile
 }

@@ -29,7 +29,7 @@ tr = lane.tap("trace", torch.int64, (16, 256)).cpu().numpy().astype(np.int64)
 ms, me, es, ee = tr[12], tr[13], tr[14], tr[15]
 n = int((ms > 0).sum())
 t0 = ms[0]
-print(f"{n} tiles on CTA 0")
+print(f"{n} tiles on CTA 0; kernel start->end per cluster below")
 for i in range(n):
     print(f"tile {i:2d}: mma {ms[i] - t0:8d} .. {me[i] - t0:8d} ({me[i] - ms[i]:6d})   epi {es[i] - t0:8d} .. {ee[i] - t0:8d} "
           f"({ee[i] - es[i]:6d})")
