@@ -21,6 +21,7 @@ with a bonus token, or a greedy prefix match, written out here in that order:
           (exponential race; P(y = x) = R(x) / sum R; ties -> lowest x)
           q NULL (one-hot at d_j): r_j = p_j(d_j); residual = p with d_{a+1} zeroed
   step 5  outputs a in [0, k], emitted = d_1..d_a, y
+  PREFILL (NEXT-3, R29): a = k, y = argmax l_k (a prompt chunk whose KV is all kept; no counters)
   a7      lane counters: steps, rows, drafted, accepted,
           emitted, accepted_independent (sum over ALL j of [u_j < r_j], or of
           [d_j == argmax l_{j-1}] in greedy), hist_accepted[a],
@@ -39,6 +40,7 @@ from .model import softmax
 
 GREEDY = 0
 SAMPLE = 1
+PREFILL = 2    # NEXT-3 chunked prefill (R29): the "drafts" are prompt tokens, all kept
 MAXK = 32
 
 
@@ -61,6 +63,11 @@ def verify_request(logits, drafts, q_rows, seed, rid, L, mode, temperature=1.0):
     logits = np.asarray(logits, dtype=np.float64)
     k = len(drafts)
     assert logits.shape[0] == k + 1
+    if mode == PREFILL:
+        # eq:prefill_computation: the chain is a chunk of the prompt, every
+        # row's KV is kept (a = k); y = argmax l_k is the model's next token after the chunk
+        y = argmax_lowest(logits[k])
+        return dict(a=k, emitted=list(drafts) + [y], indep=0, prefill=True)
     if mode == GREEDY:
         top = [argmax_lowest(logits[j]) for j in range(k + 1)]
         a = 0
@@ -128,6 +135,8 @@ def new_stats():
 
 def accumulate_stats(stats, depths, results):
     """a7: fold one verify call's per-request results into the lane counters."""
+    if any(r.get("prefill") for r in results):      # prefill chunks are not speculation
+        return stats
     stats["steps"] += 1
     for k, r in zip(depths, results):
         a = r["a"]

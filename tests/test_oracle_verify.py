@@ -270,3 +270,20 @@ def test_zero_residual_falls_back_to_target():
     logits = np.log(np.stack([p, p]))
     s = verify.race_scores(logits[0], q[0], 0, 1, 2, 3, 1.0, residual=True)
     assert np.all(np.isfinite(s))
+
+
+def test_prefill_mode_keeps_the_chunk_and_predicts_the_next_token():
+    """NEXT-3 reading R29: a = k, emitted = the chunk's tokens + argmax of the last row; equals
+    GREEDY when the chunk happens to be the greedy argmax chain; no lane counters."""
+    rng = np.random.default_rng(3)
+    V, k = 40, 6
+    lg = rng.normal(size=(k + 1, V))
+    drafts = [int(x) for x in rng.integers(0, V, size=k)]
+    r = verify.verify_request(lg, drafts, None, 1, 2, 10, verify.PREFILL)
+    assert r["a"] == k and r["emitted"] == drafts + [int(np.argmax(lg[k]))]
+    chain = [int(np.argmax(lg[j])) for j in range(k)]
+    assert verify.verify_request(lg, chain, None, 1, 2, 10, verify.PREFILL) == \
+        dict(verify.verify_request(lg, chain, None, 1, 2, 10, verify.GREEDY), indep=0, prefill=True)
+    st = verify.new_stats()
+    verify.accumulate_stats(st, [k], [r])
+    assert st["steps"] == 0 and st["emitted"] == 0
