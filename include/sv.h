@@ -66,7 +66,7 @@ typedef enum {
   SV_EDEVICE = 6   /* other device-detected error (bad token id, bad n_keep; sticky) */
 } sv_status;
 
-typedef enum { SV_GREEDY = 0, SV_SAMPLE = 1 } sv_mode;
+typedef enum { SV_GREEDY = 0, SV_SAMPLE = 1, SV_PREFILL = 2 } sv_mode;
 
 /* Device error word bits (sv_lane_stats.device_error). */
 #define SV_DERR_BAD_TOKEN 1   /* a draft / pending token outside [0, V) */
@@ -142,7 +142,9 @@ sv_status sv_append_kv(sv_ctx* ctx, int32_t slot, uint64_t request_id, const voi
  *   draft_probs  [sum k][V] fp32 rows q_j (the drafter's distributions) or NULL = one-hot drafts
  *   seed: Philox key; mode: SV_GREEDY (argmax prefix match; seed, temperature and
  *   draft_probs ignored) or SV_SAMPLE (Leviathan: accept iff u < p/q, residual /
- *   bonus exponential race); temperature > 0 in SAMPLE (p = softmax(l / T)).
+ *   bonus exponential race); temperature > 0 in SAMPLE (p = softmax(l / T)); or SV_PREFILL
+ *   (chunked prefill, NEXT-3 / DESIGN.md R29: the "drafts" are the next prompt tokens and every
+ *   row is kept, a = k; y = argmax of the last row; lane counters untouched).
  * Outputs (device, written in stream order):
  *   accepted_len [batch] int32 a_b in [0, k_b] (-1 if the request hit a device error)
  *   out_tokens   [batch][max_depth + 1] int32: d_1..d_a, y, then -1 padding
@@ -259,6 +261,23 @@ sv_status sv_kv_send(const void* kv_packed, int32_t n_layers, int32_t n_kv_heads
 sv_status sv_kv_recv_append(sv_ctx* ctx, int32_t slot, uint64_t request_id, int32_t n_tokens,
                             void* staging, int peer, void* nccl_comm);
 size_t sv_kv_packed_bytes(const sv_config* cfg, int32_t n_tokens);
+
+/* Chunked prefill (NEXT-3, eq:prefill_computation PAPER.md:248-253, R29) of a prompt of
+ * n >= 1 tokens (host array) into an EMPTY slot bound to request_id: the first token becomes the
+ * chain head; each chunk of <= `chunk` tokens (1 <= chunk <= max_depth + 1) runs one SV_PREFILL
+ * verify + commit (every row's KV kept), the next chunk's head set as the pending token. After
+ * the call the slot holds KV for all n prompt tokens and its pending token is the model's greedy
+ * next token, also written to *next_token (host, may be NULL). Synchronous (reads the token back).
+ * EINVAL: bad arguments; ESTATE: slot not EMPTY or a verify outstanding. */
+sv_status sv_prefill(sv_ctx* ctx, int32_t slot, uint64_t request_id, const int32_t* prompt, int32_t n,
+                     int32_t chunk, int32_t* next_token);
+
+/* Prefill side, after a chunked prefill in this lane: pack the first n_tokens committed KV rows
+ * of `slot` (all layers, gathered from its pages) plus its pending token into the wire format
+ * above. kv_packed: DEVICE, >= sv_kv_packed_bytes(cfg, n_tokens), 16-byte aligned. Stream-ordered
+ * on the lane's stream. EINVAL: bad slot / pointer; ESTATE: slot not ACTIVE. n_tokens beyond the
+ * slot's length sets SV_DERR_MAX_POS and packs nothing. */
+sv_status sv_kv_pack_slot(sv_ctx* ctx, int32_t slot, int32_t n_tokens, void* kv_packed);
 
 /* Append a hand-off message that is already in device memory (same-GPU prefill, or a
  * caller-side transport): kv_packed in the wire format above, n_tokens entries, the

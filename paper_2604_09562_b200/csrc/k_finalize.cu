@@ -98,7 +98,9 @@ __global__ void __launch_bounds__(FIN_THREADS) finalize_kernel(LaneDev d, const 
   // 2. accept scan (serial over k <= 32)
   if (tid == 0) {
     int a = k, indep = 0;
-    if (mode == SV_GREEDY) {
+    if (mode == SV_PREFILL) {                      // R29: the chunk's rows are all kept
+      s_y = s_top[k];
+    } else if (mode == SV_GREEDY) {
       for (int j = 1; j <= k; ++j) {
         const bool acc = drafts[doff + j - 1] == s_top[j - 1];
         indep += acc;
@@ -119,13 +121,13 @@ __global__ void __launch_bounds__(FIN_THREADS) finalize_kernel(LaneDev d, const 
     }
     s_a = a;
     s_indep = indep;
-    s_resid = (mode != SV_GREEDY) && (a < k);
+    s_resid = (mode == SV_SAMPLE) && (a < k);
   }
   __syncthreads();
   const int a = s_a;
 
   // 3. exponential race over the one selected row (sampled mode only)
-  if (mode != SV_GREEDY) {
+  if (mode == SV_SAMPLE) {
     const bool resid = s_resid;
     const float* lrow = logits + (size_t)(r0 + a) * V;
     const float m = s_m[a], invS = 1.0f / s_S[a];
@@ -178,8 +180,8 @@ __global__ void __launch_bounds__(FIN_THREADS) finalize_kernel(LaneDev d, const 
   if (tid == 0) {
     acc_out[b] = err ? -1 : a;
     if (d.acc_int) d.acc_int[b] = err ? -1 : a;
-    if (b == 0) atomicAdd(&d.stats[ST_STEPS], 1ull);
-    if (!err) {
+    if (b == 0 && mode != SV_PREFILL) atomicAdd(&d.stats[ST_STEPS], 1ull);
+    if (!err && mode != SV_PREFILL) {                 // prefill chunks are not speculation
       atomicAdd(&d.stats[ST_ROWS], (unsigned long long)(k + 1));
       atomicAdd(&d.stats[ST_DRAFTED], (unsigned long long)k);
       atomicAdd(&d.stats[ST_ACCEPTED], (unsigned long long)a);

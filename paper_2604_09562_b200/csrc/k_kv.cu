@@ -205,4 +205,38 @@ cudaError_t launch_kv_pack(const bf16* k, const bf16* v, int n_layers, int Hkv, 
   return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------ a9 prefill side: pack a slot
+// Committed rows 0..n-1 of `slot` (all layers, from its pages) + its pending token -> the wire
+// format [n_layers][n][2][Hkv][dh] bf16 + 16-byte trailer. n > len sets SV_DERR_MAX_POS.
+__global__ void kv_pack_slot_kernel(LaneDev d, int slot, int n, bf16* __restrict__ out) {
+  const int L = d.len[slot];
+  if (n > L) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(d.err, SV_DERR_MAX_POS);
+    return;
+  }
+  const int vpr = d.dh / 8;
+  const size_t per_tok = (size_t)2 * d.Hkv * vpr;
+  const size_t total = (size_t)d.n_layers * n * per_tok;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+    const int layer = int(i / ((size_t)n * per_tok));
+    const int t = int((i / per_tok) % n);
+    const int rem = int(i % per_tok);
+    const int kv = rem / (d.Hkv * vpr), h = (rem / vpr) % d.Hkv, v8 = rem % vpr;
+    const int page = d.page_table[slot * d.max_pages_per_slot + t / d.page];
+    const bf16* src = d.pool + pool_row(d, layer, page, kv, h, t % d.page) * d.dh + v8 * 8;
+    *reinterpret_cast<uint4*>(out + i * 8) = *reinterpret_cast<const uint4*>(src);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    int* trailer = reinterpret_cast<int*>(out + total * 8);
+    trailer[0] = d.pending[slot];
+    trailer[1] = trailer[2] = trailer[3] = 0;
+  }
+}
+
+cudaError_t launch_kv_pack_slot(const LaneDev& d, int slot, int n, void* packed, cudaStream_t s) {
+  SV_COUNT_LAUNCH();
+  kv_pack_slot_kernel<<<148 * 2, 256, 0, s>>>(d, slot, n, reinterpret_cast<bf16*>(packed));
+  return cudaGetLastError();
+}
+
 }  // namespace sv

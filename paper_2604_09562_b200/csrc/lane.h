@@ -126,6 +126,7 @@ cudaError_t launch_debug_uniforms(uint64_t seed, uint64_t rid, uint32_t z, int p
                                   cudaStream_t s);
 cudaError_t launch_draft_planted(const LaneDev& d, const PlanArgs& p, const int* succ, const uint8_t* mask,
                                  const int* dev_tok, int* draft_tokens, cudaStream_t s);
+cudaError_t launch_kv_pack_slot(const LaneDev& d, int slot, int n, void* packed, cudaStream_t s);
 cudaError_t launch_kv_pack(const bf16* k, const bf16* v, int n_layers, int Hkv, int dh, int n, int pending,
                            void* packed, cudaStream_t s);
 

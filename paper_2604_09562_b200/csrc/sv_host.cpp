@@ -26,7 +26,7 @@ struct Layout {
   size_t h0, h1, h2, cbuf, logits, tile_max, tile_sum, tile_arg;
   size_t a, b, z, q, kc, vc, o, u;
   size_t items, item_start, n_items, part_o, part_ml, acc_int, tok_int, batch_n;
-  size_t gemm_ws, trace;
+  size_t gemm_ws, trace, prefill;
   size_t max_items;
 
   size_t take(size_t bytes) {
@@ -112,6 +112,7 @@ Layout make_layout(const sv_config& c) {
   L.batch_n = L.take(4);
   L.gemm_ws = L.take(sv::gemm_workspace_bytes((int)T, (int)cmax));
   L.trace = L.take(8 * 16 * 256);
+  L.prefill = L.take(4 * 3 * (size_t)(c.max_depth + 2));   // sv_prefill: chunk tokens + outputs
   L.total = (L.total + 1023) & ~size_t(1023);
   return L;
 }
@@ -426,7 +427,7 @@ sv_status sv_verify(sv_ctx* c, int32_t batch, const int32_t* slots, const int32_
                     const int32_t* draft_tokens, const float* draft_probs, uint64_t seed, sv_mode mode,
                     float temperature, int32_t* accepted_len, int32_t* out_tokens, float* logits_out) {
   if (!c || !accepted_len || !out_tokens) return SV_EINVAL;
-  if (mode != SV_GREEDY && mode != SV_SAMPLE) return SV_EINVAL;
+  if (mode != SV_GREEDY && mode != SV_SAMPLE && mode != SV_PREFILL) return SV_EINVAL;
   if (mode == SV_SAMPLE && !(temperature > 0.f)) return SV_EINVAL;
   if (c->pending_verify) return SV_ESTATE;
   sv::PlanArgs p;
@@ -467,7 +468,7 @@ sv_status sv_verify(sv_ctx* c, int32_t batch, const int32_t* slots, const int32_
   e.inv_temp = inv_temp;
   // greedy decisions need only the vocab-tile statistics: the fp32 logits (T x V x 4 bytes)
   // are stored only when something reads them
-  e.write_out = c->taps || mode != SV_GREEDY || logits_out != nullptr;
+  e.write_out = c->taps || mode == SV_SAMPLE || logits_out != nullptr;
   STAGE(c, ST_LM_HEAD, gemm(c, d.z, d.lm_head, d.logits, T, d.V, d.D, sv::EPI_LOGITS, e));
   STAGE(c, ST_FINALIZE, sv::launch_finalize(d, batch, draft_tokens, draft_probs, d.logits, seed, mode, inv_temp,
                                             accepted_len, out_tokens, s));
@@ -487,7 +488,7 @@ sv_status sv_verify_logits(sv_ctx* c, int32_t batch, const int32_t* slots, const
                            uint64_t seed, sv_mode mode, float temperature, int32_t* accepted_len,
                            int32_t* out_tokens) {
   if (!c || !accepted_len || !out_tokens || !logits) return SV_EINVAL;
-  if (mode != SV_GREEDY && mode != SV_SAMPLE) return SV_EINVAL;
+  if (mode != SV_GREEDY && mode != SV_SAMPLE && mode != SV_PREFILL) return SV_EINVAL;
   if (mode == SV_SAMPLE && !(temperature > 0.f)) return SV_EINVAL;
   if (c->pending_verify) return SV_ESTATE;
   sv::PlanArgs p;
@@ -644,6 +645,46 @@ sv_status sv_draft_planted(sv_ctx* c, int32_t batch, const int32_t* slots, const
     p.T += depths[b] + 1;
   }
   STAGE(c, ST_DRAFT, sv::launch_draft_planted(c->d, p, succ, dev_mask, dev_tok, draft_tokens, c->stream));
+  return SV_OK;
+}
+
+sv_status sv_prefill(sv_ctx* c, int32_t slot, uint64_t request_id, const int32_t* prompt, int32_t n, int32_t chunk,
+                     int32_t* next_token) {
+  if (!c || slot < 0 || slot >= c->cfg.max_slots || !prompt || n < 1 || chunk < 1 || chunk > c->cfg.max_depth + 1)
+    return SV_EINVAL;
+  if (c->state[slot] != EMPTY || c->pending_verify) return SV_ESTATE;
+  for (int i = 0; i < n; ++i)
+    if (prompt[i] < 0 || prompt[i] >= c->cfg.vocab) return SV_EINVAL;
+  const int K1 = c->cfg.max_depth + 2;
+  int32_t* dtok = (int32_t*)(c->ws + c->lay.prefill);     // chunk tokens
+  int32_t* dacc = dtok + K1;                               // accepted_len [1]
+  int32_t* dout = dacc + K1;                               // out_tokens [max_depth + 1]
+  sv_status st = sv_append_kv(c, slot, request_id, nullptr, nullptr, 0, prompt[0]);
+  if (st) return st;
+  int pos = 1, k = 0;
+  for (;;) {
+    k = chunk - 1 < n - pos ? chunk - 1 : n - pos;
+    if (k > 0) SV_CUDA(cudaMemcpyAsync(dtok, prompt + pos, 4 * (size_t)k, cudaMemcpyHostToDevice, c->stream));
+    if ((st = sv_verify(c, 1, &slot, &k, dtok, nullptr, 0, SV_PREFILL, 1.0f, dacc, dout, nullptr))) return st;
+    if ((st = sv_commit(c, nullptr))) return st;
+    pos += k;
+    if (pos >= n) break;
+    if ((st = sv_append_kv(c, slot, request_id, nullptr, nullptr, 0, prompt[pos]))) return st;
+    pos += 1;
+  }
+  int32_t y = -1;
+  SV_CUDA(cudaMemcpyAsync(&y, dout + k, 4, cudaMemcpyDeviceToHost, c->stream));
+  SV_CUDA(cudaStreamSynchronize(c->stream));
+  if (y < 0) return SV_EDEVICE;
+  if (next_token) *next_token = y;
+  return SV_OK;
+}
+
+sv_status sv_kv_pack_slot(sv_ctx* c, int32_t slot, int32_t n_tokens, void* kv_packed) {
+  if (!c || slot < 0 || slot >= c->cfg.max_slots || n_tokens < 0 || !kv_packed || ((uintptr_t)kv_packed & 15))
+    return SV_EINVAL;
+  if (c->state[slot] != ACTIVE) return SV_ESTATE;
+  SV_CUDA(sv::launch_kv_pack_slot(c->d, slot, n_tokens, kv_packed, c->stream));
   return SV_OK;
 }
 

@@ -20,7 +20,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("SV_LIBSV", os.path.join(_HERE, "libsv.so"))   # override: experiments only
 
 SV_OK, SV_EINVAL, SV_ESTATE, SV_ENOKV, SV_ECUDA, SV_ENCCL, SV_EDEVICE = range(7)
-GREEDY, SAMPLE = 0, 1
+GREEDY, SAMPLE, PREFILL = 0, 1, 2
 _STATUS = {0: "SV_OK", 1: "SV_EINVAL", 2: "SV_ESTATE", 3: "SV_ENOKV", 4: "SV_ECUDA", 5: "SV_ENCCL", 6: "SV_EDEVICE"}
 
 EXPORTED = [
@@ -30,7 +30,7 @@ EXPORTED = [
     "sv_kv_recv_append", "sv_kv_packed_bytes", "sv_kv_pack", "sv_profile_enable", "sv_profile_num_stages",
     "sv_profile_stage_name", "sv_profile_read", "sv_launch_count", "sv_debug_gemm", "sv_kv_append_packed",
     "sv_kv_loopback_append", "sv_spec_default_config", "sv_spec_reset", "sv_spec_adapt", "sv_spec_step",
-    "sv_route_default_config", "sv_route_select", "sv_lane_occupancy",
+    "sv_route_default_config", "sv_route_select", "sv_lane_occupancy", "sv_kv_pack_slot", "sv_prefill",
 ]
 
 
@@ -113,6 +113,8 @@ def load():
         "sv_kv_recv_append": ([vp, i32, u64, i32, vp, ctypes.c_int, vp], ctypes.c_int),
         "sv_kv_append_packed": ([vp, i32, u64, i32, vp], ctypes.c_int),
         "sv_lane_occupancy": ([vp, P(i32), P(i32)], ctypes.c_int),
+        "sv_kv_pack_slot": ([vp, i32, i32, vp], ctypes.c_int),
+        "sv_prefill": ([vp, i32, u64, P(i32), i32, i32, P(i32)], ctypes.c_int),
         "sv_kv_loopback_append": ([vp, i32, u64, i32, vp, vp, ctypes.c_int, vp], ctypes.c_int),
         "sv_kv_packed_bytes": ([P(Config), i32], sz),
         "sv_kv_pack": ([vp, vp, i32, i32, i32, i32, i32, vp, vp], ctypes.c_int),
@@ -207,13 +209,17 @@ class Lane:
         _check(self.lib.sv_append_kv(self.ctx, slot, request_id, _ptr(k), _ptr(v), n, int(pending_token)),
                "sv_append_kv")
 
+    @staticmethod
+    def _mode(mode):
+        return {"greedy": GREEDY, "sample": SAMPLE, "prefill": PREFILL}.get(mode, mode)
+
     def verify(self, slots, depths, draft_tokens, draft_probs=None, seed=0, mode="greedy", temperature=1.0,
                logits_out=None, out=None):
         """Returns (accepted_len [B] int32, out_tokens [B][max_depth+1] int32) device tensors."""
         s, B = _i32_array(slots)
         dpt, _ = _i32_array(depths)
         acc, tok = (self._acc[:B], self._tok[:B]) if out is None else out
-        m = GREEDY if mode in ("greedy", GREEDY) else SAMPLE
+        m = self._mode(mode)
         _check(self.lib.sv_verify(self.ctx, B, s, dpt, _ptr(draft_tokens), _ptr(draft_probs), seed, m,
                                   float(temperature), _ptr(acc), _ptr(tok), _ptr(logits_out)), "sv_verify")
         return acc, tok
@@ -223,10 +229,18 @@ class Lane:
         s, B = _i32_array(slots)
         dpt, _ = _i32_array(depths)
         acc, tok = self._acc[:B], self._tok[:B]
-        m = GREEDY if mode in ("greedy", GREEDY) else SAMPLE
+        m = self._mode(mode)
         _check(self.lib.sv_verify_logits(self.ctx, B, s, dpt, _ptr(draft_tokens), _ptr(draft_probs), _ptr(logits),
                                          seed, m, float(temperature), _ptr(acc), _ptr(tok)), "sv_verify_logits")
         return acc, tok
+
+    def prefill(self, slot, request_id, prompt, chunk):
+        """Chunked prefill (sv_prefill; NEXT-3, R29) of `prompt` (host ints) into an EMPTY
+        slot. Returns the model's greedy next token after the prompt (the slot's pending token)."""
+        p, n = _i32_array(prompt)
+        nxt = ctypes.c_int32()
+        _check(self.lib.sv_prefill(self.ctx, slot, request_id, p, n, chunk, ctypes.byref(nxt)), "sv_prefill")
+        return nxt.value
 
     def commit(self, n_keep=None):
         _check(self.lib.sv_commit(self.ctx, _ptr(n_keep)), "sv_commit")
@@ -310,6 +324,11 @@ class Lane:
     def kv_recv_append(self, slot, request_id, n_tokens, staging, peer, comm):
         _check(self.lib.sv_kv_recv_append(self.ctx, slot, request_id, n_tokens, _ptr(staging), peer, comm),
                "sv_kv_recv_append")
+
+    def kv_pack_slot(self, slot, n_tokens, out):
+        """Prefill side: committed KV rows 0..n_tokens-1 of `slot` + its pending token, wire format."""
+        _check(self.lib.sv_kv_pack_slot(self.ctx, slot, n_tokens, _ptr(out)), "sv_kv_pack_slot")
+        return out
 
     def kv_append_packed(self, slot, request_id, n_tokens, packed):
         _check(self.lib.sv_kv_append_packed(self.ctx, slot, request_id, n_tokens, _ptr(packed)), "sv_kv_append_packed")
