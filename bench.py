@@ -118,8 +118,8 @@ class Clocks:
 
 
 # ------------------------------------------------------------------ workload setup
-def planted_weights(wl):
-    w = synth.model_weights(wl.cfg, seed=0, embed_std=wl.embed_std)
+def planted_weights(wl, device="cpu"):
+    w = synth.model_weights(wl.cfg, seed=0, embed_std=wl.embed_std, device=device)
     if wl.beta > 0:
         return synth.planted_successor(wl.cfg, w, seed=1, beta=wl.beta)
     return w, torch.randperm(wl.cfg.vocab, generator=torch.Generator().manual_seed(1)).to(torch.int32)
@@ -128,17 +128,19 @@ def planted_weights(wl):
 def build_lane(wl, rank, dev):
     from paper_2604_09562_b200 import sv
     cfg = wl.cfg
-    w, succ = planted_weights(wl)
+    gdev = dev if wl.gen_on_device else "cpu"
+    w, succ = planted_weights(wl, gdev)
     wd = {k: v.to(dev) for k, v in w.items()}
     lane = sv.Lane(cfg, wd)
     ctx = synth.ctx_lengths(wl, seed=100 + rank)
     reqs = []
     for i, n in enumerate(ctx):
-        k, v = synth.context_kv(cfg, n, seed=10_000 * (rank + 1) + i)
+        k, v = synth.context_kv(cfg, n, seed=10_000 * (rank + 1) + i, device=gdev)
         pend = int(synth.random_tokens(1, cfg.vocab, seed=20_000 * (rank + 1) + i)[0])
         rid = svdist.request_id(rank, i)
         lane.append_kv(i, rid, k.to(dev), v.to(dev), pend)
-        reqs.append(dict(L=n, rid=rid, pending=pend, k=k, v=v))
+        reqs.append(dict(L=n, rid=rid, pending=pend, k=None if wl.gen_on_device else k,
+                         v=None if wl.gen_on_device else v))
     torch.cuda.synchronize(dev)
     return lane, w, succ, reqs
 
@@ -155,7 +157,7 @@ def algorithmic(wl, ctx_lens, depths):
     kv_tok = 2 * cfg.n_kv_heads * cfg.head_dim * 2                       # 4096 B / token / layer
     attn_bytes = sum(L * kv_tok for L in ctx_lens) + T * kv_tok + T * 2 * cfg.n_q_heads * cfg.head_dim * 2
     lm_flops = 2.0 * T * cfg.d_model * cfg.vocab
-    return dict(T=T, attn_bytes=attn_bytes * cfg.n_layers, lm_flops=lm_flops)
+    return dict(T=T, attn_bytes=attn_bytes, lm_flops=lm_flops)      # per launch: attention runs once per layer
 
 
 class ControlledDepths:
@@ -496,10 +498,11 @@ def cpu_baseline(wl, res, budget_s=20.0):
 
 def bench_config(wl, world):
     """The workload description both arms report (the driver pairs lines by it)."""
-    return {"workload": wl.name, "model": "Llama-3-8B-shaped 1 layer + lm-head (random init, planted successor)"
-            if wl.cfg.d_model == 4096 else "toy", "batch_per_gpu": wl.batch, "depth": [wl.kmin, wl.kmax],
+    nl = wl.cfg.n_layers
+    return {"workload": wl.name, "model": f"Llama-3-8B-shaped {nl} layer{'s' if nl > 1 else ''} + lm-head (random init, "
+            "planted successor)" if wl.cfg.d_model == 4096 else "toy", "batch_per_gpu": wl.batch, "depth": [wl.kmin, wl.kmax],
             "ctx": list(wl.ctx), "mode": wl.mode, "parallelism": f"dp{world} (independent decode lanes)",
-            "l2": "inputs > L2 (weights 1.5 GB + KV >= 1 GB per step)", "drafter": f"planted alpha={wl.alpha}"}
+            "l2": "inputs > L2 (weights >= 1.5 GB + KV >= 1 GB per step)", "drafter": f"planted alpha={wl.alpha}"}
 
 
 REFERENCE_BUDGET_S = 150.0   # the reference arm's timed steps are time-boxed to this
@@ -616,7 +619,7 @@ def main():
     if args.detail:
         line["stages"] = {k: {"us": round(v["ms_per_launch"] * 1e3, 1), "share": round(v["share"], 4)}
                           for k, v in res["prof"].items()}
-    if world == 1 and not args.no_cpu_baseline:
+    if world == 1 and not args.no_cpu_baseline and not wl.gen_on_device:
         line["cpu_baseline"] = cpu_baseline(wl, res)
     print(json.dumps(line, default=_json_default), flush=True)
     if world > 1:

@@ -58,30 +58,34 @@ LLAMA = ModelConfig(n_layers=1, d_model=4096, n_q_heads=32, n_kv_heads=8, head_d
 CONFIGS = {"toy": TOY, "toy_mlp": TOY_MLP, "llama": LLAMA}
 
 
-def _gen(seed):
-    g = torch.Generator(device="cpu")
+def _gen(seed, device="cpu"):
+    g = torch.Generator(device=device)
     g.manual_seed(int(seed))
     return g
 
 
-def model_weights(cfg, seed=0, std=0.02, embed_std=1.0, norm_one=True):
+def model_weights(cfg, seed=0, std=0.02, embed_std=1.0, norm_one=True, device="cpu"):
     """Random-init weights, bf16, [out, in] row-major, layer-stacked.
 
     fp32 N(0, std^2) draws rounded once to bf16 by torch's cast (SURVEY.md §8(c)
     S19: identical values are fed to both paths). Norm gains are 1 (or
     1 + N(0, 0.1^2) with norm_one=False, to exercise the gain multiply).
     """
-    g = _gen(seed)
+    g = _gen(seed, device)
     L, D, V, F = cfg.n_layers, cfg.d_model, cfg.vocab, cfg.ffn_dim
     hd = cfg.n_q_heads * cfg.head_dim
 
     def rn(*shape, s):
-        return (torch.randn(*shape, generator=g, dtype=torch.float32) * s).to(torch.bfloat16)
+        out = torch.empty(*shape, dtype=torch.bfloat16, device=device)
+        flat = out.view(shape[0], -1)
+        for i in range(shape[0]):            # per leading index: bounded fp32 scratch for big models
+            flat[i] = (torch.randn(flat.shape[1], generator=g, dtype=torch.float32, device=device) * s).to(torch.bfloat16)
+        return out
 
     def norm(*shape):
         if norm_one:
-            return torch.ones(*shape, dtype=torch.bfloat16)
-        return (1.0 + 0.1 * torch.randn(*shape, generator=g)).to(torch.bfloat16)
+            return torch.ones(*shape, dtype=torch.bfloat16, device=device)
+        return (1.0 + 0.1 * torch.randn(*shape, generator=g, device=device)).to(torch.bfloat16)
 
     w = {
         "embed": rn(V, D, s=embed_std),
@@ -89,20 +93,20 @@ def model_weights(cfg, seed=0, std=0.02, embed_std=1.0, norm_one=True):
         "wqkv": rn(L, cfg.qkv_rows, D, s=std),
         "wo": rn(L, D, hd, s=std),
         "ffn_norm": norm(L, D),
-        "w_gate_up": rn(L, 2 * F, D, s=std) if F > 0 else torch.zeros(L, 0, D, dtype=torch.bfloat16),
-        "w_down": rn(L, D, F, s=std) if F > 0 else torch.zeros(L, D, 0, dtype=torch.bfloat16),
+        "w_gate_up": rn(L, 2 * F, D, s=std) if F > 0 else torch.zeros(L, 0, D, dtype=torch.bfloat16, device=device),
+        "w_down": rn(L, D, F, s=std) if F > 0 else torch.zeros(L, D, 0, dtype=torch.bfloat16, device=device),
         "final_norm": norm(D),
         "lm_head": rn(V, D, s=std),
     }
     return w
 
 
-def context_kv(cfg, n_tokens, seed, std=1.0):
+def context_kv(cfg, n_tokens, seed, std=1.0, device="cpu"):
     """Synthetic post-RoPE context K/V for one request: [n_layers][n][H_kv][d_h] bf16."""
-    g = _gen(seed)
+    g = _gen(seed, device)
     shape = (cfg.n_layers, n_tokens, cfg.n_kv_heads, cfg.head_dim)
-    k = (torch.randn(*shape, generator=g) * std).to(torch.bfloat16)
-    v = (torch.randn(*shape, generator=g) * std).to(torch.bfloat16)
+    k = (torch.randn(*shape, generator=g, device=device) * std).to(torch.bfloat16)
+    v = (torch.randn(*shape, generator=g, device=device) * std).to(torch.bfloat16)
     return k, v
 
 
@@ -152,7 +156,7 @@ def planted_successor(cfg, weights, seed, beta):
     E = weights["embed"].to(torch.float32)
     En = E / E.norm(dim=1, keepdim=True)
     lm = weights["lm_head"].to(torch.float32).clone()
-    lm[f] += beta * En
+    lm[f.to(lm.device)] += beta * En
     w = dict(weights)
     w["lm_head"] = lm.to(torch.bfloat16)
     return w, f.to(torch.int32)
@@ -173,6 +177,7 @@ class Workload:
     beta: float = 0.3     # planted-successor strength (logit margin ~ beta * sqrt(D))
     temperature: float = 1.0
     controller: bool = False   # depths from the SpecuStream controller (NEXT-1) instead of U{kmin..kmax}
+    gen_on_device: bool = False  # draw weights / context KV with a CUDA generator (multi-GB models)
     alpha_sigma: float = 0.0   # per-request acceptance follows AR(1) around alpha with this stationary std
 
 
@@ -185,6 +190,10 @@ def workload(name, steps_budget=64):
         n_pages, max_pos = pool(64, 4096, 8)
         cfg = LLAMA.with_(n_pages=n_pages, max_slots=64, max_batch=64, max_pos=max_pos)
         return Workload("ns", cfg, 64, (4096, 4096), 8, 8, "greedy", 0.8)
+    if name == "ns32":        # NEXT-4: the north-star batch through all 32 Llama-3-8B layers
+        n_pages, max_pos = pool(64, 4096, 8)
+        cfg = LLAMA.with_(n_layers=32, n_pages=n_pages, max_slots=64, max_batch=64, max_pos=max_pos)
+        return Workload("ns32", cfg, 64, (4096, 4096), 8, 8, "greedy", 0.8, gen_on_device=True)
     if name == "c2":          # BASELINE configs[1]: bs64, adaptive k 1-8, ALPACA-like 256-token prompts
         n_pages, max_pos = pool(64, 256, 8)
         cfg = LLAMA.with_(n_pages=n_pages, max_slots=64, max_batch=64, max_pos=max_pos)
