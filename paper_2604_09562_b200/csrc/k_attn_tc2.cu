@@ -119,7 +119,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint64_t* s_free = p_full + 2;
   uint64_t* o_full = s_free + 2;
   uint64_t* o_empty = o_full + 2;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(o_empty + 2);
+  uint64_t* s_read = o_empty + 2;                       // softmax has read S^T buffer: MMA may refill it
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(s_read + 2);
   float* thr_s = reinterpret_cast<float*>(bars + 32);   // [2][32] raise thresholds (mref + 8, or -inf)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -153,6 +154,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       tc::mbar_init(&s_free[i], 1);
       tc::mbar_init(&o_full[i], 1);
       tc::mbar_init(&o_empty[i], SOFTMAX_THREADS);
+      tc::mbar_init(&s_read[i], SOFTMAX_THREADS);
     }
     tc::fence_barrier_init();
   }
@@ -202,22 +204,29 @@ __global__ void __launch_bounds__(THREADS, 1)
       for (int t = 0; t < I.n_tiles; ++t) {
         uint8_t* dst = ring + st * KV_BYTES;
         if (t < I.n_page_tiles) {
-          if (lane == 0) {
-            const int np = min(2, I.n_pages - 2 * t);
-            int rows[2];
-            for (int pp = 0; pp < np; ++pp) {
-              const int page = d.page_table[I.slot * d.max_pages_per_slot + I.page0 + 2 * t + pp];
-              rows[pp] = ((((layer * d.n_pages + page) * 2 + kv) * d.Hkv) + I.h) * 64;
-            }
-            tc::mbar_wait(&empty[st], ph ^ 1);
-            if (is_k) SV_TR2(0, ptile);
-            tc::mbar_arrive_expect_tx(&full[st], np * (KV_BYTES / 2));
-            for (int pp = 0; pp < np; ++pp)
-              for (int hf = 0; hf < HALVES; ++hf)
-                tc::tma_load_2d_hint(dst + hf * (KT * 128) + pp * (64 * 128), &map_kv, &full[st], hf * 64, rows[pp],
-                                     pol);
-            if (is_k) SV_TR2(1, ptile);
+          // converged warp: lanes 0 / 1 look up the tile's two pages, the rows are broadcast, one
+          // elected lane issues (keeps the TMA issue out of a lane-0 waterfall loop)
+          const int np = min(2, I.n_pages - 2 * t);
+          int row = 0;
+          if (lane < np) {
+            const int page = d.page_table[I.slot * d.max_pages_per_slot + I.page0 + 2 * t + lane];
+            row = ((((layer * d.n_pages + page) * 2 + kv) * d.Hkv) + I.h) * 64;
           }
+          const int row0 = __shfl_sync(0xffffffffu, row, 0), row1 = __shfl_sync(0xffffffffu, row, 1);
+          tc::mbar_wait(&empty[st], ph ^ 1);
+          if (is_k && lane == 0) SV_TR2(0, ptile);
+          if (tc::elect_one()) {
+            tc::mbar_arrive_expect_tx(&full[st], np * (KV_BYTES / 2));
+#pragma unroll
+            for (int hf = 0; hf < HALVES; ++hf)
+              tc::tma_load_2d_hint(dst + hf * (KT * 128), &map_kv, &full[st], hf * 64, row0, pol);
+            if (np > 1) {
+#pragma unroll
+              for (int hf = 0; hf < HALVES; ++hf)
+                tc::tma_load_2d_hint(dst + hf * (KT * 128) + 64 * 128, &map_kv, &full[st], hf * 64, row1, pol);
+            }
+          }
+          if (is_k && lane == 0) SV_TR2(1, ptile);
           __syncwarp();
         } else {
           if (lane == 0) tc::mbar_wait(&empty[st], ph ^ 1);
@@ -265,7 +274,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             const int sb = g & 1;
             tc::mbar_wait(&k_full[ks], kph);
             if (lane == 0) SV_TR2(2, g);
-            tc::mbar_wait(&s_free[sb], ((g >> 1) & 1) ^ 1);
+            tc::mbar_wait(&s_read[sb], ((g >> 1) & 1) ^ 1);   // S^T(g-2) read out: refill now
             if (lane == 0) SV_TR2(3, g);
             tc::fence_after();
             const uint32_t sk = tc::smem_u32(sK + ks * KV_BYTES);
@@ -360,6 +369,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         __syncwarp();
         tc::tmem_ld32(tmem + lane_off + S_COL + sb * NQ + ch * 32, sv);
         tc::tmem_ld_wait();
+        tc::fence_before();
+        tc::mbar_arrive(&s_read[sb]);                 // the MMA may write S^T(g+2) into this buffer
         if (warp == 4 && lane == 0) SV_TR2(8, g);
         const bool chain_tile = t >= I.n_page_tiles;
         const int key = (chain_tile ? I.L : I.t0 + t * KT) + kidx;
