@@ -275,7 +275,7 @@ def run_gpu(args, wl, rank, world, dev):
     tokens = st["emitted"]
     # ----- roofline of the dominant kernels (live CUDA-event durations, averaged per launch)
     pk = peaks()
-    traffic = ncu_traffic()
+    traffic = ncu_traffic() if wl.name == "ns" else {}      # the committed capture is of the ns workload
     # per-launch algorithmic work averaged over the timed region: mean T over its steps, context
     # lengths at the region's midpoint (they grow by the emitted tokens)
     ln1 = lane.tap("len", torch.int32, (cfg.max_slots,))[:B].cpu().tolist()
