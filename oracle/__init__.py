@@ -20,7 +20,8 @@ What it computes and where the paper says so:
 Modules: ``philox`` (counter RNG), ``numerics`` (bf16 rounding), ``model``
 (stage functions), ``verify`` (decisions + lane counters), ``lane``
 (free-running dense-cache lane with the sv_* call semantics), ``specustream``
-(Alg. 4 host controller, NEXT-1).
+(Alg. 4 host controller, NEXT-1), ``flowguard`` (Alg. 2 router, NEXT-2), ``tree``
+(token-tree drafts, NEXT-4).
 
 Parity status: see each module header. Everything pinned by the tests named
 there; the exact bits of a Llama-shape verify step beyond those pins are

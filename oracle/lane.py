@@ -9,6 +9,8 @@ per-request, fp64 cache — no pages, no batching, no shared layout:
   start of KV_total; activates the slot and binds request_id (the RNG key).
 * verify     — SURVEY.md §8(c) steps 1-5 per request (model.forward_chain then
   verify.verify_request); side-effect free until commit.
+* verify_tree — token-tree drafts (oracle/tree.py, R30); commit keeps the
+  accepted root-to-node path's rows.
 * commit     — step 6: append chain K/V rows 0..a_i (tokens x_i, d_1..d_a) to
   the cache, L_i += a_i + 1, pending <- y; with n_keep: rows 0..n_keep-1,
   pending = emitted[n_keep-1]. Rejected rows are dropped (rollback).
@@ -20,7 +22,7 @@ L and has no KV yet; chain row j sits at absolute position L + j.
 """
 import numpy as np
 
-from . import model, verify
+from . import model, tree, verify
 
 
 class OracleLane:
@@ -96,6 +98,33 @@ class OracleLane:
         self.pending_batch = (list(slots), list(depths), results, chain)
         return [r["a"] for r in results], [r["emitted"] for r in results], logits_all
 
+    def verify_tree(self, slots, depths, parents, draft_tokens, draft_probs, seed, mode, temperature=1.0,
+                    logits_override=None):
+        """Token-tree verify (oracle/tree.py, R30): parents flat [sum k] (per request,
+        node n's parent in 0..n-1). Returns (accepted_len, emitted, logits, paths)."""
+        results, logits_all, chain = [], [], []
+        off = 0
+        for i, (slot, k) in enumerate(zip(slots, depths)):
+            drafts = [int(t) for t in draft_tokens[off:off + k]]
+            par = [int(t) for t in parents[off:off + k]]
+            q_rows = None if draft_probs is None else np.asarray(draft_probs[off:off + k])
+            off += k
+            st = self.slots[slot]
+            L = self.length(slot)
+            if logits_override is not None:
+                logits, kv = np.asarray(logits_override[i], dtype=np.float64), None
+            else:
+                _, logits, kv = tree.forward_tree(self.w, [st["pending"]] + drafts, par, L,
+                                                  list(zip(st["K"], st["V"])), self.cfg, self.cos, self.sin)
+            r = tree.verify_tree(logits, drafts, par, q_rows, seed, st["rid"], L, mode, temperature)
+            results.append(r)
+            logits_all.append(logits)
+            chain.append(kv)
+        verify.accumulate_stats(self.stats, list(depths), results)
+        self.pending_batch = (list(slots), list(depths), results, chain)
+        return ([r["a"] for r in results], [r["emitted"] for r in results], logits_all,
+                [r["path"] for r in results])
+
     def commit(self, n_keep=None):
         slots, depths, results, chain = self.pending_batch
         for i, slot in enumerate(slots):
@@ -103,9 +132,10 @@ class OracleLane:
             n = r["a"] + 1 if n_keep is None else min(int(n_keep[i]), r["a"] + 1)
             assert n >= 1
             st = self.slots[slot]
+            rows = list(r.get("path", range(r["a"] + 1)))[:n]     # tree: the accepted path's rows
             for layer in range(self.cfg.n_layers):
                 k, v = chain[i][layer]
-                st["K"][layer] = np.concatenate([st["K"][layer], k[:n]], axis=0)
-                st["V"][layer] = np.concatenate([st["V"][layer], v[:n]], axis=0)
+                st["K"][layer] = np.concatenate([st["K"][layer], k[rows]], axis=0)
+                st["V"][layer] = np.concatenate([st["V"][layer], v[rows]], axis=0)
             st["pending"] = int(r["emitted"][n - 1])
         self.pending_batch = None

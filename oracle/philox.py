@@ -101,3 +101,12 @@ def uniform_race(seed, rid, z, vocab):
     lane = (x & np.uint64(3)).astype(np.int64)
     w = np.choose(lane, words)
     return word_to_uniform(w)
+
+
+def uniform_accept_rank(seed, rid, z, s):
+    """Accept uniform of the s-th sibling tried at sequence index z (tree drafts, R30):
+    counter (z, rid_lo, rid_hi, ACCEPT << 28 | s >> 2), output lane s & 3 — the RACE layout with
+    x = s. s = 0 is uniform_accept(seed, rid, z): a chain is a tree of only-children."""
+    ctr = (z, rid & MASK32, (rid >> 32) & MASK32, (ACCEPT << 28) | (int(s) >> 2))
+    w = philox4x32_10(ctr, (seed & MASK32, (seed >> 32) & MASK32))[int(s) & 3]
+    return ((w >> 9) + 0.5) * (2.0 ** -23)
