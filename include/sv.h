@@ -73,6 +73,7 @@ typedef enum { SV_GREEDY = 0, SV_SAMPLE = 1, SV_PREFILL = 2 } sv_mode;
 #define SV_DERR_NO_PAGES 2    /* free list exhausted during append / commit */
 #define SV_DERR_BAD_KEEP 4    /* n_keep < 1 */
 #define SV_DERR_MAX_POS 8     /* a chain or commit would pass max_pos; that request is not committed */
+#define SV_DERR_BAD_TREE 16   /* a token-tree parent outside [0, n-1]; that request is not committed */
 
 typedef struct { /* (host) model + lane configuration */
   int32_t n_layers, d_model, n_q_heads, n_kv_heads, head_dim, vocab;
@@ -167,8 +168,39 @@ sv_status sv_verify_logits(sv_ctx* ctx, int32_t batch, const int32_t* slots, con
                            uint64_t seed, sv_mode mode, float temperature, int32_t* accepted_len,
                            int32_t* out_tokens);
 
+/* Token-tree verify (SURVEY.md §8(f) NEXT-4 "tree-structured drafts"; the paper cites draft
+ * trees as related work; semantics = DESIGN.md reading R30). Request b drafts
+ * k_b = depths[b] tree nodes n = 1..k_b (node 0 is the slot's pending token):
+ *   parents [sum k] int32 DEVICE, request-major: parents[off_b + n - 1] = parent of node n, in
+ *            [0, n - 1] (topological order); anything else sets SV_DERR_BAD_TREE and the request's
+ *            accepted_len = -1 (it is then not committed)
+ *   draft_tokens / draft_probs as in sv_verify, one entry / q row per node (q row n - 1 = the
+ *            distribution node n's token was drawn from, i.e. conditioned on its parent)
+ * Node n sits at position L + depth(n) and attends the cache and its ancestors-or-self.
+ * GREEDY walks from node 0 to the first child (ascending index) whose token is the argmax;
+ * SAMPLE tries a node's children in index order with recursive rejection (accept iff
+ * u < r(d)/q(d), r <- norm(max(0, r - q)) on rejection; u = Philox(seed, rid, L + depth + 1,
+ * ACCEPT, sibling rank)), then draws y from the final r (exponential race). Outputs as in
+ * sv_verify (a_b = depth of the last accepted node, out_tokens = the path's tokens then y), plus
+ *   accepted_nodes NULL or DEVICE [batch][max_depth + 1] int32: the accepted path's node indices
+ *            (0, n_1, .., n_a), -1 padded.
+ * sv_commit then keeps the path's K/V rows (node n_m lands at position L + m). A chain
+ * (parents[n-1] = n-1) gives exactly sv_verify's results. Limits and errors as sv_verify. */
+sv_status sv_verify_tree(sv_ctx* ctx, int32_t batch, const int32_t* slots, const int32_t* depths,
+                         const int32_t* parents, const int32_t* draft_tokens, const float* draft_probs,
+                         uint64_t seed, sv_mode mode, float temperature, int32_t* accepted_len,
+                         int32_t* out_tokens, int32_t* accepted_nodes, float* logits_out);
+
+/* Decision-only token-tree verify on caller logits [sum (k + 1)][V] fp32 (row off_b + n = node n),
+ * the tree analogue of sv_verify_logits (R30). Not committable. */
+sv_status sv_verify_tree_logits(sv_ctx* ctx, int32_t batch, const int32_t* slots, const int32_t* depths,
+                                const int32_t* parents, const int32_t* draft_tokens, const float* draft_probs,
+                                const float* logits, uint64_t seed, sv_mode mode, float temperature,
+                                int32_t* accepted_len, int32_t* out_tokens, int32_t* accepted_nodes);
+
 /* Commit the last sv_verify (eq:kv_concatenation): for each
- * request copy chain K/V rows 0..n-1 (n = a_b + 1, or min(n_keep[b], a_b + 1))
+ * request copy chain K/V rows 0..n-1 (n = a_b + 1, or min(n_keep[b], a_b + 1); the first n
+ * nodes of the accepted path after sv_verify_tree)
  * into pages at positions L..L+n-1, popping pages at page boundaries; then
  * L += n and pending <- the n-th emitted token. Rejected rows are dropped
  * (rollback). n_keep: NULL or DEVICE int32 [batch] (values >= 1).

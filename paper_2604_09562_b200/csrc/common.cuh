@@ -41,6 +41,15 @@ SV_DEV float uniform_accept(uint64_t seed, uint64_t rid, uint32_t z) {
   return word_to_uniform(philox10(c, uint32_t(seed), uint32_t(seed >> 32)).x);
 }
 
+// accept uniform of the s-th sibling tried at sequence index z (token trees, R30):
+// counter word s >> 2, lane s & 3; s = 0 is uniform_accept
+SV_DEV float uniform_accept_rank(uint64_t seed, uint64_t rid, uint32_t z, uint32_t s) {
+  u32x4 c{z, uint32_t(rid), uint32_t(rid >> 32), (uint32_t(PURPOSE_ACCEPT) << 28) | (s >> 2)};
+  const u32x4 w = philox10(c, uint32_t(seed), uint32_t(seed >> 32));
+  const uint32_t l = s & 3;
+  return word_to_uniform(l == 0 ? w.x : (l == 1 ? w.y : (l == 2 ? w.z : w.w)));
+}
+
 // four race uniforms for x = 4m .. 4m+3
 SV_DEV u32x4 race_words(uint64_t seed, uint64_t rid, uint32_t z, uint32_t m) {
   u32x4 c{z, uint32_t(rid), uint32_t(rid >> 32), (uint32_t(PURPOSE_RACE) << 28) | m};

@@ -21,7 +21,7 @@ size_t gemm_workspace_bytes(int Tmax, int max_n);
 GemmPlan* gemm_plan_create(const LaneDev& d, void* ws, cudaStream_t s);
 void gemm_plan_destroy(GemmPlan* p);
 // a3 verify attention: tcgen05 kernel when the shape allows (page 64, d_h 64/128), else SIMT
-cudaError_t attn_run(GemmPlan* p, int layer, int batch, cudaStream_t s);
+cudaError_t attn_run(GemmPlan* p, int layer, int batch, int tree, cudaStream_t s);
 // test hook: plain C = A B^T with a chosen kernel (0 default, 1 1-SM, 2 2-SM, 3 SIMT)
 cudaError_t gemm_debug(GemmPlan* p, const bf16* A, const bf16* B, float* C, int M, int N, int K, int variant,
                        cudaStream_t s);

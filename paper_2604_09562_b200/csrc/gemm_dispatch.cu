@@ -146,8 +146,9 @@ static bool encode_attn_maps(GemmPlan* p) {
   return true;
 }
 
-cudaError_t attn_run(GemmPlan* p, int layer, int batch, cudaStream_t s) {
-  const LaneDev& d = p->d;
+cudaError_t attn_run(GemmPlan* p, int layer, int batch, int tree, cudaStream_t s) {
+  LaneDev d = p->d;
+  d.tree = tree;
   if (p->use_tc2_attn && p->attn_maps_ok)
     return launch_attention_tc2(p->map_q2, p->map_kv, d, layer, p->num_sms, s);
   if (p->use_tc_attn && p->attn_maps_ok)

@@ -74,7 +74,8 @@ __global__ void __launch_bounds__(128) attn_simt_kernel(LaneDev d, int layer) {
       for (int p = tid; p < nr * AS_KC; p += 128) {
         const int rl = p / AS_KC, kt = p % AS_KC, t = c0 + kt, j = rl / G;
         float s = -INFINITY;
-        if (t < t1 && t <= L + j) {
+        // chain keys: causal (t - L <= j), or the node's ancestors-or-self for a token tree (R30)
+        if (t < t1 && (t < L || (d.tree ? ((d.row_anc[row0 + j] >> (t - L)) & 1ull) != 0 : t <= L + j))) {
           float dot = 0.f;
           const float* qr = Qs + rl * dh;
           for (int dd = 0; dd < dh; ++dd) dot = fmaf(qr[dd], Ks[dd * (AS_KC + 1) + kt], dot);

@@ -303,7 +303,17 @@ __global__ void __launch_bounds__(THREADS, 1)
           const int lim = row_valid ? min(kend, vis_end) - kbase : 0;   // columns c < lim are visible
           float s[32];
           float hm = -INFINITY;
-          if (lim >= 32) {
+          if (chain_tile && d.tree) {
+            // token tree (R30): chain key c' = kbase - L + c is visible to node j iff it is
+            // an ancestor-or-self of j
+            const unsigned long long anc = row_valid ? d.row_anc[I.row0 + j] : 0ull;
+            const int c0 = kbase - I.L;
+#pragma unroll
+            for (int c = 0; c < 32; ++c) {
+              s[c] = (c0 + c < I.R && ((anc >> (c0 + c)) & 1ull)) ? __uint_as_float(sv[c]) : -INFINITY;
+              hm = fmaxf(hm, s[c]);
+            }
+          } else if (lim >= 32) {
 #pragma unroll
             for (int c = 0; c < 32; ++c) s[c] = __uint_as_float(sv[c]);
 #pragma unroll

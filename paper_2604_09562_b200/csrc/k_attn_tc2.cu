@@ -379,8 +379,20 @@ __global__ void __launch_bounds__(THREADS, 1)
         // chain key kidx is visible to slot r iff kidx <= r / G  <=>  r >= kidx * G
         uint32_t vm = kvalid ? colok : 0u;
         if (chain_tile) {
-          const int first = (kidx << lg) - ch * 32;
-          vm &= first <= 0 ? 0xffffffffu : (first >= 32 ? 0u : (0xffffffffu << first));
+          if (d.tree) {
+            // token tree (R30): chain key kidx is visible to row j iff kidx is an
+            // ancestor-or-self of node j (row_anc bit); rows j of this half hold slots jG..jG+G-1
+            uint32_t tm = 0;
+            if (kvalid) {
+              const int j0 = (ch * 32) >> lg, j1 = min(I.R, (ch * 32 + 32) >> lg);
+              for (int j = j0; j < j1; ++j)
+                if ((d.row_anc[I.row0 + j] >> kidx) & 1ull) tm |= uint32_t((1ull << G) - 1ull) << ((j << lg) - ch * 32);
+            }
+            vm &= tm;
+          } else {
+            const int first = (kidx << lg) - ch * 32;
+            vm &= first <= 0 ? 0xffffffffu : (first >= 32 ? 0u : (0xffffffffu << first));
+          }
         }
         float x[32];
         bool need = false;

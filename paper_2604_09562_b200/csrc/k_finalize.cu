@@ -28,16 +28,198 @@ SV_DEV Best warp_best(Best v) {
   return v;
 }
 
+// ---------------------------------------------------------------- token trees (R30)
+// r(x) at the current node after `nrej` rejected children: r_0 = p_cur, r_i = max(0, r_{i-1} - q_i) / Z_i
+// (r_{i-1} when Z_i = 0); q_i = the rejected child's q row, or one-hot at its token
+struct TreeResid {
+  const float* lrow;          // logits row of the current node
+  float m, invS, inv_temp;
+  int nrej;
+  const int* rej_tok;         // [nrej] tokens of the rejected children
+  const float* const* rej_q;  // [nrej] their q rows (nullptr: one-hot)
+  const float* invZ;          // [nrej] (0: Z was 0, keep r)
+};
+
+SV_DEV float tree_r(const TreeResid& t, int x) {
+  float r = expf(t.lrow[x] * t.inv_temp - t.m) * t.invS;
+  for (int i = 0; i < t.nrej; ++i) {
+    if (t.invZ[i] == 0.f) continue;
+    const float q = t.rej_q[i] ? t.rej_q[i][x] : (x == t.rej_tok[i] ? 1.0f : 0.0f);
+    r = fmaxf(0.f, r - q) * t.invZ[i];
+  }
+  return r;
+}
+
+// The tree walk of one request (called by the whole CTA). Greedy: first child (ascending index)
+// whose token is the argmax. Sampled: recursive rejection over the children in index order, a
+// vocabulary pass per rejection for its normaliser Z, then the exponential race over the final r.
+// Writes the path (s_path[0..a]), a, indep and y.
+__device__ void tree_walk(const LaneDev& d, const int* __restrict__ drafts, const int* __restrict__ parents,
+                          const float* __restrict__ probs, const float* __restrict__ logits, uint64_t seed, int mode,
+                          float inv_temp, int b, int k, int r0, int doff, int L, unsigned long long rid,
+                          const float* s_m, const float* s_S, const int* s_top, int* s_path, int* s_a, int* s_indep,
+                          int* s_y) {
+  __shared__ int s_dep[kMaxDepth + 1], s_rank[kMaxDepth + 1];
+  __shared__ int s_cur, s_nrej, s_scan, s_act, s_cand;
+  __shared__ int s_rej_tok[kMaxDepth];
+  __shared__ const float* s_rej_q[kMaxDepth];
+  __shared__ float s_invZ[kMaxDepth];
+  __shared__ float s_red[FIN_THREADS / 32];
+  __shared__ Best s_best[FIN_THREADS / 32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = FIN_THREADS / 32;
+  const size_t V = d.V;
+  const int* par = parents + doff;                 // parent of node n at par[n - 1]
+  const int* tok = drafts + doff;
+  if (tid == 0) {
+    s_dep[0] = 0;
+    s_rank[0] = 0;
+    int bad = 0;
+    for (int n = 1; n <= k; ++n) {
+      const int p = par[n - 1];
+      if (p < 0 || p >= n) { bad = 1; s_dep[n] = 0; s_rank[n] = 0; continue; }   // plan flagged it
+      s_dep[n] = s_dep[p] + 1;
+      int rk = 0;
+      for (int c = p + 1; c < n; ++c) rk += par[c - 1] == p;
+      s_rank[n] = rk;
+    }
+    int indep = 0;
+    if (!bad) {
+      for (int n = 1; n <= k; ++n) {                 // every node's own test against its parent's target
+        const int p = par[n - 1], x = tok[n - 1];
+        if (mode == SV_GREEDY) {
+          indep += x == s_top[p];
+        } else {
+          const float pv = expf(logits[(size_t)(r0 + p) * V + x] * inv_temp - s_m[p]) / s_S[p];
+          const float qd = probs ? probs[(size_t)(doff + n - 1) * V + x] : 1.0f;
+          const float u = uniform_accept_rank(seed, rid, uint32_t(L + s_dep[p] + 1), uint32_t(s_rank[n]));
+          indep += (qd == 0.0f) || (u < pv / qd);
+        }
+      }
+    }
+    *s_indep = indep;
+    s_cur = 0;
+    s_nrej = 0;
+    s_scan = 1;
+    s_path[0] = 0;
+    *s_a = 0;
+    if (bad) k = 0;                                  // no walk: outputs are masked by req_err anyway
+    s_cand = k;                                      // (carries the possibly-zeroed k to all threads)
+  }
+  __syncthreads();
+  k = s_cand;
+  if (mode == SV_GREEDY) {
+    if (tid == 0) {
+      int cur = 0, a = 0;
+      for (;;) {
+        const int y = s_top[cur];
+        int nx = -1;
+        for (int c = cur + 1; c <= k; ++c)
+          if (par[c - 1] == cur && tok[c - 1] == y) { nx = c; break; }
+        if (nx < 0) break;
+        cur = nx;
+        s_path[++a] = cur;
+      }
+      *s_a = a;
+      *s_y = s_top[cur];
+    }
+    __syncthreads();
+    return;
+  }
+  // sampled: block-uniform loop; thread 0 decides, everyone joins the vocabulary passes
+  for (;;) {
+    if (tid == 0) {
+      const int cur = s_cur;
+      int c = s_scan;
+      while (c <= k && par[c - 1] != cur) ++c;       // next untried child of cur
+      if (c > k) {
+        s_act = 0;                                   // no child left: race over r
+      } else {
+        s_scan = c + 1;
+        const int x = tok[c - 1];
+        TreeResid t{logits + (size_t)(r0 + cur) * V, s_m[cur], 1.0f / s_S[cur], inv_temp, s_nrej, s_rej_tok, s_rej_q,
+                    s_invZ};
+        const float rv = tree_r(t, x);
+        const float qd = probs ? probs[(size_t)(doff + c - 1) * V + x] : 1.0f;
+        const float u = uniform_accept_rank(seed, rid, uint32_t(L + s_dep[cur] + 1), uint32_t(s_nrej));
+        if (qd == 0.0f || u < rv / qd) {
+          s_cur = c;
+          s_nrej = 0;
+          s_scan = c + 1;                            // children have larger indices
+          s_path[++*s_a] = c;
+          s_act = 1;
+        } else {
+          s_cand = c;
+          s_act = 2;                                 // rejected: normaliser of max(0, r - q_c)
+        }
+      }
+    }
+    __syncthreads();
+    const int act = s_act;
+    __syncthreads();                                 // everyone has read s_act before thread 0 rewrites it
+    if (act == 1) continue;
+    const int cur = s_cur, nrej = s_nrej;
+    TreeResid t{logits + (size_t)(r0 + cur) * V, s_m[cur], 1.0f / s_S[cur], inv_temp, nrej, s_rej_tok, s_rej_q, s_invZ};
+    if (act == 2) {
+      const int c = s_cand, xc = tok[c - 1];
+      const float* qc = probs ? probs + (size_t)(doff + c - 1) * V : nullptr;
+      float z = 0.f;
+      for (int x = tid; x < (int)V; x += FIN_THREADS)
+        z += fmaxf(0.f, tree_r(t, x) - (qc ? qc[x] : (x == xc ? 1.0f : 0.0f)));
+      z = warp_sum(z);
+      if (lane == 0) s_red[warp] = z;
+      __syncthreads();
+      if (tid == 0) {
+        float Z = 0.f;
+        for (int i = 0; i < nw; ++i) Z += s_red[i];
+        s_rej_tok[nrej] = xc;
+        s_rej_q[nrej] = qc;
+        s_invZ[nrej] = Z > 0.f ? 1.0f / Z : 0.f;
+        s_nrej = nrej + 1;
+      }
+      __syncthreads();
+      continue;
+    }
+    // race: y = argmax_{x: r(x) > 0} r(x) / E_x at z = L + depth(cur) + 1
+    const uint32_t z = uint32_t(L + s_dep[cur] + 1);
+    Best best{-INFINITY, 0x7fffffff};
+    const int nm = (int)((V + 3) / 4);
+    for (int mm = tid; mm < nm; mm += FIN_THREADS) {
+      const u32x4 w = race_words(seed, rid, z, uint32_t(mm));
+      const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+      for (int l = 0; l < 4; ++l) {
+        const int x = mm * 4 + l;
+        if (x >= (int)V) break;
+        const float r = tree_r(t, x);
+        const float E = -logf(word_to_uniform(ws[l]));
+        best = better(best, Best{r > 0.f ? r / E : -INFINITY, x});
+      }
+    }
+    best = warp_best(best);
+    if (lane == 0) s_best[warp] = best;
+    __syncthreads();
+    if (tid == 0) {
+      Best B = s_best[0];
+      for (int i = 1; i < nw; ++i) B = better(B, s_best[i]);
+      *s_y = B.x;
+    }
+    __syncthreads();
+    return;
+  }
+}
+
 __global__ void __launch_bounds__(FIN_THREADS) finalize_kernel(LaneDev d, const int* __restrict__ drafts,
+                                                                const int* __restrict__ parents,
                                                                 const float* __restrict__ probs,
                                                                 const float* __restrict__ logits, uint64_t seed,
                                                                 int mode, float inv_temp, int* __restrict__ acc_out,
-                                                                int* __restrict__ tok_out) {
+                                                                int* __restrict__ tok_out, int* __restrict__ nodes_out) {
   __shared__ float s_m[kMaxDepth + 1], s_S[kMaxDepth + 1];
   __shared__ int s_top[kMaxDepth + 1];
   __shared__ int s_a, s_indep, s_y, s_resid;
   __shared__ Best s_bestR[FIN_THREADS / 32], s_bestP[FIN_THREADS / 32];
   __shared__ float s_sumR[FIN_THREADS / 32];
+  __shared__ int s_path[kMaxDepth + 1];             // accepted path (chain rows); identity for chains
 
   pdl_trigger();
   pdl_wait();
@@ -96,7 +278,10 @@ __global__ void __launch_bounds__(FIN_THREADS) finalize_kernel(LaneDev d, const 
   __syncthreads();
 
   // 2. accept scan (serial over k <= 32)
-  if (tid == 0) {
+  if (parents) {
+    tree_walk(d, drafts, parents, probs, logits, seed, mode, inv_temp, b, k, r0, doff, L, rid, s_m, s_S, s_top,
+              s_path, &s_a, &s_indep, &s_y);
+  } else if (tid == 0) {
     int a = k, indep = 0;
     if (mode == SV_PREFILL) {                      // R29: the chunk's rows are all kept
       s_y = s_top[k];
@@ -122,12 +307,13 @@ __global__ void __launch_bounds__(FIN_THREADS) finalize_kernel(LaneDev d, const 
     s_a = a;
     s_indep = indep;
     s_resid = (mode == SV_SAMPLE) && (a < k);
+    for (int i = 0; i <= a; ++i) s_path[i] = i;
   }
   __syncthreads();
   const int a = s_a;
 
-  // 3. exponential race over the one selected row (sampled mode only)
-  if (mode == SV_SAMPLE) {
+  // 3. exponential race over the one selected row (sampled chains; trees race inside tree_walk)
+  if (mode == SV_SAMPLE && !parents) {
     const bool resid = s_resid;
     const float* lrow = logits + (size_t)(r0 + a) * V;
     const float m = s_m[a], invS = 1.0f / s_S[a];
@@ -173,9 +359,12 @@ __global__ void __launch_bounds__(FIN_THREADS) finalize_kernel(LaneDev d, const 
   const int K1 = d.max_depth + 1;
   for (int i = tid; i < K1; i += FIN_THREADS) {
     int t = -1;
-    if (!err) t = i < a ? drafts[doff + i] : (i == a ? s_y : -1);
+    if (!err) t = i < a ? drafts[doff + s_path[i + 1] - 1] : (i == a ? s_y : -1);
+    const int nd = (!err && i <= a) ? s_path[i] : -1;
     tok_out[(size_t)b * K1 + i] = t;
     if (d.tok_int) d.tok_int[(size_t)b * K1 + i] = t;
+    if (d.path_int) d.path_int[(size_t)b * K1 + i] = nd;
+    if (nodes_out) nodes_out[(size_t)b * K1 + i] = nd;
   }
   if (tid == 0) {
     acc_out[b] = err ? -1 : a;
@@ -194,12 +383,12 @@ __global__ void __launch_bounds__(FIN_THREADS) finalize_kernel(LaneDev d, const 
   }
 }
 
-cudaError_t launch_finalize(const LaneDev& d, int batch, const int* draft_tokens, const float* draft_probs,
-                            const float* logits, uint64_t seed, int mode, float inv_temp, int* accepted_len,
-                            int* out_tokens, cudaStream_t s) {
+cudaError_t launch_finalize(const LaneDev& d, int batch, const int* draft_tokens, const int* parents,
+                            const float* draft_probs, const float* logits, uint64_t seed, int mode, float inv_temp,
+                            int* accepted_len, int* out_tokens, int* accepted_nodes, cudaStream_t s) {
   SV_COUNT_LAUNCH();
-  return launch_pdl(finalize_kernel, dim3(batch), dim3(FIN_THREADS), 0, s, 1, d, draft_tokens, draft_probs, logits,
-                    seed, mode, inv_temp, accepted_len, out_tokens);
+  return launch_pdl(finalize_kernel, dim3(batch), dim3(FIN_THREADS), 0, s, 1, d, draft_tokens, parents, draft_probs,
+                    logits, seed, mode, inv_temp, accepted_len, out_tokens, accepted_nodes);
 }
 
 }  // namespace sv

@@ -58,6 +58,9 @@ __global__ void __launch_bounds__(256) commit_kernel(LaneDev d, const int* __res
   __syncthreads();
   if (!s_ok) return;
   const int n = s_n, row0 = d.row_off[b];
+  // the accepted path's chain rows (0..n-1 for chains; a token tree's path, R30)
+  __shared__ int s_row[kMaxDepth + 1];
+  if (threadIdx.x < n) s_row[threadIdx.x] = row0 + d.path_int[(size_t)b * (d.max_depth + 1) + threadIdx.x];
   // the <= 6 pages covering tokens L .. L + n - 1 (n <= 33, page >= 8), staged once
   __shared__ int s_pg[8];
   const int pg0 = L / d.page, npg = (L + n - 1) / d.page - pg0 + 1;
@@ -80,7 +83,7 @@ __global__ void __launch_bounds__(256) commit_kernel(LaneDev d, const int* __res
       const int c = li / per_tok, rem = li % per_tok;
       const int kv = rem / (d.Hkv * vec_per_row), h = (rem / vec_per_row) % d.Hkv, v8 = rem % vec_per_row;
       const int t = L + c;
-      const bf16* src = (kv ? d.vc : d.kc) + ((size_t)layer * d.Tmax + row0 + c) * nkv + (size_t)h * d.dh + v8 * 8;
+      const bf16* src = (kv ? d.vc : d.kc) + ((size_t)layer * d.Tmax + s_row[c]) * nkv + (size_t)h * d.dh + v8 * 8;
       v[u] = *reinterpret_cast<const uint4*>(src);
       dst[u] = d.pool + pool_row(d, layer, s_pg[t / d.page - pg0], kv, h, t % d.page) * d.dh + v8 * 8;
     }

@@ -25,7 +25,8 @@ bool pdl_enabled() {
 
 // ------------------------------------------------------------------ a1: plan
 // One CTA. Serial prefix over <= 256 requests in thread 0, then parallel fills.
-__global__ void plan_kernel(LaneDev d, PlanArgs p, const int* __restrict__ draft_tokens, int attn) {
+__global__ void plan_kernel(LaneDev d, PlanArgs p, const int* __restrict__ draft_tokens,
+                            const int* __restrict__ parents, int attn) {
   pdl_trigger();
   pdl_wait();
   __shared__ int s_off[kMaxBatch + 1];
@@ -72,7 +73,26 @@ __global__ void plan_kernel(LaneDev d, PlanArgs p, const int* __restrict__ draft
       atomicOr(&s_err[b], 1);
       tok = 0;
     }
-    int pos = s_len[b] + j;
+    // chain row j = node j: position L + depth(j), ancestor-or-self mask over the request's nodes
+    // (a chain: depth j, nodes 0..j; a token tree: follow the parents, each in [0, n-1], R30)
+    int depth = j;
+    unsigned long long anc = j >= 63 ? ~0ull : (2ull << j) - 1ull;
+    if (parents && j > 0) {
+      const int* par = parents + (s_off[b] - b);     // parent of node n at par[n - 1]
+      anc = 1ull << j;
+      depth = 0;
+      for (int n = j; n != 0; ++depth) {
+        const int pn = par[n - 1];
+        if (pn < 0 || pn >= n) {                       // not topological: the request is invalid
+          atomicOr(&s_err[b], 4);
+          break;
+        }
+        n = pn;
+        anc |= 1ull << n;
+      }
+    }
+    d.row_anc[r] = anc;
+    int pos = s_len[b] + depth;
     if (pos >= d.max_pos) {                      // chain would run past the position table
       atomicOr(&s_err[b], 2);
       pos = d.max_pos - 1;                       // keep every read in range; the request is not committed
@@ -99,12 +119,14 @@ __global__ void plan_kernel(LaneDev d, PlanArgs p, const int* __restrict__ draft
     d.req_err[b] = s_err[b];
     if (s_err[b] & 1) atomicOr(d.err, SV_DERR_BAD_TOKEN);
     if (s_err[b] & 2) atomicOr(d.err, SV_DERR_MAX_POS);
+    if (s_err[b] & 4) atomicOr(d.err, SV_DERR_BAD_TREE);
   }
 }
 
-cudaError_t launch_plan(const LaneDev& d, const PlanArgs& p, const int* draft_tokens, bool attn, cudaStream_t s) {
+cudaError_t launch_plan(const LaneDev& d, const PlanArgs& p, const int* draft_tokens, const int* parents, bool attn,
+                        cudaStream_t s) {
   SV_COUNT_LAUNCH();
-  return launch_pdl(plan_kernel, dim3(1), dim3(1024), 0, s, 1, d, p, draft_tokens, attn ? 1 : 0);
+  return launch_pdl(plan_kernel, dim3(1), dim3(1024), 0, s, 1, d, p, draft_tokens, parents, attn ? 1 : 0);
 }
 
 // ------------------------------------------------------------------ a2: embed + RMSNorm

@@ -24,6 +24,7 @@ struct LaneDev {
   // configuration
   int n_layers, D, Hq, Hkv, dh, V, F, page, n_pages, max_slots, max_batch, max_depth, max_pos;
   int max_pages_per_slot, nt, qkv_rows, Tmax;
+  int tree;                          // this verify's drafts are a token tree (R30), set per call
   float eps;
   // borrowed weights (bf16)
   const bf16 *embed, *attn_norm, *wqkv, *wo, *ffn_norm, *w_gate_up, *w_down, *final_norm, *lm_head;
@@ -47,6 +48,8 @@ struct LaneDev {
   int *item_start, *n_items;
   float *part_o, *part_ml;           // split-KV partials
   int *acc_int, *tok_int;            // internal copies of accepted_len / out_tokens for commit
+  int* path_int;                     // [max_batch][max_depth+1] accepted path's chain rows (commit)
+  unsigned long long* row_anc;       // [Tmax] ancestor-or-self node mask of each chain row
   int* batch_n;                      // [1] batch of the pending verify (device copy)
   unsigned long long* trace;         // [16][256] clock64 trace of CTA 0 (SV_TRACE=1) or nullptr
 };
@@ -103,7 +106,9 @@ struct PlanArgs {
 };
 
 // ---- launchers (stream-ordered; return cudaGetLastError()) ----
-cudaError_t launch_plan(const LaneDev& d, const PlanArgs& p, const int* draft_tokens, bool attn, cudaStream_t s);
+// parents: NULL (chains) or device [sum k] node parents of a token tree (R30)
+cudaError_t launch_plan(const LaneDev& d, const PlanArgs& p, const int* draft_tokens, const int* parents, bool attn,
+                        cudaStream_t s);
 cudaError_t launch_embed_norm(const LaneDev& d, int T, cudaStream_t s);
 cudaError_t launch_rmsnorm(const LaneDev& d, const float* x, const bf16* g, bf16* out, int T, cudaStream_t s);
 // C[M][N] (fp32) = A[M][K] (bf16) * B[N][K]^T (bf16)
@@ -114,9 +119,9 @@ cudaError_t launch_swiglu_epilogue(const LaneDev& d, int T, cudaStream_t s);
 cudaError_t launch_tile_stats(const LaneDev& d, int T, float inv_temp, cudaStream_t s);
 cudaError_t launch_attention(const LaneDev& d, int layer, int batch, cudaStream_t s);
 cudaError_t launch_attn_combine(const LaneDev& d, int T, cudaStream_t s);
-cudaError_t launch_finalize(const LaneDev& d, int batch, const int* draft_tokens, const float* draft_probs,
-                            const float* logits, uint64_t seed, int mode, float inv_temp,
-                            int* accepted_len, int* out_tokens, cudaStream_t s);
+cudaError_t launch_finalize(const LaneDev& d, int batch, const int* draft_tokens, const int* parents,
+                            const float* draft_probs, const float* logits, uint64_t seed, int mode, float inv_temp,
+                            int* accepted_len, int* out_tokens, int* accepted_nodes, cudaStream_t s);
 cudaError_t launch_commit(const LaneDev& d, const int* n_keep, int batch, cudaStream_t s);
 cudaError_t launch_append(const LaneDev& d, int slot, unsigned long long rid, const bf16* k, const bf16* v,
                           int n, int pending, const int* pending_dev, int packed, cudaStream_t s);

@@ -25,7 +25,7 @@ struct Layout {
   size_t slots, depths, row_off, row_req, row_pos, chain_tok, req_err;
   size_t h0, h1, h2, cbuf, logits, tile_max, tile_sum, tile_arg;
   size_t a, b, z, q, kc, vc, o, u;
-  size_t items, item_start, n_items, part_o, part_ml, acc_int, tok_int, batch_n;
+  size_t items, item_start, n_items, part_o, part_ml, acc_int, tok_int, batch_n, path_int, row_anc;
   size_t gemm_ws, trace, prefill;
   size_t max_items;
 
@@ -110,6 +110,8 @@ Layout make_layout(const sv_config& c) {
   L.acc_int = L.take(4 * c.max_batch);
   L.tok_int = L.take(4 * c.max_batch * (c.max_depth + 1));
   L.batch_n = L.take(4);
+  L.path_int = L.take(4 * c.max_batch * (c.max_depth + 1));
+  L.row_anc = L.take(8 * T);
   L.gemm_ws = L.take(sv::gemm_workspace_bytes((int)T, (int)cmax));
   L.trace = L.take(8 * 16 * 256);
   L.prefill = L.take(4 * 3 * (size_t)(c.max_depth + 2));   // sv_prefill: chunk tokens + outputs
@@ -337,6 +339,9 @@ sv_status sv_create(const sv_config* cfg, const sv_weights* w, void* kv_pool, vo
   d.acc_int = (int*)(ws + L.acc_int);
   d.tok_int = (int*)(ws + L.tok_int);
   d.batch_n = (int*)(ws + L.batch_n);
+  d.path_int = (int*)(ws + L.path_int);
+  d.row_anc = (unsigned long long*)(ws + L.row_anc);
+  d.tree = 0;
   d.trace = getenv("SV_TRACE") ? (unsigned long long*)(ws + L.trace) : nullptr;
 
   // RoPE table: fp64 angles pos * theta^(-2m/d_h), stored fp32 (SURVEY.md §8(c) "Model details")
@@ -423,22 +428,27 @@ static sv_status gemm(sv_ctx* c, const bf16* A, const bf16* B, float* C, int M, 
   return cuda_ok(sv::gemm_run(c->gemm, A, B, C, M, N, K, epi, e, c->stream));
 }
 
-sv_status sv_verify(sv_ctx* c, int32_t batch, const int32_t* slots, const int32_t* depths,
-                    const int32_t* draft_tokens, const float* draft_probs, uint64_t seed, sv_mode mode,
-                    float temperature, int32_t* accepted_len, int32_t* out_tokens, float* logits_out) {
+// sv_verify and sv_verify_tree (parents != NULL: token-tree drafts, R30)
+static sv_status verify_impl(sv_ctx* c, int32_t batch, const int32_t* slots, const int32_t* depths,
+                             const int32_t* parents, const int32_t* draft_tokens, const float* draft_probs,
+                             uint64_t seed, sv_mode mode, float temperature, int32_t* accepted_len,
+                             int32_t* out_tokens, int32_t* accepted_nodes, float* logits_out) {
   if (!c || !accepted_len || !out_tokens) return SV_EINVAL;
   if (mode != SV_GREEDY && mode != SV_SAMPLE && mode != SV_PREFILL) return SV_EINVAL;
+  if (parents && mode == SV_PREFILL) return SV_EINVAL;
   if (mode == SV_SAMPLE && !(temperature > 0.f)) return SV_EINVAL;
   if (c->pending_verify) return SV_ESTATE;
   sv::PlanArgs p;
   sv_status st = check_batch(c, batch, slots, depths, p);
   if (st) return st;
   if (p.T > batch && !draft_tokens) return SV_EINVAL;
-  const sv::LaneDev& d = c->d;
+  sv::LaneDev d = c->d;
+  d.tree = parents != nullptr && p.T > batch;
+  if (!d.tree) parents = nullptr;                   // no drafts: a tree of roots is the chain
   const int T = p.T;
   cudaStream_t s = c->stream;
   const float inv_temp = mode == SV_SAMPLE ? 1.0f / temperature : 1.0f;
-  STAGE(c, ST_PLAN, sv::launch_plan(d, p, draft_tokens, true, s));
+  STAGE(c, ST_PLAN, sv::launch_plan(d, p, draft_tokens, parents, true, s));
   STAGE(c, ST_EMBED, sv::launch_embed_norm(d, T, s));
   const size_t nq = (size_t)d.Hq * d.dh;
   for (int layer = 0; layer < d.n_layers; ++layer) {
@@ -448,7 +458,7 @@ sv_status sv_verify(sv_ctx* c, int32_t batch, const int32_t* slots, const int32_
     e.layer = layer;
     STAGE(c, ST_QKV, gemm(c, d.a, d.wqkv + (size_t)layer * d.qkv_rows * d.D, d.cbuf, T, d.qkv_rows, d.D,
                           sv::EPI_QKV_ROPE, e));
-    STAGE(c, ST_ATTN, sv::attn_run(c->gemm, layer, batch, s));
+    STAGE(c, ST_ATTN, sv::attn_run(c->gemm, layer, batch, d.tree, s));
     STAGE(c, ST_COMBINE, sv::launch_attn_combine(d, T, s));
     float* hattn = d.F > 0 ? d.h1 : d.h2;
     e.resid_in = hin;
@@ -470,8 +480,8 @@ sv_status sv_verify(sv_ctx* c, int32_t batch, const int32_t* slots, const int32_
   // are stored only when something reads them
   e.write_out = c->taps || mode == SV_SAMPLE || logits_out != nullptr;
   STAGE(c, ST_LM_HEAD, gemm(c, d.z, d.lm_head, d.logits, T, d.V, d.D, sv::EPI_LOGITS, e));
-  STAGE(c, ST_FINALIZE, sv::launch_finalize(d, batch, draft_tokens, draft_probs, d.logits, seed, mode, inv_temp,
-                                            accepted_len, out_tokens, s));
+  STAGE(c, ST_FINALIZE, sv::launch_finalize(d, batch, draft_tokens, parents, draft_probs, d.logits, seed, mode,
+                                            inv_temp, accepted_len, out_tokens, accepted_nodes, s));
   if (logits_out)
     SV_CUDA(cudaMemcpyAsync(logits_out, d.logits, (size_t)T * d.V * 4, cudaMemcpyDeviceToDevice, s));
   for (int b = 0; b < batch; ++b) c->state[slots[b]] = PENDING;
@@ -483,12 +493,29 @@ sv_status sv_verify(sv_ctx* c, int32_t batch, const int32_t* slots, const int32_
   return SV_OK;
 }
 
-sv_status sv_verify_logits(sv_ctx* c, int32_t batch, const int32_t* slots, const int32_t* depths,
-                           const int32_t* draft_tokens, const float* draft_probs, const float* logits,
-                           uint64_t seed, sv_mode mode, float temperature, int32_t* accepted_len,
-                           int32_t* out_tokens) {
+sv_status sv_verify(sv_ctx* c, int32_t batch, const int32_t* slots, const int32_t* depths,
+                    const int32_t* draft_tokens, const float* draft_probs, uint64_t seed, sv_mode mode,
+                    float temperature, int32_t* accepted_len, int32_t* out_tokens, float* logits_out) {
+  return verify_impl(c, batch, slots, depths, nullptr, draft_tokens, draft_probs, seed, mode, temperature,
+                     accepted_len, out_tokens, nullptr, logits_out);
+}
+
+sv_status sv_verify_tree(sv_ctx* c, int32_t batch, const int32_t* slots, const int32_t* depths,
+                         const int32_t* parents, const int32_t* draft_tokens, const float* draft_probs,
+                         uint64_t seed, sv_mode mode, float temperature, int32_t* accepted_len,
+                         int32_t* out_tokens, int32_t* accepted_nodes, float* logits_out) {
+  if (!parents) return SV_EINVAL;
+  return verify_impl(c, batch, slots, depths, parents, draft_tokens, draft_probs, seed, mode, temperature,
+                     accepted_len, out_tokens, accepted_nodes, logits_out);
+}
+
+static sv_status verify_logits_impl(sv_ctx* c, int32_t batch, const int32_t* slots, const int32_t* depths,
+                                    const int32_t* parents, const int32_t* draft_tokens, const float* draft_probs,
+                                    const float* logits, uint64_t seed, sv_mode mode, float temperature,
+                                    int32_t* accepted_len, int32_t* out_tokens, int32_t* accepted_nodes) {
   if (!c || !accepted_len || !out_tokens || !logits) return SV_EINVAL;
   if (mode != SV_GREEDY && mode != SV_SAMPLE && mode != SV_PREFILL) return SV_EINVAL;
+  if (parents && mode == SV_PREFILL) return SV_EINVAL;
   if (mode == SV_SAMPLE && !(temperature > 0.f)) return SV_EINVAL;
   if (c->pending_verify) return SV_ESTATE;
   sv::PlanArgs p;
@@ -497,14 +524,33 @@ sv_status sv_verify_logits(sv_ctx* c, int32_t batch, const int32_t* slots, const
   if (p.T > batch && !draft_tokens) return SV_EINVAL;
   const float inv_temp = mode == SV_SAMPLE ? 1.0f / temperature : 1.0f;
   sv::LaneDev d = c->d;
-  SV_CUDA(sv::launch_plan(d, p, draft_tokens, false, c->stream));
+  if (p.T == batch) parents = nullptr;
+  d.tree = parents != nullptr;
+  SV_CUDA(sv::launch_plan(d, p, draft_tokens, parents, false, c->stream));
   d.logits = const_cast<float*>(logits);
   SV_CUDA(sv::launch_tile_stats(d, p.T, inv_temp, c->stream));
-  SV_CUDA(sv::launch_finalize(d, batch, draft_tokens, draft_probs, logits, seed, mode, inv_temp, accepted_len,
-                              out_tokens, c->stream));
+  SV_CUDA(sv::launch_finalize(d, batch, draft_tokens, parents, draft_probs, logits, seed, mode, inv_temp,
+                              accepted_len, out_tokens, accepted_nodes, c->stream));
   c->last_T = p.T;
   c->last_batch = batch;
   return SV_OK;
+}
+
+sv_status sv_verify_logits(sv_ctx* c, int32_t batch, const int32_t* slots, const int32_t* depths,
+                           const int32_t* draft_tokens, const float* draft_probs, const float* logits,
+                           uint64_t seed, sv_mode mode, float temperature, int32_t* accepted_len,
+                           int32_t* out_tokens) {
+  return verify_logits_impl(c, batch, slots, depths, nullptr, draft_tokens, draft_probs, logits, seed, mode,
+                            temperature, accepted_len, out_tokens, nullptr);
+}
+
+sv_status sv_verify_tree_logits(sv_ctx* c, int32_t batch, const int32_t* slots, const int32_t* depths,
+                                const int32_t* parents, const int32_t* draft_tokens, const float* draft_probs,
+                                const float* logits, uint64_t seed, sv_mode mode, float temperature,
+                                int32_t* accepted_len, int32_t* out_tokens, int32_t* accepted_nodes) {
+  if (!parents) return SV_EINVAL;
+  return verify_logits_impl(c, batch, slots, depths, parents, draft_tokens, draft_probs, logits, seed, mode,
+                            temperature, accepted_len, out_tokens, accepted_nodes);
 }
 
 sv_status sv_commit(sv_ctx* c, const int32_t* n_keep) {

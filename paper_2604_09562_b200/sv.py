@@ -31,6 +31,7 @@ EXPORTED = [
     "sv_profile_stage_name", "sv_profile_read", "sv_launch_count", "sv_debug_gemm", "sv_kv_append_packed",
     "sv_kv_loopback_append", "sv_spec_default_config", "sv_spec_reset", "sv_spec_adapt", "sv_spec_step",
     "sv_route_default_config", "sv_route_select", "sv_lane_occupancy", "sv_kv_pack_slot", "sv_prefill",
+    "sv_verify_tree", "sv_verify_tree_logits",
 ]
 
 
@@ -99,6 +100,10 @@ def load():
                       ctypes.c_int),
         "sv_verify_logits": ([vp, i32, P(i32), P(i32), vp, vp, vp, u64, ctypes.c_int, ctypes.c_float, vp, vp],
                              ctypes.c_int),
+        "sv_verify_tree": ([vp, i32, P(i32), P(i32), vp, vp, vp, u64, ctypes.c_int, ctypes.c_float, vp, vp, vp, vp],
+                           ctypes.c_int),
+        "sv_verify_tree_logits": ([vp, i32, P(i32), P(i32), vp, vp, vp, vp, u64, ctypes.c_int, ctypes.c_float, vp,
+                                   vp, vp], ctypes.c_int),
         "sv_commit": ([vp, vp], ctypes.c_int),
         "sv_release": ([vp, i32], ctypes.c_int),
         "sv_stats": ([vp, P(LaneStats), ctypes.c_int], ctypes.c_int),
@@ -191,6 +196,7 @@ class Lane:
         K1 = self.cfg.max_depth + 1
         self._acc = torch.empty(self.cfg.max_batch, dtype=torch.int32, device=self.device)
         self._tok = torch.empty(self.cfg.max_batch, K1, dtype=torch.int32, device=self.device)
+        self._nodes = torch.empty(self.cfg.max_batch, K1, dtype=torch.int32, device=self.device)
 
     def close(self):
         if getattr(self, "ctx", None):
@@ -233,6 +239,30 @@ class Lane:
         _check(self.lib.sv_verify_logits(self.ctx, B, s, dpt, _ptr(draft_tokens), _ptr(draft_probs), _ptr(logits),
                                          seed, m, float(temperature), _ptr(acc), _ptr(tok)), "sv_verify_logits")
         return acc, tok
+
+    def verify_tree(self, slots, depths, parents, draft_tokens, draft_probs=None, seed=0, mode="greedy",
+                    temperature=1.0, logits_out=None, nodes_out=None):
+        """Token-tree verify (R30). parents: device int32 [sum k] (node n's parent in 0..n-1).
+        Returns (accepted_len [B], out_tokens [B][max_depth+1], accepted_nodes [B][max_depth+1])."""
+        s, B = _i32_array(slots)
+        dpt, _ = _i32_array(depths)
+        acc, tok = self._acc[:B], self._tok[:B]
+        nodes = self._nodes[:B] if nodes_out is None else nodes_out
+        _check(self.lib.sv_verify_tree(self.ctx, B, s, dpt, _ptr(parents), _ptr(draft_tokens), _ptr(draft_probs),
+                                       seed, self._mode(mode), float(temperature), _ptr(acc), _ptr(tok), _ptr(nodes),
+                                       _ptr(logits_out)), "sv_verify_tree")
+        return acc, tok, nodes
+
+    def verify_tree_logits(self, slots, depths, parents, draft_tokens, logits, draft_probs=None, seed=0,
+                           mode="greedy", temperature=1.0):
+        s, B = _i32_array(slots)
+        dpt, _ = _i32_array(depths)
+        acc, tok, nodes = self._acc[:B], self._tok[:B], self._nodes[:B]
+        _check(self.lib.sv_verify_tree_logits(self.ctx, B, s, dpt, _ptr(parents), _ptr(draft_tokens),
+                                              _ptr(draft_probs), _ptr(logits), seed, self._mode(mode),
+                                              float(temperature), _ptr(acc), _ptr(tok), _ptr(nodes)),
+               "sv_verify_tree_logits")
+        return acc, tok, nodes
 
     def prefill(self, slot, request_id, prompt, chunk):
         """Chunked prefill (sv_prefill; NEXT-3, R29) of `prompt` (host ints) into an EMPTY
