@@ -43,7 +43,7 @@ import numpy as np
 from . import model
 from .numerics import round_bf16
 from .philox import uniform_accept_rank, uniform_race
-from .verify import GREEDY, SAMPLE, argmax_lowest, target_probs
+from .verify import GREEDY, SAMPLE, argmax_lowest, filtered_probs
 
 
 def check_parents(parents):
@@ -114,7 +114,7 @@ def forward_tree(w, tokens, parents, L, caches, cfg, cos, sin):
     return z, model.lm_head(z, w["lm_head"]), chain_kv
 
 
-def verify_tree(logits, drafts, parents, q_rows, seed, rid, L, mode, temperature=1.0):
+def verify_tree(logits, drafts, parents, q_rows, seed, rid, L, mode, temperature=1.0, top_k=0, top_p=1.0):
     """Decide one request's token tree. logits [k+1][V] (row n = node n); drafts [k] (d_n =
     drafts[n-1]); parents [k]; q_rows [k][V] (row n-1 = the distribution d_n was drawn from) or
     None (one-hot). Returns dict(a, emitted, path, indep, tests) where tests lists the sampled
@@ -139,7 +139,7 @@ def verify_tree(logits, drafts, parents, q_rows, seed, rid, L, mode, temperature
         return dict(a=dep[cur], emitted=[int(drafts[n - 1]) for n in walk[1:]] + [top[cur]], path=walk,
                     indep=indep, tests=[])
     assert mode == SAMPLE
-    p = target_probs(logits, temperature)
+    p = filtered_probs(logits, temperature, top_k, top_p)     # R31 filtering (NEXT-4)
     V = p.shape[1]
 
     def qrow(c):

@@ -8,7 +8,8 @@ The paper relies on but never defines the verification step (PAPER.md:37
 SURVEY.md §8(c) steps 2-5 and S1-S9, S14, S20) is Leviathan rejection sampling
 with a bonus token, or a greedy prefix match, written out here in that order:
 
-  step 2  p_{j+1} = softmax(l_j / temperature), j = 0..k (row j of the chain)
+  step 2  p_{j+1} = softmax(l_j / temperature), j = 0..k (row j of the chain), then optionally
+          top-k / top-p filtered (filtered_target, R31; NEXT-4) before everything below
   step 3  GREEDY: a = largest m <= k with d_j = argmax l_{j-1} for all j <= m
           (ties -> lowest id); emit d_1..d_a, y = argmax l_a
   step 4  SAMPLE: for j = 1..k
@@ -54,7 +55,45 @@ def target_probs(logits, temperature):
     return softmax(np.asarray(logits, dtype=np.float64) / float(temperature), axis=-1)
 
 
-def verify_request(logits, drafts, q_rows, seed, rid, L, mode, temperature=1.0):
+def filtered_target(p_row, logits_row, top_k=0, top_p=1.0):
+    """Top-k / top-p filtered target (reading R31), fp64:
+
+      order the tokens by (scaled logit descending, token id ascending);
+      n_k = top_k if 0 < top_k < V else V;
+      n_p = V if top_p >= 1 else the smallest n with p(o_1) + ... + p(o_n) >= top_p
+            (cumulative sum in that order);
+      keep the first min(n_k, n_p) tokens; p' = p * [kept] / sum of the kept p.
+
+    Temperature is applied before filtering (p = softmax(l / T), the logits row given here is
+    l / T). top_k = 0 and top_p >= 1 return p unchanged."""
+    p_row = np.asarray(p_row, dtype=np.float64)
+    V = p_row.shape[0]
+    n_k = top_k if 0 < top_k < V else V
+    if n_k == V and top_p >= 1.0:
+        return p_row
+    ids = np.arange(V)
+    order = np.lexsort((ids, -np.asarray(logits_row, dtype=np.float64)))
+    if top_p >= 1.0:
+        n_p = V
+    else:
+        cum = np.cumsum(p_row[order])
+        n_p = int(np.argmax(cum >= top_p)) + 1 if (cum >= top_p).any() else V
+    keep = order[:min(n_k, n_p)]
+    out = np.zeros(V)
+    out[keep] = p_row[keep]
+    return out / out.sum()
+
+
+def filtered_probs(logits, temperature, top_k=0, top_p=1.0):
+    """Rows of softmax(l / T), each filtered by filtered_target."""
+    lg = np.asarray(logits, dtype=np.float64) / float(temperature)
+    p = softmax(lg, axis=-1)
+    if top_k <= 0 and top_p >= 1.0:
+        return p
+    return np.stack([filtered_target(p[j], lg[j], top_k, top_p) for j in range(p.shape[0])])
+
+
+def verify_request(logits, drafts, q_rows, seed, rid, L, mode, temperature=1.0, top_k=0, top_p=1.0):
     """Decide one request. logits [k+1][V]; drafts [k] ints; q_rows [k][V] or None.
 
     L is the request's cache length at verify time (the chain head sits at
@@ -77,7 +116,7 @@ def verify_request(logits, drafts, q_rows, seed, rid, L, mode, temperature=1.0):
         y = top[a]
         return dict(a=a, emitted=list(drafts[:a]) + [y], indep=indep)
 
-    p = target_probs(logits, temperature)           # p[j] = p_{j+1}
+    p = filtered_probs(logits, temperature, top_k, top_p)   # p[j] = p_{j+1} (R31 filtering)
     V = p.shape[1]
     a = k
     indep = 0
@@ -108,9 +147,9 @@ def verify_request(logits, drafts, q_rows, seed, rid, L, mode, temperature=1.0):
     return dict(a=a, emitted=list(int(t) for t in drafts[:a]) + [y], indep=indep)
 
 
-def race_scores(logits_row, q_row, d_reject, seed, rid, z, temperature, residual):
+def race_scores(logits_row, q_row, d_reject, seed, rid, z, temperature, residual, top_k=0, top_p=1.0):
     """The race scores R(x)/E_x used for one selected row (for borderline analysis)."""
-    p = target_probs(logits_row, temperature)
+    p = filtered_probs(np.asarray(logits_row)[None], temperature, top_k, top_p)[0]
     V = p.shape[0]
     if residual:
         if q_row is None:
