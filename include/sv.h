@@ -198,6 +198,16 @@ sv_status sv_verify_tree_logits(sv_ctx* ctx, int32_t batch, const int32_t* slots
                                 const float* logits, uint64_t seed, sv_mode mode, float temperature,
                                 int32_t* accepted_len, int32_t* out_tokens, int32_t* accepted_nodes);
 
+/* Top-k / top-p filtered targets for SV_SAMPLE verifies of this lane (
+ * DESIGN.md reading R31; the paper fixes no sampler): p = softmax(l / T) is restricted to the first
+ * min(n_k, n_p) tokens in (scaled logit desc, token id asc) order — n_k = top_k (0 = no limit),
+ * n_p = the smallest n whose cumulative p reaches top_p (>= 1 = no limit) — and renormalised; the
+ * filtered p' replaces p in the accept test, the residual and the bonus draw (chains and trees).
+ * Kept masses are summed in 2^-40 fixed point, so the kept set does not depend on summation
+ * order. Greedy and prefill verifies are unaffected. Default (0, 1.0) = off. EINVAL: top_k < 0
+ * or top_p <= 0 / NaN. ESTATE while a verify is uncommitted. */
+sv_status sv_set_filter(sv_ctx* ctx, int32_t top_k, float top_p);
+
 /* Commit the last sv_verify (eq:kv_concatenation): for each
  * request copy chain K/V rows 0..n-1 (n = a_b + 1, or min(n_keep[b], a_b + 1); the first n
  * nodes of the accepted path after sv_verify_tree)

@@ -28,10 +28,177 @@ SV_DEV Best warp_best(Best v) {
   return v;
 }
 
+// ---------------------------------------------------------------- top-k / top-p filter (R31)
+// One CTA per chain row: radix select (4 passes of 8 bits, most significant first) of the
+// threshold element in (scaled logit desc, id asc) order — the first element at which the kept
+// count reaches top_k or the kept mass reaches top_p of the row's mass. Masses are sums of
+// e(x) = exp(l_x / T - m) in 2^-40 fixed point (u64), so every decision and S_keep are
+// independent of summation order (deterministic). Ties at the threshold key are kept in id
+// order up to the count / mass limit. Output per row: threshold key, the largest kept id among
+// the ties, 1 / S_keep and the row max m.
+constexpr int FLT_THREADS = 1024;
+constexpr double kFx = 1099511627776.0;            // 2^40
+
+SV_DEV uint32_t flt_key(float v) {
+  const uint32_t u = v == 0.0f ? 0u : __float_as_uint(v);     // -0 and +0 are the same value (a tie)
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+SV_DEV float key_flt(uint32_t k) { return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k); }
+
+__global__ void __launch_bounds__(FLT_THREADS) filter_kernel(LaneDev d, float inv_temp, int top_k, float top_p) {
+  __shared__ unsigned int h_cnt[256];
+  __shared__ unsigned long long h_mass[256];
+  __shared__ float s_redf[FLT_THREADS / 32];
+  __shared__ unsigned long long s_redu[FLT_THREADS / 32];
+  __shared__ uint32_t s_prefix, s_D;
+  __shared__ unsigned int s_cnt_above, s_run;
+  __shared__ unsigned long long s_mass_above, s_total;
+  __shared__ int s_tie_lim, s_nkeep;
+  pdl_trigger();
+  pdl_wait();
+  const int r = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = FLT_THREADS / 32;
+  const int V = d.V;
+  const float* row = d.logits + (size_t)r * V;
+  // row max m (exact: max over the tile maxima of the same scaled values)
+  float m = -INFINITY;
+  for (int t = tid; t < d.nt; t += FLT_THREADS) m = fmaxf(m, d.tile_max[(size_t)r * d.nt + t]);
+  m = warp_max(m);
+  if (lane == 0) s_redf[warp] = m;
+  __syncthreads();
+  m = s_redf[0];
+  for (int i = 1; i < nw; ++i) m = fmaxf(m, s_redf[i]);
+  const bool use_k = top_k > 0 && top_k < V, use_p = top_p < 1.0f;
+  // total mass (fixed point)
+  unsigned long long tot = 0;
+  for (int x = tid; x < V; x += FLT_THREADS) tot += (unsigned long long)llrint((double)expf(row[x] * inv_temp - m) * kFx);
+  for (int o = 16; o; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+  if (lane == 0) s_redu[warp] = tot;
+  if (tid == 0) { s_prefix = 0; s_cnt_above = 0; s_mass_above = 0; }
+  __syncthreads();
+  if (tid == 0) {
+    unsigned long long t2 = 0;
+    for (int i = 0; i < nw; ++i) t2 += s_redu[i];
+    s_total = t2;
+  }
+  __syncthreads();
+  // mass target: smallest prefix with mass >= top_p * total (compared in fixed point)
+  const unsigned long long target = use_p ? (unsigned long long)((double)top_p * (double)s_total) : ~0ull;
+  for (int pass = 0; pass < 4; ++pass) {
+    const int shift = 24 - 8 * pass;
+    const uint32_t hi_mask = pass == 0 ? 0u : (0xffffffffu << (shift + 8));
+    for (int i = tid; i < 256; i += FLT_THREADS) { h_cnt[i] = 0; h_mass[i] = 0; }
+    __syncthreads();
+    const uint32_t prefix = s_prefix;
+    for (int x = tid; x < V; x += FLT_THREADS) {
+      const float v = row[x] * inv_temp;
+      const uint32_t k = flt_key(v);
+      if ((k & hi_mask) == prefix) {
+        const int dg = (k >> shift) & 255;
+        atomicAdd(&h_cnt[dg], 1u);
+        atomicAdd(&h_mass[dg], (unsigned long long)llrint((double)expf(v - m) * kFx));   // S_keep needs it
+      }
+    }
+    __syncthreads();
+    if (tid == 0) {
+      unsigned int c = s_cnt_above;
+      unsigned long long ms = s_mass_above;
+      int D = 0;
+      for (int dg = 255; dg >= 0; --dg) {
+        const unsigned int c2 = c + h_cnt[dg];
+        const unsigned long long m2 = ms + h_mass[dg];
+        if (h_cnt[dg] && ((use_k && c2 >= (unsigned)top_k) || (use_p && m2 >= target) || dg == 0)) { D = dg; break; }
+        c = c2;
+        ms = m2;
+      }
+      // the lowest non-empty bin is the fallback (no limit reached: keep everything from here on)
+      if (h_cnt[D] == 0) {
+        for (int dg = 0; dg < 256; ++dg) if (h_cnt[dg]) { D = dg; break; }
+      }
+      s_cnt_above = c;
+      s_mass_above = ms;
+      s_prefix = prefix | (uint32_t(D) << shift);
+      s_D = D;
+    }
+    __syncthreads();
+  }
+  // ties: every element with key == s_prefix; keep them in id order up to the limits
+  if (tid == 0) {
+    const unsigned int n_ties = h_cnt[s_D];
+    const float vstar = key_flt(s_prefix);
+    const unsigned long long e = (unsigned long long)llrint((double)expf(vstar - m) * kFx);
+    unsigned long long n = n_ties;
+    if (use_k) n = min(n, (unsigned long long)(top_k - s_cnt_above));
+    if (use_p && e > 0 && target > s_mass_above) {
+      const unsigned long long need = (target - s_mass_above + e - 1) / e;   // ceil
+      n = min(n, max(1ull, need));
+    } else if (use_p) {
+      n = 1;
+    }
+    if (n < 1) n = 1;
+    s_nkeep = (int)n;
+    s_tie_lim = n >= n_ties ? V : -1;
+    s_run = 0;
+    const unsigned long long keep = s_mass_above + n * e;
+    d.filt_key[r] = s_prefix;
+    d.filt_inv[r] = (float)(kFx / (double)keep);
+    d.filt_m[r] = m;
+  }
+  __syncthreads();
+  if (s_tie_lim < 0) {                                 // the n-th tie in id order
+    const uint32_t kstar = s_prefix;
+    const int n = s_nkeep;
+    for (int x0 = 0; x0 < V; x0 += FLT_THREADS) {
+      const int x = x0 + tid;
+      const bool tie = x < V && flt_key(row[x] * inv_temp) == kstar;
+      const unsigned int bal = __ballot_sync(0xffffffffu, tie);
+      if (lane == 0) h_cnt[warp] = __popc(bal);
+      __syncthreads();
+      if (tid == 0) {
+        unsigned int run = s_run;
+        for (int w = 0; w < nw; ++w) {
+          if (run + h_cnt[w] >= (unsigned)n) {         // in warp w: the (n - run)-th set lane
+            s_D = w;
+            s_tie_lim = -2 - (int)(n - run);           // marker: resolve below
+            break;
+          }
+          run += h_cnt[w];
+        }
+        s_run = run;
+      }
+      __syncthreads();
+      if (s_tie_lim <= -2) {
+        if (warp == (int)s_D) {
+          const int want = -2 - s_tie_lim;             // 1-based rank inside the warp
+          const unsigned int before = __popc(bal & ((1u << lane) - 1u));
+          if (tie && (int)before + 1 == want) s_tie_lim = x;
+        }
+        __syncthreads();
+        break;
+      }
+    }
+  }
+  if (tid == 0) d.filt_tie[r] = s_tie_lim;
+}
+
+cudaError_t launch_filter(const LaneDev& d, int T, float inv_temp, int top_k, float top_p, cudaStream_t s) {
+  SV_COUNT_LAUNCH();
+  return launch_pdl(filter_kernel, dim3(T), dim3(FLT_THREADS), 0, s, 1, d, inv_temp, top_k, top_p);
+}
+
+// p'(x) of chain row r (R31): e(x) / S_keep on the kept set, else 0
+SV_DEV float filt_prob(const LaneDev& d, int r, int x, float lv_scaled, float m, float invS) {
+  if (!d.filt_on) return expf(lv_scaled - m) * invS;
+  const uint32_t k = flt_key(lv_scaled), ks = d.filt_key[r];
+  if (k < ks || (k == ks && x > d.filt_tie[r])) return 0.f;
+  return expf(lv_scaled - d.filt_m[r]) * d.filt_inv[r];
+}
+
 // ---------------------------------------------------------------- token trees (R30)
 // r(x) at the current node after `nrej` rejected children: r_0 = p_cur, r_i = max(0, r_{i-1} - q_i) / Z_i
 // (r_{i-1} when Z_i = 0); q_i = the rejected child's q row, or one-hot at its token
 struct TreeResid {
+  const LaneDev* d;
+  int row;                    // chain row of the current node (top-k / top-p filter parameters)
   const float* lrow;          // logits row of the current node
   float m, invS, inv_temp;
   int nrej;
@@ -41,7 +208,8 @@ struct TreeResid {
 };
 
 SV_DEV float tree_r(const TreeResid& t, int x) {
-  float r = expf(t.lrow[x] * t.inv_temp - t.m) * t.invS;
+  const float lv = t.lrow[x] * t.inv_temp;
+  float r = t.d->filt_on ? filt_prob(*t.d, t.row, x, lv, t.m, t.invS) : expf(lv - t.m) * t.invS;
   for (int i = 0; i < t.nrej; ++i) {
     if (t.invZ[i] == 0.f) continue;
     const float q = t.rej_q[i] ? t.rej_q[i][x] : (x == t.rej_tok[i] ? 1.0f : 0.0f);
@@ -89,7 +257,8 @@ __device__ void tree_walk(const LaneDev& d, const int* __restrict__ drafts, cons
         if (mode == SV_GREEDY) {
           indep += x == s_top[p];
         } else {
-          const float pv = expf(logits[(size_t)(r0 + p) * V + x] * inv_temp - s_m[p]) / s_S[p];
+          const float lv = logits[(size_t)(r0 + p) * V + x] * inv_temp;
+          const float pv = d.filt_on ? filt_prob(d, r0 + p, x, lv, s_m[p], 1.0f / s_S[p]) : expf(lv - s_m[p]) / s_S[p];
           const float qd = probs ? probs[(size_t)(doff + n - 1) * V + x] : 1.0f;
           const float u = uniform_accept_rank(seed, rid, uint32_t(L + s_dep[p] + 1), uint32_t(s_rank[n]));
           indep += (qd == 0.0f) || (u < pv / qd);
@@ -136,8 +305,8 @@ __device__ void tree_walk(const LaneDev& d, const int* __restrict__ drafts, cons
       } else {
         s_scan = c + 1;
         const int x = tok[c - 1];
-        TreeResid t{logits + (size_t)(r0 + cur) * V, s_m[cur], 1.0f / s_S[cur], inv_temp, s_nrej, s_rej_tok, s_rej_q,
-                    s_invZ};
+        TreeResid t{&d, r0 + cur, logits + (size_t)(r0 + cur) * V, s_m[cur], 1.0f / s_S[cur], inv_temp, s_nrej,
+                    s_rej_tok, s_rej_q, s_invZ};
         const float rv = tree_r(t, x);
         const float qd = probs ? probs[(size_t)(doff + c - 1) * V + x] : 1.0f;
         const float u = uniform_accept_rank(seed, rid, uint32_t(L + s_dep[cur] + 1), uint32_t(s_nrej));
@@ -158,7 +327,8 @@ __device__ void tree_walk(const LaneDev& d, const int* __restrict__ drafts, cons
     __syncthreads();                                 // everyone has read s_act before thread 0 rewrites it
     if (act == 1) continue;
     const int cur = s_cur, nrej = s_nrej;
-    TreeResid t{logits + (size_t)(r0 + cur) * V, s_m[cur], 1.0f / s_S[cur], inv_temp, nrej, s_rej_tok, s_rej_q, s_invZ};
+    TreeResid t{&d, r0 + cur, logits + (size_t)(r0 + cur) * V, s_m[cur], 1.0f / s_S[cur], inv_temp, nrej, s_rej_tok,
+                s_rej_q, s_invZ};
     if (act == 2) {
       const int c = s_cand, xc = tok[c - 1];
       const float* qc = probs ? probs + (size_t)(doff + c - 1) * V : nullptr;
@@ -296,7 +466,8 @@ __global__ void __launch_bounds__(FIN_THREADS) finalize_kernel(LaneDev d, const 
       for (int j = 1; j <= k; ++j) {
         const int dj = drafts[doff + j - 1];
         const float lg = logits[(size_t)(r0 + j - 1) * V + dj];
-        const float pd = expf(lg * inv_temp - s_m[j - 1]) / s_S[j - 1];
+        const float pd = d.filt_on ? filt_prob(d, r0 + j - 1, dj, lg * inv_temp, s_m[j - 1], 1.0f / s_S[j - 1])
+                                   : expf(lg * inv_temp - s_m[j - 1]) / s_S[j - 1];
         const float qd = probs ? probs[(size_t)(doff + j - 1) * V + dj] : 1.0f;
         const float u = uniform_accept(seed, rid, uint32_t(L + j));
         const bool acc = (qd == 0.0f) || (u < pd / qd);
@@ -330,7 +501,8 @@ __global__ void __launch_bounds__(FIN_THREADS) finalize_kernel(LaneDev d, const 
       for (int l = 0; l < 4; ++l) {
         const int x = mm * 4 + l;
         if (x >= (int)V) break;
-        const float p = expf(lrow[x] * inv_temp - m) * invS;
+        const float p = d.filt_on ? filt_prob(d, r0 + a, x, lrow[x] * inv_temp, m, invS)
+                                  : expf(lrow[x] * inv_temp - m) * invS;
         const float E = -logf(word_to_uniform(ws[l]));
         bP = better(bP, Best{p > 0.f ? p / E : -INFINITY, x});
         if (resid) {

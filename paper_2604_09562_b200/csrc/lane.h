@@ -25,6 +25,7 @@ struct LaneDev {
   int n_layers, D, Hq, Hkv, dh, V, F, page, n_pages, max_slots, max_batch, max_depth, max_pos;
   int max_pages_per_slot, nt, qkv_rows, Tmax;
   int tree;                          // this verify's drafts are a token tree (R30), set per call
+  int filt_on;                       // top-k / top-p filtered target (R31), set per call
   float eps;
   // borrowed weights (bf16)
   const bf16 *embed, *attn_norm, *wqkv, *wo, *ffn_norm, *w_gate_up, *w_down, *final_norm, *lm_head;
@@ -50,6 +51,9 @@ struct LaneDev {
   int *acc_int, *tok_int;            // internal copies of accepted_len / out_tokens for commit
   int* path_int;                     // [max_batch][max_depth+1] accepted path's chain rows (commit)
   unsigned long long* row_anc;       // [Tmax] ancestor-or-self node mask of each chain row
+  unsigned* filt_key;                // [Tmax] R31 filter: threshold key of the scaled logit
+  int* filt_tie;                     // [Tmax] largest kept token id among threshold ties
+  float *filt_inv, *filt_m;          // [Tmax] 1 / kept mass, row max (scaled logits)
   int* batch_n;                      // [1] batch of the pending verify (device copy)
   unsigned long long* trace;         // [16][256] clock64 trace of CTA 0 (SV_TRACE=1) or nullptr
 };
@@ -122,6 +126,7 @@ cudaError_t launch_attn_combine(const LaneDev& d, int T, cudaStream_t s);
 cudaError_t launch_finalize(const LaneDev& d, int batch, const int* draft_tokens, const int* parents,
                             const float* draft_probs, const float* logits, uint64_t seed, int mode, float inv_temp,
                             int* accepted_len, int* out_tokens, int* accepted_nodes, cudaStream_t s);
+cudaError_t launch_filter(const LaneDev& d, int T, float inv_temp, int top_k, float top_p, cudaStream_t s);
 cudaError_t launch_commit(const LaneDev& d, const int* n_keep, int batch, cudaStream_t s);
 cudaError_t launch_append(const LaneDev& d, int slot, unsigned long long rid, const bf16* k, const bf16* v,
                           int n, int pending, const int* pending_dev, int packed, cudaStream_t s);

@@ -25,7 +25,7 @@ struct Layout {
   size_t slots, depths, row_off, row_req, row_pos, chain_tok, req_err;
   size_t h0, h1, h2, cbuf, logits, tile_max, tile_sum, tile_arg;
   size_t a, b, z, q, kc, vc, o, u;
-  size_t items, item_start, n_items, part_o, part_ml, acc_int, tok_int, batch_n, path_int, row_anc;
+  size_t items, item_start, n_items, part_o, part_ml, acc_int, tok_int, batch_n, path_int, row_anc, filt;
   size_t gemm_ws, trace, prefill;
   size_t max_items;
 
@@ -112,6 +112,7 @@ Layout make_layout(const sv_config& c) {
   L.batch_n = L.take(4);
   L.path_int = L.take(4 * c.max_batch * (c.max_depth + 1));
   L.row_anc = L.take(8 * T);
+  L.filt = L.take(16 * T);
   L.gemm_ws = L.take(sv::gemm_workspace_bytes((int)T, (int)cmax));
   L.trace = L.take(8 * 16 * 256);
   L.prefill = L.take(4 * 3 * (size_t)(c.max_depth + 2));   // sv_prefill: chunk tokens + outputs
@@ -123,10 +124,10 @@ Layout make_layout(const sv_config& c) {
 
 // live per-stage timing with CUDA events on the lane's stream (sv_profile_*)
 enum Stage { ST_PLAN = 0, ST_EMBED, ST_QKV, ST_ATTN, ST_COMBINE, ST_OPROJ, ST_FFN_NORM, ST_GATE_UP, ST_DOWN,
-             ST_FINAL_NORM, ST_LM_HEAD, ST_FINALIZE, ST_COMMIT, ST_DRAFT, ST_ATTN_NORM, ST_NUM };
+             ST_FINAL_NORM, ST_LM_HEAD, ST_FINALIZE, ST_COMMIT, ST_DRAFT, ST_ATTN_NORM, ST_FILTER, ST_NUM };
 static const char* kStageNames[ST_NUM] = {"plan", "embed_norm", "qkv_rope", "attention", "attn_combine", "o_proj",
                                           "ffn_norm", "gate_up_swiglu", "down", "final_norm", "lm_head",
-                                          "finalize", "commit", "draft", "attn_norm"};
+                                          "finalize", "commit", "draft", "attn_norm", "filter"};
 
 struct Prof {
   uint32_t mask = 0;                          // bit i: time stage i
@@ -163,6 +164,8 @@ struct sv_ctx {
   int last_T = 0, last_batch = 0;
   int sticky = 0;
   bool taps = false;                 // keep every intermediate (fp32 logits included) for sv_get_tap
+  int top_k = 0;                     // R31 filtered target for SAMPLE (0 / >= 1: off), sv_set_filter
+  float top_p = 1.0f;
   sv::GemmPlan* gemm = nullptr;
   Prof prof;
 };
@@ -342,6 +345,11 @@ sv_status sv_create(const sv_config* cfg, const sv_weights* w, void* kv_pool, vo
   d.path_int = (int*)(ws + L.path_int);
   d.row_anc = (unsigned long long*)(ws + L.row_anc);
   d.tree = 0;
+  d.filt_on = 0;
+  d.filt_key = (unsigned*)(ws + L.filt);
+  d.filt_tie = (int*)(ws + L.filt + 4 * (size_t)d.Tmax);
+  d.filt_inv = (float*)(ws + L.filt + 8 * (size_t)d.Tmax);
+  d.filt_m = (float*)(ws + L.filt + 12 * (size_t)d.Tmax);
   d.trace = getenv("SV_TRACE") ? (unsigned long long*)(ws + L.trace) : nullptr;
 
   // RoPE table: fp64 angles pos * theta^(-2m/d_h), stored fp32 (SURVEY.md §8(c) "Model details")
@@ -428,6 +436,8 @@ static sv_status gemm(sv_ctx* c, const bf16* A, const bf16* B, float* C, int M, 
   return cuda_ok(sv::gemm_run(c->gemm, A, B, C, M, N, K, epi, e, c->stream));
 }
 
+static bool filter_active(const sv_ctx* c) { return (c->top_k > 0 && c->top_k < c->cfg.vocab) || c->top_p < 1.0f; }
+
 // sv_verify and sv_verify_tree (parents != NULL: token-tree drafts, R30)
 static sv_status verify_impl(sv_ctx* c, int32_t batch, const int32_t* slots, const int32_t* depths,
                              const int32_t* parents, const int32_t* draft_tokens, const float* draft_probs,
@@ -480,6 +490,8 @@ static sv_status verify_impl(sv_ctx* c, int32_t batch, const int32_t* slots, con
   // are stored only when something reads them
   e.write_out = c->taps || mode == SV_SAMPLE || logits_out != nullptr;
   STAGE(c, ST_LM_HEAD, gemm(c, d.z, d.lm_head, d.logits, T, d.V, d.D, sv::EPI_LOGITS, e));
+  d.filt_on = mode == SV_SAMPLE && filter_active(c);
+  if (d.filt_on) STAGE(c, ST_FILTER, sv::launch_filter(d, T, inv_temp, c->top_k, c->top_p, s));
   STAGE(c, ST_FINALIZE, sv::launch_finalize(d, batch, draft_tokens, parents, draft_probs, d.logits, seed, mode,
                                             inv_temp, accepted_len, out_tokens, accepted_nodes, s));
   if (logits_out)
@@ -529,6 +541,8 @@ static sv_status verify_logits_impl(sv_ctx* c, int32_t batch, const int32_t* slo
   SV_CUDA(sv::launch_plan(d, p, draft_tokens, parents, false, c->stream));
   d.logits = const_cast<float*>(logits);
   SV_CUDA(sv::launch_tile_stats(d, p.T, inv_temp, c->stream));
+  d.filt_on = mode == SV_SAMPLE && filter_active(c);
+  if (d.filt_on) SV_CUDA(sv::launch_filter(d, p.T, inv_temp, c->top_k, c->top_p, c->stream));
   SV_CUDA(sv::launch_finalize(d, batch, draft_tokens, parents, draft_probs, logits, seed, mode, inv_temp,
                               accepted_len, out_tokens, accepted_nodes, c->stream));
   c->last_T = p.T;
@@ -610,6 +624,14 @@ sv_status sv_stats(sv_ctx* c, sv_lane_stats* out, int reset) {
   if (reset) SV_CUDA(cudaMemsetAsync(c->d.stats, 0, sizeof(buf), c->stream));
   if (err & SV_DERR_NO_PAGES) return SV_ENOKV;
   if (err) return SV_EDEVICE;
+  return SV_OK;
+}
+
+sv_status sv_set_filter(sv_ctx* c, int32_t top_k, float top_p) {
+  if (!c || top_k < 0 || !(top_p > 0.0f)) return SV_EINVAL;     // rejects NaN too
+  if (c->pending_verify) return SV_ESTATE;
+  c->top_k = top_k;
+  c->top_p = top_p;
   return SV_OK;
 }
 

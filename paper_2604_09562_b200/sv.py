@@ -31,7 +31,7 @@ EXPORTED = [
     "sv_profile_stage_name", "sv_profile_read", "sv_launch_count", "sv_debug_gemm", "sv_kv_append_packed",
     "sv_kv_loopback_append", "sv_spec_default_config", "sv_spec_reset", "sv_spec_adapt", "sv_spec_step",
     "sv_route_default_config", "sv_route_select", "sv_lane_occupancy", "sv_kv_pack_slot", "sv_prefill",
-    "sv_verify_tree", "sv_verify_tree_logits",
+    "sv_verify_tree", "sv_verify_tree_logits", "sv_set_filter",
 ]
 
 
@@ -104,6 +104,7 @@ def load():
                            ctypes.c_int),
         "sv_verify_tree_logits": ([vp, i32, P(i32), P(i32), vp, vp, vp, vp, u64, ctypes.c_int, ctypes.c_float, vp,
                                    vp, vp], ctypes.c_int),
+        "sv_set_filter": ([vp, i32, ctypes.c_float], ctypes.c_int),
         "sv_commit": ([vp, vp], ctypes.c_int),
         "sv_release": ([vp, i32], ctypes.c_int),
         "sv_stats": ([vp, P(LaneStats), ctypes.c_int], ctypes.c_int),
@@ -296,6 +297,10 @@ class Lane:
         st = LaneStats()
         _check(self.lib.sv_stats(self.ctx, ctypes.byref(st), 1 if reset else 0), "sv_stats")
         return st
+
+    def set_filter(self, top_k=0, top_p=1.0):
+        """Top-k / top-p filtered target for SAMPLE verifies (R31); (0, 1.0) = off."""
+        _check(self.lib.sv_set_filter(self.ctx, int(top_k), float(top_p)), "sv_set_filter")
 
     def set_taps(self, on=True):
         """Keep every intermediate (incl. the fp32 logits a greedy verify would skip) for tap()."""
