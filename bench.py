@@ -2,7 +2,7 @@
 """Benchmark of the speculative-verify hot path (BASELINE.json metric):
 accepted tokens/s of the verify step, verify-step us, % of the HBM / tensor roofline.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload ns|c2|c3|c4|toy]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload ns|ns32|ns_tree|c2|c2_filter|c3|c4|toy]
     python bench.py --impl reference ...        # the fp64 CPU oracle arm
     torchrun --nproc-per-node N bench.py --gpus N ...
 
@@ -141,8 +141,25 @@ def build_lane(wl, rank, dev):
         lane.append_kv(i, rid, k.to(dev), v.to(dev), pend)
         reqs.append(dict(L=n, rid=rid, pending=pend, k=None if wl.gen_on_device else k,
                          v=None if wl.gen_on_device else v))
+    if wl.top_k or wl.top_p < 1.0:
+        lane.set_filter(wl.top_k, wl.top_p)          # R31 filtered target (SAMPLE workloads)
     torch.cuda.synchronize(dev)
     return lane, w, succ, reqs
+
+
+def draft_and_verify(lane, wl, slots, ks, succ_d, mask_d, devtok_d, drafts, seed, out, parents_d=None):
+    """One drafter launch + one verify through the public API (chain, or token tree for tree workloads)."""
+    if wl.tree:
+        lane.draft_planted_tree(slots, ks, parents_d, succ_d, mask_d, devtok_d, drafts)
+        lane.verify_tree(slots, ks, parents_d, drafts, None, seed=seed, mode=wl.mode, temperature=wl.temperature,
+                         out=out)
+    else:
+        lane.draft_planted(slots, ks, succ_d, mask_d, devtok_d, drafts)
+        lane.verify(slots, ks, drafts, None, seed=seed, mode=wl.mode, temperature=wl.temperature, out=out)
+
+
+def tree_parents(wl, dev):
+    return torch.tensor(list(wl.tree) * wl.batch, dtype=torch.int32, device=dev) if wl.tree else None
 
 
 def depths_for(wl, n_steps, seed):
@@ -226,14 +243,13 @@ def run_gpu(args, wl, rank, world, dev):
     acc = torch.empty(B, dtype=torch.int32, device=dev)
     tok = torch.empty(B, cfg.max_depth + 1, dtype=torch.int32, device=dev)
     slots = list(range(B))
-    mode = wl.mode
+    par_d = tree_parents(wl, dev)
 
     def step(i):
         if ctl:
             ctl.prepare(i, masks_d, devtok_d)
-        lane.draft_planted(slots, depths[i], succ_d, masks_d[i], devtok_d[i], drafts)
-        lane.verify(slots, depths[i], drafts, None, seed=1234 + i, mode=mode, temperature=wl.temperature,
-                    out=(acc, tok))
+        draft_and_verify(lane, wl, slots, depths[i], succ_d, masks_d[i], devtok_d[i], drafts, 1234 + i, (acc, tok),
+                         par_d)
         lane.commit()
 
     for i in range(args.warmup):
@@ -310,8 +326,9 @@ def run_gpu(args, wl, rank, world, dev):
             ctl.prepare(i)
     if args.e2e_steps > 0:
         e2e = run_e2e(args, wl, lane, succ, depths, masks, devtok, dev, total)
-        e2e_host = run_e2e_host_drafter(args, wl, lane, succ, depths, masks, devtok, dev, total + args.e2e_steps,
-                                        HOST_DRAFTER_STEPS)
+        if not wl.tree:                               # the host drafter variant drafts chains only
+            e2e_host = run_e2e_host_drafter(args, wl, lane, succ, depths, masks, devtok, dev,
+                                            total + args.e2e_steps, HOST_DRAFTER_STEPS)
     return dict(elapsed_ms=elapsed_ms, tokens=tokens, per_step=per_step, prof=kern, roof=roof, dominant=dominant,
                 launches=launches, clocks=clk.summary(), stats=st, e2e=e2e, e2e_host=e2e_host, w=w, succ=succ, reqs=reqs,
                 depths=depths, masks=masks, devtok=devtok, alg=alg,
@@ -343,6 +360,7 @@ def run_e2e(args, wl, lane, succ, depths, masks, devtok, dev, start):
     done = [torch.cuda.Event() for _ in range(2)]
     stream = torch.cuda.current_stream(dev)
     emitted_host = 0
+    par_d = tree_parents(wl, dev)
 
     def consume(slot):
         nonlocal emitted_host
@@ -358,9 +376,7 @@ def run_e2e(args, wl, lane, succ, depths, masks, devtok, dev, start):
         sl = s_ & 1
         d_mask[sl].copy_(h_mask[s_], non_blocking=True)
         d_dev[sl].copy_(h_dev[s_], non_blocking=True)
-        lane.draft_planted(slots, depths[i], succ_d, d_mask[sl], d_dev[sl], drafts)
-        lane.verify(slots, depths[i], drafts, None, seed=99 + i, mode=wl.mode, temperature=wl.temperature,
-                    out=(acc, tok))
+        draft_and_verify(lane, wl, slots, depths[i], succ_d, d_mask[sl], d_dev[sl], drafts, 99 + i, (acc, tok), par_d)
         lane.commit()
         h_acc[sl].copy_(acc, non_blocking=True)
         h_tok[sl].copy_(tok, non_blocking=True)
@@ -460,15 +476,21 @@ def oracle_steps(wl, lane, n_req, succ, depths, masks, devtok, step_ids):
         m, dt = masks[i].numpy(), devtok[i].numpy()
         drafts, off = [], 0
         for b in range(n_req):
-            prev = lane.slots[b]["pending"]
+            toks = [lane.slots[b]["pending"]]
             for j in range(ks[b]):
-                t = int(dt[off + j]) if m[off + j] else int(succ_h[prev])
+                par = wl.tree[j] if wl.tree else j
+                t = int(dt[off + j]) if m[off + j] else int(succ_h[toks[par]])
                 drafts.append(t)
-                prev = t
+                toks.append(t)
             off += ks[b]
         mode = ov.GREEDY if wl.mode == "greedy" else ov.SAMPLE
         t0 = time.perf_counter()
-        acc, em, _ = lane.verify(list(range(n_req)), ks, drafts, None, 1234 + i, mode, wl.temperature)
+        if wl.tree:
+            acc, em, _, _ = lane.verify_tree(list(range(n_req)), ks, list(wl.tree) * n_req, drafts, None, 1234 + i,
+                                             mode, wl.temperature, top_k=wl.top_k, top_p=wl.top_p)
+        else:
+            acc, em, _ = lane.verify(list(range(n_req)), ks, drafts, None, 1234 + i, mode, wl.temperature,
+                                     top_k=wl.top_k, top_p=wl.top_p)
         lane.commit()
         secs += time.perf_counter() - t0
         tokens += sum(a + 1 for a in acc)
@@ -502,7 +524,9 @@ def bench_config(wl, world):
     return {"workload": wl.name, "model": f"Llama-3-8B-shaped {nl} layer{'s' if nl > 1 else ''} + lm-head (random init, "
             "planted successor)" if wl.cfg.d_model == 4096 else "toy", "batch_per_gpu": wl.batch, "depth": [wl.kmin, wl.kmax],
             "ctx": list(wl.ctx), "mode": wl.mode, "parallelism": f"dp{world} (independent decode lanes)",
-            "l2": "inputs > L2 (weights >= 1.5 GB + KV >= 1 GB per step)", "drafter": f"planted alpha={wl.alpha}"}
+            "l2": "inputs > L2 (weights >= 1.5 GB + KV >= 1 GB per step)", "drafter": f"planted alpha={wl.alpha}",
+            **({"tree_parents": list(wl.tree)} if wl.tree else {}),
+            **({"top_k": wl.top_k, "top_p": wl.top_p} if (wl.top_k or wl.top_p < 1.0) else {})}
 
 
 REFERENCE_BUDGET_S = 150.0   # the reference arm's timed steps are time-boxed to this

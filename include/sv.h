@@ -268,6 +268,13 @@ sv_status sv_draft_planted(sv_ctx* ctx, int32_t batch, const int32_t* slots, con
                            const int32_t* succ, const uint8_t* dev_mask, const int32_t* dev_tok,
                            int32_t* draft_tokens);
 
+/* The same fixture for token trees (R30): node n's token is succ[token of parents[n-1]] (node 0 =
+ * the pending token) unless dev_mask marks it, then dev_tok. parents: DEVICE [sum k] as in
+ * sv_verify_tree. One launch. */
+sv_status sv_draft_planted_tree(sv_ctx* ctx, int32_t batch, const int32_t* slots, const int32_t* depths,
+                                const int32_t* parents, const int32_t* succ, const uint8_t* dev_mask,
+                                const int32_t* dev_tok, int32_t* draft_tokens);
+
 /* Measurement hooks (bench.py): per-stage CUDA-event timing on the lane's stream.
  * sv_profile_enable(ctx, mask) brackets stage i of sv_verify / sv_commit /
  * sv_draft_planted with cudaEventRecord when bit i of mask is set (-1 = all

@@ -72,7 +72,7 @@ class OracleLane:
         return model.forward_chain(self.w, tokens, pos, caches, self.cfg, self.cos, self.sin)
 
     def verify(self, slots, depths, draft_tokens, draft_probs, seed, mode, temperature=1.0,
-               logits_override=None):
+               logits_override=None, top_k=0, top_p=1.0):
         """Returns (accepted_len list, emitted token lists, per-request logits).
 
         draft_tokens: flat [sum k]; draft_probs: flat [sum k][V] or None.
@@ -90,7 +90,7 @@ class OracleLane:
             else:
                 _, logits, kv = self.forward(slot, drafts)
             r = verify.verify_request(logits, drafts, q_rows, seed, self.slots[slot]["rid"],
-                                      self.length(slot), mode, temperature)
+                                      self.length(slot), mode, temperature, top_k, top_p)
             results.append(r)
             logits_all.append(logits)
             chain.append(kv)
@@ -99,7 +99,7 @@ class OracleLane:
         return [r["a"] for r in results], [r["emitted"] for r in results], logits_all
 
     def verify_tree(self, slots, depths, parents, draft_tokens, draft_probs, seed, mode, temperature=1.0,
-                    logits_override=None):
+                    logits_override=None, top_k=0, top_p=1.0):
         """Token-tree verify (oracle/tree.py, R30): parents flat [sum k] (per request,
         node n's parent in 0..n-1). Returns (accepted_len, emitted, logits, paths)."""
         results, logits_all, chain = [], [], []
@@ -116,7 +116,7 @@ class OracleLane:
             else:
                 _, logits, kv = tree.forward_tree(self.w, [st["pending"]] + drafts, par, L,
                                                   list(zip(st["K"], st["V"])), self.cfg, self.cos, self.sin)
-            r = tree.verify_tree(logits, drafts, par, q_rows, seed, st["rid"], L, mode, temperature)
+            r = tree.verify_tree(logits, drafts, par, q_rows, seed, st["rid"], L, mode, temperature, top_k, top_p)
             results.append(r)
             logits_all.append(logits)
             chain.append(kv)

@@ -8,6 +8,8 @@
 //   y = argmax_{x: R(x) > 0} R(x) / (-ln U(seed, rid, L + a + 1, RACE, x)), ties -> lowest x,
 //   R = max(0, p_{a+1} - q_{a+1}) (p_{a+1} if that sums to 0) when a < k, else p_{k+1}.
 //   Greedy: a = longest prefix with d_j == argmax l_{j-1} (lowest id), y = argmax l_a.
+#include <algorithm>
+
 #include "common.cuh"
 #include "lane.h"
 #include "../../include/sv.h"
@@ -39,80 +41,232 @@ SV_DEV Best warp_best(Best v) {
 constexpr int FLT_THREADS = 1024;
 constexpr double kFx = 1099511627776.0;            // 2^40
 
+// e in (0, 1] -> round(e * 2^40): the float product is exact (power-of-two scale), then rounded
+SV_DEV unsigned long long fx_mass(float e) { return __float2ull_rn(e * 1099511627776.0f); }
+
 SV_DEV uint32_t flt_key(float v) {
   const uint32_t u = v == 0.0f ? 0u : __float_as_uint(v);     // -0 and +0 are the same value (a tie)
   return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
 }
 SV_DEV float key_flt(uint32_t k) { return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k); }
 
+constexpr int FLT_CAP = 4096;                     // fast path: candidate capacity (shared memory)
+constexpr size_t FLT_SMEM = (FLT_THREADS / 32) * 256 * (8 + 4);   // 96 KB: private histograms / candidates
+static_assert(FLT_CAP * 16 + FLT_THREADS * 4 <= FLT_SMEM, "filter candidate buffers exceed the smem budget");
+
 __global__ void __launch_bounds__(FLT_THREADS) filter_kernel(LaneDev d, float inv_temp, int top_k, float top_p) {
+  extern __shared__ unsigned long long flt_smem[];
+  // slow path: per-warp private histograms [NW][256] (mass u64, count u32)
+  unsigned long long* w_mass = flt_smem;
+  unsigned int* w_cnt = reinterpret_cast<unsigned int*>(flt_smem + (FLT_THREADS / 32) * 256);
+  // fast path (same memory): candidate masses / keys / ids, and the sorted tile maxima
+  unsigned long long* c_mass = flt_smem;
+  uint32_t* c_key = reinterpret_cast<uint32_t*>(c_mass + FLT_CAP);
+  int* c_id = reinterpret_cast<int*>(c_key + FLT_CAP);
+  float* srt = reinterpret_cast<float*>(c_id + FLT_CAP);          // [FLT_THREADS]
   __shared__ unsigned int h_cnt[256];
   __shared__ unsigned long long h_mass[256];
   __shared__ float s_redf[FLT_THREADS / 32];
   __shared__ unsigned long long s_redu[FLT_THREADS / 32];
   __shared__ uint32_t s_prefix, s_D;
-  __shared__ unsigned int s_cnt_above, s_run;
-  __shared__ unsigned long long s_mass_above, s_total;
-  __shared__ int s_tie_lim, s_nkeep;
+  __shared__ unsigned int s_cnt_above, s_nc;
+  __shared__ unsigned long long s_mass_above, s_target, s_cmass;
+  __shared__ int s_tie_lim, s_nkeep, s_fast;
+  __shared__ float s_tau;
   pdl_trigger();
   pdl_wait();
   const int r = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = FLT_THREADS / 32;
-  const int V = d.V;
+  const int V = d.V, nt = d.nt;
   const float* row = d.logits + (size_t)r * V;
-  // row max m (exact: max over the tile maxima of the same scaled values)
-  float m = -INFINITY;
-  for (int t = tid; t < d.nt; t += FLT_THREADS) m = fmaxf(m, d.tile_max[(size_t)r * d.nt + t]);
-  m = warp_max(m);
-  if (lane == 0) s_redf[warp] = m;
-  __syncthreads();
-  m = s_redf[0];
-  for (int i = 1; i < nw; ++i) m = fmaxf(m, s_redf[i]);
+  const float* tmax = d.tile_max + (size_t)r * nt;
+  const float* tsum = d.tile_sum + (size_t)r * nt;
   const bool use_k = top_k > 0 && top_k < V, use_p = top_p < 1.0f;
-  // total mass (fixed point)
+
+  // 1. tile maxima sorted descending (bitonic, in shared memory): the row max m, and a lower bound
+  //    tau on the kept set — the top_k-th largest tile maximum (the k largest tile maxima are k
+  //    distinct elements), and the largest tile maximum whose running mass (tile maxima only) already
+  //    reaches top_p of the row's mass with a 1e-3 margin. Every kept element is >= tau.
+  const bool sortable = nt <= FLT_THREADS;
+  float m;
+  if (sortable) {
+    srt[tid] = tid < nt ? tmax[tid] : -INFINITY;
+    __syncthreads();
+    for (int k2 = 2; k2 <= FLT_THREADS; k2 <<= 1)
+      for (int j = k2 >> 1; j > 0; j >>= 1) {
+        const int o = tid ^ j;
+        if (o > tid) {
+          const float x = srt[tid], y = srt[o];
+          const bool desc = (tid & k2) == 0;
+          if (desc ? (x < y) : (x > y)) { srt[tid] = y; srt[o] = x; }
+        }
+        __syncthreads();
+      }
+    m = srt[0];
+  } else {
+    float mm = -INFINITY;
+    for (int t = tid; t < nt; t += FLT_THREADS) mm = fmaxf(mm, tmax[t]);
+    mm = warp_max(mm);
+    if (lane == 0) s_redf[warp] = mm;
+    __syncthreads();
+    m = s_redf[0];
+    for (int i = 1; i < nw; ++i) m = fmaxf(m, s_redf[i]);
+    __syncthreads();
+  }
+  if (tid == 0) { s_prefix = 0; s_cnt_above = 0; s_mass_above = 0; s_nc = 0; s_cmass = 0; s_tau = -INFINITY; }
+  if (sortable) {
+    float tau = -INFINITY;
+    if (use_k && top_k <= nt) tau = srt[top_k - 1];
+    if (use_p) {
+      // S estimate from the tile statistics; prefix sums of e(tile max) in sorted order (warp scans)
+      float se = 0.f;
+      for (int t = tid; t < nt; t += FLT_THREADS) se += tsum[t] * expf(tmax[t] - m);
+      se = warp_sum(se);
+      if (lane == 0) s_redf[warp] = se;
+      __syncthreads();
+      float S = 0.f;
+      for (int i = 0; i < nw; ++i) S += s_redf[i];
+      float e = tid < nt ? expf(srt[tid] - m) : 0.f;
+      float incl = e;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const float y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      __syncthreads();
+      if (lane == 31) s_redf[warp] = incl;
+      __syncthreads();
+      float before = 0.f;
+      for (int i = 0; i < warp; ++i) before += s_redf[i];
+      incl += before;
+      __syncthreads();                                 // every warp has read s_redf
+      const float need = top_p * S * 1.001f;
+      const bool hit = tid < nt && incl >= need && incl - e < need;   // the first index reaching it
+      if (hit) s_redf[0] = srt[tid];                    // (at most one thread)
+      __syncthreads();
+      const bool any = __syncthreads_or(hit);
+      if (any) tau = fmaxf(tau, s_redf[0]);
+    }
+    if (tid == 0) s_tau = tau;
+  }
+  __syncthreads();
+  const float tau = s_tau;
+
+  // 2. one pass over the row: fixed-point total mass; candidates >= tau into shared memory
   unsigned long long tot = 0;
-  for (int x = tid; x < V; x += FLT_THREADS) tot += (unsigned long long)llrint((double)expf(row[x] * inv_temp - m) * kFx);
+  constexpr int U = 8;                                 // loads of U elements in flight per thread
+  for (int x0 = tid; x0 < V; x0 += FLT_THREADS * U) {
+    float vv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int x = x0 + u * FLT_THREADS;
+      vv[u] = x < V ? row[x] * inv_temp : -INFINITY;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const float v = vv[u];
+      const unsigned long long e = v == -INFINITY ? 0ull : fx_mass(expf(v - m));
+      tot += e;
+      if (tau > -INFINITY && v >= tau) {
+        const unsigned pos = atomicAdd(&s_nc, 1u);
+        if (pos < FLT_CAP) {
+          c_key[pos] = flt_key(v);
+          c_id[pos] = x0 + u * FLT_THREADS;
+          c_mass[pos] = e;
+          atomicAdd(&s_cmass, e);
+        }
+      }
+    }
+  }
   for (int o = 16; o; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
   if (lane == 0) s_redu[warp] = tot;
-  if (tid == 0) { s_prefix = 0; s_cnt_above = 0; s_mass_above = 0; }
   __syncthreads();
   if (tid == 0) {
     unsigned long long t2 = 0;
     for (int i = 0; i < nw; ++i) t2 += s_redu[i];
-    s_total = t2;
+    const unsigned long long target = use_p ? (unsigned long long)((double)top_p * (double)t2) : ~0ull;
+    s_target = target;
+    // the kept set lies inside the candidates iff a limit is reached inside them
+    s_fast = tau > -INFINITY && s_nc <= (unsigned)FLT_CAP &&
+             ((use_k && s_nc >= (unsigned)top_k) || (use_p && s_cmass >= target));
   }
   __syncthreads();
-  // mass target: smallest prefix with mass >= top_p * total (compared in fixed point)
-  const unsigned long long target = use_p ? (unsigned long long)((double)top_p * (double)s_total) : ~0ull;
+  const bool fast = s_fast;
+  const unsigned nc = s_nc;
+  const unsigned long long target = s_target;
+  unsigned long long* my_mass = w_mass + warp * 256;
+  unsigned int* my_cnt = w_cnt + warp * 256;
+
+  // 3. radix select of the threshold element, 8 bits per pass, most significant first
   for (int pass = 0; pass < 4; ++pass) {
     const int shift = 24 - 8 * pass;
     const uint32_t hi_mask = pass == 0 ? 0u : (0xffffffffu << (shift + 8));
-    for (int i = tid; i < 256; i += FLT_THREADS) { h_cnt[i] = 0; h_mass[i] = 0; }
-    __syncthreads();
     const uint32_t prefix = s_prefix;
-    for (int x = tid; x < V; x += FLT_THREADS) {
-      const float v = row[x] * inv_temp;
-      const uint32_t k = flt_key(v);
-      if ((k & hi_mask) == prefix) {
-        const int dg = (k >> shift) & 255;
-        atomicAdd(&h_cnt[dg], 1u);
-        atomicAdd(&h_mass[dg], (unsigned long long)llrint((double)expf(v - m) * kFx));   // S_keep needs it
+    if (fast) {
+      for (int i = tid; i < 256; i += FLT_THREADS) { h_cnt[i] = 0; h_mass[i] = 0; }
+      __syncthreads();
+      for (unsigned i = tid; i < nc; i += FLT_THREADS) {
+        const uint32_t k = c_key[i];
+        if ((k & hi_mask) == prefix) {
+          const int dg = (k >> shift) & 255;
+          atomicAdd(&h_cnt[dg], 1u);
+          atomicAdd(&h_mass[dg], c_mass[i]);
+        }
       }
+      __syncthreads();
+    } else {
+      for (int i = lane; i < 256; i += 32) { my_cnt[i] = 0; my_mass[i] = 0; }
+      __syncwarp();
+      // warp-aggregated private histograms: lanes with the same digit add count and mass with one
+      // reduction (most of a warp in the early passes, where neighbouring logits share an exponent)
+      for (int x0 = warp * 32; x0 < V; x0 += FLT_THREADS) {
+        const int x = x0 + lane;
+        float v = 0.f;
+        int dg = -1;
+        if (x < V) {
+          v = row[x] * inv_temp;
+          const uint32_t k = flt_key(v);
+          if ((k & hi_mask) == prefix) dg = (k >> shift) & 255;
+        }
+        const unsigned peers = __match_any_sync(0xffffffffu, dg);
+        if (dg >= 0) {
+          const unsigned long long e = fx_mass(expf(v - m));
+          const unsigned lo = (unsigned)e, hi = (unsigned)(e >> 32);
+          const unsigned s0 = __reduce_add_sync(peers, lo & 0xffffu);
+          const unsigned s1 = __reduce_add_sync(peers, lo >> 16);
+          const unsigned s2 = __reduce_add_sync(peers, hi);
+          if (lane == __ffs(peers) - 1) {
+            my_cnt[dg] += (unsigned)__popc(peers);
+            my_mass[dg] += (unsigned long long)s0 + ((unsigned long long)s1 << 16) + ((unsigned long long)s2 << 32);
+          }
+        }
+      }
+      __syncthreads();
+      for (int bin = tid; bin < 256; bin += FLT_THREADS) {     // fixed-order merge of the warps
+        unsigned int c = 0;
+        unsigned long long ms = 0;
+        for (int w = 0; w < nw; ++w) { c += w_cnt[w * 256 + bin]; ms += w_mass[w * 256 + bin]; }
+        h_cnt[bin] = c;
+        h_mass[bin] = ms;
+      }
+      __syncthreads();
     }
-    __syncthreads();
     if (tid == 0) {
       unsigned int c = s_cnt_above;
       unsigned long long ms = s_mass_above;
-      int D = 0;
+      int D = -1;
       for (int dg = 255; dg >= 0; --dg) {
+        if (!h_cnt[dg]) continue;
         const unsigned int c2 = c + h_cnt[dg];
         const unsigned long long m2 = ms + h_mass[dg];
-        if (h_cnt[dg] && ((use_k && c2 >= (unsigned)top_k) || (use_p && m2 >= target) || dg == 0)) { D = dg; break; }
+        D = dg;
+        if ((use_k && c2 >= (unsigned)top_k) || (use_p && m2 >= target)) break;
         c = c2;
         ms = m2;
       }
-      // the lowest non-empty bin is the fallback (no limit reached: keep everything from here on)
-      if (h_cnt[D] == 0) {
-        for (int dg = 0; dg < 256; ++dg) if (h_cnt[dg]) { D = dg; break; }
+      if (D < 0) D = 0;                                // (unreachable: a limit is always reached)
+      else if (!((use_k && c + h_cnt[D] >= (unsigned)top_k) || (use_p && ms + h_mass[D] >= target))) {
+        c -= h_cnt[D];                                 // no limit reached: the lowest bin is the cut
+        ms -= h_mass[D];
       }
       s_cnt_above = c;
       s_mass_above = ms;
@@ -121,11 +275,11 @@ __global__ void __launch_bounds__(FLT_THREADS) filter_kernel(LaneDev d, float in
     }
     __syncthreads();
   }
-  // ties: every element with key == s_prefix; keep them in id order up to the limits
+  // 4. ties at the threshold key: keep them in id order up to the count / mass limit
   if (tid == 0) {
     const unsigned int n_ties = h_cnt[s_D];
     const float vstar = key_flt(s_prefix);
-    const unsigned long long e = (unsigned long long)llrint((double)expf(vstar - m) * kFx);
+    const unsigned long long e = fx_mass(expf(vstar - m));
     unsigned long long n = n_ties;
     if (use_k) n = min(n, (unsigned long long)(top_k - s_cnt_above));
     if (use_p && e > 0 && target > s_mass_above) {
@@ -137,60 +291,80 @@ __global__ void __launch_bounds__(FLT_THREADS) filter_kernel(LaneDev d, float in
     if (n < 1) n = 1;
     s_nkeep = (int)n;
     s_tie_lim = n >= n_ties ? V : -1;
-    s_run = 0;
     const unsigned long long keep = s_mass_above + n * e;
     d.filt_key[r] = s_prefix;
     d.filt_inv[r] = (float)(kFx / (double)keep);
     d.filt_m[r] = m;
   }
   __syncthreads();
-  if (s_tie_lim < 0) {                                 // the n-th tie in id order
+  if (s_tie_lim < 0) {                                 // the n-th smallest id among the ties
     const uint32_t kstar = s_prefix;
     const int n = s_nkeep;
-    for (int x0 = 0; x0 < V; x0 += FLT_THREADS) {
-      const int x = x0 + tid;
-      const bool tie = x < V && flt_key(row[x] * inv_temp) == kstar;
-      const unsigned int bal = __ballot_sync(0xffffffffu, tie);
-      if (lane == 0) h_cnt[warp] = __popc(bal);
-      __syncthreads();
-      if (tid == 0) {
-        unsigned int run = s_run;
-        for (int w = 0; w < nw; ++w) {
-          if (run + h_cnt[w] >= (unsigned)n) {         // in warp w: the (n - run)-th set lane
-            s_D = w;
-            s_tie_lim = -2 - (int)(n - run);           // marker: resolve below
-            break;
-          }
-          run += h_cnt[w];
-        }
-        s_run = run;
+    if (fast) {
+      for (unsigned i = tid; i < nc; i += FLT_THREADS) {
+        if (c_key[i] != kstar) continue;
+        int rank = 0;
+        for (unsigned j = 0; j < nc; ++j) rank += c_key[j] == kstar && c_id[j] < c_id[i];
+        if (rank == n - 1) s_tie_lim = c_id[i];
       }
-      __syncthreads();
-      if (s_tie_lim <= -2) {
-        if (warp == (int)s_D) {
-          const int want = -2 - s_tie_lim;             // 1-based rank inside the warp
-          const unsigned int before = __popc(bal & ((1u << lane) - 1u));
-          if (tie && (int)before + 1 == want) s_tie_lim = x;
+    } else {
+      unsigned int run = 0;                            // (thread 0's running count)
+      for (int x0 = 0; x0 < V; x0 += FLT_THREADS) {
+        const int x = x0 + tid;
+        const bool tie = x < V && flt_key(row[x] * inv_temp) == kstar;
+        const unsigned int bal = __ballot_sync(0xffffffffu, tie);
+        if (lane == 0) h_cnt[warp] = __popc(bal);
+        __syncthreads();
+        if (tid == 0) {
+          for (int w = 0; w < nw; ++w) {
+            if (run + h_cnt[w] >= (unsigned)n) {       // in warp w: the (n - run)-th set lane
+              s_D = w;
+              s_tie_lim = -2 - (int)(n - run);         // marker: resolve below
+              break;
+            }
+            run += h_cnt[w];
+          }
         }
         __syncthreads();
-        break;
+        if (s_tie_lim <= -2) {
+          if (warp == (int)s_D) {
+            const int want = -2 - s_tie_lim;           // 1-based rank inside the warp
+            const unsigned int before = __popc(bal & ((1u << lane) - 1u));
+            if (tie && (int)before + 1 == want) s_tie_lim = x;
+          }
+          __syncthreads();
+          break;
+        }
       }
     }
+    __syncthreads();
   }
   if (tid == 0) d.filt_tie[r] = s_tie_lim;
 }
 
 cudaError_t launch_filter(const LaneDev& d, int T, float inv_temp, int top_k, float top_p, cudaStream_t s) {
   SV_COUNT_LAUNCH();
-  return launch_pdl(filter_kernel, dim3(T), dim3(FLT_THREADS), 0, s, 1, d, inv_temp, top_k, top_p);
+  constexpr size_t smem = FLT_SMEM;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(filter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  return launch_pdl(filter_kernel, dim3(T), dim3(FLT_THREADS), smem, s, 1, d, inv_temp, top_k, top_p);
 }
 
-// p'(x) of chain row r (R31): e(x) / S_keep on the kept set, else 0
+// p'(x) of one chain row (R31): e(x) / S_keep on the kept set, else 0. The row's filter
+// parameters are loaded once (FiltRow) by loops over the vocabulary.
+struct FiltRow { uint32_t key; int tie; float m, inv; };
+SV_DEV FiltRow filt_row(const LaneDev& d, int r) { return FiltRow{d.filt_key[r], d.filt_tie[r], d.filt_m[r], d.filt_inv[r]}; }
+SV_DEV float filt_p(const FiltRow& f, int x, float lv_scaled) {
+  const uint32_t k = flt_key(lv_scaled);
+  if (k < f.key || (k == f.key && x > f.tie)) return 0.f;
+  return expf(lv_scaled - f.m) * f.inv;
+}
 SV_DEV float filt_prob(const LaneDev& d, int r, int x, float lv_scaled, float m, float invS) {
   if (!d.filt_on) return expf(lv_scaled - m) * invS;
-  const uint32_t k = flt_key(lv_scaled), ks = d.filt_key[r];
-  if (k < ks || (k == ks && x > d.filt_tie[r])) return 0.f;
-  return expf(lv_scaled - d.filt_m[r]) * d.filt_inv[r];
+  return filt_p(filt_row(d, r), x, lv_scaled);
 }
 
 // ---------------------------------------------------------------- token trees (R30)
@@ -199,6 +373,8 @@ SV_DEV float filt_prob(const LaneDev& d, int r, int x, float lv_scaled, float m,
 struct TreeResid {
   const LaneDev* d;
   int row;                    // chain row of the current node (top-k / top-p filter parameters)
+  bool filt;
+  FiltRow fr;
   const float* lrow;          // logits row of the current node
   float m, invS, inv_temp;
   int nrej;
@@ -209,7 +385,7 @@ struct TreeResid {
 
 SV_DEV float tree_r(const TreeResid& t, int x) {
   const float lv = t.lrow[x] * t.inv_temp;
-  float r = t.d->filt_on ? filt_prob(*t.d, t.row, x, lv, t.m, t.invS) : expf(lv - t.m) * t.invS;
+  float r = t.filt ? filt_p(t.fr, x, lv) : expf(lv - t.m) * t.invS;
   for (int i = 0; i < t.nrej; ++i) {
     if (t.invZ[i] == 0.f) continue;
     const float q = t.rej_q[i] ? t.rej_q[i][x] : (x == t.rej_tok[i] ? 1.0f : 0.0f);
@@ -305,8 +481,9 @@ __device__ void tree_walk(const LaneDev& d, const int* __restrict__ drafts, cons
       } else {
         s_scan = c + 1;
         const int x = tok[c - 1];
-        TreeResid t{&d, r0 + cur, logits + (size_t)(r0 + cur) * V, s_m[cur], 1.0f / s_S[cur], inv_temp, s_nrej,
-                    s_rej_tok, s_rej_q, s_invZ};
+        TreeResid t{&d, r0 + cur, d.filt_on != 0, d.filt_on ? filt_row(d, r0 + cur) : FiltRow{},
+                    logits + (size_t)(r0 + cur) * V, s_m[cur], 1.0f / s_S[cur], inv_temp, s_nrej, s_rej_tok, s_rej_q,
+                    s_invZ};
         const float rv = tree_r(t, x);
         const float qd = probs ? probs[(size_t)(doff + c - 1) * V + x] : 1.0f;
         const float u = uniform_accept_rank(seed, rid, uint32_t(L + s_dep[cur] + 1), uint32_t(s_nrej));
@@ -327,8 +504,8 @@ __device__ void tree_walk(const LaneDev& d, const int* __restrict__ drafts, cons
     __syncthreads();                                 // everyone has read s_act before thread 0 rewrites it
     if (act == 1) continue;
     const int cur = s_cur, nrej = s_nrej;
-    TreeResid t{&d, r0 + cur, logits + (size_t)(r0 + cur) * V, s_m[cur], 1.0f / s_S[cur], inv_temp, nrej, s_rej_tok,
-                s_rej_q, s_invZ};
+    TreeResid t{&d, r0 + cur, d.filt_on != 0, d.filt_on ? filt_row(d, r0 + cur) : FiltRow{},
+                logits + (size_t)(r0 + cur) * V, s_m[cur], 1.0f / s_S[cur], inv_temp, nrej, s_rej_tok, s_rej_q, s_invZ};
     if (act == 2) {
       const int c = s_cand, xc = tok[c - 1];
       const float* qc = probs ? probs + (size_t)(doff + c - 1) * V : nullptr;
@@ -491,18 +668,21 @@ __global__ void __launch_bounds__(FIN_THREADS) finalize_kernel(LaneDev d, const 
     const float* qrow = (resid && probs) ? probs + (size_t)(doff + a) * V : nullptr;
     const int dnext = resid ? drafts[doff + a] : -1;
     const uint32_t z = uint32_t(L + a + 1);
+    const bool filt = d.filt_on != 0;
+    const FiltRow fr = filt ? filt_row(d, r0 + a) : FiltRow{};
     Best bR{-INFINITY, 0x7fffffff}, bP{-INFINITY, 0x7fffffff};
     float sumR = 0.f;
     const int nm = (int)((V + 3) / 4);
-    for (int mm = tid; mm < nm; mm += FIN_THREADS) {
+    const int RS = gridDim.y, sidx = blockIdx.y;      // vocabulary slice of this CTA (race words of 4)
+    const int per = (nm + RS - 1) / RS, m_lo = sidx * per, m_hi = min(nm, m_lo + per);
+    for (int mm = m_lo + tid; mm < m_hi; mm += FIN_THREADS) {
       const u32x4 w = race_words(seed, rid, z, uint32_t(mm));
       const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
       for (int l = 0; l < 4; ++l) {
         const int x = mm * 4 + l;
         if (x >= (int)V) break;
-        const float p = d.filt_on ? filt_prob(d, r0 + a, x, lrow[x] * inv_temp, m, invS)
-                                  : expf(lrow[x] * inv_temp - m) * invS;
+        const float p = filt ? filt_p(fr, x, lrow[x] * inv_temp) : expf(lrow[x] * inv_temp - m) * invS;
         const float E = -logf(word_to_uniform(ws[l]));
         bP = better(bP, Best{p > 0.f ? p / E : -INFINITY, x});
         if (resid) {
@@ -518,13 +698,37 @@ __global__ void __launch_bounds__(FIN_THREADS) finalize_kernel(LaneDev d, const 
     sumR = warp_sum(sumR);
     if (lane == 0) { s_bestR[warp] = bR; s_bestP[warp] = bP; s_sumR[warp] = sumR; }
     __syncthreads();
+    __shared__ int s_last;
     if (tid == 0) {
       Best R = s_bestR[0], P = s_bestP[0];
       float sr = s_sumR[0];
       for (int i = 1; i < nw; ++i) { R = better(R, s_bestR[i]); P = better(P, s_bestP[i]); sr += s_sumR[i]; }
+      s_last = 1;
+      if (RS > 1) {
+        // split race: publish this vocabulary slice's bests; the last CTA of the request to finish
+        // merges the slices in slice order (deterministic) and writes the outputs
+        RacePart* part = d.fin_part + (size_t)b * kMaxRaceSplits;
+        part[sidx] = RacePart{R.s, R.x, P.s, P.x, sr};
+        __threadfence();
+        s_last = atomicAdd(&d.fin_cnt[b], 1) == RS - 1;
+        if (s_last) {
+          __threadfence();
+          volatile RacePart* vp = part;
+          R = Best{vp[0].rs, vp[0].rx};
+          P = Best{vp[0].ps, vp[0].px};
+          sr = vp[0].sr;
+          for (int i = 1; i < RS; ++i) {
+            R = better(R, Best{vp[i].rs, vp[i].rx});
+            P = better(P, Best{vp[i].ps, vp[i].px});
+            sr += vp[i].sr;
+          }
+          d.fin_cnt[b] = 0;                           // ready for the next verify
+        }
+      }
       s_y = (resid && sr > 0.f) ? R.x : P.x;
     }
     __syncthreads();
+    if (!s_last) return;                              // another slice of this request finishes it
   }
 
   // 4. outputs + lane counters (a7)
@@ -559,7 +763,11 @@ cudaError_t launch_finalize(const LaneDev& d, int batch, const int* draft_tokens
                             const float* draft_probs, const float* logits, uint64_t seed, int mode, float inv_temp,
                             int* accepted_len, int* out_tokens, int* accepted_nodes, cudaStream_t s) {
   SV_COUNT_LAUNCH();
-  return launch_pdl(finalize_kernel, dim3(batch), dim3(FIN_THREADS), 0, s, 1, d, draft_tokens, parents, draft_probs,
+  // sampled chains: the race over the vocabulary is split across RS CTAs per request so the grid
+  // covers every SM about twice (148 SMs); the other modes need one CTA per request
+  int RS = 1;
+  if (mode == SV_SAMPLE && !parents) RS = std::min(kMaxRaceSplits, std::max(1, (2 * 148 + batch - 1) / batch));
+  return launch_pdl(finalize_kernel, dim3(batch, RS), dim3(FIN_THREADS), 0, s, 1, d, draft_tokens, parents, draft_probs,
                     logits, seed, mode, inv_temp, accepted_len, out_tokens, accepted_nodes);
 }
 

@@ -412,27 +412,30 @@ cudaError_t launch_debug_uniforms(uint64_t seed, uint64_t rid, uint32_t z, int p
 // planted-successor drafter (bench fixture): one thread per request
 __global__ void draft_planted_kernel(LaneDev d, PlanArgs p, const int* __restrict__ succ,
                                      const uint8_t* __restrict__ mask, const int* __restrict__ dev_tok,
-                                     int* __restrict__ out) {
+                                     const int* __restrict__ parents, int* __restrict__ out) {
   pdl_trigger();
   pdl_wait();
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= p.batch) return;
   int off = 0;
   for (int i = 0; i < b; ++i) off += p.depths[i];
-  int prev = d.pending[p.slots[b]];
+  int tok[kMaxDepth + 1];                          // node tokens (node 0 = the pending token)
+  tok[0] = d.pending[p.slots[b]];
   for (int j = 0; j < p.depths[b]; ++j) {
-    int t = succ[prev];
+    int par = parents ? parents[off + j] : j;      // tree: the node's parent; chain: the previous node
+    if (par < 0 || par > j) par = j;               // (the verify flags a bad tree; keep reads in range)
+    int t = succ[tok[par]];
     if (mask[off + j]) t = dev_tok[off + j];
     out[off + j] = t;
-    prev = t;
+    tok[j + 1] = t;
   }
 }
 
 cudaError_t launch_draft_planted(const LaneDev& d, const PlanArgs& p, const int* succ, const uint8_t* mask,
-                                 const int* dev_tok, int* draft_tokens, cudaStream_t s) {
+                                 const int* dev_tok, const int* parents, int* draft_tokens, cudaStream_t s) {
   SV_COUNT_LAUNCH();
   return launch_pdl(draft_planted_kernel, dim3((p.batch + 127) / 128), dim3(128), 0, s, 1, d, p, succ, mask, dev_tok,
-                    draft_tokens);
+                    parents, draft_tokens);
 }
 
 // ------------------------------------------------------------------ lane state init

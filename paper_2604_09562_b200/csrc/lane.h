@@ -15,6 +15,9 @@ constexpr int kVocabTile = 128;    // lm-head epilogue statistics tile (SURVEY.m
 constexpr int kAttnRows = 64;      // max (k+1) * G query rows per (request, kv head)
 constexpr int kSplitKeys = 1024;   // page keys per split-KV work item
 constexpr int kNumStats = 6 + 3 * (kMaxDepth + 1);
+constexpr int kMaxRaceSplits = 16;  // finalize: CTAs per request sharing a sampled row's race
+
+struct RacePart { float rs; int rx; float ps; int px; float sr; int pad[3]; };   // one race slice's result
 
 // indices into the u64 stats array (mirrors sv_lane_stats)
 enum { ST_STEPS = 0, ST_ROWS, ST_DRAFTED, ST_ACCEPTED, ST_EMITTED, ST_INDEP, ST_HIST,
@@ -51,6 +54,8 @@ struct LaneDev {
   int *acc_int, *tok_int;            // internal copies of accepted_len / out_tokens for commit
   int* path_int;                     // [max_batch][max_depth+1] accepted path's chain rows (commit)
   unsigned long long* row_anc;       // [Tmax] ancestor-or-self node mask of each chain row
+  int* fin_cnt;                      // [max_batch] finished race slices (zero between verifies)
+  RacePart* fin_part;                // [max_batch][kMaxRaceSplits]
   unsigned* filt_key;                // [Tmax] R31 filter: threshold key of the scaled logit
   int* filt_tie;                     // [Tmax] largest kept token id among threshold ties
   float *filt_inv, *filt_m;          // [Tmax] 1 / kept mass, row max (scaled logits)
@@ -135,7 +140,7 @@ cudaError_t launch_init_state(const LaneDev& d, cudaStream_t s);
 cudaError_t launch_debug_uniforms(uint64_t seed, uint64_t rid, uint32_t z, int purpose, int x0, int n, float* u,
                                   cudaStream_t s);
 cudaError_t launch_draft_planted(const LaneDev& d, const PlanArgs& p, const int* succ, const uint8_t* mask,
-                                 const int* dev_tok, int* draft_tokens, cudaStream_t s);
+                                 const int* dev_tok, const int* parents, int* draft_tokens, cudaStream_t s);
 cudaError_t launch_kv_pack_slot(const LaneDev& d, int slot, int n, void* packed, cudaStream_t s);
 cudaError_t launch_kv_pack(const bf16* k, const bf16* v, int n_layers, int Hkv, int dh, int n, int pending,
                            void* packed, cudaStream_t s);

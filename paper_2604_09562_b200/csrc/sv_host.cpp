@@ -25,7 +25,7 @@ struct Layout {
   size_t slots, depths, row_off, row_req, row_pos, chain_tok, req_err;
   size_t h0, h1, h2, cbuf, logits, tile_max, tile_sum, tile_arg;
   size_t a, b, z, q, kc, vc, o, u;
-  size_t items, item_start, n_items, part_o, part_ml, acc_int, tok_int, batch_n, path_int, row_anc, filt;
+  size_t items, item_start, n_items, part_o, part_ml, acc_int, tok_int, batch_n, path_int, row_anc, filt, fin_cnt, fin_part;
   size_t gemm_ws, trace, prefill;
   size_t max_items;
 
@@ -113,6 +113,8 @@ Layout make_layout(const sv_config& c) {
   L.path_int = L.take(4 * c.max_batch * (c.max_depth + 1));
   L.row_anc = L.take(8 * T);
   L.filt = L.take(16 * T);
+  L.fin_cnt = L.take(4 * c.max_batch);
+  L.fin_part = L.take(sizeof(sv::RacePart) * sv::kMaxRaceSplits * c.max_batch);
   L.gemm_ws = L.take(sv::gemm_workspace_bytes((int)T, (int)cmax));
   L.trace = L.take(8 * 16 * 256);
   L.prefill = L.take(4 * 3 * (size_t)(c.max_depth + 2));   // sv_prefill: chunk tokens + outputs
@@ -346,6 +348,8 @@ sv_status sv_create(const sv_config* cfg, const sv_weights* w, void* kv_pool, vo
   d.row_anc = (unsigned long long*)(ws + L.row_anc);
   d.tree = 0;
   d.filt_on = 0;
+  d.fin_cnt = (int*)(ws + L.fin_cnt);
+  d.fin_part = (sv::RacePart*)(ws + L.fin_part);
   d.filt_key = (unsigned*)(ws + L.filt);
   d.filt_tie = (int*)(ws + L.filt + 4 * (size_t)d.Tmax);
   d.filt_inv = (float*)(ws + L.filt + 8 * (size_t)d.Tmax);
@@ -370,6 +374,7 @@ sv_status sv_create(const sv_config* cfg, const sv_weights* w, void* kv_pool, vo
                                                     cfg->page_size * cfg->head_dim * 2, c->stream))) ||
       (st = cuda_ok(cudaMemsetAsync(ws + L.page_table, 0xff, 4 * (size_t)cfg->max_slots * d.max_pages_per_slot,
                                     c->stream))) ||
+      (st = cuda_ok(cudaMemsetAsync(ws + L.fin_cnt, 0, 4 * (size_t)cfg->max_batch, c->stream))) ||
       (st = cuda_ok(sv::launch_init_state(d, c->stream)))) {
     delete c;
     return st;
@@ -697,9 +702,9 @@ sv_status sv_debug_gemm(sv_ctx* c, const void* A, const void* B, float* C, int32
   return SV_OK;
 }
 
-sv_status sv_draft_planted(sv_ctx* c, int32_t batch, const int32_t* slots, const int32_t* depths,
-                           const int32_t* succ, const uint8_t* dev_mask, const int32_t* dev_tok,
-                           int32_t* draft_tokens) {
+static sv_status draft_planted_impl(sv_ctx* c, int32_t batch, const int32_t* slots, const int32_t* depths,
+                                    const int32_t* parents, const int32_t* succ, const uint8_t* dev_mask,
+                                    const int32_t* dev_tok, int32_t* draft_tokens) {
   if (!c || !succ || !dev_mask || !dev_tok || !draft_tokens) return SV_EINVAL;
   sv::PlanArgs p;
   if (batch < 1 || batch > c->cfg.max_batch || !slots || !depths) return SV_EINVAL;
@@ -712,8 +717,21 @@ sv_status sv_draft_planted(sv_ctx* c, int32_t batch, const int32_t* slots, const
     p.depths[b] = depths[b];
     p.T += depths[b] + 1;
   }
-  STAGE(c, ST_DRAFT, sv::launch_draft_planted(c->d, p, succ, dev_mask, dev_tok, draft_tokens, c->stream));
+  STAGE(c, ST_DRAFT, sv::launch_draft_planted(c->d, p, succ, dev_mask, dev_tok, parents, draft_tokens, c->stream));
   return SV_OK;
+}
+
+sv_status sv_draft_planted(sv_ctx* c, int32_t batch, const int32_t* slots, const int32_t* depths,
+                           const int32_t* succ, const uint8_t* dev_mask, const int32_t* dev_tok,
+                           int32_t* draft_tokens) {
+  return draft_planted_impl(c, batch, slots, depths, nullptr, succ, dev_mask, dev_tok, draft_tokens);
+}
+
+sv_status sv_draft_planted_tree(sv_ctx* c, int32_t batch, const int32_t* slots, const int32_t* depths,
+                                const int32_t* parents, const int32_t* succ, const uint8_t* dev_mask,
+                                const int32_t* dev_tok, int32_t* draft_tokens) {
+  if (!parents) return SV_EINVAL;
+  return draft_planted_impl(c, batch, slots, depths, parents, succ, dev_mask, dev_tok, draft_tokens);
 }
 
 sv_status sv_prefill(sv_ctx* c, int32_t slot, uint64_t request_id, const int32_t* prompt, int32_t n, int32_t chunk,

@@ -31,7 +31,7 @@ EXPORTED = [
     "sv_profile_stage_name", "sv_profile_read", "sv_launch_count", "sv_debug_gemm", "sv_kv_append_packed",
     "sv_kv_loopback_append", "sv_spec_default_config", "sv_spec_reset", "sv_spec_adapt", "sv_spec_step",
     "sv_route_default_config", "sv_route_select", "sv_lane_occupancy", "sv_kv_pack_slot", "sv_prefill",
-    "sv_verify_tree", "sv_verify_tree_logits", "sv_set_filter",
+    "sv_verify_tree", "sv_verify_tree_logits", "sv_set_filter", "sv_draft_planted_tree",
 ]
 
 
@@ -112,6 +112,7 @@ def load():
         "sv_get_tap": ([vp, ctypes.c_char_p, P(vp), P(sz)], ctypes.c_int),
         "sv_debug_uniforms": ([vp, u64, u64, ctypes.c_uint32, i32, i32, i32, vp], ctypes.c_int),
         "sv_draft_planted": ([vp, i32, P(i32), P(i32), vp, vp, vp, vp], ctypes.c_int),
+        "sv_draft_planted_tree": ([vp, i32, P(i32), P(i32), vp, vp, vp, vp, vp], ctypes.c_int),
         "sv_nccl_unique_id": ([ctypes.c_char_p], ctypes.c_int),
         "sv_nccl_comm_init": ([ctypes.c_int, ctypes.c_char_p, ctypes.c_int, P(vp)], ctypes.c_int),
         "sv_nccl_comm_destroy": ([vp], ctypes.c_int),
@@ -242,12 +243,12 @@ class Lane:
         return acc, tok
 
     def verify_tree(self, slots, depths, parents, draft_tokens, draft_probs=None, seed=0, mode="greedy",
-                    temperature=1.0, logits_out=None, nodes_out=None):
+                    temperature=1.0, logits_out=None, nodes_out=None, out=None):
         """Token-tree verify (R30). parents: device int32 [sum k] (node n's parent in 0..n-1).
         Returns (accepted_len [B], out_tokens [B][max_depth+1], accepted_nodes [B][max_depth+1])."""
         s, B = _i32_array(slots)
         dpt, _ = _i32_array(depths)
-        acc, tok = self._acc[:B], self._tok[:B]
+        acc, tok = (self._acc[:B], self._tok[:B]) if out is None else out
         nodes = self._nodes[:B] if nodes_out is None else nodes_out
         _check(self.lib.sv_verify_tree(self.ctx, B, s, dpt, _ptr(parents), _ptr(draft_tokens), _ptr(draft_probs),
                                        seed, self._mode(mode), float(temperature), _ptr(acc), _ptr(tok), _ptr(nodes),
@@ -333,6 +334,13 @@ class Lane:
         dpt, _ = _i32_array(depths)
         _check(self.lib.sv_draft_planted(self.ctx, B, s, dpt, _ptr(succ), _ptr(dev_mask), _ptr(dev_tok), _ptr(out)),
                "sv_draft_planted")
+        return out
+
+    def draft_planted_tree(self, slots, depths, parents, succ, dev_mask, dev_tok, out):
+        s, B = _i32_array(slots)
+        dpt, _ = _i32_array(depths)
+        _check(self.lib.sv_draft_planted_tree(self.ctx, B, s, dpt, _ptr(parents), _ptr(succ), _ptr(dev_mask),
+                                              _ptr(dev_tok), _ptr(out)), "sv_draft_planted_tree")
         return out
 
     # ------------------------------------------------------------------ measurement hooks

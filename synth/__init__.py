@@ -179,6 +179,9 @@ class Workload:
     controller: bool = False   # depths from the SpecuStream controller (NEXT-1) instead of U{kmin..kmax}
     gen_on_device: bool = False  # draw weights / context KV with a CUDA generator (multi-GB models)
     alpha_sigma: float = 0.0   # per-request acceptance follows AR(1) around alpha with this stationary std
+    tree: tuple = ()           # NEXT-4 token trees (R30): every request drafts this tree (parents of nodes 1..k)
+    top_k: int = 0             # NEXT-4 filtered targets (R31), SAMPLE only
+    top_p: float = 1.0
 
 
 def workload(name, steps_budget=64):
@@ -206,6 +209,14 @@ def workload(name, steps_budget=64):
         n_pages, max_pos = pool(32, 8192, 8)
         cfg = LLAMA.with_(n_pages=n_pages, max_slots=32, max_batch=32, max_pos=max_pos)
         return Workload("c4", cfg, 32, (8192, 8192), 8, 8, "greedy", 0.85)
+    if name == "ns_tree":     # NEXT-4: the north-star batch drafting 8-node token trees (R30)
+        n_pages, max_pos = pool(64, 4096, 8)
+        cfg = LLAMA.with_(n_pages=n_pages, max_slots=64, max_batch=64, max_pos=max_pos)
+        return Workload("ns_tree", cfg, 64, (4096, 4096), 8, 8, "greedy", 0.7, tree=(0, 0, 1, 1, 2, 3, 5, 7))
+    if name == "c2_filter":   # NEXT-4: configs[1] sampled with a top-k 50 / top-p 0.9 filtered target (R31)
+        n_pages, max_pos = pool(64, 256, 8)
+        cfg = LLAMA.with_(n_pages=n_pages, max_slots=64, max_batch=64, max_pos=max_pos)
+        return Workload("c2_filter", cfg, 64, (256, 256), 1, 8, "sample", 0.75, top_k=50, top_p=0.9)
     if name == "toy":         # BASELINE configs[0]
         n_pages, max_pos = pool(4, 128, 4)
         cfg = TOY.with_(n_pages=n_pages, max_slots=4, max_batch=4, max_pos=max_pos)
