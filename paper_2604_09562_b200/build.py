@@ -41,7 +41,7 @@ def build(verbose=False, jobs=8):
     inc, lib = _nccl_dirs()
     os.makedirs(BUILD, exist_ok=True)
     common = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-I", inc, "-I", os.path.join(ROOT, "include"),
-              "--expt-relaxed-constexpr"] + ARCH
+              "--expt-relaxed-constexpr"] + ARCH + os.environ.get("SV_NVCC_FLAGS", "").split()   # flags: experiments
     objs, procs = [], []
     srcs = sources()
     newest_hdr = max(os.path.getmtime(os.path.join(CSRC, f)) for f in os.listdir(CSRC))
