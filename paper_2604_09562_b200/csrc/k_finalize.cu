@@ -628,7 +628,7 @@ __global__ void __launch_bounds__(FIN_THREADS) finalize_kernel(LaneDev d, const 
   if (parents) {
     tree_walk(d, drafts, parents, probs, logits, seed, mode, inv_temp, b, k, r0, doff, L, rid, s_m, s_S, s_top,
               s_path, &s_a, &s_indep, &s_y);
-  } else if (tid == 0) {
+  } else if (tid == 0 && mode != SV_SAMPLE) {
     int a = k, indep = 0;
     if (mode == SV_PREFILL) {                      // R29: the chunk's rows are all kept
       s_y = s_top[k];
@@ -639,23 +639,37 @@ __global__ void __launch_bounds__(FIN_THREADS) finalize_kernel(LaneDev d, const 
         if (!acc && a == k) a = j - 1;
       }
       s_y = s_top[a];
-    } else {
-      for (int j = 1; j <= k; ++j) {
-        const int dj = drafts[doff + j - 1];
-        const float lg = logits[(size_t)(r0 + j - 1) * V + dj];
-        const float pd = d.filt_on ? filt_prob(d, r0 + j - 1, dj, lg * inv_temp, s_m[j - 1], 1.0f / s_S[j - 1])
-                                   : expf(lg * inv_temp - s_m[j - 1]) / s_S[j - 1];
-        const float qd = probs ? probs[(size_t)(doff + j - 1) * V + dj] : 1.0f;
-        const float u = uniform_accept(seed, rid, uint32_t(L + j));
-        const bool acc = (qd == 0.0f) || (u < pd / qd);
-        indep += acc;
-        if (!acc && a == k) a = j - 1;
-      }
     }
     s_a = a;
     s_indep = indep;
-    s_resid = (mode == SV_SAMPLE) && (a < k);
+    s_resid = 0;
     for (int i = 0; i <= a; ++i) s_path[i] = i;
+  }
+  if (!parents && mode == SV_SAMPLE && warp == 0) {
+    // the k <= 32 accept tests are independent: lane j - 1 evaluates test j (its loads and its
+    // Philox draw in parallel), a = index of the first failing lane (k if none)
+    const int j = lane + 1;
+    bool acc = true;
+    if (j <= k) {
+      const int dj = drafts[doff + j - 1];
+      const float lg = logits[(size_t)(r0 + j - 1) * V + dj];
+      const float qd = probs ? probs[(size_t)(doff + j - 1) * V + dj] : 1.0f;
+      const float pd = d.filt_on ? filt_prob(d, r0 + j - 1, dj, lg * inv_temp, s_m[j - 1], 1.0f / s_S[j - 1])
+                                 : expf(lg * inv_temp - s_m[j - 1]) / s_S[j - 1];
+      const float u = uniform_accept(seed, rid, uint32_t(L + j));
+      acc = (qd == 0.0f) || (u < pd / qd);
+    }
+    const unsigned kmask = k >= 32 ? 0xffffffffu : ((1u << k) - 1u);
+    const unsigned okm = __ballot_sync(0xffffffffu, acc) & kmask;
+    const unsigned fail = ~okm & kmask;
+    const int a = fail ? __ffs(fail) - 1 : k;
+    if (lane == 0) {
+      s_a = a;
+      s_indep = __popc(okm);
+      s_resid = a < k;
+    }
+    if (lane <= a) s_path[lane] = lane;
+    if (a == 32 && lane == 0) s_path[32] = 32;
   }
   __syncthreads();
   const int a = s_a;
@@ -675,23 +689,46 @@ __global__ void __launch_bounds__(FIN_THREADS) finalize_kernel(LaneDev d, const 
     const int nm = (int)((V + 3) / 4);
     const int RS = gridDim.y, sidx = blockIdx.y;      // vocabulary slice of this CTA (race words of 4)
     const int per = (nm + RS - 1) / RS, m_lo = sidx * per, m_hi = min(nm, m_lo + per);
-    for (int mm = m_lo + tid; mm < m_hi; mm += FIN_THREADS) {
+    // 4 vocabulary entries per Philox word; rows are 16-byte aligned when V % 4 == 0, then the logits
+    // and q of a word come in one float4 each, and two words per thread are in flight
+    const bool vec = (V & 3) == 0;
+    auto race4 = [&](int mm, const float4 l4, const float4 q4) {
       const u32x4 w = race_words(seed, rid, z, uint32_t(mm));
       const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+      const float lv[4] = {l4.x, l4.y, l4.z, l4.w};
+      const float qv[4] = {q4.x, q4.y, q4.z, q4.w};
 #pragma unroll
       for (int l = 0; l < 4; ++l) {
         const int x = mm * 4 + l;
         if (x >= (int)V) break;
-        const float p = filt ? filt_p(fr, x, lrow[x] * inv_temp) : expf(lrow[x] * inv_temp - m) * invS;
+        const float p = filt ? filt_p(fr, x, lv[l] * inv_temp) : expf(lv[l] * inv_temp - m) * invS;
         const float E = -logf(word_to_uniform(ws[l]));
         bP = better(bP, Best{p > 0.f ? p / E : -INFINITY, x});
         if (resid) {
-          const float q = qrow ? qrow[x] : (x == dnext ? 1.0f : 0.0f);
+          const float q = qrow ? qv[l] : (x == dnext ? 1.0f : 0.0f);
           const float R = fmaxf(0.f, p - q);
           sumR += R;
           bR = better(bR, Best{R > 0.f ? R / E : -INFINITY, x});
         }
       }
+    };
+    auto load4 = [&](const float* row, int mm) {
+      if (vec) return *reinterpret_cast<const float4*>(row + mm * 4);
+      float t[4];
+#pragma unroll
+      for (int l = 0; l < 4; ++l) t[l] = mm * 4 + l < (int)V ? row[mm * 4 + l] : 0.f;
+      return make_float4(t[0], t[1], t[2], t[3]);
+    };
+    const float4 zero4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int mm = m_lo + tid; mm < m_hi; mm += 2 * FIN_THREADS) {
+      const int mm2 = mm + FIN_THREADS;
+      const bool two = mm2 < m_hi;
+      const float4 l0 = load4(lrow, mm);
+      const float4 l1 = two ? load4(lrow, mm2) : zero4;
+      const float4 q0 = qrow ? load4(qrow, mm) : zero4;
+      const float4 q1 = (qrow && two) ? load4(qrow, mm2) : zero4;
+      race4(mm, l0, q0);
+      if (two) race4(mm2, l1, q1);
     }
     bR = warp_best(bR);
     bP = warp_best(bP);
