@@ -538,8 +538,8 @@ __device__ void tree_walk(const LaneDev& d, const int* __restrict__ drafts, cons
         const int x = mm * 4 + l;
         if (x >= (int)V) break;
         const float r = tree_r(t, x);
-        const float E = -logf(word_to_uniform(ws[l]));
-        best = better(best, Best{r > 0.f ? r / E : -INFINITY, x});
+        const float invE = __frcp_rn(-logf(word_to_uniform(ws[l])));   // score r / E as r * (1/E):
+        best = better(best, Best{r > 0.f ? r * invE : -INFINITY, x});  // no fp32 division slow path
       }
     }
     best = warp_best(best);
@@ -702,13 +702,15 @@ __global__ void __launch_bounds__(FIN_THREADS) finalize_kernel(LaneDev d, const 
         const int x = mm * 4 + l;
         if (x >= (int)V) break;
         const float p = filt ? filt_p(fr, x, lv[l] * inv_temp) : expf(lv[l] * inv_temp - m) * invS;
-        const float E = -logf(word_to_uniform(ws[l]));
-        bP = better(bP, Best{p > 0.f ? p / E : -INFINITY, x});
+        // score p / E as p * (1/E): one correctly rounded reciprocal per entry, and no division,
+        // whose special-case path (zero numerators: filtered or zero residual mass) dominated
+        const float invE = __frcp_rn(-logf(word_to_uniform(ws[l])));
+        bP = better(bP, Best{p > 0.f ? p * invE : -INFINITY, x});
         if (resid) {
           const float q = qrow ? qv[l] : (x == dnext ? 1.0f : 0.0f);
           const float R = fmaxf(0.f, p - q);
           sumR += R;
-          bR = better(bR, Best{R > 0.f ? R / E : -INFINITY, x});
+          bR = better(bR, Best{R > 0.f ? R * invE : -INFINITY, x});
         }
       }
     };
@@ -801,9 +803,18 @@ cudaError_t launch_finalize(const LaneDev& d, int batch, const int* draft_tokens
                             int* accepted_len, int* out_tokens, int* accepted_nodes, cudaStream_t s) {
   SV_COUNT_LAUNCH();
   // sampled chains: the race over the vocabulary is split across RS CTAs per request so the grid
-  // covers every SM about twice (148 SMs); the other modes need one CTA per request
+  // fills the resident CTA slots once; the other modes need one CTA per request
+  // (RS * batch <= the resident CTA slots, so the grid is a single wave)
+  static int slots = 0;
+  if (!slots) {
+    int dev = 0, sms = 148, occ = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, finalize_kernel, FIN_THREADS, 0);
+    slots = std::max(1, occ) * sms;
+  }
   int RS = 1;
-  if (mode == SV_SAMPLE && !parents) RS = std::min(kMaxRaceSplits, std::max(1, (2 * 148 + batch - 1) / batch));
+  if (mode == SV_SAMPLE && !parents) RS = std::min(kMaxRaceSplits, std::max(1, slots / batch));
   return launch_pdl(finalize_kernel, dim3(batch, RS), dim3(FIN_THREADS), 0, s, 1, d, draft_tokens, parents, draft_probs,
                     logits, seed, mode, inv_temp, accepted_len, out_tokens, accepted_nodes);
 }
