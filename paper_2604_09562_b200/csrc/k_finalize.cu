@@ -38,7 +38,8 @@ SV_DEV Best warp_best(Best v) {
 // independent of summation order (deterministic). Ties at the threshold key are kept in id
 // order up to the count / mass limit. Output per row: threshold key, the largest kept id among
 // the ties, 1 / S_keep and the row max m.
-constexpr int FLT_THREADS = 1024;
+constexpr int FLT_THREADS = 512;                 // 4 CTAs (rows) per SM
+constexpr int SORT_N = 1024;                     // tile maxima sorted in shared memory (nt <= 1024)
 constexpr double kFx = 1099511627776.0;            // 2^40
 
 // e in (0, 1] -> round(e * 2^40): the float product is exact (power-of-two scale), then rounded
@@ -50,9 +51,9 @@ SV_DEV uint32_t flt_key(float v) {
 }
 SV_DEV float key_flt(uint32_t k) { return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k); }
 
-constexpr int FLT_CAP = 4096;                     // fast path: candidate capacity (shared memory)
-constexpr size_t FLT_SMEM = (FLT_THREADS / 32) * 256 * (8 + 4);   // 96 KB: private histograms / candidates
-static_assert(FLT_CAP * 16 + FLT_THREADS * 4 <= FLT_SMEM, "filter candidate buffers exceed the smem budget");
+constexpr int FLT_CAP = 2048;                     // fast path: candidate capacity (shared memory)
+constexpr size_t FLT_SMEM = (FLT_THREADS / 32) * 256 * (8 + 4);   // 48 KB: private histograms / candidates
+static_assert(FLT_CAP * 16 + SORT_N * 4 <= FLT_SMEM, "filter candidate buffers exceed the smem budget");
 
 __global__ void __launch_bounds__(FLT_THREADS) filter_kernel(LaneDev d, float inv_temp, int top_k, float top_p) {
   extern __shared__ unsigned long long flt_smem[];
@@ -63,7 +64,7 @@ __global__ void __launch_bounds__(FLT_THREADS) filter_kernel(LaneDev d, float in
   unsigned long long* c_mass = flt_smem;
   uint32_t* c_key = reinterpret_cast<uint32_t*>(c_mass + FLT_CAP);
   int* c_id = reinterpret_cast<int*>(c_key + FLT_CAP);
-  float* srt = reinterpret_cast<float*>(c_id + FLT_CAP);          // [FLT_THREADS]
+  float* srt = reinterpret_cast<float*>(c_id + FLT_CAP);          // [SORT_N]
   __shared__ unsigned int h_cnt[256];
   __shared__ unsigned long long h_mass[256];
   __shared__ float s_redf[FLT_THREADS / 32];
@@ -86,18 +87,18 @@ __global__ void __launch_bounds__(FLT_THREADS) filter_kernel(LaneDev d, float in
   //    tau on the kept set — the top_k-th largest tile maximum (the k largest tile maxima are k
   //    distinct elements), and the largest tile maximum whose running mass (tile maxima only) already
   //    reaches top_p of the row's mass with a 1e-3 margin. Every kept element is >= tau.
-  const bool sortable = nt <= FLT_THREADS;
+  const bool sortable = nt <= SORT_N;
   float m;
   if (sortable) {
-    srt[tid] = tid < nt ? tmax[tid] : -INFINITY;
+    for (int i = tid; i < SORT_N; i += FLT_THREADS) srt[i] = i < nt ? tmax[i] : -INFINITY;
     __syncthreads();
-    for (int k2 = 2; k2 <= FLT_THREADS; k2 <<= 1)
+    for (int k2 = 2; k2 <= SORT_N; k2 <<= 1)          // bitonic: each thread one compare-exchange pair
       for (int j = k2 >> 1; j > 0; j >>= 1) {
-        const int o = tid ^ j;
-        if (o > tid) {
-          const float x = srt[tid], y = srt[o];
-          const bool desc = (tid & k2) == 0;
-          if (desc ? (x < y) : (x > y)) { srt[tid] = y; srt[o] = x; }
+        for (int i = tid; i < SORT_N / 2; i += FLT_THREADS) {
+          const int lo = 2 * j * (i / j) + (i % j), hi = lo + j;
+          const float x = srt[lo], y = srt[hi];
+          const bool desc = (lo & k2) == 0;
+          if (desc ? (x < y) : (x > y)) { srt[lo] = y; srt[hi] = x; }
         }
         __syncthreads();
       }
@@ -125,8 +126,10 @@ __global__ void __launch_bounds__(FLT_THREADS) filter_kernel(LaneDev d, float in
       __syncthreads();
       float S = 0.f;
       for (int i = 0; i < nw; ++i) S += s_redf[i];
-      float e = tid < nt ? expf(srt[tid] - m) : 0.f;
-      float incl = e;
+      static_assert(SORT_N == 2 * FLT_THREADS, "the scan gives each thread two sorted maxima");
+      const int i0 = 2 * tid, i1 = i0 + 1;            // a contiguous pair per thread
+      const float e0 = i0 < nt ? expf(srt[i0] - m) : 0.f, e1 = i1 < nt ? expf(srt[i1] - m) : 0.f;
+      float incl = e0 + e1;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const float y = __shfl_up_sync(0xffffffffu, incl, o);
@@ -137,11 +140,13 @@ __global__ void __launch_bounds__(FLT_THREADS) filter_kernel(LaneDev d, float in
       __syncthreads();
       float before = 0.f;
       for (int i = 0; i < warp; ++i) before += s_redf[i];
-      incl += before;
+      const float c0 = before + incl - e1, c1 = c0 + e1;     // running mass through i0, i1
       __syncthreads();                                 // every warp has read s_redf
       const float need = top_p * S * 1.001f;
-      const bool hit = tid < nt && incl >= need && incl - e < need;   // the first index reaching it
-      if (hit) s_redf[0] = srt[tid];                    // (at most one thread)
+      const bool hit0 = i0 < nt && c0 >= need && c0 - e0 < need;   // the first index reaching it
+      const bool hit1 = i1 < nt && c1 >= need && c0 < need;
+      const bool hit = hit0 || hit1;
+      if (hit) s_redf[0] = srt[hit0 ? i0 : i1];         // (at most one thread)
       __syncthreads();
       const bool any = __syncthreads_or(hit);
       if (any) tau = fmaxf(tau, s_redf[0]);
