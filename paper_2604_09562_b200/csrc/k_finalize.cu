@@ -583,9 +583,12 @@ __global__ void __launch_bounds__(FIN_THREADS) finalize_kernel(LaneDev d, const 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = FIN_THREADS / 32;
   const size_t V = d.V;
 
+  // an intermediate prefill chunk (no lm-head ran): every row is kept and no token is predicted
+  const bool nohead = mode == kPrefillNoHead;
+  if (nohead) mode = SV_PREFILL;
   // 1. combine the vocab-tile statistics of each chain row (warp per row): one online pass,
   //    loads batched 8 deep per lane so the memory round trips overlap
-  for (int j = warp; j <= k; j += nw) {
+  for (int j = warp; j <= (nohead ? -1 : k); j += nw) {
     const float* tm = d.tile_max + (size_t)(r0 + j) * d.nt;
     const float* ts = d.tile_sum + (size_t)(r0 + j) * d.nt;
     const int* ta = d.tile_arg + (size_t)(r0 + j) * d.nt;
@@ -636,7 +639,7 @@ __global__ void __launch_bounds__(FIN_THREADS) finalize_kernel(LaneDev d, const 
   } else if (tid == 0 && mode != SV_SAMPLE) {
     int a = k, indep = 0;
     if (mode == SV_PREFILL) {                      // R29: the chunk's rows are all kept
-      s_y = s_top[k];
+      s_y = nohead ? -1 : s_top[k];
     } else if (mode == SV_GREEDY) {
       for (int j = 1; j <= k; ++j) {
         const bool acc = drafts[doff + j - 1] == s_top[j - 1];

@@ -15,7 +15,8 @@ constexpr int kVocabTile = 128;    // lm-head epilogue statistics tile (SURVEY.m
 constexpr int kAttnRows = 64;      // max (k+1) * G query rows per (request, kv head)
 constexpr int kSplitKeys = 1024;   // page keys per split-KV work item
 constexpr int kNumStats = 6 + 3 * (kMaxDepth + 1);
-constexpr int kMaxRaceSplits = 16;  // finalize: CTAs per request sharing a sampled row's race
+constexpr int kMaxRaceSplits = 16;
+constexpr int kPrefillNoHead = 3;  // internal finalize mode: a prefill chunk whose lm-head was skipped  // finalize: CTAs per request sharing a sampled row's race
 
 struct RacePart { float rs; int rx; float ps; int px; float sr; int pad[3]; };   // one race slice's result
 

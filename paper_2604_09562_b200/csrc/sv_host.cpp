@@ -444,10 +444,12 @@ static sv_status gemm(sv_ctx* c, const bf16* A, const bf16* B, float* C, int M, 
 static bool filter_active(const sv_ctx* c) { return (c->top_k > 0 && c->top_k < c->cfg.vocab) || c->top_p < 1.0f; }
 
 // sv_verify and sv_verify_tree (parents != NULL: token-tree drafts, R30)
+// head = false (sv_prefill's intermediate chunks only): no final norm / lm-head; the chunk's rows
+// are kept and no next token is predicted
 static sv_status verify_impl(sv_ctx* c, int32_t batch, const int32_t* slots, const int32_t* depths,
                              const int32_t* parents, const int32_t* draft_tokens, const float* draft_probs,
                              uint64_t seed, sv_mode mode, float temperature, int32_t* accepted_len,
-                             int32_t* out_tokens, int32_t* accepted_nodes, float* logits_out) {
+                             int32_t* out_tokens, int32_t* accepted_nodes, float* logits_out, bool head = true) {
   if (!c || !accepted_len || !out_tokens) return SV_EINVAL;
   if (mode != SV_GREEDY && mode != SV_SAMPLE && mode != SV_PREFILL) return SV_EINVAL;
   if (parents && mode == SV_PREFILL) return SV_EINVAL;
@@ -488,17 +490,20 @@ static sv_status verify_impl(sv_ctx* c, int32_t batch, const int32_t* slots, con
       STAGE(c, ST_DOWN, gemm(c, d.u, d.w_down + (size_t)layer * d.D * d.F, d.cbuf, T, d.D, d.F, sv::EPI_RESIDUAL, e));
     }
   }
-  STAGE(c, ST_FINAL_NORM, sv::launch_rmsnorm(d, d.h2, d.final_norm, d.z, T, s));
-  sv::GemmEpi e{};
-  e.inv_temp = inv_temp;
-  // greedy decisions need only the vocab-tile statistics: the fp32 logits (T x V x 4 bytes)
-  // are stored only when something reads them
-  e.write_out = c->taps || mode == SV_SAMPLE || logits_out != nullptr;
-  STAGE(c, ST_LM_HEAD, gemm(c, d.z, d.lm_head, d.logits, T, d.V, d.D, sv::EPI_LOGITS, e));
+  if (head) {
+    STAGE(c, ST_FINAL_NORM, sv::launch_rmsnorm(d, d.h2, d.final_norm, d.z, T, s));
+    sv::GemmEpi e{};
+    e.inv_temp = inv_temp;
+    // greedy decisions need only the vocab-tile statistics: the fp32 logits (T x V x 4 bytes)
+    // are stored only when something reads them
+    e.write_out = c->taps || mode == SV_SAMPLE || logits_out != nullptr;
+    STAGE(c, ST_LM_HEAD, gemm(c, d.z, d.lm_head, d.logits, T, d.V, d.D, sv::EPI_LOGITS, e));
+  }
   d.filt_on = mode == SV_SAMPLE && filter_active(c);
   if (d.filt_on) STAGE(c, ST_FILTER, sv::launch_filter(d, T, inv_temp, c->top_k, c->top_p, s));
-  STAGE(c, ST_FINALIZE, sv::launch_finalize(d, batch, draft_tokens, parents, draft_probs, d.logits, seed, mode,
-                                            inv_temp, accepted_len, out_tokens, accepted_nodes, s));
+  STAGE(c, ST_FINALIZE, sv::launch_finalize(d, batch, draft_tokens, parents, draft_probs, d.logits, seed,
+                                            head ? (int)mode : sv::kPrefillNoHead, inv_temp, accepted_len,
+                                            out_tokens, accepted_nodes, s));
   if (logits_out)
     SV_CUDA(cudaMemcpyAsync(logits_out, d.logits, (size_t)T * d.V * 4, cudaMemcpyDeviceToDevice, s));
   for (int b = 0; b < batch; ++b) c->state[slots[b]] = PENDING;
@@ -751,7 +756,11 @@ sv_status sv_prefill(sv_ctx* c, int32_t slot, uint64_t request_id, const int32_t
   for (;;) {
     k = chunk - 1 < n - pos ? chunk - 1 : n - pos;
     if (k > 0) SV_CUDA(cudaMemcpyAsync(dtok, prompt + pos, 4 * (size_t)k, cudaMemcpyHostToDevice, c->stream));
-    if ((st = sv_verify(c, 1, &slot, &k, dtok, nullptr, 0, SV_PREFILL, 1.0f, dacc, dout, nullptr))) return st;
+    // only the last chunk's lm-head matters (its last row predicts the next token)
+    const bool last = pos + k >= n;
+    if ((st = verify_impl(c, 1, &slot, &k, nullptr, dtok, nullptr, 0, SV_PREFILL, 1.0f, dacc, dout, nullptr, nullptr,
+                          last)))
+      return st;
     if ((st = sv_commit(c, nullptr))) return st;
     pos += k;
     if (pos >= n) break;
