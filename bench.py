@@ -125,13 +125,13 @@ def planted_weights(wl, device="cpu"):
     return w, torch.randperm(wl.cfg.vocab, generator=torch.Generator().manual_seed(1)).to(torch.int32)
 
 
-def build_lane(wl, rank, dev):
+def build_lane(wl, rank, dev, stream=None):
     from paper_2604_09562_b200 import sv
     cfg = wl.cfg
     gdev = dev if wl.gen_on_device else "cpu"
     w, succ = planted_weights(wl, gdev)
     wd = {k: v.to(dev) for k, v in w.items()}
-    lane = sv.Lane(cfg, wd)
+    lane = sv.Lane(cfg, wd, stream=stream)
     ctx = synth.ctx_lengths(wl, seed=100 + rank)
     reqs = []
     for i, n in enumerate(ctx):
@@ -334,6 +334,71 @@ def run_gpu(args, wl, rank, world, dev):
                 depths=depths, masks=masks, devtok=devtok, alg=alg,
                 controller=({"window_steps": ControlledDepths.WINDOW, "final_depth": ctl.d, "trace": ctl.trace[-6:]}
                             if ctl else None))
+
+
+def run_graph(args, wl, rank, world, dev):
+    """--graph: the step (planted drafter + verify + commit) captured once as a CUDA graph
+    (sv_graph_*) and replayed; each step's drafter inputs are copied into the buffers the graph
+    reads. Depths are fixed per request (the graph freezes kernel arguments): k_max for fixed-depth
+    workloads, request i drafting 1 + i % k_max for toy (BASELINE configs[0]: k = {1, 2, 3, 4}).
+    For launch-bound small configurations; no per-kernel events (no roofline) in this mode."""
+    from paper_2604_09562_b200 import sv
+    import torch.distributed as dist
+    if wl.controller or (wl.kmin != wl.kmax and wl.name != "toy"):
+        raise SystemExit(f"--graph needs fixed depths (workload {wl.name} draws them per step)")
+    stream = torch.cuda.Stream(dev)
+    with torch.cuda.stream(stream):
+        lane, w, succ, reqs = build_lane(wl, rank, dev, stream)
+        cfg, B = wl.cfg, wl.batch
+        total = args.warmup + args.steps
+        ks = [wl.kmax] * B if wl.kmin == wl.kmax else [1 + i % wl.kmax for i in range(B)]
+        depths = [ks] * total
+        rows = B * wl.kmax
+        masks, devtok = synth.planted_masks(total, rows, wl.alpha, cfg.vocab, seed=9 + rank)
+        masks_d, devtok_d, succ_d = masks.to(dev), devtok.to(dev), succ.to(dev)
+        m_stage = torch.empty(rows, dtype=masks.dtype, device=dev)
+        t_stage = torch.empty(rows, dtype=torch.int32, device=dev)
+        drafts = torch.empty(rows, dtype=torch.int32, device=dev)
+        acc = torch.empty(B, dtype=torch.int32, device=dev)
+        tok = torch.empty(B, cfg.max_depth + 1, dtype=torch.int32, device=dev)
+        slots = list(range(B))
+        par_d = tree_parents(wl, dev)
+
+        def eager():
+            draft_and_verify(lane, wl, slots, ks, succ_d, m_stage, t_stage, drafts, 1234, (acc, tok), par_d)
+            lane.commit()
+
+        for i in range(args.warmup):
+            m_stage.copy_(masks_d[i])
+            t_stage.copy_(devtok_d[i])
+            eager()
+        lane.graph_begin()
+        eager()                                       # captured, not run
+        g = lane.graph_end()
+        torch.cuda.synchronize(dev)
+        lane.stats(reset=True)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+        launches0 = sv.launch_count()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        with Clocks(dev.index) as clk:
+            ev[0].record(stream)
+            for i in range(args.steps):
+                m_stage.copy_(masks_d[args.warmup + i])
+                t_stage.copy_(devtok_d[args.warmup + i])
+                lane.graph_launch(g)
+                ev[i + 1].record(stream)
+            torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        launches = sv.launch_count() - launches0
+        st = lane.stats()
+        lane.graph_destroy(g)
+    return dict(elapsed_ms=ev[0].elapsed_time(ev[-1]), tokens=st["emitted"],
+                per_step=[ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)], prof={}, roof={}, dominant=None,
+                launches=launches, clocks=clk.summary(), stats=st, e2e=None, e2e_host=None, w=w, succ=succ, reqs=reqs,
+                depths=depths, masks=masks, devtok=devtok, alg=None, controller=None, graph=True)
 
 
 def run_e2e(args, wl, lane, succ, depths, masks, devtok, dev, start):
@@ -579,6 +644,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=50)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--detail", action="store_true", help="add per-stage breakdown to the JSON line")
+    ap.add_argument("--graph", action="store_true", help="replay the step as a CUDA graph (fixed depths)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -603,7 +669,7 @@ def main():
             dist.init_process_group("gloo")
         else:
             dist.init_process_group("nccl", device_id=dev)
-    res = run_gpu(args, wl, rank, world, dev)
+    res = (run_graph if args.graph else run_gpu)(args, wl, rank, world, dev)
     elapsed, tokens = res["elapsed_ms"], res["tokens"]
     if world > 1:                                 # whole job: all ranks' tokens / the slowest rank's time
         elapsed, tokens = svdist.reduce_region(elapsed, tokens, device=red_dev)
@@ -640,6 +706,9 @@ def main():
         "controller": res.get("controller"),
         "peaks": peaks()["src"],
     }
+    if res.get("graph"):
+        line["config"]["graph"] = "CUDA graph replay of drafter + verify + commit; depths fixed per request"
+        line["config"]["depth"] = sorted(set(res["depths"][0]))
     if args.detail:
         line["stages"] = {k: {"us": round(v["ms_per_launch"] * 1e3, 1), "share": round(v["share"], 4)}
                           for k, v in res["prof"].items()}

@@ -198,6 +198,21 @@ sv_status sv_verify_tree_logits(sv_ctx* ctx, int32_t batch, const int32_t* slots
                                 const float* logits, uint64_t seed, sv_mode mode, float temperature,
                                 int32_t* accepted_len, int32_t* out_tokens, int32_t* accepted_nodes);
 
+/* CUDA graphs of a fixed step (launch-bound small configurations): between sv_graph_begin and
+ * sv_graph_end the lane's calls (e.g. sv_draft_planted + sv_verify + sv_commit) are captured from
+ * its stream instead of running — the host-side checks and state changes happen once, at capture —
+ * and sv_graph_launch replays the captured kernels with the same arguments (slots, depths, seed,
+ * device pointers: inputs that change per step are refreshed by the caller in the buffers the
+ * graph reads). The lane's stream must be a created stream (not the legacy default stream), its
+ * profiling off, and every captured sv_verify committed inside the capture (else sv_graph_end
+ * returns SV_ESTATE). Replays advance the device state (lengths, pages, counters) exactly like
+ * the captured calls. sv_graph_destroy frees the instantiated graph. */
+typedef struct sv_graph sv_graph;
+sv_status sv_graph_begin(sv_ctx* ctx);
+sv_status sv_graph_end(sv_ctx* ctx, sv_graph** graph);
+sv_status sv_graph_launch(sv_ctx* ctx, const sv_graph* graph);
+sv_status sv_graph_destroy(sv_graph* graph);
+
 /* Top-k / top-p filtered targets for SV_SAMPLE verifies of this lane (
  * DESIGN.md reading R31; the paper fixes no sampler): p = softmax(l / T) is restricted to the first
  * min(n_k, n_p) tokens in (scaled logit desc, token id asc) order — n_k = top_k (0 = no limit),

@@ -166,6 +166,8 @@ struct sv_ctx {
   int last_T = 0, last_batch = 0;
   int sticky = 0;
   bool taps = false;                 // keep every intermediate (fp32 logits included) for sv_get_tap
+  bool capturing = false;            // between sv_graph_begin and sv_graph_end
+  unsigned long long capture_launches0 = 0;
   int top_k = 0;                     // R31 filtered target for SAMPLE (0 / >= 1: off), sv_set_filter
   float top_p = 1.0f;
   sv::GemmPlan* gemm = nullptr;
@@ -829,6 +831,56 @@ sv_status sv_profile_read(sv_ctx* c, double* ms_total, int64_t* count, int32_t n
 }
 
 uint64_t sv_launch_count(void) { return sv::g_launch_count; }
+
+// ---------------------------------------------------------------- CUDA graphs of a fixed step
+struct sv_graph {
+  cudaGraphExec_t exec;
+  unsigned long long kernels;        // kernel launches captured (added to sv_launch_count per replay)
+};
+
+sv_status sv_graph_begin(sv_ctx* c) {
+  if (!c || !c->stream) return SV_EINVAL;                 // the legacy default stream cannot be captured
+  if (c->capturing || c->pending_verify || c->prof.mask) return SV_ESTATE;
+  SV_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+  c->capturing = true;
+  c->capture_launches0 = sv::g_launch_count;
+  return SV_OK;
+}
+
+sv_status sv_graph_end(sv_ctx* c, sv_graph** out) {
+  if (!c || !out) return SV_EINVAL;
+  if (!c->capturing) return SV_ESTATE;
+  cudaGraph_t g = nullptr;
+  const cudaError_t e = cudaStreamEndCapture(c->stream, &g);
+  c->capturing = false;
+  if (e != cudaSuccess) return SV_ECUDA;
+  if (c->pending_verify) {                                // a captured verify must be committed in it
+    cudaGraphDestroy(g);
+    return SV_ESTATE;
+  }
+  cudaGraphExec_t x = nullptr;
+  const cudaError_t e2 = cudaGraphInstantiate(&x, g, 0);
+  cudaGraphDestroy(g);
+  if (e2 != cudaSuccess) return SV_ECUDA;
+  *out = new sv_graph{x, sv::g_launch_count - c->capture_launches0};
+  sv::g_launch_count = c->capture_launches0;              // captured launches run at replay
+  return SV_OK;
+}
+
+sv_status sv_graph_launch(sv_ctx* c, const sv_graph* g) {
+  if (!c || !g) return SV_EINVAL;
+  if (c->capturing || c->pending_verify) return SV_ESTATE;
+  SV_CUDA(cudaGraphLaunch(g->exec, c->stream));
+  sv::g_launch_count += g->kernels;
+  return SV_OK;
+}
+
+sv_status sv_graph_destroy(sv_graph* g) {
+  if (!g) return SV_EINVAL;
+  cudaGraphExecDestroy(g->exec);
+  delete g;
+  return SV_OK;
+}
 
 }  // extern "C"
 

@@ -31,7 +31,8 @@ EXPORTED = [
     "sv_profile_stage_name", "sv_profile_read", "sv_launch_count", "sv_debug_gemm", "sv_kv_append_packed",
     "sv_kv_loopback_append", "sv_spec_default_config", "sv_spec_reset", "sv_spec_adapt", "sv_spec_step",
     "sv_route_default_config", "sv_route_select", "sv_lane_occupancy", "sv_kv_pack_slot", "sv_prefill",
-    "sv_verify_tree", "sv_verify_tree_logits", "sv_set_filter", "sv_draft_planted_tree",
+    "sv_verify_tree", "sv_verify_tree_logits", "sv_set_filter", "sv_draft_planted_tree", "sv_graph_begin",
+    "sv_graph_end", "sv_graph_launch", "sv_graph_destroy",
 ]
 
 
@@ -105,6 +106,10 @@ def load():
         "sv_verify_tree_logits": ([vp, i32, P(i32), P(i32), vp, vp, vp, vp, u64, ctypes.c_int, ctypes.c_float, vp,
                                    vp, vp], ctypes.c_int),
         "sv_set_filter": ([vp, i32, ctypes.c_float], ctypes.c_int),
+        "sv_graph_begin": ([vp], ctypes.c_int),
+        "sv_graph_end": ([vp, P(vp)], ctypes.c_int),
+        "sv_graph_launch": ([vp, vp], ctypes.c_int),
+        "sv_graph_destroy": ([vp], ctypes.c_int),
         "sv_commit": ([vp, vp], ctypes.c_int),
         "sv_release": ([vp, i32], ctypes.c_int),
         "sv_stats": ([vp, P(LaneStats), ctypes.c_int], ctypes.c_int),
@@ -298,6 +303,22 @@ class Lane:
         st = LaneStats()
         _check(self.lib.sv_stats(self.ctx, ctypes.byref(st), 1 if reset else 0), "sv_stats")
         return st
+
+    # ------------------------------------------------------------------ CUDA graphs
+    def graph_begin(self):
+        """Capture the lane's next calls into a CUDA graph (sv_graph_begin; needs a created stream)."""
+        _check(self.lib.sv_graph_begin(self.ctx), "sv_graph_begin")
+
+    def graph_end(self):
+        g = ctypes.c_void_p()
+        _check(self.lib.sv_graph_end(self.ctx, ctypes.byref(g)), "sv_graph_end")
+        return g
+
+    def graph_launch(self, g):
+        _check(self.lib.sv_graph_launch(self.ctx, g), "sv_graph_launch")
+
+    def graph_destroy(self, g):
+        _check(self.lib.sv_graph_destroy(g), "sv_graph_destroy")
 
     def set_filter(self, top_k=0, top_p=1.0):
         """Top-k / top-p filtered target for SAMPLE verifies (R31); (0, 1.0) = off."""

@@ -1,0 +1,94 @@
+"""CUDA-graph replay of a fixed step (sv_graph_*): a captured planted-drafter + verify + commit step
+replayed N times gives exactly the outputs, lane counters and cache lengths of the same N steps run
+eagerly (per-step drafter inputs refreshed in the buffers the graph reads), in greedy and sampled
+mode; capture rules (created stream, committed verify) are enforced."""
+import pytest
+import torch
+
+import synth
+from paper_2604_09562_b200 import sv
+
+pytestmark = pytest.mark.gpu
+
+
+def _lane(cfg, w, stream):
+    lane = sv.Lane(cfg, {k: v.cuda() for k, v in w.items()}, stream=stream)
+    for i in range(4):
+        k, v = synth.context_kv(cfg, 50 + 30 * i, seed=10 + i)
+        lane.append_kv(i, 100 + i, k.cuda(), v.cuda(), 3 + i)
+    return lane
+
+
+@pytest.mark.parametrize("mode", ["greedy", "sample"])
+def test_graph_replay_equals_eager_steps(mode):
+    cfg = synth.TOY_MLP
+    w = synth.model_weights(cfg, seed=0, norm_one=False)
+    w, succ = synth.planted_successor(cfg, w, seed=1, beta=0.3)
+    depths = [4, 2, 3, 1]
+    rows = sum(depths)
+    n = 6
+    masks, devtok = synth.planted_masks(n, rows, 0.7, cfg.vocab, seed=2)
+    outs = {}
+    for kind in ("eager", "graph"):
+        stream = torch.cuda.Stream()
+        with torch.cuda.stream(stream):
+            lane = _lane(cfg, w, stream)
+            succ_d = succ.cuda()
+            m_stage = torch.empty(rows, dtype=torch.uint8, device="cuda")
+            t_stage = torch.empty(rows, dtype=torch.int32, device="cuda")
+            drafts = torch.empty(rows, dtype=torch.int32, device="cuda")
+            acc = torch.empty(4, dtype=torch.int32, device="cuda")
+            tok = torch.empty(4, cfg.max_depth + 1, dtype=torch.int32, device="cuda")
+
+            def step():
+                lane.draft_planted([0, 1, 2, 3], depths, succ_d, m_stage, t_stage, drafts)
+                lane.verify([0, 1, 2, 3], depths, drafts, None, seed=77, mode=mode, temperature=0.9, out=(acc, tok))
+                lane.commit()
+
+            res = []
+            g = None
+            for i in range(n):
+                m_stage.copy_(masks[i].cuda())
+                t_stage.copy_(devtok[i].cuda())
+                if kind == "eager" or i == 0:
+                    step()                               # (the graph lane's step 0 warms every kernel up)
+                elif g is None:
+                    lane.graph_begin()
+                    step()                               # captured, not run
+                    g = lane.graph_end()
+                    lane.graph_launch(g)
+                else:
+                    lane.graph_launch(g)
+                stream.synchronize()
+                res.append((acc.cpu().clone(), tok.cpu().clone()))
+            st = lane.stats()
+            ln = lane.tap("len", torch.int32, (cfg.max_slots,))[:4].cpu().clone()
+            if g is not None:
+                lane.graph_destroy(g)
+            lane.close()
+        outs[kind] = (res, st, ln)
+    (re, se, le), (rg, sg, lg) = outs["eager"], outs["graph"]
+    for i in range(n):
+        assert torch.equal(re[i][0], rg[i][0]) and torch.equal(re[i][1], rg[i][1]), i
+    assert se == sg and torch.equal(le, lg)
+    assert se["steps"] == n and (mode == "sample" or se["accepted"] > 0)
+
+
+def test_graph_capture_rules():
+    cfg = synth.TOY
+    w = synth.model_weights(cfg, seed=0)
+    lane = _lane(cfg, w, torch.cuda.current_stream())        # legacy default stream: not capturable
+    with pytest.raises(sv.SvError):
+        lane.graph_begin()
+    lane.close()
+    stream = torch.cuda.Stream()
+    with torch.cuda.stream(stream):
+        lane = _lane(cfg, w, stream)
+        d = synth.random_tokens(4, cfg.vocab, seed=3).cuda()
+        lane.verify([0], [4], d)                          # warm-up (and committed)
+        lane.commit()
+        lane.graph_begin()
+        lane.verify([0], [4], d)                          # captured verify left uncommitted
+        with pytest.raises(sv.SvError):
+            lane.graph_end()
+        lane.close()
