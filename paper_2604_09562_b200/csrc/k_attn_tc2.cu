@@ -231,13 +231,15 @@ __global__ void __launch_bounds__(THREADS, 1)
         } else {
           if (lane == 0) tc::mbar_wait(&empty[st], ph ^ 1);
           __syncwarp();
-          // chain tile: keys L + c (c < R) from the chain scratch, zero rows beyond R
+          // chain tile: keys L + c (c < R) from the chain scratch. Only the R real rows are written:
+          // rows beyond R keep the slot's earlier contents — finite (the ring is zeroed at kernel
+          // start and only ever holds KV data), so their masked scores and zero P^T columns add
+          // nothing (the same invariant as a tile's skipped second page)
           const bf16* src = (is_k ? d.kc : d.vc) + (size_t)layer * d.Tmax * nkv;
           constexpr int CH = DH / 8;
-          for (int i = lane; i < KT * CH; i += 32) {
+          for (int i = lane; i < I.R * CH; i += 32) {
             const int c = i / CH, cq = i % CH;
-            uint4 v = make_uint4(0, 0, 0, 0);
-            if (c < I.R) v = *reinterpret_cast<const uint4*>(src + (size_t)(I.row0 + c) * nkv + (size_t)I.h * DH + cq * 8);
+            const uint4 v = *reinterpret_cast<const uint4*>(src + (size_t)(I.row0 + c) * nkv + (size_t)I.h * DH + cq * 8);
             const int hf = cq / 8, cc = cq % 8;
             *reinterpret_cast<uint4*>(dst + hf * (KT * 128) + c * 128 + ((cc ^ (c & 7)) * 16)) = v;
           }
