@@ -54,6 +54,7 @@ constexpr int P_BYTES = KT * NQ * 2;       // 16 KB per P^T buffer (two buffers)
 constexpr int XCOL_FLOATS = 2 * 2 * 4 * 32;  // [tile parity][slot half][quadrant][32]
 constexpr int SMEM = (KST + VST) * KV_BYTES + Q_BYTES + 2 * P_BYTES + 4 * XCOL_FLOATS + 512 + 512;
 static_assert(SMEM <= 232448, "attention smem exceeds the 227 KB per-CTA limit");
+static_assert(kSplitKeys / 64 <= 32, "an item's pages are held one per producer lane");
 constexpr uint32_t IDESC_QK = tc::idesc_bf16(128, NQ);          // A = K (K-major), B = Q (K-major)
 constexpr uint32_t IDESC_PV = tc::idesc_bf16(128, NQ, 1, 1);    // A = V^T (MN-major), B = P^T (MN-major)
 constexpr uint32_t IDESC_L = tc::idesc_bf16(128, NQ, 0, 1);     // A = ones (TMEM), B = P^T (MN-major)
@@ -193,8 +194,30 @@ __global__ void __launch_bounds__(THREADS, 1)
     uint32_t ph = 0;
     int iter = 0;
     uint32_t ptile = 0;
+    // Each item's page rows are looked up once (lane p holds page p of the item, <= 16 pages), and
+    // the next item's descriptor and page rows are fetched while this item streams, so neither
+    // dependent-load chain sits between a free ring slot and its TMA issue.
+    auto page_rows = [&](const Item2& J) {
+      int row = 0;
+      if (lane < J.n_pages) {
+        const int page = d.page_table[J.slot * d.max_pages_per_slot + J.page0 + lane];
+        row = ((((layer * d.n_pages + page) * 2 + kv) * d.Hkv) + J.h) * 64;
+      }
+      return row;
+    };
+    Item2 I;
+    int prow = 0;
+    if ((int)blockIdx.x < n_items) {
+      I = item2(d, blockIdx.x);
+      prow = page_rows(I);
+    }
     for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++iter) {
-      const Item2 I = item2(d, it);
+      Item2 In = I;
+      int prown = 0;
+      if (it + (int)gridDim.x < n_items) {            // prefetch: used by the next iteration
+        In = item2(d, it + gridDim.x);
+        prown = page_rows(In);
+      }
       if (is_k && lane == 0) {
         tc::mbar_wait(q_empty, (iter & 1) ^ 1);
         tc::mbar_arrive_expect_tx(q_full, HALVES * NQ * 128);
@@ -207,12 +230,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           // converged warp: lanes 0 / 1 look up the tile's two pages, the rows are broadcast, one
           // elected lane issues (keeps the TMA issue out of a lane-0 waterfall loop)
           const int np = min(2, I.n_pages - 2 * t);
-          int row = 0;
-          if (lane < np) {
-            const int page = d.page_table[I.slot * d.max_pages_per_slot + I.page0 + 2 * t + lane];
-            row = ((((layer * d.n_pages + page) * 2 + kv) * d.Hkv) + I.h) * 64;
-          }
-          const int row0 = __shfl_sync(0xffffffffu, row, 0), row1 = __shfl_sync(0xffffffffu, row, 1);
+          const int row0 = __shfl_sync(0xffffffffu, prow, 2 * t), row1 = __shfl_sync(0xffffffffu, prow, 2 * t + 1);
           tc::mbar_wait(&empty[st], ph ^ 1);
           if (is_k && lane == 0) SV_TR2(0, ptile);
           if (tc::elect_one()) {
@@ -237,11 +255,23 @@ __global__ void __launch_bounds__(THREADS, 1)
           // nothing (the same invariant as a tile's skipped second page)
           const bf16* src = (is_k ? d.kc : d.vc) + (size_t)layer * d.Tmax * nkv;
           constexpr int CH = DH / 8;
-          for (int i = lane; i < I.R * CH; i += 32) {
-            const int c = i / CH, cq = i % CH;
-            const uint4 v = *reinterpret_cast<const uint4*>(src + (size_t)(I.row0 + c) * nkv + (size_t)I.h * DH + cq * 8);
-            const int hf = cq / 8, cc = cq % 8;
-            *reinterpret_cast<uint4*>(dst + hf * (KT * 128) + c * 128 + ((cc ^ (c & 7)) * 16)) = v;
+          // R <= 64 / G <= 64 rows x 16 chunks: up to 32 per lane; all loads issued before the stores
+          // (one memory round trip per chain tile instead of one per row group)
+          constexpr int CU = 8;
+          for (int i0 = lane; i0 < I.R * CH; i0 += 32 * CU) {
+            uint4 v[CU];
+#pragma unroll
+            for (int u = 0; u < CU; ++u) {
+              const int i = i0 + 32 * u, c = i / CH, cq = i % CH;
+              if (i < I.R * CH)
+                v[u] = *reinterpret_cast<const uint4*>(src + (size_t)(I.row0 + c) * nkv + (size_t)I.h * DH + cq * 8);
+            }
+#pragma unroll
+            for (int u = 0; u < CU; ++u) {
+              const int i = i0 + 32 * u, c = i / CH, cq = i % CH;
+              const int hf = cq / 8, cc = cq % 8;
+              if (i < I.R * CH) *reinterpret_cast<uint4*>(dst + hf * (KT * 128) + c * 128 + ((cc ^ (c & 7)) * 16)) = v[u];
+            }
           }
           tc::fence_proxy_async();
           __syncwarp();
@@ -250,6 +280,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (++st == nst) { st = 0; ph ^= 1; }
         ++ptile;
       }
+      I = In;
+      prow = prown;
     }
   } else if (warp == 1) {
     // ======================= MMA issuer: the whole warp runs the loop (warp-uniform state, so
