@@ -13,7 +13,10 @@ constexpr int kMaxBatch = 256;     // PlanArgs capacity (requests per verify)
 constexpr int kMaxDepth = 32;      // k_i <= 32 (sv_lane_stats histograms have 33 bins)
 constexpr int kVocabTile = 128;    // lm-head epilogue statistics tile
 constexpr int kAttnRows = 64;      // max (k+1) * G query rows per (request, kv head)
-constexpr int kSplitKeys = 1024;   // page keys per split-KV work item
+#ifndef SV_SPLIT_KEYS
+#define SV_SPLIT_KEYS 1024
+#endif
+constexpr int kSplitKeys = SV_SPLIT_KEYS;   // page keys per split-KV work item
 constexpr int kNumStats = 6 + 3 * (kMaxDepth + 1);
 constexpr int kMaxRaceSplits = 16;
 constexpr int kPrefillNoHead = 3;  // internal finalize mode: a prefill chunk whose lm-head was skipped  // finalize: CTAs per request sharing a sampled row's race
