@@ -223,10 +223,46 @@ class ControlledDepths:
         self.s0, self.t0 = s1, now
 
 
+VERIFY_GRAPH_REPLAYS = 100   # verify-step µs as SURVEY.md §8(d) defines it (graph replay, drafting excluded)
+
+
 def run_gpu(args, wl, rank, world, dev):
+    """The lane runs on a created stream (capturable), made torch's current stream so the bench's
+    events and copies order with the lane's kernels."""
+    stream = torch.cuda.Stream(dev)
+    with torch.cuda.stream(stream):
+        return _run_gpu(args, wl, rank, world, dev, stream)
+
+
+def verify_step_graph(lane, wl, slots, ks, drafts, seed, out, par_d, dev, n):
+    """Verify-step µs per SURVEY.md §8(d): CUDA-event time of one graph replay of sv_verify +
+    sv_commit with the drafting excluded (the last timed step's depths and drafts, replayed n times)."""
+    lane.graph_begin()
+    if wl.tree:
+        lane.verify_tree(slots, ks, par_d, drafts, None, seed=seed, mode=wl.mode, temperature=wl.temperature, out=out)
+    else:
+        lane.verify(slots, ks, drafts, None, seed=seed, mode=wl.mode, temperature=wl.temperature, out=out)
+    lane.commit()
+    g = lane.graph_end()
+    stream = torch.cuda.current_stream(dev)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n)]
+    lane.graph_launch(g)                              # warm replay
+    for a, b in ev:
+        a.record(stream)
+        lane.graph_launch(g)
+        b.record(stream)
+    torch.cuda.synchronize(dev)
+    lane.graph_destroy(g)
+    us = sorted(1e3 * a.elapsed_time(b) for a, b in ev)
+    return {"median": round(statistics.median(us), 1), "p10": round(us[len(us) // 10], 1),
+            "p90": round(us[(9 * len(us)) // 10], 1), "replays": n,
+            "what": "CUDA graph replay of sv_verify + sv_commit, drafting excluded (SURVEY.md §8(d))"}
+
+
+def _run_gpu(args, wl, rank, world, dev, stream):
     from paper_2604_09562_b200 import sv
     import torch.distributed as dist
-    lane, w, succ, reqs = build_lane(wl, rank, dev)
+    lane, w, succ, reqs = build_lane(wl, rank, dev, stream)
     cfg = wl.cfg
     B = wl.batch
     total = args.warmup + args.steps
@@ -319,6 +355,7 @@ def run_gpu(args, wl, rank, world, dev):
                              "traffic_src": traffic.get("attention", {}).get("src"),
                              "us_per_launch": round(at["ms_per_launch"] * 1e3, 2)}
     dominant = max(kern.items(), key=lambda kv: kv[1]["ms_per_launch"] * kv[1]["launches"])[0] if kern else None
+    vg_depths = depths[total - 1]
     # ----- e2e through host buffers: pinned H2D inputs and D2H results every step (see run_e2e)
     e2e = e2e_host = None
     if ctl:                                           # later regions draft at the controller's last depth
@@ -329,9 +366,11 @@ def run_gpu(args, wl, rank, world, dev):
         if not wl.tree:                               # the host drafter variant drafts chains only
             e2e_host = run_e2e_host_drafter(args, wl, lane, succ, depths, masks, devtok, dev,
                                             total + args.e2e_steps, HOST_DRAFTER_STEPS)
+    # verify-step µs as SURVEY.md §8(d) defines it, after the e2e runs (its replays commit tokens too)
+    vgraph = verify_step_graph(lane, wl, slots, vg_depths, drafts, 4321, (acc, tok), par_d, dev, VERIFY_GRAPH_REPLAYS)
     return dict(elapsed_ms=elapsed_ms, tokens=tokens, per_step=per_step, prof=kern, roof=roof, dominant=dominant,
                 launches=launches, clocks=clk.summary(), stats=st, e2e=e2e, e2e_host=e2e_host, w=w, succ=succ, reqs=reqs,
-                depths=depths, masks=masks, devtok=devtok, alg=alg,
+                depths=depths, masks=masks, devtok=devtok, alg=alg, verify_graph=vgraph,
                 controller=({"window_steps": ControlledDepths.WINDOW, "final_depth": ctl.d, "trace": ctl.trace[-6:]}
                             if ctl else None))
 
@@ -650,7 +689,8 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    wl = synth.workload(args.workload, steps_budget=args.warmup + args.steps + args.e2e_steps + HOST_DRAFTER_STEPS + 8)
+    wl = synth.workload(args.workload, steps_budget=args.warmup + args.steps + args.e2e_steps + HOST_DRAFTER_STEPS
+                        + VERIFY_GRAPH_REPLAYS + 9)
 
     if args.impl == "reference":
         if rank == 0:
@@ -692,7 +732,9 @@ def main():
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "config": bench_config(wl, world),
         "verify_step_us": {"median": round(1e3 * statistics.median(ps), 1), "p10": round(1e3 * ps[len(ps) // 10], 1),
-                           "p90": round(1e3 * ps[(9 * len(ps)) // 10], 1)},
+                           "p90": round(1e3 * ps[(9 * len(ps)) // 10], 1),
+                           "what": "timed-region step (drafter + verify + commit), CUDA events"},
+        "verify_step_us_graph": res.get("verify_graph"),
         "acceptance": {"a_t": round(st["accepted"] / max(1, st["drafted"]), 4),
                        "tokens_per_request_step": round(st["emitted"] / max(1, args.steps * wl.batch), 3)},
         "roofline": {k: v for k, v in roof.items() if k in ("bound", "achieved", "peak", "unit", "frac", "traffic")}
