@@ -74,6 +74,57 @@ def test_graph_replay_equals_eager_steps(mode):
     assert se["steps"] == n and (mode == "sample" or se["accepted"] > 0)
 
 
+def test_graph_replay_of_a_filtered_sampled_tree_verify():
+    """A token-tree verify with a top-k / top-p filtered target (R30 + R31), captured and replayed,
+    equals the same calls run eagerly (the filter and the tree walk run inside the graph)."""
+    cfg = synth.TOY_MLP
+    w = synth.model_weights(cfg, seed=4, norm_one=False)
+    parents = [0, 0, 1, 1, 2, 0]
+    depths = [len(parents)] * 4
+    par = torch.tensor(parents * 4, dtype=torch.int32)
+    n = 4
+    draws = [synth.random_tokens(sum(depths), cfg.vocab, seed=20 + i) for i in range(n)]
+    outs = {}
+    for kind in ("eager", "graph"):
+        stream = torch.cuda.Stream()
+        with torch.cuda.stream(stream):
+            lane = _lane(cfg, w, stream)
+            lane.set_filter(40, 0.9)
+            par_d = par.cuda()
+            d_stage = torch.empty(sum(depths), dtype=torch.int32, device="cuda")
+            acc = torch.empty(4, dtype=torch.int32, device="cuda")
+            tok = torch.empty(4, cfg.max_depth + 1, dtype=torch.int32, device="cuda")
+
+            def step():
+                lane.verify_tree([0, 1, 2, 3], depths, par_d, d_stage, None, seed=5, mode="sample", temperature=0.8,
+                                 out=(acc, tok))
+                lane.commit()
+
+            res, g = [], None
+            for i in range(n):
+                d_stage.copy_(draws[i].cuda())
+                if kind == "eager" or i == 0:
+                    step()
+                elif g is None:
+                    lane.graph_begin()
+                    step()
+                    g = lane.graph_end()
+                    lane.graph_launch(g)
+                else:
+                    lane.graph_launch(g)
+                stream.synchronize()
+                res.append((acc.cpu().clone(), tok.cpu().clone()))
+            st = lane.stats()
+            if g is not None:
+                lane.graph_destroy(g)
+            lane.close()
+        outs[kind] = (res, st)
+    for i in range(n):
+        assert torch.equal(outs["eager"][0][i][0], outs["graph"][0][i][0])
+        assert torch.equal(outs["eager"][0][i][1], outs["graph"][0][i][1])
+    assert outs["eager"][1] == outs["graph"][1]
+
+
 def test_graph_capture_rules():
     cfg = synth.TOY
     w = synth.model_weights(cfg, seed=0)
