@@ -108,56 +108,89 @@ cudaError_t launch_commit(const LaneDev& d, const int* n_keep, int batch, cudaSt
 // verify; append keeps its old length in n_items[1] (workspace word reserved for it).
 __global__ void append_alloc_kernel(LaneDev d, int slot, unsigned long long rid, int n, int pending,
                                     const int* pending_dev, int* scratch) {
-  const int L = d.len[slot];
-  const int have = (L + d.page - 1) / d.page, need = (L + n + d.page - 1) / d.page;
-  int ok = 1;
-  if (L + n > d.max_pos || need > d.max_pages_per_slot) { atomicOr(d.err, SV_DERR_MAX_POS); ok = 0; }
-  if (ok) ok = pop_pages(d, slot, have, need - have);
-  int pend = pending_dev ? *pending_dev : pending;
-  if (pend < 0 || pend >= d.V) { atomicOr(d.err, SV_DERR_BAD_TOKEN); pend = 0; }
-  scratch[0] = L;
-  scratch[1] = ok;
-  if (ok) {
-    d.len[slot] = L + n;
-    d.pending[slot] = pend;
-    d.rid[slot] = rid;
+  // thread 0 checks and reserves the pages (one atomic on the free-list top); the block copies the
+  // popped page ids into the slot's table in parallel (a long prompt pops hundreds of pages)
+  __shared__ int s_old, s_cnt, s_first;
+  if (threadIdx.x == 0) {
+    const int L = d.len[slot];
+    const int have = (L + d.page - 1) / d.page, need = (L + n + d.page - 1) / d.page;
+    int ok = 1, cnt = need - have, old = 0;
+    if (L + n > d.max_pos || need > d.max_pages_per_slot) { atomicOr(d.err, SV_DERR_MAX_POS); ok = 0; }
+    if (ok && cnt > 0) {
+      old = atomicSub(d.free_top, cnt);
+      if (old - cnt < 0) {
+        atomicAdd(d.free_top, cnt);                  // undo: the pages were not taken
+        atomicOr(d.err, SV_DERR_NO_PAGES);
+        ok = 0;
+      }
+    }
+    int pend = pending_dev ? *pending_dev : pending;
+    if (pend < 0 || pend >= d.V) { atomicOr(d.err, SV_DERR_BAD_TOKEN); pend = 0; }
+    scratch[0] = L;
+    scratch[1] = ok;
+    if (ok) {
+      d.len[slot] = L + n;
+      d.pending[slot] = pend;
+      d.rid[slot] = rid;
+    }
+    s_old = old;
+    s_cnt = ok ? cnt : 0;
+    s_first = have;
   }
+  __syncthreads();
+  for (int i = threadIdx.x; i < s_cnt; i += blockDim.x)
+    d.page_table[slot * d.max_pages_per_slot + s_first + i] = d.free_list[s_old - s_cnt + i];
 }
 
-// k, v: [n_layers][n][Hkv][dh] (packed = 0) or one buffer [n_layers][n][2][Hkv][dh] (packed = 1)
+// The KV copies below move "row sets": the Hkv x d_h/8 16-byte vectors of one (layer, token, K|V).
+// One warp per row set: the page is looked up once (a broadcast load), all of the warp's loads are
+// issued before its stores, and the packed side is one contiguous segment (Hkv * d_h * 2 bytes).
+constexpr int KV_U = 8;                          // vectors per lane in flight (row sets <= 256 vectors per pass)
+
 __global__ void append_copy_kernel(LaneDev d, int slot, const bf16* __restrict__ k, const bf16* __restrict__ v,
                                    int n, int packed, const int* __restrict__ scratch) {
   if (!scratch[1]) return;
   const int L = scratch[0];
-  const int vec_per_row = d.dh / 8;
-  const size_t per_tok = (size_t)2 * d.Hkv * vec_per_row;
-  const size_t total = (size_t)d.n_layers * n * per_tok;
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
-    const size_t lt = i / per_tok;
-    const int rem = int(i % per_tok);
-    const int layer = int(lt / n), c = int(lt % n);
-    const int kv = rem / (d.Hkv * vec_per_row), h = (rem / vec_per_row) % d.Hkv, v8 = rem % vec_per_row;
-    const bf16* src;
-    if (packed) src = k + ((((size_t)layer * n + c) * 2 + kv) * d.Hkv + h) * d.dh + v8 * 8;
-    else src = (kv ? v : k) + (((size_t)layer * n + c) * d.Hkv + h) * d.dh + v8 * 8;
-    const int t = L + c;
+  const int vpr = d.dh / 8, nvec = d.Hkv * vpr, nsets = d.n_layers * n * 2;
+  const size_t nkv = (size_t)d.Hkv * d.dh;
+  const int lane = threadIdx.x & 31, nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int set = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; set < nsets; set += nwarps) {
+    const int kv = set & 1, lt = set >> 1, layer = lt / n, c = lt - layer * n, t = L + c;
     const int page = d.page_table[slot * d.max_pages_per_slot + t / d.page];
-    bf16* dst = d.pool + pool_row(d, layer, page, kv, h, t % d.page) * d.dh + v8 * 8;
-    *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(src);
+    bf16* dst0 = d.pool + pool_row(d, layer, page, kv, 0, t % d.page) * d.dh;
+    const bf16* src0 = packed ? k + (((size_t)layer * n + c) * 2 + kv) * nkv : (kv ? v : k) + ((size_t)layer * n + c) * nkv;
+    for (int e0 = 0; e0 < nvec; e0 += 32 * KV_U) {
+      uint4 buf[KV_U];
+#pragma unroll
+      for (int u = 0; u < KV_U; ++u) {
+        const int e = e0 + lane + 32 * u;
+        if (e < nvec) buf[u] = *reinterpret_cast<const uint4*>(src0 + (size_t)e * 8);
+      }
+#pragma unroll
+      for (int u = 0; u < KV_U; ++u) {
+        const int e = e0 + lane + 32 * u;
+        if (e < nvec) {
+          const int h = e / vpr, v8 = e - h * vpr;
+          *reinterpret_cast<uint4*>(dst0 + (size_t)h * d.page * d.dh + v8 * 8) = buf[u];
+        }
+      }
+    }
   }
+}
+
+static int kv_copy_grid(int nsets) {                // 8 warps per block, at most 8 blocks per SM
+  const int blocks = (nsets + 7) / 8;
+  return blocks < 148 * 8 ? (blocks > 0 ? blocks : 1) : 148 * 8;
 }
 
 cudaError_t launch_append(const LaneDev& d, int slot, unsigned long long rid, const bf16* k, const bf16* v, int n,
                           int pending, const int* pending_dev, int packed, cudaStream_t s) {
   int* scratch = d.n_items + 1;                  // two spare workspace words
   SV_COUNT_LAUNCH();
-  append_alloc_kernel<<<1, 1, 0, s>>>(d, slot, rid, n, pending, pending_dev, scratch);
+  append_alloc_kernel<<<1, 256, 0, s>>>(d, slot, rid, n, pending, pending_dev, scratch);
   if (n > 0) {
-    const size_t total = (size_t)d.n_layers * n * 2 * d.Hkv * (d.dh / 8);
-    int grid = (int)((total + 255) / 256);
-    if (grid > 148 * 8) grid = 148 * 8;
     SV_COUNT_LAUNCH();
-    append_copy_kernel<<<grid, 256, 0, s>>>(d, slot, k, v, n, packed, scratch);
+    append_copy_kernel<<<kv_copy_grid(d.n_layers * n * 2), 256, 0, s>>>(d, slot, k, v, n, packed, scratch);
   }
   return cudaGetLastError();
 }
@@ -184,18 +217,29 @@ cudaError_t launch_release(const LaneDev& d, int slot, cudaStream_t s) {
 // ------------------------------------------------------------------ hand-off packing
 __global__ void kv_pack_kernel(const bf16* __restrict__ k, const bf16* __restrict__ v, int n_layers, int Hkv, int dh,
                                int n, int pending, bf16* __restrict__ out) {
-  const int vpr = dh / 8;
-  const size_t per_tok = (size_t)2 * Hkv * vpr;
-  const size_t total = (size_t)n_layers * n * per_tok;
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
-    const size_t lt = i / per_tok;
-    const int rem = int(i % per_tok);
-    const int kv = rem / (Hkv * vpr), h = (rem / vpr) % Hkv, v8 = rem % vpr;
-    const bf16* src = (kv ? v : k) + (lt * Hkv + h) * dh + v8 * 8;
-    *reinterpret_cast<uint4*>(out + i * 8) = *reinterpret_cast<const uint4*>(src);
+  const int nvec = Hkv * dh / 8, nsets = n_layers * n * 2;
+  const size_t nkv = (size_t)Hkv * dh;
+  const int lane = threadIdx.x & 31, nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int set = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; set < nsets; set += nwarps) {
+    const int kv = set & 1, lt = set >> 1;             // lt = layer * n + token
+    const bf16* src0 = (kv ? v : k) + (size_t)lt * nkv;
+    bf16* dst0 = out + (size_t)set * nkv;               // [layer][token][kv] = set
+    for (int e0 = 0; e0 < nvec; e0 += 32 * KV_U) {
+      uint4 buf[KV_U];
+#pragma unroll
+      for (int u = 0; u < KV_U; ++u) {
+        const int e = e0 + lane + 32 * u;
+        if (e < nvec) buf[u] = *reinterpret_cast<const uint4*>(src0 + (size_t)e * 8);
+      }
+#pragma unroll
+      for (int u = 0; u < KV_U; ++u) {
+        const int e = e0 + lane + 32 * u;
+        if (e < nvec) *reinterpret_cast<uint4*>(dst0 + (size_t)e * 8) = buf[u];
+      }
+    }
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
-    int* trailer = reinterpret_cast<int*>(out + total * 8);
+    int* trailer = reinterpret_cast<int*>(out + (size_t)nsets * nkv);
     trailer[0] = pending;
     trailer[1] = trailer[2] = trailer[3] = 0;
   }
@@ -204,7 +248,8 @@ __global__ void kv_pack_kernel(const bf16* __restrict__ k, const bf16* __restric
 cudaError_t launch_kv_pack(const bf16* k, const bf16* v, int n_layers, int Hkv, int dh, int n, int pending,
                            void* packed, cudaStream_t s) {
   SV_COUNT_LAUNCH();
-  kv_pack_kernel<<<148 * 2, 256, 0, s>>>(k, v, n_layers, Hkv, dh, n, pending, reinterpret_cast<bf16*>(packed));
+  kv_pack_kernel<<<kv_copy_grid(n_layers * n * 2), 256, 0, s>>>(k, v, n_layers, Hkv, dh, n, pending,
+                                                                reinterpret_cast<bf16*>(packed));
   return cudaGetLastError();
 }
 
@@ -217,20 +262,33 @@ __global__ void kv_pack_slot_kernel(LaneDev d, int slot, int n, bf16* __restrict
     if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(d.err, SV_DERR_MAX_POS);
     return;
   }
-  const int vpr = d.dh / 8;
-  const size_t per_tok = (size_t)2 * d.Hkv * vpr;
-  const size_t total = (size_t)d.n_layers * n * per_tok;
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
-    const int layer = int(i / ((size_t)n * per_tok));
-    const int t = int((i / per_tok) % n);
-    const int rem = int(i % per_tok);
-    const int kv = rem / (d.Hkv * vpr), h = (rem / vpr) % d.Hkv, v8 = rem % vpr;
+  const int vpr = d.dh / 8, nvec = d.Hkv * vpr, nsets = d.n_layers * n * 2;
+  const size_t nkv = (size_t)d.Hkv * d.dh;
+  const int lane = threadIdx.x & 31, nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int set = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; set < nsets; set += nwarps) {
+    const int kv = set & 1, lt = set >> 1, layer = lt / n, t = lt - layer * n;
     const int page = d.page_table[slot * d.max_pages_per_slot + t / d.page];
-    const bf16* src = d.pool + pool_row(d, layer, page, kv, h, t % d.page) * d.dh + v8 * 8;
-    *reinterpret_cast<uint4*>(out + i * 8) = *reinterpret_cast<const uint4*>(src);
+    const bf16* src0 = d.pool + pool_row(d, layer, page, kv, 0, t % d.page) * d.dh;
+    bf16* dst0 = out + (size_t)set * nkv;
+    for (int e0 = 0; e0 < nvec; e0 += 32 * KV_U) {
+      uint4 buf[KV_U];
+#pragma unroll
+      for (int u = 0; u < KV_U; ++u) {
+        const int e = e0 + lane + 32 * u;
+        if (e < nvec) {
+          const int h = e / vpr, v8 = e - h * vpr;
+          buf[u] = *reinterpret_cast<const uint4*>(src0 + (size_t)h * d.page * d.dh + v8 * 8);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < KV_U; ++u) {
+        const int e = e0 + lane + 32 * u;
+        if (e < nvec) *reinterpret_cast<uint4*>(dst0 + (size_t)e * 8) = buf[u];
+      }
+    }
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
-    int* trailer = reinterpret_cast<int*>(out + total * 8);
+    int* trailer = reinterpret_cast<int*>(out + (size_t)nsets * nkv);
     trailer[0] = d.pending[slot];
     trailer[1] = trailer[2] = trailer[3] = 0;
   }
@@ -238,7 +296,7 @@ __global__ void kv_pack_slot_kernel(LaneDev d, int slot, int n, bf16* __restrict
 
 cudaError_t launch_kv_pack_slot(const LaneDev& d, int slot, int n, void* packed, cudaStream_t s) {
   SV_COUNT_LAUNCH();
-  kv_pack_slot_kernel<<<148 * 2, 256, 0, s>>>(d, slot, n, reinterpret_cast<bf16*>(packed));
+  kv_pack_slot_kernel<<<kv_copy_grid(d.n_layers * n * 2), 256, 0, s>>>(d, slot, n, reinterpret_cast<bf16*>(packed));
   return cudaGetLastError();
 }
 
