@@ -117,7 +117,8 @@ Layout make_layout(const sv_config& c) {
   L.fin_part = L.take(sizeof(sv::RacePart) * sv::kMaxRaceSplits * c.max_batch);
   L.gemm_ws = L.take(sv::gemm_workspace_bytes((int)T, (int)cmax));
   L.trace = L.take(8 * 16 * 256);
-  L.prefill = L.take(4 * 3 * (size_t)(c.max_depth + 2));   // sv_prefill: chunk tokens + outputs
+  // sv_prefill: outputs of a chunk + the whole prompt (copied to the device once, <= max_pos tokens)
+  L.prefill = L.take(4 * (2 * (size_t)(c.max_depth + 2) + (size_t)c.max_pos));
   L.total = (L.total + 1023) & ~size_t(1023);
   return L;
 }
@@ -749,15 +750,19 @@ sv_status sv_prefill(sv_ctx* c, int32_t slot, uint64_t request_id, const int32_t
   for (int i = 0; i < n; ++i)
     if (prompt[i] < 0 || prompt[i] >= c->cfg.vocab) return SV_EINVAL;
   const int K1 = c->cfg.max_depth + 2;
-  int32_t* dtok = (int32_t*)(c->ws + c->lay.prefill);     // chunk tokens
-  int32_t* dacc = dtok + K1;                               // accepted_len [1]
+  int32_t* dacc = (int32_t*)(c->ws + c->lay.prefill);     // accepted_len [1]
   int32_t* dout = dacc + K1;                               // out_tokens [max_depth + 1]
+  int32_t* dprompt = dout + K1;                            // the prompt [n <= max_pos]
+  if (n > c->cfg.max_pos) return SV_EINVAL;
+  // one copy of the whole prompt (a per-chunk copy from pageable memory would block the host on
+  // every chunk's previous work); the chunks then read their tokens in place
+  SV_CUDA(cudaMemcpyAsync(dprompt, prompt, 4 * (size_t)n, cudaMemcpyHostToDevice, c->stream));
   sv_status st = sv_append_kv(c, slot, request_id, nullptr, nullptr, 0, prompt[0]);
   if (st) return st;
   int pos = 1, k = 0;
   for (;;) {
     k = chunk - 1 < n - pos ? chunk - 1 : n - pos;
-    if (k > 0) SV_CUDA(cudaMemcpyAsync(dtok, prompt + pos, 4 * (size_t)k, cudaMemcpyHostToDevice, c->stream));
+    const int32_t* dtok = dprompt + pos;
     // only the last chunk's lm-head matters (its last row predicts the next token)
     const bool last = pos + k >= n;
     if ((st = verify_impl(c, 1, &slot, &k, nullptr, dtok, nullptr, 0, SV_PREFILL, 1.0f, dacc, dout, nullptr, nullptr,
