@@ -158,28 +158,53 @@ __global__ void __launch_bounds__(FLT_THREADS) filter_kernel(LaneDev d, float in
 
   // 2. one pass over the row: fixed-point total mass; candidates >= tau into shared memory
   unsigned long long tot = 0;
-  constexpr int U = 8;                                 // loads of U elements in flight per thread
-  for (int x0 = tid; x0 < V; x0 += FLT_THREADS * U) {
-    float vv[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int x = x0 + u * FLT_THREADS;
-      vv[u] = x < V ? row[x] * inv_temp : -INFINITY;
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const float v = vv[u];
-      const unsigned long long e = v == -INFINITY ? 0ull : fx_mass(expf(v - m));
-      tot += e;
-      if (tau > -INFINITY && v >= tau) {
-        const unsigned pos = atomicAdd(&s_nc, 1u);
-        if (pos < FLT_CAP) {
-          c_key[pos] = flt_key(v);
-          c_id[pos] = x0 + u * FLT_THREADS;
-          c_mass[pos] = e;
-          atomicAdd(&s_cmass, e);
-        }
+  auto visit = [&](float v, int x) {
+    const unsigned long long e = v == -INFINITY ? 0ull : fx_mass(expf(v - m));
+    tot += e;
+    if (tau > -INFINITY && v >= tau) {
+      const unsigned pos = atomicAdd(&s_nc, 1u);
+      if (pos < FLT_CAP) {
+        c_key[pos] = flt_key(v);
+        c_id[pos] = x;
+        c_mass[pos] = e;
+        atomicAdd(&s_cmass, e);
       }
+    }
+  };
+  if ((V & 3) == 0) {
+    // 16-byte loads (rows are 16-byte aligned when V % 4 == 0), U of them in flight per thread:
+    // the pass is load-latency bound, so bytes in flight per load instruction is what counts
+    constexpr int U = 4;
+    const int V4 = V >> 2;
+    const float4* row4 = reinterpret_cast<const float4*>(row);
+    for (int x0 = tid; x0 < V4; x0 += FLT_THREADS * U) {
+      float4 vv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int x = x0 + u * FLT_THREADS;
+        vv[u] = x < V4 ? row4[x] : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int x = 4 * (x0 + u * FLT_THREADS);
+        const float4 q = vv[u];
+        visit(q.x == -INFINITY ? q.x : q.x * inv_temp, x);
+        visit(q.y == -INFINITY ? q.y : q.y * inv_temp, x + 1);
+        visit(q.z == -INFINITY ? q.z : q.z * inv_temp, x + 2);
+        visit(q.w == -INFINITY ? q.w : q.w * inv_temp, x + 3);
+      }
+    }
+  } else {
+    constexpr int U = 8;                               // loads of U elements in flight per thread
+    for (int x0 = tid; x0 < V; x0 += FLT_THREADS * U) {
+      float vv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int x = x0 + u * FLT_THREADS;
+        vv[u] = x < V ? row[x] * inv_temp : -INFINITY;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) visit(vv[u], x0 + u * FLT_THREADS);
     }
   }
   for (int o = 16; o; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
