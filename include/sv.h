@@ -26,6 +26,8 @@
  *    nothing. Device-detected problems set a sticky device error word that
  *    is reported by the next sv_stats / sv_commit (see sv_status).
  *  - A context is one decode lane on one GPU; it is not thread-safe.
+ *  - fp32 row buffers (draft_probs, logits, logits_out) must be 16-byte aligned (rows are read
+ *    with 16-byte vector loads when V % 4 == 0); a misaligned pointer is SV_EINVAL.
  *
  * Sequence convention (SURVEY.md §8 "Verify rows"): a request with n
  * committed tokens has cache length L = n - 1; its "pending" token (index L)

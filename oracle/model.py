@@ -25,7 +25,10 @@ details fixed for both paths").
 Pinned by tests/test_oracle_model.py: attention vs torch
 scaled_dot_product_attention (fp64, causal on a dense copy), softmax vs
 torch.log_softmax, RMSNorm and RoPE closed forms (constant vectors,
-position-0 identity, pair norms, relative-position property), silu closed form.
+position-0 identity, pair norms, relative-position property), silu closed form;
+and the layer COMPOSITION (layer_forward / forward_chain: residual placement, MLP input,
+final norm, GQA mapping, cache semantics) by tests/test_oracle_llama_pin.py against
+transformers' LlamaForCausalLM in fp64 with the bf16 rounding points switched off.
 """
 import numpy as np
 

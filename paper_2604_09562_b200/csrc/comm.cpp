@@ -10,6 +10,8 @@
 
 sv_status sv_internal_append_packed(sv_ctx* c, int32_t slot, uint64_t request_id, const void* packed,
                                     int32_t n_tokens);
+sv_status sv_internal_append_check(sv_ctx* c, int32_t slot, uint64_t request_id, const void* packed,
+                                   int32_t n_tokens);
 cudaStream_t sv_internal_stream(sv_ctx* c);
 size_t sv_internal_packed_bytes(sv_ctx* c, int32_t n_tokens);
 size_t sv_kv_packed_bytes(const sv_config* cfg, int32_t n_tokens);
@@ -65,6 +67,8 @@ sv_status sv_kv_send(const void* kv_packed, int32_t n_layers, int32_t n_kv_heads
 sv_status sv_kv_recv_append(sv_ctx* ctx, int32_t slot, uint64_t request_id, int32_t n_tokens, void* staging,
                             int peer, void* nccl_comm) {
   if (!ctx || !staging || !nccl_comm || n_tokens < 0 || peer < 0) return SV_EINVAL;
+  const sv_status chk = sv_internal_append_check(ctx, slot, request_id, staging, n_tokens);
+  if (chk) return chk;
   const size_t bytes = sv_internal_packed_bytes(ctx, n_tokens);
   cudaStream_t st = sv_internal_stream(ctx);
   sv_status s = nccl_ok(ncclGroupStart());
@@ -85,6 +89,8 @@ sv_status sv_kv_loopback_append(sv_ctx* ctx, int32_t slot, uint64_t request_id, 
                                 const void* kv_packed, void* staging, int rank, void* nccl_comm) {
   if (!ctx || !kv_packed || !staging || !nccl_comm || n_tokens < 0 || rank < 0) return SV_EINVAL;
   if (((uintptr_t)kv_packed | (uintptr_t)staging) & 15) return SV_EINVAL;
+  const sv_status chk = sv_internal_append_check(ctx, slot, request_id, staging, n_tokens);
+  if (chk) return chk;
   const size_t bytes = sv_internal_packed_bytes(ctx, n_tokens);
   cudaStream_t st = sv_internal_stream(ctx);
   sv_status s = nccl_ok(ncclGroupStart());

@@ -125,10 +125,9 @@ __global__ void __launch_bounds__(128) attn_simt_kernel(LaneDev d, int layer) {
 cudaError_t launch_attention(const LaneDev& d, int layer, int batch, cudaStream_t s) {
   const size_t smem = sizeof(float) * ((size_t)kAttnRows * d.dh + (size_t)d.dh * (AS_KC + 1) +
                                        (size_t)AS_KC * d.dh + kAttnRows * AS_KC + 3 * kAttnRows);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(attn_simt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
-    attr = true;
+  {
+    const cudaError_t e = smem_optin((const void*)attn_simt_kernel, (int)(100 * 1024));
+    if (e != cudaSuccess) return e;
   }
   SV_COUNT_LAUNCH();
   attn_simt_kernel<<<148 * 4, 128, smem, s>>>(d, layer);

@@ -421,12 +421,9 @@ int attn_tc_smem_bytes(int dh) { return dh == 128 ? AttnCfg<128>::SMEM : AttnCfg
 template <int DH>
 static cudaError_t launch_dh(const CUtensorMap& map_q, const CUtensorMap& map_kv, const LaneDev& d, int layer,
                              int num_sms, int q_box_tokens, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e =
-        cudaFuncSetAttribute(attn_tc_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, AttnCfg<DH>::SMEM);
+  {
+    const cudaError_t e = smem_optin((const void*)attn_tc_kernel<DH>, (int)(AttnCfg<DH>::SMEM));
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   SV_COUNT_LAUNCH();
   attn_tc_kernel<DH><<<num_sms, THREADS, AttnCfg<DH>::SMEM, s>>>(map_q, map_kv, d, layer, q_box_tokens);

@@ -572,11 +572,9 @@ int attn_tc2_smem_bytes() { return SMEM; }
 
 cudaError_t launch_attention_tc2(const CUtensorMap& map_q, const CUtensorMap& map_kv, const LaneDev& d, int layer,
                                  int num_sms, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(attn_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+  {
+    const cudaError_t e = smem_optin((const void*)attn_tc2_kernel, (int)(SMEM));
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   SV_COUNT_LAUNCH();
   return launch_pdl(attn_tc2_kernel, dim3(num_sms), dim3(THREADS), SMEM, s, 1, map_q, map_kv, d, layer);

@@ -356,9 +356,14 @@ __global__ void __launch_bounds__(FLT_THREADS) filter_kernel(LaneDev d, float in
           }
         }
         __syncthreads();
-        if (s_tie_lim <= -2) {
-          if (warp == (int)s_D) {
-            const int want = -2 - s_tie_lim;           // 1-based rank inside the warp
+        // every thread reads the marker into a register before anyone overwrites it, so all
+        // warps take the same branch (and the same barriers) below
+        const int mk = s_tie_lim;
+        const int wd = s_D;
+        __syncthreads();
+        if (mk <= -2) {
+          if (warp == wd) {
+            const int want = -2 - mk;                  // 1-based rank inside the warp
             const unsigned int before = __popc(bal & ((1u << lane) - 1u));
             if (tie && (int)before + 1 == want) s_tie_lim = x;
           }
@@ -375,10 +380,9 @@ __global__ void __launch_bounds__(FLT_THREADS) filter_kernel(LaneDev d, float in
 cudaError_t launch_filter(const LaneDev& d, int T, float inv_temp, int top_k, float top_p, cudaStream_t s) {
   SV_COUNT_LAUNCH();
   constexpr size_t smem = FLT_SMEM;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(filter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
+  {
+    const cudaError_t e = smem_optin((const void*)filter_kernel, (int)((int)smem));
+    if (e != cudaSuccess) return e;
   }
   return launch_pdl(filter_kernel, dim3(T), dim3(FLT_THREADS), smem, s, 1, d, inv_temp, top_k, top_p);
 }

@@ -560,11 +560,9 @@ int gemm_sw_smem_bytes() { return SMEM_BYTES; }
 
 cudaError_t launch_gemm_sw(const CUtensorMap& map_w, const CUtensorMap& map_x, const GemmTcArgs& g, int num_sms,
                            cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_sw_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+  {
+    const cudaError_t e = smem_optin((const void*)gemm_sw_kernel, (int)(SMEM_BYTES));
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   if (g.M <= 0) return cudaSuccess;
   const int num_mp = g.kind == GEMM_EPI_SWIGLU ? g.F / 128 : (g.N + 255) / 256;

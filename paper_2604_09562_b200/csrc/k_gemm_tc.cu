@@ -515,11 +515,9 @@ size_t gemm_tc_partial_bytes(int num_sms) { return (size_t)num_sms * 2 * BM * BN
 
 cudaError_t launch_gemm_tc(const CUtensorMap& map_a, const CUtensorMap& map_b, const GemmTcArgs& g_in, int num_sms,
                            cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+  {
+    const cudaError_t e = smem_optin((const void*)gemm_tc_kernel, (int)(SMEM_BYTES));
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   if (g_in.M <= 0) return cudaSuccess;
   GemmTcArgs g = g_in;
@@ -682,11 +680,9 @@ __global__ void __launch_bounds__(THREADS, 1)
 
 cudaError_t launch_gemm_tc2(const CUtensorMap& map_a, const CUtensorMap& map_b, const GemmTcArgs& g, int num_sms,
                             cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_BYTES);
+  {
+    const cudaError_t e = smem_optin((const void*)gemm_tc2_kernel, (int)(SMEM2_BYTES));
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   if (g.M <= 0) return cudaSuccess;
   const int num_tiles = ((g.M + PAIR_M - 1) / PAIR_M) * g.n_tiles;

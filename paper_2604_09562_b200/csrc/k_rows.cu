@@ -7,6 +7,10 @@
 // lane-state initialisation.
 #include <stdlib.h>
 
+#include <mutex>
+#include <set>
+#include <utility>
+
 #include "common.cuh"
 #include "lane.h"
 #include "../../include/sv.h"
@@ -14,6 +18,19 @@
 namespace sv {
 
 unsigned long long g_launch_count = 0;
+
+cudaError_t smem_optin(const void* kernel, int bytes) {
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> g(mu);
+  if (done.count({kernel, dev})) return cudaSuccess;
+  e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.insert({kernel, dev});
+  return e;
+}
 
 bool pdl_enabled() {
   static const bool on = [] {

@@ -85,6 +85,11 @@ extern unsigned long long g_launch_count;
 // touches anything an earlier kernel of the step writes, so only its prologue (barrier / TMEM
 // setup, weight prefetch) overlaps. SV_PDL=0 launches them normally.
 bool pdl_enabled();
+
+// Opt `kernel` into `bytes` of dynamic shared memory on the CURRENT device. The attribute is per
+// device and one process may create lanes on several GPUs, so the opt-in is remembered per
+// (kernel, device), not once per process.
+cudaError_t smem_optin(const void* kernel, int bytes);
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                               int cluster_x, Args&&... args) {

@@ -457,6 +457,7 @@ static sv_status verify_impl(sv_ctx* c, int32_t batch, const int32_t* slots, con
   if (mode != SV_GREEDY && mode != SV_SAMPLE && mode != SV_PREFILL) return SV_EINVAL;
   if (parents && mode == SV_PREFILL) return SV_EINVAL;
   if (mode == SV_SAMPLE && !(temperature > 0.f)) return SV_EINVAL;
+  if (((uintptr_t)draft_probs | (uintptr_t)logits_out) & 15) return SV_EINVAL;   // float4 row loads / copies
   if (c->pending_verify) return SV_ESTATE;
   sv::PlanArgs p;
   sv_status st = check_batch(c, batch, slots, depths, p);
@@ -539,6 +540,7 @@ static sv_status verify_logits_impl(sv_ctx* c, int32_t batch, const int32_t* slo
                                     const float* logits, uint64_t seed, sv_mode mode, float temperature,
                                     int32_t* accepted_len, int32_t* out_tokens, int32_t* accepted_nodes) {
   if (!c || !accepted_len || !out_tokens || !logits) return SV_EINVAL;
+  if (((uintptr_t)draft_probs | (uintptr_t)logits) & 15) return SV_EINVAL;        // float4 row loads
   if (mode != SV_GREEDY && mode != SV_SAMPLE && mode != SV_PREFILL) return SV_EINVAL;
   if (parents && mode == SV_PREFILL) return SV_EINVAL;
   if (mode == SV_SAMPLE && !(temperature > 0.f)) return SV_EINVAL;
@@ -890,11 +892,21 @@ sv_status sv_graph_destroy(sv_graph* g) {
 }  // extern "C"
 
 // used by comm.cpp (hand-off receive): append from a packed device buffer
-sv_status sv_internal_append_packed(sv_ctx* c, int32_t slot, uint64_t request_id, const void* packed,
-                                    int32_t n_tokens) {
+// host-checkable preconditions of an append from a packed message (checked BEFORE any NCCL
+// receive is posted, so a refused call consumes no message)
+sv_status sv_internal_append_check(sv_ctx* c, int32_t slot, uint64_t request_id, const void* packed,
+                                   int32_t n_tokens) {
   if (!c || slot < 0 || slot >= c->cfg.max_slots || n_tokens < 0 || !packed) return SV_EINVAL;
+  if ((uintptr_t)packed & 15) return SV_EINVAL;
   if (c->state[slot] == PENDING) return SV_ESTATE;
   if (c->state[slot] == ACTIVE && c->rid[slot] != request_id) return SV_EINVAL;
+  return SV_OK;
+}
+
+sv_status sv_internal_append_packed(sv_ctx* c, int32_t slot, uint64_t request_id, const void* packed,
+                                    int32_t n_tokens) {
+  const sv_status chk = sv_internal_append_check(c, slot, request_id, packed, n_tokens);
+  if (chk) return chk;
   const size_t body = (size_t)c->cfg.n_layers * n_tokens * 2 * c->cfg.n_kv_heads * c->cfg.head_dim * 2;
   const int* trailer = (const int*)((const char*)packed + body);
   SV_CUDA(sv::launch_append(c->d, slot, request_id, (const bf16*)packed, nullptr, n_tokens, 0, trailer, 1,

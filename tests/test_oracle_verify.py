@@ -114,6 +114,49 @@ def test_first_emitted_token_follows_target(dense):
     assert _chisq(counts, p1, n) > ALPHA
 
 
+@pytest.mark.parametrize("temperature", [0.5, 1.7])
+@pytest.mark.parametrize("dense", [True, False])
+def test_first_emitted_token_follows_tempered_target(temperature, dense):
+    """P1 at T != 1: the first emitted token ~ softmax(l / T). The expected law is written as
+    p^(1/T) / sum p^(1/T) with p = softmax(l) (a different route from the oracle's scaled-logit
+    softmax), so a temperature applied twice, inverted or dropped fails here."""
+    rng = np.random.default_rng(int(10 * temperature) + (5 if dense else 0))
+    V, k, n = 10, 2, 12000
+    base = np.stack([_rand_simplex(rng, V, sharp=1.0) for _ in range(k + 1)])
+    logits = np.log(base) + rng.normal(size=(1, 1))         # a row offset the softmax must ignore
+    q = np.stack([_rand_simplex(rng, V, zeros=2) for _ in range(k)])
+    counts = np.zeros(V)
+    for rid in range(n):
+        drafts = [int(rng.choice(V, p=q[j])) for j in range(k)]
+        r = verify.verify_request(logits, drafts, q if dense else None, 91, rid, 12, verify.SAMPLE, temperature)
+        counts[r["emitted"][0]] += 1
+    pT = base[0] ** (1.0 / temperature)
+    pT /= pT.sum()
+    assert _chisq(counts, pT, n) > ALPHA
+    # and the law at T is not the T = 1 law (the test has power to see a dropped temperature)
+    p1 = base[0] / base[0].sum()
+    assert _chisq(counts, p1, n) < 1e-6
+
+
+def test_tempered_acceptance_probability_closed_form():
+    """With one-hot drafts d ~ q the acceptance probability at T is sum_x q(x) min(1, p_T(x)),
+    p_T = p^(1/T) normalised (Leviathan's beta for q = the drafter's law, one-hot verification
+    compares p_T(d) against 1)."""
+    rng = np.random.default_rng(3)
+    V, n, T = 6, 20000, 0.6
+    base = _rand_simplex(rng, V, sharp=1.0)
+    q = _rand_simplex(rng, V)
+    logits = np.log(np.stack([base, base]))
+    acc = 0
+    for rid in range(n):
+        d = int(rng.choice(V, p=q))
+        acc += verify.verify_request(logits, [d], None, 17, rid, 3, verify.SAMPLE, T)["a"]
+    pT = base ** (1.0 / T)
+    pT /= pT.sum()
+    beta = float(np.sum(q * np.minimum(1.0, pT)))
+    assert abs(acc / n - beta) < 4 * np.sqrt(beta * (1 - beta) / n)
+
+
 # ------------------------------------------------------------------ P2 brute force
 
 def _exact_law(p, q):
