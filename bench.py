@@ -77,6 +77,7 @@ class Clocks:
     def __init__(self, index):
         self.index = index
         self.sm, self.reasons, self.max_mhz = [], set(), None
+        self.reason_count = {}
         self.stop = threading.Event()
 
     def __enter__(self):
@@ -101,6 +102,7 @@ class Clocks:
                 for name, bit in self.REASONS.items():
                     if r & bit:
                         self.reasons.add(name)
+                        self.reason_count[name] = self.reason_count.get(name, 0) + 1
             except Exception:
                 pass
             time.sleep(0.002)
@@ -114,7 +116,13 @@ class Clocks:
         if not self.sm:
             return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"], "samples": 0}
         return {"sm_mhz": statistics.median(self.sm), "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
-                "samples": len(self.sm)}
+                "samples": len(self.sm),
+                "reason_frac": {k: round(v / len(self.sm), 3) for k, v in sorted(self.reason_count.items())}}
+
+    def power_capped(self):
+        """True when sw_power_cap held for most of the region: the kernels then ran at the clocks
+        the sustained peak was measured at, so that is the roofline denominator; else the burst."""
+        return bool(self.sm) and self.reason_count.get("sw_power_cap", 0) > 0.5 * len(self.sm)
 
 
 # ------------------------------------------------------------------ workload setup
@@ -259,6 +267,149 @@ def verify_step_graph(lane, wl, slots, ks, drafts, seed, out, par_d, dev, n):
             "what": "CUDA graph replay of sv_verify + sv_commit, drafting excluded (SURVEY.md §8(d))"}
 
 
+def kernels_from(prof):
+    tot = max(1e-9, sum(v[0] for v in prof.values()))
+    return {name: dict(ms_per_launch=ms / n, launches=n, share=ms / tot) for name, (ms, n) in prof.items() if n}
+
+
+def roofline(kern, alg, pk, capped, traffic=None):
+    """Roofline of the two dominant kernels: achieved = algorithmic work per launch / measured launch
+    time. The peak follows the clock record of the region: the sustained bf16 peak when sw_power_cap
+    held for most of it (the regime that peak was measured in), else the burst peak; both fractions
+    are printed. HBM has one measured peak (copy bandwidth)."""
+    traffic = traffic or {}
+    lm, at = kern.get("lm_head"), kern.get("attention")
+    roof = {}
+    if lm:
+        ach = alg["lm_flops"] / (lm["ms_per_launch"] * 1e-3) / 1e12
+        peak = pk["bf16_sus"] if capped else pk["bf16"]
+        roof["lm_head"] = {"bound": "tensor", "achieved": round(ach, 2), "peak": peak, "unit": "TFLOP/s",
+                           "frac": round(ach / peak, 4), "peak_kind": "sustained" if capped else "burst",
+                           "frac_burst": round(ach / pk["bf16"], 4), "frac_sustained": round(ach / pk["bf16_sus"], 4),
+                           "traffic": traffic.get("lm_head", {}).get("bytes"),
+                           "traffic_src": traffic.get("lm_head", {}).get("src"),
+                           "flops_per_launch": alg["lm_flops"], "us_per_launch": round(lm["ms_per_launch"] * 1e3, 2)}
+    if at:
+        ach = alg["attn_bytes"] / (at["ms_per_launch"] * 1e-3) / 1e9
+        roof["attention"] = {"bound": "hbm", "achieved": round(ach, 1), "peak": pk["hbm"], "unit": "GB/s",
+                             "frac": round(ach / pk["hbm"], 4), "frac_of_8tbs": round(ach / 8000.0, 4),
+                             "traffic": traffic.get("attention", {}).get("bytes"), "bytes_per_launch": alg["attn_bytes"],
+                             "traffic_src": traffic.get("attention", {}).get("src"),
+                             "us_per_launch": round(at["ms_per_launch"] * 1e3, 2)}
+    return roof
+
+
+STEADY_MAX_STEPS = 2000      # steady-state phase: >= --steady-s seconds of steps, at most this many
+
+
+def steady_cap(wl):
+    return STEADY_MAX_STEPS if wl.cfg.n_layers == 1 else 100
+
+
+def steady_state(args, wl, lane, depths, ms_step, pk, dev, stream):
+    """Steady-state phase right after the timed region (VERDICT r1 "make the roofline line honest"):
+    >= args.steady_s seconds of steps, the timed region's depths and drafter inputs replayed in order,
+    each step committing ONE token per request (n_keep = 1) so contexts grow by one token per step
+    instead of a+1 (the algorithmic bytes use the measured lengths). Reports ms/step, the two
+    roofline kernels' µs and fractions and the clocks of this phase."""
+    if args.steady_s <= 0 or args.steps < 1:
+        return None
+    cfg, B = wl.cfg, wl.batch
+    n = int(min(steady_cap(wl), max(10, args.steady_s * 1e3 / max(ms_step, 1e-3))))
+    keep1 = torch.ones(B, dtype=torch.int32, device=dev)
+    slots = list(range(B))
+    masks_d, devtok_d = args._masks_d, args._devtok_d
+    succ_d, drafts, out, par_d = args._succ_d, args._drafts, args._out, args._par_d
+    ln0 = lane.tap("len", torch.int32, (cfg.max_slots,))[:B].cpu().tolist()
+    lane.profile(["lm_head", "attention"])
+    lane.profile_read(reset=True)
+    lane.stats(reset=True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize(dev)
+    with Clocks(dev.index) as clk:
+        e0.record(stream)
+        for i in range(n):
+            j = args.warmup + i % args.steps
+            draft_and_verify(lane, wl, slots, depths[j], succ_d, masks_d[j], devtok_d[j], drafts, 777 + i, out, par_d)
+            lane.commit(keep1)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1)
+    prof = lane.profile_read(reset=True)
+    lane.profile(False)
+    st = lane.stats(reset=True)
+    ln1 = lane.tap("len", torch.int32, (cfg.max_slots,))[:B].cpu().tolist()
+    mid = [(x + y) / 2.0 for x, y in zip(ln0, ln1)]
+    algs = [algorithmic(wl, mid, depths[args.warmup + i % args.steps]) for i in range(n)]
+    alg = {k: sum(a[k] for a in algs) / len(algs) for k in algs[0]}
+    kk = kernels_from(prof)
+    roof = roofline(kk, alg, pk, clk.power_capped())
+    return {"steps": n, "seconds": round(ms * 1e-3, 3), "ms_per_step": round(ms / n, 4),
+            "verified_rows_per_s": round(st["rows"] / (ms * 1e-3), 1),
+            "kernels": {k: {x: v[x] for x in ("us_per_launch", "achieved", "unit", "frac", "peak", "peak_kind",
+                                              "frac_burst", "frac_sustained", "frac_of_8tbs") if x in v}
+                        for k, v in roof.items()},
+            "ctx_mean": [round(sum(ln0) / B, 1), round(sum(ln1) / B, 1)], "clocks": clk.summary(),
+            "what": "steps right after the timed region, n_keep = 1 (context +1 token/step), same depths/drafter"}
+
+
+def decision_check(wl, lane, reqs, succ, masks, devtok, depths, start, dev):
+    """Teacher-forced decision parity at the bench's own configuration:
+    one more verify with logits_out; the oracle's decision rule (oracle/verify.py) is run on the GPU's
+    fp32 logits for EVERY request and the decisions are compared. Sampled-mode mismatches are
+    counted as borderline when |u - p/q| < 1e-5 or the race's top-2 scores are within 1e-5 relative
+    (north_star: "those borderline flips are counted and reported"); any other mismatch is an error."""
+    from oracle import verify as ov
+    from oracle.philox import uniform_accept
+    if wl.tree:
+        return {"skipped": "token-tree workload (tree decisions are checked in tests/test_gpu_tree*.py)"}
+    cfg, B = wl.cfg, wl.batch
+    ks = depths[start - 1]
+    T = sum(k + 1 for k in ks)
+    lg = torch.empty(T, cfg.vocab, dtype=torch.float32, device=dev)
+    drafts = torch.empty(max(1, B * wl.kmax), dtype=torch.int32, device=dev)
+    acc = torch.empty(B, dtype=torch.int32, device=dev)
+    tok = torch.empty(B, cfg.max_depth + 1, dtype=torch.int32, device=dev)
+    ln = lane.tap("len", torch.int32, (cfg.max_slots,))[:B].cpu().tolist()
+    slots = list(range(B))
+    lane.draft_planted(slots, ks, succ.to(dev), masks[start - 1].to(dev), devtok[start - 1].to(dev), drafts)
+    seed = 31337
+    lane.verify(slots, ks, drafts, None, seed=seed, mode=wl.mode, temperature=wl.temperature, logits_out=lg,
+                out=(acc, tok))
+    torch.cuda.synchronize(dev)
+    lane.commit()
+    L = lg.cpu().numpy().astype(np.float64)
+    a_g, t_g, d_h = acc.cpu().numpy(), tok.cpu().numpy(), drafts.cpu().numpy()
+    mode = ov.GREEDY if wl.mode == "greedy" else ov.SAMPLE
+    mism = border = 0
+    r0 = off = 0
+    t0 = time.perf_counter()
+    for b in range(B):
+        k = ks[b]
+        rows = L[r0:r0 + k + 1]
+        dr = [int(x) for x in d_h[off:off + k]]
+        rid = reqs[b]["rid"]
+        r = ov.verify_request(rows, dr, None, seed, rid, ln[b], mode, wl.temperature, wl.top_k, wl.top_p)
+        if int(a_g[b]) != r["a"] or list(t_g[b][:r["a"] + 1]) != r["emitted"]:
+            bl = False
+            if mode == ov.SAMPLE:
+                p = ov.filtered_probs(rows, wl.temperature, wl.top_k, wl.top_p)
+                bl = any(abs(uniform_accept(seed, rid, ln[b] + j) - p[j - 1][dr[j - 1]]) < 1e-5
+                         for j in range(1, k + 1))
+                a = r["a"]
+                sc = ov.race_scores(rows[a], None, dr[a] if a < k else -1, seed, rid, ln[b] + a + 1, wl.temperature,
+                                    a < k, wl.top_k, wl.top_p)
+                top2 = np.sort(sc[np.isfinite(sc)])[-2:]
+                bl = bl or (len(top2) == 2 and top2[1] - top2[0] <= 1e-5 * abs(top2[1]))
+            border += int(bl)
+            mism += int(not bl)
+        r0 += k + 1
+        off += k
+    return {"requests": B, "rows": T, "mismatches": mism, "borderline_flips": border,
+            "oracle_seconds": round(time.perf_counter() - t0, 2),
+            "what": "oracle decision rule on the GPU's fp32 logits of one extra verify, every request (S12/S13)"}
+
+
 def _run_gpu(args, wl, rank, world, dev, stream):
     from paper_2604_09562_b200 import sv
     import torch.distributed as dist
@@ -280,6 +431,8 @@ def _run_gpu(args, wl, rank, world, dev, stream):
     tok = torch.empty(B, cfg.max_depth + 1, dtype=torch.int32, device=dev)
     slots = list(range(B))
     par_d = tree_parents(wl, dev)
+    args._masks_d, args._devtok_d, args._succ_d, args._drafts, args._out, args._par_d = \
+        masks_d, devtok_d, succ_d, drafts, (acc, tok), par_d
 
     def step(i):
         if ctl:
@@ -328,34 +481,20 @@ def _run_gpu(args, wl, rank, world, dev, stream):
     # ----- roofline of the dominant kernels (live CUDA-event durations, averaged per launch)
     pk = peaks()
     traffic = ncu_traffic() if wl.name == "ns" else {}      # the committed capture is of the ns workload
+    capped = clk.power_capped()
     # per-launch algorithmic work averaged over the timed region: mean T over its steps, context
     # lengths at the region's midpoint (they grow by the emitted tokens)
     ln1 = lane.tap("len", torch.int32, (cfg.max_slots,))[:B].cpu().tolist()
     mid = [(x + y) / 2.0 for x, y in zip(ln, ln1)]
     algs = [algorithmic(wl, mid, depths[args.warmup + i]) for i in range(args.steps)]
     alg = {k: sum(a[k] for a in algs) / len(algs) for k in algs[0]}
-    kern = {}
-    for name, (ms, n) in prof.items():
-        if n:
-            kern[name] = dict(ms_per_launch=ms / n, launches=n, share=ms / max(1e-9, sum(v[0] for v in prof.values())))
-    lm = kern.get("lm_head")
-    at = kern.get("attention")
-    roof = {}
-    if lm:
-        ach = alg["lm_flops"] / (lm["ms_per_launch"] * 1e-3) / 1e12
-        roof["lm_head"] = {"bound": "tensor", "achieved": round(ach, 2), "peak": pk["bf16_sus"], "unit": "TFLOP/s",
-                           "frac": round(ach / pk["bf16_sus"], 4), "traffic": traffic.get("lm_head", {}).get("bytes"),
-                           "traffic_src": traffic.get("lm_head", {}).get("src"),
-                           "flops_per_launch": alg["lm_flops"], "us_per_launch": round(lm["ms_per_launch"] * 1e3, 2)}
-    if at:
-        ach = alg["attn_bytes"] / (at["ms_per_launch"] * 1e-3) / 1e9
-        roof["attention"] = {"bound": "hbm", "achieved": round(ach, 1), "peak": pk["hbm"], "unit": "GB/s",
-                             "frac": round(ach / pk["hbm"], 4), "frac_of_8tbs": round(ach / 8000.0, 4),
-                             "traffic": traffic.get("attention", {}).get("bytes"), "bytes_per_launch": alg["attn_bytes"],
-                             "traffic_src": traffic.get("attention", {}).get("src"),
-                             "us_per_launch": round(at["ms_per_launch"] * 1e3, 2)}
+    kern = kernels_from(prof)
+    roof = roofline(kern, alg, pk, capped, traffic)
     dominant = max(kern.items(), key=lambda kv: kv[1]["ms_per_launch"] * kv[1]["launches"])[0] if kern else None
     vg_depths = depths[total - 1]
+    # verify-step µs as SURVEY.md §8(d) defines it, right after the timed region (same power state)
+    vgraph = verify_step_graph(lane, wl, slots, vg_depths, drafts, 4321, (acc, tok), par_d, dev, VERIFY_GRAPH_REPLAYS)
+    steady = steady_state(args, wl, lane, depths, elapsed_ms / args.steps, pk, dev, stream)
     # ----- e2e through host buffers: pinned H2D inputs and D2H results every step (see run_e2e)
     e2e = e2e_host = None
     if ctl:                                           # later regions draft at the controller's last depth
@@ -366,9 +505,9 @@ def _run_gpu(args, wl, rank, world, dev, stream):
         if not wl.tree:                               # the host drafter variant drafts chains only
             e2e_host = run_e2e_host_drafter(args, wl, lane, succ, depths, masks, devtok, dev,
                                             total + args.e2e_steps, HOST_DRAFTER_STEPS)
-    # verify-step µs as SURVEY.md §8(d) defines it, after the e2e runs (its replays commit tokens too)
-    vgraph = verify_step_graph(lane, wl, slots, vg_depths, drafts, 4321, (acc, tok), par_d, dev, VERIFY_GRAPH_REPLAYS)
-    return dict(elapsed_ms=elapsed_ms, tokens=tokens, per_step=per_step, prof=kern, roof=roof, dominant=dominant,
+    check = decision_check(wl, lane, reqs, succ, masks, devtok, depths, total + args.e2e_steps + HOST_DRAFTER_STEPS,
+                           dev) if args.check_steps > 0 else None
+    return dict(check=check, steady=steady, elapsed_ms=elapsed_ms, tokens=tokens, per_step=per_step, prof=kern, roof=roof, dominant=dominant,
                 launches=launches, clocks=clk.summary(), stats=st, e2e=e2e, e2e_host=e2e_host, w=w, succ=succ, reqs=reqs,
                 depths=depths, masks=masks, devtok=devtok, alg=alg, verify_graph=vgraph,
                 controller=({"window_steps": ControlledDepths.WINDOW, "final_depth": ctl.d, "trace": ctl.trace[-6:]}
@@ -622,13 +761,40 @@ def cpu_baseline(wl, res, budget_s=20.0):
             "seconds": round(secs, 2), "tokens": tokens}
 
 
+def cpu_baseline_1thread(wl, res, budget_s=8.0):
+    """The same oracle sample with the BLAS pool limited to one thread."""
+    try:
+        from threadpoolctl import threadpool_limits
+    except Exception:
+        return None
+    with threadpool_limits(limits=1):
+        lane = oracle_lane_for(wl, res["w"], res["reqs"], 1)
+        tokens, secs, steps = 0, 0.0, 0
+        while secs < budget_s and steps < 2:
+            t, s_ = oracle_steps(wl, lane, 1, res["succ"], res["depths"], res["masks"], res["devtok"], [steps])
+            tokens, secs, steps = tokens + t, secs + s_, steps + 1
+    return {"value": round(tokens / secs, 3), "unit": UNIT, "cores": 1, "steps": steps, "seconds": round(secs, 2)}
+
+
+def l2_note(wl):
+    c = wl.cfg
+    w = 2 * (c.vocab * c.d_model + c.n_layers * (c.qkv_rows * c.d_model + c.d_model * c.n_q_heads * c.head_dim
+                                                   + 3 * c.ffn_dim * c.d_model))
+    kv = wl.batch * (sum(wl.ctx) / 2) * c.n_layers * 2 * c.n_kv_heads * c.head_dim * 2
+    if w + kv < 126e6:
+        return (f"inputs fit the 126 MB L2 ({(w + kv) / 1e6:.1f} MB; launch-bound toy config, L2 not flushed: "
+                "not the headline workload)")
+    return (f"no flush: every step streams {w / 1e9:.2f} GB of weights + {kv / 1e9:.2f} GB of KV, "
+            f"> the 126 MB L2")
+
+
 def bench_config(wl, world):
     """The workload description both arms report (the driver pairs lines by it)."""
     nl = wl.cfg.n_layers
     return {"workload": wl.name, "model": f"Llama-3-8B-shaped {nl} layer{'s' if nl > 1 else ''} + lm-head (random init, "
             "planted successor)" if wl.cfg.d_model == 4096 else "toy", "batch_per_gpu": wl.batch, "depth": [wl.kmin, wl.kmax],
             "ctx": list(wl.ctx), "mode": wl.mode, "parallelism": f"dp{world} (independent decode lanes)",
-            "l2": "inputs > L2 (weights >= 1.5 GB + KV >= 1 GB per step)", "drafter": f"planted alpha={wl.alpha}",
+            "l2": l2_note(wl), "drafter": f"planted alpha={wl.alpha}",
             **({"tree_parents": list(wl.tree)} if wl.tree else {}),
             **({"top_k": wl.top_k, "top_p": wl.top_p} if (wl.top_k or wl.top_p < 1.0) else {})}
 
@@ -684,13 +850,17 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--detail", action="store_true", help="add per-stage breakdown to the JSON line")
     ap.add_argument("--graph", action="store_true", help="replay the step as a CUDA graph (fixed depths)")
+    ap.add_argument("--steady-s", type=float, default=1.0, help="seconds of steady-state steps after the timed region")
+    ap.add_argument("--check-steps", type=int, default=1, help="teacher-forced decision check after the runs (0 = off)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    wl0 = synth.workload(args.workload)
+    steady_budget = (steady_cap(wl0) + wl0.kmin) // (wl0.kmin + 1) + 1 if args.steady_s > 0 else 0
     wl = synth.workload(args.workload, steps_budget=args.warmup + args.steps + args.e2e_steps + HOST_DRAFTER_STEPS
-                        + VERIFY_GRAPH_REPLAYS + 9)
+                        + VERIFY_GRAPH_REPLAYS + steady_budget + args.check_steps + 9)
 
     if args.impl == "reference":
         if rank == 0:
@@ -737,8 +907,14 @@ def main():
         "verify_step_us_graph": res.get("verify_graph"),
         "acceptance": {"a_t": round(st["accepted"] / max(1, st["drafted"]), 4),
                        "tokens_per_request_step": round(st["emitted"] / max(1, args.steps * wl.batch), 3)},
-        "roofline": {k: v for k, v in roof.items() if k in ("bound", "achieved", "peak", "unit", "frac", "traffic")}
+        "roofline": {k: v for k, v in roof.items() if k in ("bound", "achieved", "peak", "unit", "frac", "traffic",
+                                                            "peak_kind", "frac_burst", "frac_sustained")}
         | {"kernel": dom},
+        "steady_state": res.get("steady"),
+        "decision_check": res.get("check"),
+        "device": {"l2_bytes": torch.cuda.get_device_properties(dev).L2_cache_size,
+                   "sms": torch.cuda.get_device_properties(dev).multi_processor_count,
+                   "name": torch.cuda.get_device_name(dev)},
         "kernels": res["roof"],
         "gpu_launches": res["launches"],
         "launches_per_step": round(res["launches"] / args.steps, 2),
@@ -756,6 +932,7 @@ def main():
                           for k, v in res["prof"].items()}
     if world == 1 and not args.no_cpu_baseline and not wl.gen_on_device:
         line["cpu_baseline"] = cpu_baseline(wl, res)
+        line["cpu_baseline"]["one_thread"] = cpu_baseline_1thread(wl, res)
     print(json.dumps(line, default=_json_default), flush=True)
     if world > 1:
         dist.destroy_process_group()

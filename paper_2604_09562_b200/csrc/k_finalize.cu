@@ -486,6 +486,7 @@ __device__ void tree_walk(const LaneDev& d, const int* __restrict__ drafts, cons
   }
   __syncthreads();
   k = s_cand;
+  __syncthreads();                                   // every thread has read s_cand before thread 0 reuses it
   if (mode == SV_GREEDY) {
     if (tid == 0) {
       int cur = 0, a = 0;

@@ -59,7 +59,19 @@ def _logits_with_ties(T, V, rng):
 @pytest.mark.parametrize("top_k,top_p", [(5, 1.0), (0, 0.9), (40, 0.7), (3, 0.95), (1, 1.0), (0, 0.3)])
 @pytest.mark.parametrize("dense", [True, False])
 def test_filtered_chain_decisions_on_exact_logits(top_k, top_p, dense):
-    cfg = synth.TOY.with_(max_batch=16, max_slots=16)
+    _filtered_chain_case(top_k, top_p, dense, synth.TOY.vocab)
+
+
+@pytest.mark.parametrize("top_k,top_p", [(5, 1.0), (0, 0.9), (40, 0.7)])
+@pytest.mark.parametrize("dense", [True, False])
+def test_filtered_chain_decisions_odd_vocab(top_k, top_p, dense):
+    """V % 4 != 0 (GPT-2-like odd vocabularies): the filter's scalar row pass and the race's
+    scalar loads (the float4 paths need V % 4 == 0) against the oracle."""
+    _filtered_chain_case(top_k, top_p, dense, 509)
+
+
+def _filtered_chain_case(top_k, top_p, dense, vocab):
+    cfg = synth.TOY.with_(max_batch=16, max_slots=16, vocab=vocab)
     S = Setup(cfg, [10 + 9 * i for i in range(16)], seed=1)
     S.lane.set_filter(top_k, top_p)
     rng = np.random.default_rng(top_k * 7 + int(100 * top_p) + dense)
@@ -208,3 +220,32 @@ def test_full_model_sampled_verify_with_filter():
         S.lane.set_filter(-1, 0.5)
     with pytest.raises(Exception):
         S.lane.set_filter(3, 0.0)
+
+
+@pytest.mark.parametrize("filt", [(0, 1.0), (30, 0.85)])
+def test_full_model_sampled_verify_odd_vocab(filt):
+    """Toy+mlp lane with V = 509 (ragged last vocab tile, V % 4 != 0): lm-head logits within the
+    north_star tolerance of the fp64 product of the GPU's z, and sampled decisions (dense q, with and
+    without a filter) teacher-forced on the GPU logits."""
+    from oracle import model
+    cfg = synth.TOY_MLP.with_(vocab=509)
+    S = Setup(cfg, [128, 40, 300, 7], seed=18)
+    S.lane.set_filter(*filt)
+    depths = [4, 0, 8, 2]
+    drafts = synth.random_tokens(sum(depths), cfg.vocab, seed=19)
+    probs = synth.draft_probs_dense(sum(depths), cfg.vocab, seed=20)
+    T = sum(depths) + 4
+    lg = torch.empty(T, cfg.vocab, device="cuda")
+    acc, tok = S.lane.verify([0, 1, 2, 3], depths, drafts.cuda(), probs.cuda(), seed=21, mode="sample",
+                             temperature=0.9, logits_out=lg)
+    torch.cuda.synchronize()
+    z = S.tap("z", torch.bfloat16, (T, cfg.d_model))
+    ref = model.lm_head(f64(z), S.wnp["lm_head"])
+    err = np.abs(f64(lg) - ref).max(axis=1) / np.maximum(1.0, np.abs(ref).max(axis=1))
+    assert err.max() <= 2e-3, err.max()
+    res = _chain_decisions(S, [0, 1, 2, 3], depths, drafts, probs, f64(lg), 21, 0.9, *filt)
+    acc, tok = acc.cpu().numpy(), tok.cpu().numpy()
+    for b, r in enumerate(res):
+        if not (acc[b] == r["a"] and list(tok[b][: r["a"] + 1]) == r["emitted"]):
+            assert r["borderline"], (b, acc[b], tok[b], r)
+    S.lane.commit()

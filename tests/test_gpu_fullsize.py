@@ -17,7 +17,7 @@ import synth
 from oracle import model, verify
 
 from gpu_util import f64
-from test_gpu_parity import LOGIT_REL, RESID_REL, attention_tolerance
+from test_gpu_parity import ATTN_REL, LOGIT_REL, RESID_REL, attention_tolerance, survey_attention_error
 
 pytestmark = pytest.mark.gpu
 
@@ -56,7 +56,7 @@ def step():
 def test_attention_sampled_requests(step):
     s, cfg = step, step["cfg"]
     R = s["wl"].kmax + 1
-    worst = 0.0
+    worst, worst_survey = 0.0, 0.0
     for b in (0, 21, 42, 63):
         r0 = b * R
         q = f64(s["q"][r0:r0 + R])
@@ -65,9 +65,12 @@ def test_attention_sampled_requests(step):
         kc, vc = f64(s["kc"][r0:r0 + R]), f64(s["vc"][r0:r0 + R])
         ref = model.verify_attention(q, ck, cv, kc, vc).reshape(R, cfg.n_q_heads, cfg.head_dim)
         g = f64(s["o"][r0:r0 + R]).reshape(R, cfg.n_q_heads, cfg.head_dim)
-        tol = attention_tolerance(q, ck, cv, kc, vc)
+        tol, exact = attention_tolerance(q, ck, cv, kc, vc, with_exact=True)
         worst = max(worst, float((np.abs(g - ref) / tol).max()))
+        worst_survey = max(worst_survey, survey_attention_error(g, exact))
+    print("ns attention: max err / derived tol", worst, "survey criterion (x rms)", worst_survey)
     assert worst <= 1.0, worst
+    assert worst_survey <= ATTN_REL, worst_survey
 
 
 def test_residual_and_logits_sampled_rows(step):
@@ -106,3 +109,33 @@ def test_greedy_decisions_all_requests_bit_exact(step):
         assert 0 <= a <= K and list(s["tok"][b][:a]) == dr[:a]
     # the planted drafter makes acceptance realistic at this size
     assert 0.2 < s["acc"].mean() / K < 0.8
+
+
+def test_greedy_decisions_all_rows_on_fp64_logits_from_gpu_z(step):
+    """the oracle recomputes every row's logits in fp64 from the GPU's bf16 z
+    (all 576 rows x 128256), takes the lowest-index argmax and runs the accept scan. A decision
+    may differ from the GPU's only on a row whose oracle top-2 gap is below 2 * max|l_gpu - l_oracle|
+    of that row (the excuse rule); such rows are counted and must be rare."""
+    s, cfg, W = step, step["cfg"], step["w"]
+    K, T = s["wl"].kmax, s["T"]
+    z = f64(s["z"])
+    ref = model.lm_head(z, W["lm_head"].float().numpy())             # [576, 128256] fp64
+    lg = s["logits"].numpy().astype(np.float64)
+    row_err = np.abs(lg - ref).max(axis=1)
+    srt = np.sort(ref, axis=1)
+    gap = srt[:, -1] - srt[:, -2]
+    near_tie = gap < 2.0 * row_err
+    excused = 0
+    for b in range(64):
+        c = s["reqs"][b]
+        rows = slice(b * (K + 1), (b + 1) * (K + 1))
+        dr = [int(t) for t in s["drafts"][b * K:(b + 1) * K]]
+        r = verify.verify_request(ref[rows], dr, None, 1234, c["rid"], c["L"], verify.GREEDY, 1.0)
+        a = int(s["acc"][b])
+        if a != r["a"] or list(s["tok"][b][:a + 1]) != r["emitted"]:
+            # excused only if a row the two decisions depend on is a near tie
+            assert near_tie[rows][:min(a, r["a"]) + 1].any(), (b, a, r["a"], gap[rows], row_err[rows])
+            excused += 1
+    print("ns greedy on fp64 logits: excused", excused, "near-tie rows", int(near_tie.sum()),
+          "max row err", float(row_err.max()), "min gap", float(gap.min()))
+    assert excused <= 1

@@ -80,7 +80,7 @@ def run_and_check(S, slots, depths, drafts, mode, seed=1234, temperature=1.0, pr
     # a3: attention, fed the GPU's q and chain k/v
     go = S.tap("o", torch.bfloat16, (T, Hq * dh))
     if check_attention:
-        worst, worst_sig = 0.0, 0.0
+        worst, worst_sig, worst_survey = 0.0, 0.0, 0.0
         r0 = 0
         for s, kk in zip(slots, depths):
             c = S.ctx[s]
@@ -92,11 +92,13 @@ def run_and_check(S, slots, depths, drafts, mode, seed=1234, temperature=1.0, pr
             err = np.abs(g - ref)
             rms = np.sqrt((ref ** 2).mean(axis=2))
             worst = max(worst, float((err.max(axis=2) / np.maximum(rms, 1e-30)).max()))
-            tol = attention_tolerance(q_, ck, cv, kc_, vc_)
+            tol, exact = attention_tolerance(q_, ck, cv, kc_, vc_, with_exact=True)
             worst_sig = max(worst_sig, float((err / tol).max()))
+            worst_survey = max(worst_survey, survey_attention_error(g, exact))
             r0 += R
-        report["o"] = dict(max_rel=worst, max_err_over_tol=worst_sig)
+        report["o"] = dict(max_rel=worst, max_err_over_tol=worst_sig, survey_rel=worst_survey)
         assert worst_sig <= 1.0, (worst_sig, worst)
+        assert worst_survey <= ATTN_REL, worst_survey
     # a4: O-proj + residual, MLP
     h1 = S.tap("h1", torch.float32, (T, D))
     ref_h1 = model.attn_out(f64(h0), f64(go), W["wo"][0])
@@ -140,7 +142,19 @@ def run_and_check(S, slots, depths, drafts, mode, seed=1234, temperature=1.0, pr
     return report, acc, tok
 
 
-def attention_tolerance(q, ck, cv, kc, vc):
+def survey_attention_error(g, exact):
+    """SURVEY.md §8(c) a3 criterion, max|dO| <= 1e-2 rms(O_ref) per (row, head), measured against
+    the UNROUNDED fp64 output with the GPU's own final bf16 rounding (<= 1/2 ulp of its output)
+    taken out (reading R32): an element of 2.5 rms sits where one bf16 ulp is 1.6e-2 rms,
+    so comparing two independently rounded outputs would fail the criterion on a single rounding
+    flip that neither side can avoid. Returns max over (row, head) of that error / rms."""
+    half_ulp = np.ldexp(1.0, np.frexp(np.abs(g))[1] - 9)          # bf16: 8 significant bits
+    e = np.maximum(np.abs(g - exact) - half_ulp, 0.0)
+    rms = np.sqrt((exact ** 2).mean(axis=2))
+    return float((e.max(axis=2) / np.maximum(rms, 1e-30)).max())
+
+
+def attention_tolerance(q, ck, cv, kc, vc, with_exact=False):
     """Per-element tolerance of the GPU attention output (a3).
 
     The GPU rounds the softmax weights P to bf16 (8 significant bits) before the P.V
@@ -154,6 +168,7 @@ def attention_tolerance(q, ck, cv, kc, vc):
     G = Hq // Hkv
     L = ck.shape[0]
     tol = np.zeros((R, Hq, dh))
+    exact = np.zeros((R, Hq, dh))
     for j in range(R):
         keys = np.concatenate([ck[:L], kc[: j + 1]])
         vals = np.concatenate([cv[:L], vc[: j + 1]])
@@ -163,7 +178,8 @@ def attention_tolerance(q, ck, cv, kc, vc):
             o = w @ v
             sig = 2.0 ** -8 / np.sqrt(3.0) * np.sqrt((w[:, None] ** 2 * (v - o[None]) ** 2).sum(axis=0))
             tol[j, hq] = 6 * sig + 2.0 ** -7 * np.abs(o) + 1e-6 * np.abs(v).max()
-    return tol
+            exact[j, hq] = o
+    return (tol, exact) if with_exact else tol
 
 
 def _cmp_resid(name, g, ref, report):
