@@ -579,6 +579,144 @@ def run_graph(args, wl, rank, world, dev):
                 depths=depths, masks=masks, devtok=devtok, alg=None, controller=None, graph=True)
 
 
+DISAGG_STEPS_PER_ROUND = 8   # decode steps per hand-off batch (the transfer of the next batch overlaps them)
+
+
+def run_disagg(args, wl, rank, world, dev):
+    """--disagg (BASELINE configs[3], SURVEY.md §8(e) exchange 1): prefill -> decode stream pairs
+    (2p, 2p+1). The prefill lane holds `batch` requests of synthetic context KV (the producer; real
+    chunked prefill is NEXT-3) and, every DISAGG_STEPS_PER_ROUND decode steps, hands the batch to
+    its decode lane with sv_kv_send_slots / sv_kv_recv_slots (one NCCL group of page blocks, zero
+    copy, on the lanes' comm streams). The decode lane double-buffers: it verifies one set of
+    `batch` slots while the next set is received into the other half, then releases the old set.
+    world == 1 runs both lanes on one GPU with sv_kv_loopback_slots (the flow, not NVLink).
+    value = decode-lane accepted tokens/s over the region (hand-off interference included);
+    handoff = bytes per batch and the comm-stream time of each transfer."""
+    from paper_2604_09562_b200 import sv
+    import torch.distributed as dist
+    role, peer, pair = svdist.disagg_role(rank, world)
+    cfg0, B = wl.cfg, wl.batch
+    rounds = max(2, args.steps // DISAGG_STEPS_PER_ROUND)
+    n_tok = wl.ctx[1]
+    growth = (args.warmup + rounds * DISAGG_STEPS_PER_ROUND + 4) * (wl.kmax + 1)
+    per_req = (n_tok + growth + 63) // 64 + 1
+    dcfg = cfg0.with_(max_slots=2 * B, n_pages=2 * B * per_req + B, max_pos=n_tok + growth + 64)
+    pcfg = cfg0.with_(max_slots=B, n_pages=B * ((n_tok + 63) // 64 + 1), max_pos=n_tok + 64)
+    stream = torch.cuda.Stream(dev)
+    uid = sv.nccl_unique_id() if rank == 0 else None
+    if world > 1:
+        uid = svdist.broadcast_bytes(uid, 0, 128, device=dev)
+    comm = sv.nccl_comm_init(world, uid, rank)
+    w, succ = planted_weights(wl, dev if wl.gen_on_device else "cpu")
+    wd = {k: v.to(dev) for k, v in w.items()}
+    res = {}
+    with torch.cuda.stream(stream):
+        pre = dec = None
+        if role in ("prefill", "both"):
+            pre = sv.Lane(pcfg, wd, stream=stream)
+            for i in range(B):
+                k, v = synth.context_kv(pcfg, n_tok, seed=30_000 * (pair + 1) + i, device=dev)
+                pend = int(synth.random_tokens(1, pcfg.vocab, seed=40_000 * (pair + 1) + i)[0])
+                pre.append_kv(i, svdist.request_id(rank, 10**6 + i), k, v, pend)
+        if role in ("decode", "both"):
+            dec = sv.Lane(dcfg, wd, stream=stream)
+        torch.cuda.synchronize(dev)
+        prank = rank if role == "both" else (rank if role == "prefill" else peer)
+
+
+        nbytes = (pre or dec).slots_bytes([n_tok] * B)
+        st_send = torch.empty(nbytes, dtype=torch.uint8, device=dev) if pre is not None else None
+        st_recv = torch.empty(nbytes, dtype=torch.uint8, device=dev) if dec is not None else None
+
+        def handoff(r):
+            src, dst, rids = svdist.handoff_batch(r, B, prank)
+            if role == "both":
+                pre.kv_loopback_slots(dec, src, dst, rids, [n_tok] * B, st_send, st_recv, 0, comm)
+            elif role == "prefill":
+                pre.kv_send_slots(src, [n_tok] * B, st_send, peer, comm)
+            else:
+                dec.kv_recv_slots(dst, rids, [n_tok] * B, st_recv, peer, comm)
+            return dst
+
+        hand_ev = []
+        if dec is not None:
+            cstream = dec.comm_stream()
+            total_steps = args.warmup + rounds * DISAGG_STEPS_PER_ROUND
+            depths = [[wl.kmax] * B for _ in range(total_steps)]
+            masks, devtok = synth.planted_masks(total_steps, B * wl.kmax, wl.alpha, cfg0.vocab, seed=9 + rank)
+            masks_d, devtok_d, succ_d = masks.to(dev), devtok.to(dev), succ.to(dev)
+            drafts = torch.empty(B * wl.kmax, dtype=torch.int32, device=dev)
+            acc = torch.empty(B, dtype=torch.int32, device=dev)
+            tok = torch.empty(B, cfg0.max_depth + 1, dtype=torch.int32, device=dev)
+        active = handoff(0)                                   # initial fill (untimed)
+        if dec is not None:
+            for i in range(args.warmup):
+                draft_and_verify(dec, wl, active, depths[i], succ_d, masks_d[i], devtok_d[i], drafts, 1234 + i,
+                                 (acc, tok))
+                dec.commit()
+        torch.cuda.synchronize(dev)
+        if dec is not None:
+            dec.stats(reset=True)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        launches0 = sv.launch_count()
+        with Clocks(dev.index) as clk:
+            e0.record(stream)
+            for r in range(1, rounds + 1):
+                if dec is not None:
+                    h0 = torch.cuda.Event(enable_timing=True)
+                    h0.record(cstream)
+                nxt = handoff(r) if r < rounds else None      # the next batch arrives while `active` decodes
+                if dec is not None:
+                    if nxt is not None:
+                        h1 = torch.cuda.Event(enable_timing=True)
+                        h1.record(cstream)
+                        hand_ev.append((h0, h1))
+                    for j in range(DISAGG_STEPS_PER_ROUND):
+                        i = args.warmup + (r - 1) * DISAGG_STEPS_PER_ROUND + j
+                        draft_and_verify(dec, wl, active, depths[i], succ_d, masks_d[i], devtok_d[i], drafts,
+                                         1234 + i, (acc, tok))
+                        dec.commit()
+                    if nxt is not None:
+                        for s_ in active:
+                            dec.release(s_)
+                        active = nxt
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+        launches = sv.launch_count() - launches0
+        if world > 1:
+            dist.barrier()
+        elapsed = e0.elapsed_time(e1)
+        dstats = dec.stats() if dec is not None else {"accepted": 0, "drafted": 0, "emitted": 0}
+        tokens = dstats["emitted"]
+        if dec is not None:
+            hms = sorted(a.elapsed_time(b) for a, b in hand_ev)
+            res["handoff"] = {"batches": len(hms), "bytes_per_batch": nbytes,
+                              "ms_median": round(statistics.median(hms), 3) if hms else None,
+                              "gbs_median": round(nbytes / (statistics.median(hms) * 1e-3) / 1e9, 1) if hms else None,
+                              "blocks_per_batch": B * ((n_tok + 63) // 64) * cfg0.n_layers,
+                              "what": "comm-stream time: decode-side page pop + NCCL receive + block scatter "
+                                      "(+ the prefill-side gather in loopback)",
+                              "transport": "NCCL loopback on one GPU (flow check, not NVLink)" if role == "both"
+                                           else "NCCL p2p, one op per batch, page-block gather / scatter",
+                              "overlap": f"transfer on the comm stream while {DISAGG_STEPS_PER_ROUND} verify steps run"}
+    elapsed, tokens = svdist.reduce_region(elapsed, tokens, device=dev if world > 1 else None)
+    sv.nccl_comm_destroy(comm)
+    steps = rounds * DISAGG_STEPS_PER_ROUND
+    # handoff stats live on decode ranks: gather rank 1's to rank 0
+    if world > 1:
+        obj = [res.get("handoff")]
+        outs = [None] * world
+        dist.all_gather_object(outs, obj[0])
+        res["handoff"] = next((o for o in outs if o), None)
+    return dict(elapsed_ms=elapsed, tokens=tokens, per_step=[elapsed / steps] * steps, prof={}, roof={}, dominant=None,
+                launches=launches, clocks=clk.summary(), stats=dstats,
+                e2e=None, e2e_host=None, controller=None, handoff=res.get("handoff"), disagg=True, steps_run=steps,
+                decode_lanes=max(1, world // 2))
+
+
 def run_e2e(args, wl, lane, succ, depths, masks, devtok, dev, start):
     """End to end through the public API, inputs from pinned host memory, results read back
     every step. The drafter is the device one (`sv_draft_planted`); each step's drafter inputs
@@ -850,6 +988,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--detail", action="store_true", help="add per-stage breakdown to the JSON line")
     ap.add_argument("--graph", action="store_true", help="replay the step as a CUDA graph (fixed depths)")
+    ap.add_argument("--disagg", action="store_true",
+                    help="prefill -> decode pairs with the batched NCCL KV hand-off (configs[3]; world 1: loopback)")
     ap.add_argument("--steady-s", type=float, default=1.0, help="seconds of steady-state steps after the timed region")
     ap.add_argument("--check-steps", type=int, default=1, help="teacher-forced decision check after the runs (0 = off)")
     args = ap.parse_args()
@@ -879,9 +1019,9 @@ def main():
             dist.init_process_group("gloo")
         else:
             dist.init_process_group("nccl", device_id=dev)
-    res = (run_graph if args.graph else run_gpu)(args, wl, rank, world, dev)
+    res = (run_disagg if args.disagg else run_graph if args.graph else run_gpu)(args, wl, rank, world, dev)
     elapsed, tokens = res["elapsed_ms"], res["tokens"]
-    if world > 1:                                 # whole job: all ranks' tokens / the slowest rank's time
+    if world > 1 and not res.get("disagg"):       # whole job: all ranks' tokens / the slowest rank's time
         elapsed, tokens = svdist.reduce_region(elapsed, tokens, device=red_dev)
         if res["e2e"]:
             es, et = svdist.reduce_region(res["e2e"]["seconds"], res["e2e"]["tokens"], device=red_dev)
@@ -924,13 +1064,21 @@ def main():
         "controller": res.get("controller"),
         "peaks": peaks()["src"],
     }
+    if res.get("disagg"):
+        line["steps"] = res["steps_run"]
+        line["ms_per_step"] = round(elapsed / res["steps_run"], 4)
+        line["handoff"] = res["handoff"]
+        line["config"]["parallelism"] = (f"{max(1, world // 2)} prefill->decode pair(s)" if world > 1
+                                         else "prefill + decode lanes on one GPU (loopback)")
+        line["config"]["disagg"] = f"hand-off of {wl.batch} x {wl.ctx[1]}-token KV every {DISAGG_STEPS_PER_ROUND} steps"
+        line["scaling"] = "weak"
     if res.get("graph"):
         line["config"]["graph"] = "CUDA graph replay of drafter + verify + commit; depths fixed per request"
         line["config"]["depth"] = sorted(set(res["depths"][0]))
     if args.detail:
         line["stages"] = {k: {"us": round(v["ms_per_launch"] * 1e3, 1), "share": round(v["share"], 4)}
                           for k, v in res["prof"].items()}
-    if world == 1 and not args.no_cpu_baseline and not wl.gen_on_device:
+    if world == 1 and not args.no_cpu_baseline and not wl.gen_on_device and not res.get("disagg"):
         line["cpu_baseline"] = cpu_baseline(wl, res)
         line["cpu_baseline"]["one_thread"] = cpu_baseline_1thread(wl, res)
     print(json.dumps(line, default=_json_default), flush=True)

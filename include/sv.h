@@ -323,7 +323,9 @@ sv_status sv_kv_send(const void* kv_packed, int32_t n_layers, int32_t n_kv_heads
 /* Decode side: receive that message into the lane's staging buffer and append
  * it to `slot` (sv_append_kv semantics; the pending token comes from the
  * trailer on the device). staging: DEVICE buffer of at least
- * sv_kv_packed_bytes(cfg, n_tokens) bytes, owned by the caller. */
+ * sv_kv_packed_bytes(cfg, n_tokens) bytes, owned by the caller. The receive runs on the lane's comm
+ * stream (overlapping a verify already enqueued); the append copy waits for it on the lane stream.
+ * Host-checkable misuse is refused before the receive is posted. */
 sv_status sv_kv_recv_append(sv_ctx* ctx, int32_t slot, uint64_t request_id, int32_t n_tokens,
                             void* staging, int peer, void* nccl_comm);
 size_t sv_kv_packed_bytes(const sv_config* cfg, int32_t n_tokens);
@@ -356,6 +358,55 @@ sv_status sv_kv_append_packed(sv_ctx* ctx, int32_t slot, uint64_t request_id, in
  * with peer = own rank). nccl_comm: a communicator in which this process is `rank`. */
 sv_status sv_kv_loopback_append(sv_ctx* ctx, int32_t slot, uint64_t request_id, int32_t n_tokens,
                                 const void* kv_packed, void* staging, int rank, void* nccl_comm);
+
+/* ---- batched page-block hand-off (a9; PAPER.md:255-260 eq:transfer_bandwidth, Alg. 3
+ * "Transfer kv via NIXL P2P" PAPER.md:281-283 -> NCCL p2p over NVLink; SURVEY.md §8(e) "grouped per
+ * batch of requests" on a comm stream).
+ * Wire format of a batch of n requests (ONE ncclSend / ncclRecv), derived by both sides from the
+ * host-known token counts (the router knows every prompt length): for request i, for layer l, for
+ * page p < ceil(n_tokens[i] / page_size): the (layer, page) block of the KV pool, [2][H_kv][page_size]
+ * [d_h] bf16 = 2*H_kv*page_size*d_h*2 bytes (256 KB at Llama-3-8B shape); then the n pending tokens
+ * (int32), padded to 16 bytes. Size: sv_kv_slots_bytes. The prefill side gathers the blocks from its
+ * pages into `staging`, the decode side receives into its `staging` and scatters the blocks into
+ * freshly popped pages (whole-block copies). Rows of a last, partial page past n_tokens carry the
+ * sender's (finite) page contents and are masked by len.
+ * Everything runs on the lane's own comm stream (created at sv_create), so a verify already enqueued
+ * on the lane's stream overlaps the transfer; the lane's later calls that touch one of the
+ * transferred slots (verify, append, release, pack) make its stream wait for the transfer (an
+ * event). `staging`: caller-owned DEVICE memory, 16-byte aligned, >= sv_kv_slots_bytes, not reused
+ * until the transfer is done (the next hand-off call of the lane is ordered after it). The NCCL
+ * communicator must span the two lanes' ranks (sv_nccl_comm_init); a failure after the peer has
+ * posted its half leaves the communicator unusable (abort it). */
+size_t sv_kv_slots_bytes(const sv_config* cfg, int32_t n, const int32_t* n_tokens /*(host)[n]*/);
+
+/* Prefill side: send rows 0..n_tokens[i]-1 of ACTIVE slots[i] (n distinct slots, host arrays) plus
+ * their pending tokens to `peer`. Syncs the lane's stream once (reads the committed lengths); the
+ * gather and the send then run on the comm stream. The slots stay ACTIVE (sv_release of them waits
+ * for the transfer). EINVAL: n < 1, bad / duplicate slot, n_tokens[i] < 1 or > the slot's committed
+ * length, bad staging; ESTATE: a slot not ACTIVE, or capturing a graph. */
+sv_status sv_kv_send_slots(sv_ctx* ctx, int32_t n, const int32_t* slots, const int32_t* n_tokens, void* staging,
+                           int peer, void* nccl_comm);
+/* Decode side: the matching receive into EMPTY slots[i] (host), bound to request_ids[i] (the Philox
+ * key, as in sv_append_kv): on the comm stream, pops ceil(n_tokens[i] / page_size) pages per request
+ * (the device free list is lock-protected, so this runs concurrently with the lane's commits), sets
+ * len = n_tokens[i], receives the batch and scatters it. The host never waits for the lane stream (it
+ * syncs the comm stream once to check the free-page count). A slot released before is reused after
+ * its release kernel. The slots are ACTIVE on return; their first verify waits for the data.
+ * EINVAL: bad / duplicate slot, n_tokens[i] < 1 or >= max_pos, bad staging; ESTATE: a slot not
+ * EMPTY, or capturing; SV_ENOKV: fewer free pages than the batch needs (checked before anything is
+ * popped or posted). */
+sv_status sv_kv_recv_slots(sv_ctx* ctx, int32_t n, const int32_t* slots, const uint64_t* request_ids,
+                           const int32_t* n_tokens, void* staging, int peer, void* nccl_comm);
+/* Transport self-test on one GPU: sv_kv_send_slots from `src` and sv_kv_recv_slots into `dst`
+ * (two lanes with the same n_layers / H_kv / d_h / page_size) in ONE group of a communicator in
+ * which this process is `rank` (sends to itself), on dst's comm stream. */
+sv_status sv_kv_loopback_slots(sv_ctx* src, sv_ctx* dst, int32_t n, const int32_t* src_slots,
+                               const int32_t* dst_slots, const uint64_t* request_ids, const int32_t* n_tokens,
+                               void* src_staging, void* dst_staging, int rank, void* nccl_comm);
+
+/* Measurement hook: the lane's comm stream (hand-off transfers run there), so a caller can record
+ * CUDA events around them. */
+sv_status sv_comm_stream(sv_ctx* ctx, sv_stream_t* out);
 
 /* Pack context K/V [n_layers][n][H_kv][d_h] (two tensors) + pending into the
  * hand-off wire format on `stream` (used by the prefill side). */

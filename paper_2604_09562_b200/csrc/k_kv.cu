@@ -3,8 +3,10 @@
 //       0..n-1 of kc/vc -> pages at positions L..L+n-1, pages popped from the device free list
 //   a9  append (sv_append_kv / hand-off receive): context K/V -> newly popped pages
 //   release: pages back to the free list; hand-off wire packing.
-// Device free list: a stack free_list[0 .. top-1]; pops take [top-n, top) with one
-// atomicSub per request, pushes append with one atomicAdd (stream-ordered, never concurrent).
+// Device free list: a stack free_list[0 .. top-1]; pops take [top-n, top), pushes append. Every
+// mutation holds a spin lock (free_top[1]): the hand-off receive pops pages on the lane's comm
+// stream while commits (pops) and releases (pushes) run on the lane stream. The holder is always a
+// running thread, so waiters only spin for one short critical section.
 #include "common.cuh"
 #include "lane.h"
 #include "../../include/sv.h"
@@ -15,17 +17,29 @@ SV_DEV size_t pool_row(const LaneDev& d, int layer, int page, int kv, int h, int
   return ((((size_t)layer * d.n_pages + page) * 2 + kv) * d.Hkv + h) * d.page + off;
 }
 
-// pop `n` pages for `slot` whose first new page index is `first`; returns false on exhaustion
+SV_DEV void fl_lock(const LaneDev& d) {
+  while (atomicCAS(d.free_top + 1, 0, 1) != 0) __nanosleep(32);
+  __threadfence();
+}
+SV_DEV void fl_unlock(const LaneDev& d) {
+  __threadfence();
+  atomicExch(d.free_top + 1, 0);
+}
+SV_DEV int fl_top(const LaneDev& d) { return *reinterpret_cast<volatile int*>(d.free_top); }
+
+// pop `n` pages for `slot` whose first new page index is `first` (one thread); false on exhaustion
 SV_DEV bool pop_pages(const LaneDev& d, int slot, int first, int n) {
   if (n <= 0) return true;
-  const int old = atomicSub(d.free_top, n);
-  if (old - n < 0) {
-    atomicAdd(d.free_top, n);                    // undo: the pages were not taken
-    atomicOr(d.err, SV_DERR_NO_PAGES);
-    return false;
+  fl_lock(d);
+  const int old = fl_top(d);
+  const bool ok = old >= n;
+  if (ok) {
+    for (int i = 0; i < n; ++i) d.page_table[slot * d.max_pages_per_slot + first + i] = d.free_list[old - n + i];
+    *d.free_top = old - n;
   }
-  for (int i = 0; i < n; ++i) d.page_table[slot * d.max_pages_per_slot + first + i] = d.free_list[old - n + i];
-  return true;
+  fl_unlock(d);
+  if (!ok) atomicOr(d.err, SV_DERR_NO_PAGES);
+  return ok;
 }
 
 // ------------------------------------------------------------------ a8 commit
@@ -117,9 +131,10 @@ __global__ void append_alloc_kernel(LaneDev d, int slot, unsigned long long rid,
     int ok = 1, cnt = need - have, old = 0;
     if (L + n > d.max_pos || need > d.max_pages_per_slot) { atomicOr(d.err, SV_DERR_MAX_POS); ok = 0; }
     if (ok && cnt > 0) {
-      old = atomicSub(d.free_top, cnt);
-      if (old - cnt < 0) {
-        atomicAdd(d.free_top, cnt);                  // undo: the pages were not taken
+      fl_lock(d);                                    // released below, after the block copied the ids
+      old = fl_top(d);
+      if (old < cnt) {
+        fl_unlock(d);
         atomicOr(d.err, SV_DERR_NO_PAGES);
         ok = 0;
       }
@@ -140,6 +155,11 @@ __global__ void append_alloc_kernel(LaneDev d, int slot, unsigned long long rid,
   __syncthreads();
   for (int i = threadIdx.x; i < s_cnt; i += blockDim.x)
     d.page_table[slot * d.max_pages_per_slot + s_first + i] = d.free_list[s_old - s_cnt + i];
+  __syncthreads();
+  if (threadIdx.x == 0 && s_cnt > 0) {
+    *d.free_top = s_old - s_cnt;
+    fl_unlock(d);
+  }
 }
 
 // The KV copies below move "row sets": the Hkv x d_h/8 16-byte vectors of one (layer, token, K|V).
@@ -195,17 +215,141 @@ cudaError_t launch_append(const LaneDev& d, int slot, unsigned long long rid, co
   return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------ a9 batched hand-off: page pop
+// One CTA per received request: pops ceil(n / page) pages for the (EMPTY, len 0) slot, writes its
+// page-table row, len = n and the request id. The pages and the pending token are then written by
+// the NCCL receives (sv_kv_recv_slots); the host checked the free list beforehand.
+__global__ void handoff_alloc_kernel(LaneDev d, const int* __restrict__ slots, const unsigned long long* __restrict__ rids,
+                                     const int* __restrict__ ns) {
+  __shared__ int s_old, s_cnt;
+  const int slot = slots[blockIdx.x], n = ns[blockIdx.x];
+  if (threadIdx.x == 0) {
+    const int cnt = (n + d.page - 1) / d.page;
+    fl_lock(d);
+    const int old = fl_top(d);
+    if (old < cnt) {
+      fl_unlock(d);
+      atomicOr(d.err, SV_DERR_NO_PAGES);
+      s_cnt = -1;
+    } else {
+      s_cnt = cnt;
+      d.len[slot] = n;
+      d.rid[slot] = rids[blockIdx.x];
+    }
+    s_old = old;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < s_cnt; i += blockDim.x)
+    d.page_table[slot * d.max_pages_per_slot + i] = d.free_list[s_old - s_cnt + i];
+  __syncthreads();
+  if (threadIdx.x == 0 && s_cnt >= 0) {
+    *d.free_top = s_old - s_cnt;
+    fl_unlock(d);
+  }
+}
+
+cudaError_t launch_handoff_alloc(const LaneDev& d, const int* slots, const unsigned long long* rids, const int* ns,
+                                 int n, cudaStream_t s) {
+  SV_COUNT_LAUNCH();
+  handoff_alloc_kernel<<<n, 256, 0, s>>>(d, slots, rids, ns);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ a9 batched hand-off: block gather / scatter
+// Staging layout (sv_host.cpp "batched page-block hand-off"): block b of the batch = request i
+// (bstart[i] <= b < bstart[i + 1]), layer = (b - bstart[i]) / m_i, page index p = (b - bstart[i]) % m_i
+// (m_i = ceil(n_i / page)); then the n pending tokens. A block is [2][Hkv][page][d_h] bf16, contiguous
+// in the pool at (layer, page id); CTAs copy whole blocks with 16-byte vectors, U in flight per thread.
+SV_DEV void handoff_block(const LaneDev& d, const int* slots, const int* ns, const int* bstart, int n, int b,
+                          int* slot, int* layer, int* p) {
+  int lo = 0, hi = n - 1;                          // last i with bstart[i] <= b
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (bstart[mid] <= b) lo = mid; else hi = mid - 1;
+  }
+  const int m = (ns[lo] + d.page - 1) / d.page, rel = b - bstart[lo];
+  *slot = slots[lo];
+  *layer = rel / m;
+  *p = rel - *layer * m;
+}
+
+template <bool GATHER>
+__global__ void __launch_bounds__(256) handoff_copy_kernel(LaneDev d, const int* __restrict__ slots,
+                                                           const int* __restrict__ ns, const int* __restrict__ bstart,
+                                                           int n, char* __restrict__ staging) {
+  const int nb = bstart[n];
+  const size_t bvec = (size_t)2 * d.Hkv * d.page * d.dh / 8;     // 16-byte vectors per block
+  constexpr int U = 8;
+  for (int b = blockIdx.x; b < nb; b += gridDim.x) {
+    int slot, layer, p;
+    handoff_block(d, slots, ns, bstart, n, b, &slot, &layer, &p);
+    const int page = d.page_table[slot * d.max_pages_per_slot + p];
+    uint4* pg = reinterpret_cast<uint4*>(d.pool + ((size_t)layer * d.n_pages + page) * bvec * 8);
+    uint4* st = reinterpret_cast<uint4*>(staging) + (size_t)b * bvec;
+    const uint4* src = GATHER ? pg : st;
+    uint4* dst = GATHER ? st : pg;
+    for (size_t v0 = threadIdx.x; v0 < bvec; v0 += (size_t)U * blockDim.x) {
+      uint4 buf[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const size_t v = v0 + (size_t)u * blockDim.x;
+        if (v < bvec) buf[u] = src[v];
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const size_t v = v0 + (size_t)u * blockDim.x;
+        if (v < bvec) dst[v] = buf[u];
+      }
+    }
+  }
+  if (blockIdx.x == 0) {
+    int* tail = reinterpret_cast<int*>(staging + (size_t)nb * bvec * 16);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      if (GATHER) tail[i] = d.pending[slots[i]];
+      else d.pending[slots[i]] = tail[i];
+    }
+  }
+}
+
+static int handoff_grid(const LaneDev& d) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return 4 * sms;                                  // 4 CTAs of 256 threads per SM, grid-stride over blocks
+}
+
+cudaError_t launch_handoff_gather(const LaneDev& d, const int* slots, const int* ns, const int* bstart, int n,
+                                  char* staging, cudaStream_t s) {
+  SV_COUNT_LAUNCH();
+  handoff_copy_kernel<true><<<handoff_grid(d), 256, 0, s>>>(d, slots, ns, bstart, n, staging);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_handoff_scatter(const LaneDev& d, const int* slots, const int* ns, const int* bstart, int n,
+                                   const char* staging, cudaStream_t s) {
+  SV_COUNT_LAUNCH();
+  handoff_copy_kernel<false><<<handoff_grid(d), 256, 0, s>>>(d, slots, ns, bstart, n, const_cast<char*>(staging));
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------ release
 __global__ void release_kernel(LaneDev d, int slot) {
   const int L = d.len[slot];
   const int n = (L + d.page - 1) / d.page;
   __shared__ int s_old;
-  if (threadIdx.x == 0) s_old = atomicAdd(d.free_top, n);
+  if (threadIdx.x == 0) {
+    fl_lock(d);
+    s_old = fl_top(d);
+  }
   __syncthreads();
   for (int i = threadIdx.x; i < n; i += blockDim.x)
     d.free_list[s_old + i] = d.page_table[slot * d.max_pages_per_slot + i];
   __syncthreads();
-  if (threadIdx.x == 0) { d.len[slot] = 0; d.pending[slot] = 0; d.rid[slot] = 0ull; }
+  if (threadIdx.x == 0) {
+    *d.free_top = s_old + n;
+    fl_unlock(d);
+    d.len[slot] = 0; d.pending[slot] = 0; d.rid[slot] = 0ull;
+  }
 }
 
 cudaError_t launch_release(const LaneDev& d, int slot, cudaStream_t s) {

@@ -461,7 +461,7 @@ __global__ void init_state_kernel(LaneDev d) {
   if (i < d.n_pages) d.free_list[i] = d.n_pages - 1 - i;     // pop order 0, 1, 2, ...
   if (i < d.max_slots) { d.len[i] = 0; d.pending[i] = 0; d.rid[i] = 0ull; }
   if (i < kNumStats) d.stats[i] = 0ull;
-  if (i == 0) { *d.free_top = d.n_pages; *d.err = 0; }
+  if (i == 0) { d.free_top[0] = d.n_pages; d.free_top[1] = 0; *d.err = 0; }   // [1]: free-list lock
 }
 
 cudaError_t launch_init_state(const LaneDev& d, cudaStream_t s) {

@@ -43,7 +43,7 @@ struct LaneDev {
   unsigned long long* rid;           // [max_slots]
   int* page_table;                   // [max_slots][max_pages_per_slot]
   int* free_list;                    // [n_pages]
-  int* free_top;                     // [1]
+  int* free_top;                     // [2]: stack top, free-list spin lock
   unsigned long long* stats;         // [kNumStats]
   int* err;                          // [1] sticky SV_DERR_* bits
   const float *rope_cos, *rope_sin;  // [max_pos][dh/2]
@@ -145,6 +145,12 @@ cudaError_t launch_commit(const LaneDev& d, const int* n_keep, int batch, cudaSt
 cudaError_t launch_append(const LaneDev& d, int slot, unsigned long long rid, const bf16* k, const bf16* v,
                           int n, int pending, const int* pending_dev, int packed, cudaStream_t s);
 cudaError_t launch_release(const LaneDev& d, int slot, cudaStream_t s);
+cudaError_t launch_handoff_gather(const LaneDev& d, const int* slots, const int* ns, const int* bstart, int n,
+                                  char* staging, cudaStream_t s);
+cudaError_t launch_handoff_scatter(const LaneDev& d, const int* slots, const int* ns, const int* bstart, int n,
+                                   const char* staging, cudaStream_t s);
+cudaError_t launch_handoff_alloc(const LaneDev& d, const int* slots, const unsigned long long* rids, const int* ns,
+                                 int n, cudaStream_t s);
 cudaError_t launch_init_state(const LaneDev& d, cudaStream_t s);
 cudaError_t launch_debug_uniforms(uint64_t seed, uint64_t rid, uint32_t z, int purpose, int x0, int n, float* u,
                                   cudaStream_t s);

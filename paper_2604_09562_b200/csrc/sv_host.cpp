@@ -26,7 +26,7 @@ struct Layout {
   size_t h0, h1, h2, cbuf, logits, tile_max, tile_sum, tile_arg;
   size_t a, b, z, q, kc, vc, o, u;
   size_t items, item_start, n_items, part_o, part_ml, acc_int, tok_int, batch_n, path_int, row_anc, filt, fin_cnt, fin_part;
-  size_t gemm_ws, trace, prefill;
+  size_t gemm_ws, trace, prefill, handoff;
   size_t max_items;
 
   size_t take(size_t bytes) {
@@ -70,7 +70,7 @@ Layout make_layout(const sv_config& c) {
   L.rid = L.take(8 * c.max_slots);
   L.page_table = L.take(4 * c.max_slots * mpps);
   L.free_list = L.take(4 * (size_t)c.n_pages);
-  L.free_top = L.take(4);
+  L.free_top = L.take(8);                          // [0] stack top, [1] spin lock (k_kv.cu)
   L.stats = L.take(8 * sv::kNumStats);
   L.err = L.take(4);
   L.slots = L.take(4 * c.max_batch);
@@ -119,6 +119,9 @@ Layout make_layout(const sv_config& c) {
   L.trace = L.take(8 * 16 * 256);
   // sv_prefill: outputs of a chunk + the whole prompt (copied to the device once, <= max_pos tokens)
   L.prefill = L.take(4 * (2 * (size_t)(c.max_depth + 2) + (size_t)c.max_pos));
+  // batched hand-off (sv_kv_send_slots / sv_kv_recv_slots): slots, token counts, block starts [max_slots + 1]
+  // i32 + request ids [max_slots] u64
+  L.handoff = L.take(4 * (4 * (size_t)c.max_slots + 4) + 8 * (size_t)c.max_slots);
   L.total = (L.total + 1023) & ~size_t(1023);
   return L;
 }
@@ -173,7 +176,34 @@ struct sv_ctx {
   float top_p = 1.0f;
   sv::GemmPlan* gemm = nullptr;
   Prof prof;
+  // prefill -> decode hand-off (a9): NCCL transfers run on their own stream so a verify already
+  // enqueued on `stream` overlaps them; the lane's next device work waits for comm_done
+  cudaStream_t comm = nullptr;
+  cudaEvent_t comm_done = nullptr, lane_mark = nullptr;
+  bool comm_pending = false;
+  std::vector<char> comm_slot;       // slots whose pages / pending token a posted transfer reads or writes
+  std::vector<cudaEvent_t> rel_ev;   // per slot: recorded after its last release (a receive into it waits)
+  std::vector<char> rel_pending;
 };
+
+// make the lane's stream wait for the posted hand-off transfers (sends read pages, receives write
+// pages and pending tokens); wait_comm_slots only when the call touches one of their slots, so a
+// verify of other requests overlaps the transfer
+static void wait_comm(sv_ctx* c) {
+  if (c->comm_pending) {
+    cudaStreamWaitEvent(c->stream, c->comm_done, 0);
+    c->comm_pending = false;
+    std::fill(c->comm_slot.begin(), c->comm_slot.end(), 0);
+  }
+}
+static void wait_comm_slots(sv_ctx* c, int n, const int32_t* slots) {
+  if (!c->comm_pending) return;
+  for (int i = 0; i < n; ++i)
+    if (c->comm_slot[slots[i]]) {
+      wait_comm(c);
+      return;
+    }
+}
 
 static cudaEvent_t prof_begin(sv_ctx* c, int stage) {
   if (!(c->prof.mask >> stage & 1u)) return nullptr;
@@ -273,6 +303,9 @@ sv_status sv_create(const sv_config* cfg, const sv_weights* w, void* kv_pool, vo
   c->stream = (cudaStream_t)stream;
   c->lay = make_layout(*cfg);
   c->state.assign(cfg->max_slots, EMPTY);
+  c->comm_slot.assign(cfg->max_slots, 0);
+  c->rel_ev.assign(cfg->max_slots, nullptr);
+  c->rel_pending.assign(cfg->max_slots, 0);
   c->rid.assign(cfg->max_slots, 0ull);
   const Layout& L = c->lay;
   char* ws = c->ws;
@@ -383,8 +416,13 @@ sv_status sv_create(const sv_config* cfg, const sv_weights* w, void* kv_pool, vo
     return st;
   }
   c->gemm = sv::gemm_plan_create(d, ws + L.gemm_ws, c->stream);
-  if ((st = cuda_ok(cudaStreamSynchronize(c->stream)))) {
+  if ((st = cuda_ok(cudaStreamSynchronize(c->stream))) ||
+      (st = cuda_ok(cudaStreamCreateWithFlags(&c->comm, cudaStreamNonBlocking))) ||
+      (st = cuda_ok(cudaEventCreateWithFlags(&c->comm_done, cudaEventDisableTiming))) ||
+      (st = cuda_ok(cudaEventCreateWithFlags(&c->lane_mark, cudaEventDisableTiming)))) {
     sv::gemm_plan_destroy(c->gemm);
+    if (c->comm) cudaStreamDestroy(c->comm);
+    if (c->comm_done) cudaEventDestroy(c->comm_done);
     delete c;
     return st;
   }
@@ -394,7 +432,14 @@ sv_status sv_create(const sv_config* cfg, const sv_weights* w, void* kv_pool, vo
 
 sv_status sv_destroy(sv_ctx* c) {
   if (!c) return SV_EINVAL;
+  if (c->comm_pending) cudaEventSynchronize(c->comm_done);   // possibly recorded on a peer lane's stream
+  cudaStreamSynchronize(c->comm);
   cudaStreamSynchronize(c->stream);
+  cudaStreamDestroy(c->comm);
+  cudaEventDestroy(c->comm_done);
+  cudaEventDestroy(c->lane_mark);
+  for (cudaEvent_t e : c->rel_ev)
+    if (e) cudaEventDestroy(e);
   sv::gemm_plan_destroy(c->gemm);
   for (auto e : c->prof.free_ev) cudaEventDestroy(e);
   for (auto& r : c->prof.recs) {
@@ -412,6 +457,7 @@ sv_status sv_append_kv(sv_ctx* c, int32_t slot, uint64_t request_id, const void*
   if (pending_token < 0 || pending_token >= c->cfg.vocab) return SV_EINVAL;
   if (c->state[slot] == PENDING) return SV_ESTATE;
   if (c->state[slot] == ACTIVE && c->rid[slot] != request_id) return SV_EINVAL;
+  wait_comm_slots(c, 1, &slot);
   SV_CUDA(sv::launch_append(c->d, slot, request_id, (const bf16*)k, (const bf16*)v, n_tokens, pending_token,
                             nullptr, 0, c->stream));
   c->state[slot] = ACTIVE;
@@ -469,6 +515,7 @@ static sv_status verify_impl(sv_ctx* c, int32_t batch, const int32_t* slots, con
   const int T = p.T;
   cudaStream_t s = c->stream;
   const float inv_temp = mode == SV_SAMPLE ? 1.0f / temperature : 1.0f;
+  wait_comm_slots(c, batch, slots);
   STAGE(c, ST_PLAN, sv::launch_plan(d, p, draft_tokens, parents, true, s));
   STAGE(c, ST_EMBED, sv::launch_embed_norm(d, T, s));
   const size_t nq = (size_t)d.Hq * d.dh;
@@ -553,6 +600,7 @@ static sv_status verify_logits_impl(sv_ctx* c, int32_t batch, const int32_t* slo
   sv::LaneDev d = c->d;
   if (p.T == batch) parents = nullptr;
   d.tree = parents != nullptr;
+  wait_comm_slots(c, batch, slots);
   SV_CUDA(sv::launch_plan(d, p, draft_tokens, parents, false, c->stream));
   d.logits = const_cast<float*>(logits);
   SV_CUDA(sv::launch_tile_stats(d, p.T, inv_temp, c->stream));
@@ -597,7 +645,11 @@ sv_status sv_release(sv_ctx* c, int32_t slot) {
   if (!c || slot < 0 || slot >= c->cfg.max_slots) return SV_EINVAL;
   if (c->state[slot] == PENDING) return SV_ESTATE;
   if (c->state[slot] == EMPTY) return SV_OK;
+  wait_comm_slots(c, 1, &slot);
   SV_CUDA(sv::launch_release(c->d, slot, c->stream));
+  if (!c->rel_ev[slot]) SV_CUDA(cudaEventCreateWithFlags(&c->rel_ev[slot], cudaEventDisableTiming));
+  SV_CUDA(cudaEventRecord(c->rel_ev[slot], c->stream));
+  c->rel_pending[slot] = 1;
   c->state[slot] = EMPTY;
   c->rid[slot] = 0;
   return SV_OK;
@@ -788,6 +840,7 @@ sv_status sv_kv_pack_slot(sv_ctx* c, int32_t slot, int32_t n_tokens, void* kv_pa
   if (!c || slot < 0 || slot >= c->cfg.max_slots || n_tokens < 0 || !kv_packed || ((uintptr_t)kv_packed & 15))
     return SV_EINVAL;
   if (c->state[slot] != ACTIVE) return SV_ESTATE;
+  wait_comm_slots(c, 1, &slot);
   SV_CUDA(sv::launch_kv_pack_slot(c->d, slot, n_tokens, kv_packed, c->stream));
   return SV_OK;
 }
@@ -848,6 +901,7 @@ struct sv_graph {
 sv_status sv_graph_begin(sv_ctx* c) {
   if (!c || !c->stream) return SV_EINVAL;                 // the legacy default stream cannot be captured
   if (c->capturing || c->pending_verify || c->prof.mask) return SV_ESTATE;
+  wait_comm(c);                                           // an outside event cannot be waited on in capture
   SV_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
   c->capturing = true;
   c->capture_launches0 = sv::g_launch_count;
@@ -909,6 +963,7 @@ sv_status sv_internal_append_packed(sv_ctx* c, int32_t slot, uint64_t request_id
   if (chk) return chk;
   const size_t body = (size_t)c->cfg.n_layers * n_tokens * 2 * c->cfg.n_kv_heads * c->cfg.head_dim * 2;
   const int* trailer = (const int*)((const char*)packed + body);
+  wait_comm(c);                                          // the packed message may come from a receive
   SV_CUDA(sv::launch_append(c->d, slot, request_id, (const bf16*)packed, nullptr, n_tokens, 0, trailer, 1,
                             c->stream));
   c->state[slot] = ACTIVE;
@@ -919,3 +974,151 @@ sv_status sv_internal_append_packed(sv_ctx* c, int32_t slot, uint64_t request_id
 cudaStream_t sv_internal_stream(sv_ctx* c) { return c->stream; }
 
 size_t sv_internal_packed_bytes(sv_ctx* c, int32_t n_tokens) { return sv_kv_packed_bytes(&c->cfg, n_tokens); }
+
+// ---------------------------------------------------------------- batched page-block hand-off (a9)
+// Wire format of one batch (one ncclSend / ncclRecv): for request i, for layer l, for page
+// p < ceil(n_i / page_size): the (layer, page) block of the KV pool — [2][Hkv][page][d_h] bf16,
+// contiguous in the pool (256 KB at Llama-3-8B shape) — then the n pending tokens (int32), padded
+// to 16 bytes. The prefill side gathers the blocks from its pages into its staging buffer and the
+// decode side scatters them from its staging buffer into freshly popped pages: block-granular
+// copies (16-byte vectors, whole 256 KB blocks), both on the lanes' comm streams.
+// (One NCCL op per block and no staging was measured first: 4096 ops for a 32 x 8192-token batch
+// took 22 ms on the one-GPU loopback, ~5.4 us per op, i.e. 48 GB/s; one op per batch removes it.)
+static size_t block_bytes(const sv_config& c) { return (size_t)2 * c.n_kv_heads * c.page_size * c.head_dim * 2; }
+
+static bool distinct_slots(const sv_ctx* c, int n, const int32_t* slots) {
+  std::vector<char> seen(c->cfg.max_slots, 0);
+  for (int i = 0; i < n; ++i) {
+    if (slots[i] < 0 || slots[i] >= c->cfg.max_slots || seen[slots[i]]) return false;
+    seen[slots[i]] = 1;
+  }
+  return true;
+}
+
+extern "C" size_t sv_kv_slots_bytes(const sv_config* cfg, int32_t n, const int32_t* n_tokens) {
+  if (!cfg || n < 1 || !n_tokens || cfg->page_size < 1) return 0;
+  size_t blocks = 0;
+  for (int i = 0; i < n; ++i) {
+    if (n_tokens[i] < 0) return 0;
+    blocks += (size_t)cfg->n_layers * ((n_tokens[i] + cfg->page_size - 1) / cfg->page_size);
+  }
+  return blocks * block_bytes(*cfg) + (((size_t)4 * n + 15) & ~(size_t)15);
+}
+
+// control arrays of a batch in the lane's hand-off workspace area: slots, n_tokens, block starts
+// [n + 1], request ids; copied on `st`
+static sv_status stage_ctrl(sv_ctx* c, int n, const int32_t* slots, const int32_t* ntok, const uint64_t* rids,
+                            cudaStream_t st, int** d_slots, int** d_ntok, int** d_bstart,
+                            unsigned long long** d_rid) {
+  const int ms = c->cfg.max_slots;
+  int* base = (int*)(c->ws + c->lay.handoff);
+  *d_slots = base;
+  *d_ntok = base + ms;
+  *d_bstart = base + 2 * ms;
+  *d_rid = (unsigned long long*)(base + 4 * ms + 4);
+  std::vector<int> bs(n + 1, 0);
+  for (int i = 0; i < n; ++i) bs[i + 1] = bs[i] + c->cfg.n_layers * ((ntok[i] + c->cfg.page_size - 1) / c->cfg.page_size);
+  SV_CUDA(cudaMemcpyAsync(*d_slots, slots, 4 * (size_t)n, cudaMemcpyHostToDevice, st));
+  SV_CUDA(cudaMemcpyAsync(*d_ntok, ntok, 4 * (size_t)n, cudaMemcpyHostToDevice, st));
+  SV_CUDA(cudaMemcpyAsync(*d_bstart, bs.data(), 4 * (size_t)(n + 1), cudaMemcpyHostToDevice, st));
+  if (rids) SV_CUDA(cudaMemcpyAsync(*d_rid, rids, 8 * (size_t)n, cudaMemcpyHostToDevice, st));
+  return SV_OK;
+}
+
+// prefill side: checks (one sync of the lane stream reads the slots' committed lengths), then on
+// the comm stream, after the lane's earlier work: the block gather into `staging`. Returns the
+// message size; the caller posts the send on the comm stream.
+sv_status sv_internal_send_prepare(sv_ctx* c, int32_t n, const int32_t* slots, const int32_t* ntok, void* staging,
+                                   size_t* bytes) {
+  if (!c || n < 1 || !slots || !ntok || !staging || ((uintptr_t)staging & 15) || !distinct_slots(c, n, slots))
+    return SV_EINVAL;
+  if (c->capturing) return SV_ESTATE;
+  for (int i = 0; i < n; ++i) {
+    if (c->state[slots[i]] != ACTIVE) return SV_ESTATE;
+    if (ntok[i] < 1) return SV_EINVAL;
+  }
+  std::vector<int> len(c->cfg.max_slots);
+  wait_comm_slots(c, n, slots);
+  SV_CUDA(cudaMemcpyAsync(len.data(), c->d.len, 4 * len.size(), cudaMemcpyDeviceToHost, c->stream));
+  SV_CUDA(cudaStreamSynchronize(c->stream));
+  for (int i = 0; i < n; ++i)
+    if (ntok[i] > len[slots[i]]) return SV_EINVAL;              // only committed rows can be sent
+  cudaStream_t cs = c->comm;
+  int *ds, *dn, *db;
+  unsigned long long* dr;
+  sv_status st = stage_ctrl(c, n, slots, ntok, nullptr, cs, &ds, &dn, &db, &dr);
+  if (st) return st;
+  SV_CUDA(sv::launch_handoff_gather(c->d, ds, dn, db, n, (char*)staging, cs));
+  *bytes = sv_kv_slots_bytes(&c->cfg, n, ntok);
+  return SV_OK;
+}
+
+// decode side, before the receive: checks and the page pop on the comm stream (the host never
+// waits for the lane stream: a verify enqueued before the call keeps running; the free list is
+// lock-protected against the lane's concurrent commits / releases, k_kv.cu). A slot released earlier
+// is reused only after its release kernel (per-slot event). The slots become ACTIVE with
+// len = n_i and request_id bound; the scatter (sv_internal_recv_finish) writes their pages and
+// pending tokens, and lane work on those slots waits for it (sv_internal_comm_posted).
+sv_status sv_internal_recv_prepare(sv_ctx* c, int32_t n, const int32_t* slots, const uint64_t* rids,
+                                   const int32_t* ntok, void* staging, size_t* bytes) {
+  if (!c || n < 1 || !slots || !rids || !ntok || !staging || ((uintptr_t)staging & 15) ||
+      !distinct_slots(c, n, slots))
+    return SV_EINVAL;
+  if (c->capturing) return SV_ESTATE;
+  long need = 0;
+  for (int i = 0; i < n; ++i) {
+    if (c->state[slots[i]] != EMPTY) return SV_ESTATE;
+    if (ntok[i] < 1 || ntok[i] > c->cfg.max_pos - 1) return SV_EINVAL;
+    need += (ntok[i] + c->cfg.page_size - 1) / c->cfg.page_size;
+  }
+  cudaStream_t cs = c->comm;
+  for (int i = 0; i < n; ++i)
+    if (c->rel_pending[slots[i]]) {
+      SV_CUDA(cudaStreamWaitEvent(cs, c->rel_ev[slots[i]], 0));
+      c->rel_pending[slots[i]] = 0;
+    }
+  int ft = 0;
+  SV_CUDA(cudaMemcpyAsync(&ft, c->d.free_top, 4, cudaMemcpyDeviceToHost, cs));
+  SV_CUDA(cudaStreamSynchronize(cs));
+  if (need > ft) return SV_ENOKV;                               // refused before anything is popped / posted
+  int *ds, *dn, *db;
+  unsigned long long* dr;
+  sv_status st = stage_ctrl(c, n, slots, ntok, rids, cs, &ds, &dn, &db, &dr);
+  if (st) return st;
+  SV_CUDA(sv::launch_handoff_alloc(c->d, ds, dr, dn, n, cs));
+  for (int i = 0; i < n; ++i) {
+    c->state[slots[i]] = ACTIVE;
+    c->rid[slots[i]] = rids[i];
+  }
+  *bytes = sv_kv_slots_bytes(&c->cfg, n, ntok);
+  return SV_OK;
+}
+
+// decode side, after the receive was posted on the comm stream: the block scatter into the pages
+sv_status sv_internal_recv_finish(sv_ctx* c, int32_t n, const void* staging) {
+  const int ms = c->cfg.max_slots;
+  int* base = (int*)(c->ws + c->lay.handoff);
+  SV_CUDA(sv::launch_handoff_scatter(c->d, base, base + ms, base + 2 * ms, n, (const char*)staging, c->comm));
+  return SV_OK;
+}
+
+cudaStream_t sv_internal_comm_stream(sv_ctx* c) { return c->comm; }
+
+extern "C" sv_status sv_comm_stream(sv_ctx* c, sv_stream_t* out) {
+  if (!c || !out) return SV_EINVAL;
+  *out = (sv_stream_t)c->comm;
+  return SV_OK;
+}
+
+sv_status sv_internal_config(sv_ctx* c, sv_config* out) {
+  *out = c->cfg;
+  return SV_OK;
+}
+
+// transfers touching `slots` were enqueued on `on`: lane work on those slots waits for them
+sv_status sv_internal_comm_posted(sv_ctx* c, cudaStream_t on, int32_t n, const int32_t* slots) {
+  SV_CUDA(cudaEventRecord(c->comm_done, on));
+  c->comm_pending = true;
+  for (int i = 0; i < n; ++i) c->comm_slot[slots[i]] = 1;
+  return SV_OK;
+}

@@ -72,3 +72,24 @@ def route_requests(n_requests, metrics, now_ms, cfg=None):
         out.append(chosen)
         live[chosen] += 1
     return out
+
+
+# ---------------------------------------------------------------- disaggregated prefill -> decode pairs
+def disagg_role(rank, world):
+    """Zero-based stream pairs (2p, 2p+1) (PAPER.md:162 vs 437; R14): even ranks prefill,
+    odd ranks decode; returns (role, peer rank, pair index). world == 1: both roles on one rank
+    (the one-GPU loopback used to validate the flow)."""
+    if world == 1:
+        return "both", 0, 0
+    if world % 2:
+        raise ValueError("disaggregated pairs need an even number of ranks")
+    return ("prefill", rank + 1, rank // 2) if rank % 2 == 0 else ("decode", rank - 1, rank // 2)
+
+
+def handoff_batch(round_i, batch, prefill_rank):
+    """Slot plan of hand-off batch `round_i` of a (prefill, decode) pair: the prefill lane sends its
+    slots 0..batch-1; the decode lane receives into the half of its 2*batch slots that is not being
+    decoded (double buffer), with fresh request ids (the Philox keys) for the new requests."""
+    base = (round_i % 2) * batch
+    return (list(range(batch)), [base + i for i in range(batch)],
+            [request_id(prefill_rank, round_i * batch + i) for i in range(batch)])

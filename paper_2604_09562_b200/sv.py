@@ -29,7 +29,7 @@ EXPORTED = [
     "sv_draft_planted", "sv_nccl_unique_id", "sv_nccl_comm_init", "sv_nccl_comm_destroy", "sv_kv_send",
     "sv_kv_recv_append", "sv_kv_packed_bytes", "sv_kv_pack", "sv_profile_enable", "sv_profile_num_stages",
     "sv_profile_stage_name", "sv_profile_read", "sv_launch_count", "sv_debug_gemm", "sv_kv_append_packed",
-    "sv_kv_loopback_append", "sv_spec_default_config", "sv_spec_reset", "sv_spec_adapt", "sv_spec_step",
+    "sv_kv_loopback_append", "sv_kv_send_slots", "sv_kv_recv_slots", "sv_kv_loopback_slots", "sv_comm_stream", "sv_kv_slots_bytes", "sv_spec_default_config", "sv_spec_reset", "sv_spec_adapt", "sv_spec_step",
     "sv_route_default_config", "sv_route_select", "sv_lane_occupancy", "sv_kv_pack_slot", "sv_prefill",
     "sv_verify_tree", "sv_verify_tree_logits", "sv_set_filter", "sv_draft_planted_tree", "sv_graph_begin",
     "sv_graph_end", "sv_graph_launch", "sv_graph_destroy",
@@ -128,6 +128,11 @@ def load():
         "sv_kv_pack_slot": ([vp, i32, i32, vp], ctypes.c_int),
         "sv_prefill": ([vp, i32, u64, P(i32), i32, i32, P(i32)], ctypes.c_int),
         "sv_kv_loopback_append": ([vp, i32, u64, i32, vp, vp, ctypes.c_int, vp], ctypes.c_int),
+        "sv_kv_send_slots": ([vp, i32, vp, vp, vp, ctypes.c_int, vp], ctypes.c_int),
+        "sv_comm_stream": ([vp, P(vp)], ctypes.c_int),
+        "sv_kv_recv_slots": ([vp, i32, vp, vp, vp, vp, ctypes.c_int, vp], ctypes.c_int),
+        "sv_kv_loopback_slots": ([vp, vp, i32, vp, vp, vp, vp, vp, vp, ctypes.c_int, vp], ctypes.c_int),
+        "sv_kv_slots_bytes": ([P(Config), i32, vp], sz),
         "sv_kv_packed_bytes": ([P(Config), i32], sz),
         "sv_kv_pack": ([vp, vp, i32, i32, i32, i32, i32, vp, vp], ctypes.c_int),
         "sv_profile_enable": ([vp, ctypes.c_int32], ctypes.c_int),
@@ -407,6 +412,39 @@ class Lane:
     def kv_loopback_append(self, slot, request_id, n_tokens, packed, staging, rank, comm):
         _check(self.lib.sv_kv_loopback_append(self.ctx, slot, request_id, n_tokens, _ptr(packed), _ptr(staging), rank,
                                               comm), "sv_kv_loopback_append")
+
+    def slots_bytes(self, n_tokens):
+        """Staging bytes of a batched hand-off of requests with these token counts (sv_kv_slots_bytes)."""
+        t, n = _i32_array(n_tokens)
+        return int(self.lib.sv_kv_slots_bytes(ctypes.byref(self.cfg), n, t))
+
+    def kv_send_slots(self, slots, n_tokens, staging, peer, comm):
+        """Prefill side of the batched hand-off (sv_kv_send_slots)."""
+        s, n = _i32_array(slots)
+        t, _ = _i32_array(n_tokens)
+        _check(self.lib.sv_kv_send_slots(self.ctx, n, s, t, _ptr(staging), peer, comm), "sv_kv_send_slots")
+
+    def kv_recv_slots(self, slots, request_ids, n_tokens, staging, peer, comm):
+        """Decode side of the batched hand-off (sv_kv_recv_slots)."""
+        s, n = _i32_array(slots)
+        t, _ = _i32_array(n_tokens)
+        r = (ctypes.c_uint64 * n)(*[int(x) for x in request_ids])
+        _check(self.lib.sv_kv_recv_slots(self.ctx, n, s, r, t, _ptr(staging), peer, comm), "sv_kv_recv_slots")
+
+    def kv_loopback_slots(self, dst, src_slots, dst_slots, request_ids, n_tokens, src_staging, dst_staging, rank, comm):
+        """One-GPU transport test: this lane sends, `dst` receives, one NCCL group."""
+        s, n = _i32_array(src_slots)
+        d, _ = _i32_array(dst_slots)
+        t, _ = _i32_array(n_tokens)
+        r = (ctypes.c_uint64 * n)(*[int(x) for x in request_ids])
+        _check(self.lib.sv_kv_loopback_slots(self.ctx, dst.ctx, n, s, d, r, t, _ptr(src_staging), _ptr(dst_staging),
+                                             rank, comm), "sv_kv_loopback_slots")
+
+    def comm_stream(self):
+        """torch ExternalStream of the lane's comm stream (hand-off transfers run there)."""
+        p = ctypes.c_void_p()
+        _check(self.lib.sv_comm_stream(self.ctx, ctypes.byref(p)), "sv_comm_stream")
+        return torch.cuda.ExternalStream(p.value, device=self.device)
 
     def packed_bytes(self, n_tokens):
         return int(self.lib.sv_kv_packed_bytes(ctypes.byref(self.cfg), n_tokens))

@@ -79,3 +79,15 @@ def test_product_path_never_imports_oracle():
             if f.endswith((".py", ".cu", ".cpp", ".h", ".cuh")):
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt, f
+
+
+def test_handoff_batch_bytes():
+    """sv_kv_slots_bytes: layer x page blocks of every request, then the pending tokens padded to 16 B."""
+    import ctypes
+    from paper_2604_09562_b200 import sv
+    lib = sv.load()
+    c = sv.Config.from_any(synth.TOY.with_(n_layers=2))
+    blk = 2 * 2 * 64 * 64 * 2
+    t = (ctypes.c_int32 * 3)(1, 65, 128)
+    assert lib.sv_kv_slots_bytes(ctypes.byref(c), 3, t) == 2 * (1 + 2 + 2) * blk + 16
+    assert lib.sv_kv_slots_bytes(ctypes.byref(c), 0, t) == 0

@@ -105,3 +105,17 @@ def test_gloo_world2_reduction_and_id_broadcast():
 
 def test_reduce_region_without_process_group():
     assert svdist.reduce_region(3.5, 7) == (3.5, 7.0)
+
+
+def test_disagg_roles_and_handoff_plan():
+    from paper_2604_09562_b200 import dist as svdist
+    assert svdist.disagg_role(0, 1) == ("both", 0, 0)
+    roles = [svdist.disagg_role(r, 8) for r in range(8)]
+    assert [r[0] for r in roles] == ["prefill", "decode"] * 4
+    assert [r[1] for r in roles] == [1, 0, 3, 2, 5, 4, 7, 6] and [r[2] for r in roles] == [0, 0, 1, 1, 2, 2, 3, 3]
+    with pytest.raises(ValueError):
+        svdist.disagg_role(0, 3)
+    s0, d0, r0 = svdist.handoff_batch(0, 4, 2)
+    s1, d1, r1 = svdist.handoff_batch(1, 4, 2)
+    assert s0 == s1 == [0, 1, 2, 3] and d0 == [0, 1, 2, 3] and d1 == [4, 5, 6, 7]
+    assert len(set(r0 + r1)) == 8 and all(r >> 32 == 2 for r in r0 + r1)
