@@ -331,9 +331,13 @@ sv_status sv_kv_recv_append(sv_ctx* ctx, int32_t slot, uint64_t request_id, int3
 size_t sv_kv_packed_bytes(const sv_config* cfg, int32_t n_tokens);
 
 /* Chunked prefill (NEXT-3, eq:prefill_computation PAPER.md:248-253, R29) of a prompt of
- * n >= 1 tokens (host array) into an EMPTY slot bound to request_id: the first token becomes the
- * chain head; each chunk of <= `chunk` tokens (1 <= chunk <= max_depth + 1) runs one SV_PREFILL
- * verify + commit (every row's KV kept), the next chunk's head set as the pending token. After
+ * n >= 1 tokens (host array) into an EMPTY slot bound to request_id, in chunks of <= `chunk` prompt
+ * tokens, 1 <= chunk <= max_batch * (max_depth + 1) (the workspace's rows). Each chunk runs as C rows
+ * at positions L..L+C-1 through the layer stack: its K/V rows are written to their pages first and
+ * the attention reads every key from the pages with a per-row causal limit (k_attn_prefill.cu,
+ * tcgen05, 128 / G rows of each of the G q heads per work item); only the last chunk runs the final
+ * norm + lm-head, on its last row. (If that attention is unavailable — SV_ATTN=simt, G not in
+ * {1, 2, 4} — chunks of <= max_depth + 1 run as SV_PREFILL verifies + commits instead.) After
  * the call the slot holds KV for all n prompt tokens and its pending token is the model's greedy
  * next token, also written to *next_token (host, may be NULL). Synchronous (reads the token back).
  * EINVAL: bad arguments; ESTATE: slot not EMPTY or a verify outstanding. */

@@ -17,4 +17,8 @@ cudaError_t launch_attention_tc(const CUtensorMap& map_q, const CUtensorMap& map
 int attn_tc2_smem_bytes();
 cudaError_t launch_attention_tc2(const CUtensorMap& map_q, const CUtensorMap& map_kv, const LaneDev& d, int layer,
                                  int num_sms, cudaStream_t s);
+// long-chunk prefill attention (k_attn_prefill.cu): map_q 3-D (d_h, Hq, Tmax), box (64, 1, 128 / G);
+// every key from the pages (the chunk's rows committed first), per-row causal limit, normalised O.
+cudaError_t launch_attention_prefill(const CUtensorMap& map_q, const CUtensorMap& map_kv, const LaneDev& d, int layer,
+                                     int n_items, int num_sms, cudaStream_t s);
 }  // namespace sv

@@ -22,6 +22,9 @@ GemmPlan* gemm_plan_create(const LaneDev& d, void* ws, cudaStream_t s);
 void gemm_plan_destroy(GemmPlan* p);
 // a3 verify attention: tcgen05 kernel when the shape allows (page 64, d_h 64/128), else SIMT
 cudaError_t attn_run(GemmPlan* p, int layer, int batch, int tree, cudaStream_t s);
+// NEXT-3 long-chunk prefill attention (tcgen05 rows-on-lanes, G in {1, 2, 4})
+bool attn_prefill_supported(GemmPlan* p);
+cudaError_t attn_prefill_run(GemmPlan* p, int layer, int n_items, cudaStream_t s);
 // test hook: plain C = A B^T with a chosen kernel (0 default, 1 1-SM, 2 2-SM, 3 SIMT)
 cudaError_t gemm_debug(GemmPlan* p, const bf16* A, const bf16* B, float* C, int M, int N, int K, int variant,
                        cudaStream_t s);

@@ -31,6 +31,8 @@ struct GemmPlan {
   bool use_streamk = false;
   bool use_2sm = false;            // token-major 2-SM kernel (SV_GEMM=tc2)
   bool use_1sm = false;            // token-major 1-SM kernel (SV_GEMM=tc1)
+  bool prefill_map_ok = false;     // map_qp: Q box (64, 1, 128 / G) for the long-chunk prefill attention
+  CUtensorMap map_qp;
 };
 
 static size_t counter_bytes(int Tmax, int max_n) {
@@ -154,6 +156,29 @@ cudaError_t attn_run(GemmPlan* p, int layer, int batch, int tree, cudaStream_t s
   if (p->use_tc_attn && p->attn_maps_ok)
     return launch_attention_tc(p->map_q, p->map_kv, d, layer, p->num_sms, p->q_box_tokens, s);
   return launch_attention(d, layer, batch, s);
+}
+
+bool attn_prefill_supported(GemmPlan* p) {
+  const LaneDev& d = p->d;
+  const int G = d.Hq / d.Hkv;
+  return p->use_tc_attn && p->attn_maps_ok && (G == 1 || G == 2 || G == 4);
+}
+
+cudaError_t attn_prefill_run(GemmPlan* p, int layer, int n_items, cudaStream_t s) {
+  const LaneDev& d = p->d;
+  const int G = d.Hq / d.Hkv;
+  if (!p->prefill_map_ok) {
+    cuuint64_t qdims[3] = {(cuuint64_t)d.dh, (cuuint64_t)d.Hq, (cuuint64_t)d.Tmax};
+    cuuint64_t qstr[2] = {(cuuint64_t)d.dh * 2, (cuuint64_t)d.Hq * d.dh * 2};
+    cuuint32_t qbox[3] = {64, 1, (cuuint32_t)(128 / G)};
+    cuuint32_t es3[3] = {1, 1, 1};
+    if (p->encode(&p->map_qp, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, d.q, qdims, qstr, qbox, es3,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+    p->prefill_map_ok = true;
+  }
+  return launch_attention_prefill(p->map_qp, p->map_kv, d, layer, n_items, p->num_sms, s);
 }
 
 static cudaError_t gemm_simt(GemmPlan* p, const bf16* A, const bf16* B, float* C, int M, int N, int K, int epi,

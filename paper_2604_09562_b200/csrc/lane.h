@@ -156,6 +156,10 @@ cudaError_t launch_debug_uniforms(uint64_t seed, uint64_t rid, uint32_t z, int p
                                   cudaStream_t s);
 cudaError_t launch_draft_planted(const LaneDev& d, const PlanArgs& p, const int* succ, const uint8_t* mask,
                                  const int* dev_tok, const int* parents, int* draft_tokens, cudaStream_t s);
+// NEXT-3 long-chunk prefill (k_prefill.cu, k_attn_prefill.cu via attn_prefill_run)
+cudaError_t launch_prefill_plan(const LaneDev& d, int slot, const int* tokens, int C, cudaStream_t s);
+cudaError_t launch_prefill_kv(const LaneDev& d, int layer, int C, cudaStream_t s);
+cudaError_t launch_prefill_finish(const LaneDev& d, int C, int next_token, int* y_out, cudaStream_t s);
 cudaError_t launch_kv_pack_slot(const LaneDev& d, int slot, int n, void* packed, cudaStream_t s);
 cudaError_t launch_kv_pack(const bf16* k, const bf16* v, int n_layers, int Hkv, int dh, int n, int pending,
                            void* packed, cudaStream_t s);

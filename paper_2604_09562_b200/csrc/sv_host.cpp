@@ -796,11 +796,59 @@ sv_status sv_draft_planted_tree(sv_ctx* c, int32_t batch, const int32_t* slots, 
   return draft_planted_impl(c, batch, slots, depths, parents, succ, dev_mask, dev_tok, draft_tokens);
 }
 
+// one long chunk of a prompt (k_prefill.cu): C rows at positions L..L+C-1, every key from the pages;
+// last: final norm + lm-head of the last row, y -> pending / y_out; else pending = next_token
+static sv_status prefill_chunk(sv_ctx* c, int32_t slot, const int32_t* dtok, int C, bool last, int next_token,
+                               int32_t* y_out) {
+  sv::LaneDev d = c->d;
+  d.tree = 0;
+  d.filt_on = 0;
+  cudaStream_t s = c->stream;
+  const int G = d.Hq / d.Hkv, nqb = (C + 128 / G - 1) / (128 / G);
+  STAGE(c, ST_PLAN, sv::launch_prefill_plan(d, slot, dtok, C, s));
+  STAGE(c, ST_EMBED, sv::launch_embed_norm(d, C, s));
+  const size_t nq = (size_t)d.Hq * d.dh;
+  for (int layer = 0; layer < d.n_layers; ++layer) {
+    const float* hin = layer == 0 ? d.h0 : d.h2;
+    if (layer > 0) STAGE(c, ST_ATTN_NORM, sv::launch_rmsnorm(d, hin, d.attn_norm + (size_t)layer * d.D, d.a, C, s));
+    sv::GemmEpi e{};
+    e.layer = layer;
+    STAGE(c, ST_QKV, gemm(c, d.a, d.wqkv + (size_t)layer * d.qkv_rows * d.D, d.cbuf, C, d.qkv_rows, d.D,
+                          sv::EPI_QKV_ROPE, e));
+    STAGE(c, ST_COMMIT, sv::launch_prefill_kv(d, layer, C, s));
+    STAGE(c, ST_ATTN, sv::attn_prefill_run(c->gemm, layer, d.Hkv * nqb, s));
+    float* hattn = d.F > 0 ? d.h1 : d.h2;
+    e.resid_in = hin;
+    e.resid_out = hattn;
+    STAGE(c, ST_OPROJ, gemm(c, d.o, d.wo + (size_t)layer * d.D * nq, d.cbuf, C, d.D, (int)nq, sv::EPI_RESIDUAL, e));
+    if (d.F > 0) {
+      STAGE(c, ST_FFN_NORM, sv::launch_rmsnorm(d, d.h1, d.ffn_norm + (size_t)layer * d.D, d.b, C, s));
+      STAGE(c, ST_GATE_UP, gemm(c, d.b, d.w_gate_up + (size_t)layer * 2 * d.F * d.D, d.cbuf, C, 2 * d.F, d.D,
+                                sv::EPI_SWIGLU, e));
+      e.resid_in = d.h1;
+      e.resid_out = d.h2;
+      STAGE(c, ST_DOWN, gemm(c, d.u, d.w_down + (size_t)layer * d.D * d.F, d.cbuf, C, d.D, d.F, sv::EPI_RESIDUAL, e));
+    }
+  }
+  if (last) {                                   // only the last row predicts the next token
+    STAGE(c, ST_FINAL_NORM, sv::launch_rmsnorm(d, d.h2 + (size_t)(C - 1) * d.D, d.final_norm, d.z, 1, s));
+    sv::GemmEpi e{};
+    e.inv_temp = 1.0f;
+    e.write_out = c->taps;
+    STAGE(c, ST_LM_HEAD, gemm(c, d.z, d.lm_head, d.logits, 1, d.V, d.D, sv::EPI_LOGITS, e));
+  }
+  STAGE(c, ST_FINALIZE, sv::launch_prefill_finish(d, C, last ? -1 : next_token, y_out, s));
+  c->last_T = C;
+  c->last_batch = 1;
+  return SV_OK;
+}
+
 sv_status sv_prefill(sv_ctx* c, int32_t slot, uint64_t request_id, const int32_t* prompt, int32_t n, int32_t chunk,
                      int32_t* next_token) {
-  if (!c || slot < 0 || slot >= c->cfg.max_slots || !prompt || n < 1 || chunk < 1 || chunk > c->cfg.max_depth + 1)
-    return SV_EINVAL;
-  if (c->state[slot] != EMPTY || c->pending_verify) return SV_ESTATE;
+  if (!c || slot < 0 || slot >= c->cfg.max_slots || !prompt || n < 1 || chunk < 1) return SV_EINVAL;
+  const bool long_path = sv::attn_prefill_supported(c->gemm);
+  if (chunk > (long_path ? c->d.Tmax : c->cfg.max_depth + 1)) return SV_EINVAL;
+  if (c->state[slot] != EMPTY || c->pending_verify || c->capturing) return SV_ESTATE;
   for (int i = 0; i < n; ++i)
     if (prompt[i] < 0 || prompt[i] >= c->cfg.vocab) return SV_EINVAL;
   const int K1 = c->cfg.max_depth + 2;
@@ -808,30 +856,47 @@ sv_status sv_prefill(sv_ctx* c, int32_t slot, uint64_t request_id, const int32_t
   int32_t* dout = dacc + K1;                               // out_tokens [max_depth + 1]
   int32_t* dprompt = dout + K1;                            // the prompt [n <= max_pos]
   if (n > c->cfg.max_pos) return SV_EINVAL;
+  wait_comm_slots(c, 1, &slot);
   // one copy of the whole prompt (a per-chunk copy from pageable memory would block the host on
   // every chunk's previous work); the chunks then read their tokens in place
   SV_CUDA(cudaMemcpyAsync(dprompt, prompt, 4 * (size_t)n, cudaMemcpyHostToDevice, c->stream));
   sv_status st = sv_append_kv(c, slot, request_id, nullptr, nullptr, 0, prompt[0]);
   if (st) return st;
-  int pos = 1, k = 0;
-  for (;;) {
-    k = chunk - 1 < n - pos ? chunk - 1 : n - pos;
-    const int32_t* dtok = dprompt + pos;
-    // only the last chunk's lm-head matters (its last row predicts the next token)
-    const bool last = pos + k >= n;
-    if ((st = verify_impl(c, 1, &slot, &k, nullptr, dtok, nullptr, 0, SV_PREFILL, 1.0f, dacc, dout, nullptr, nullptr,
-                          last)))
-      return st;
-    if ((st = sv_commit(c, nullptr))) return st;
-    pos += k;
-    if (pos >= n) break;
-    if ((st = sv_append_kv(c, slot, request_id, nullptr, nullptr, 0, prompt[pos]))) return st;
-    pos += 1;
-  }
   int32_t y = -1;
-  SV_CUDA(cudaMemcpyAsync(&y, dout + k, 4, cudaMemcpyDeviceToHost, c->stream));
+  if (long_path) {
+    // chunks of the prompt itself: rows prompt[pos .. pos+C-1] at positions pos.. (the pending token
+    // set above is prompt[0], the first row of the first chunk)
+    for (int pos = 0; pos < n; pos += chunk) {
+      const int C = chunk < n - pos ? chunk : n - pos;
+      const bool last = pos + C >= n;
+      if ((st = prefill_chunk(c, slot, dprompt + pos, C, last, last ? -1 : prompt[pos + C], dacc))) return st;
+    }
+    SV_CUDA(cudaMemcpyAsync(&y, dacc, 4, cudaMemcpyDeviceToHost, c->stream));
+  } else {
+    // short chunks through the verify machinery (SV_PREFILL verifies, R29)
+    int pos = 1, k = 0;
+    for (;;) {
+      k = chunk - 1 < n - pos ? chunk - 1 : n - pos;
+      const int32_t* dtok = dprompt + pos;
+      // only the last chunk's lm-head matters (its last row predicts the next token)
+      const bool last = pos + k >= n;
+      if ((st = verify_impl(c, 1, &slot, &k, nullptr, dtok, nullptr, 0, SV_PREFILL, 1.0f, dacc, dout, nullptr,
+                            nullptr, last)))
+        return st;
+      if ((st = sv_commit(c, nullptr))) return st;
+      pos += k;
+      if (pos >= n) break;
+      if ((st = sv_append_kv(c, slot, request_id, nullptr, nullptr, 0, prompt[pos]))) return st;
+      pos += 1;
+    }
+    SV_CUDA(cudaMemcpyAsync(&y, dout + k, 4, cudaMemcpyDeviceToHost, c->stream));
+  }
   SV_CUDA(cudaStreamSynchronize(c->stream));
   if (y < 0) return SV_EDEVICE;
+  int err = 0;
+  SV_CUDA(cudaMemcpy(&err, c->d.err, 4, cudaMemcpyDeviceToHost));
+  c->sticky = err;
+  if (err & SV_DERR_NO_PAGES) return SV_ENOKV;
   if (next_token) *next_token = y;
   return SV_OK;
 }
