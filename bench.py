@@ -612,12 +612,18 @@ def run_disagg(args, wl, rank, world, dev):
     res = {}
     with torch.cuda.stream(stream):
         pre = dec = None
+        prefill_ms = None
         if role in ("prefill", "both"):
+            # the producer: real chunked prefill (NEXT-3, sv_prefill) of B random prompts, untimed
             pre = sv.Lane(pcfg, wd, stream=stream)
+            chunk = min(pcfg.max_batch * (pcfg.max_depth + 1), 1024)
+            t0 = time.perf_counter()
             for i in range(B):
-                k, v = synth.context_kv(pcfg, n_tok, seed=30_000 * (pair + 1) + i, device=dev)
-                pend = int(synth.random_tokens(1, pcfg.vocab, seed=40_000 * (pair + 1) + i)[0])
-                pre.append_kv(i, svdist.request_id(rank, 10**6 + i), k, v, pend)
+                prompt = synth.random_tokens(n_tok, pcfg.vocab, seed=30_000 * (pair + 1) + i).tolist()
+                pre.prefill(i, svdist.request_id(rank, 10**6 + i), prompt, chunk)
+            torch.cuda.synchronize(dev)
+            prefill_ms = {"requests": B, "tokens_each": n_tok, "chunk": chunk,
+                          "ms": round(1e3 * (time.perf_counter() - t0), 1)}
         if role in ("decode", "both"):
             dec = sv.Lane(dcfg, wd, stream=stream)
         torch.cuda.synchronize(dev)
@@ -701,7 +707,8 @@ def run_disagg(args, wl, rank, world, dev):
                                       "(+ the prefill-side gather in loopback)",
                               "transport": "NCCL loopback on one GPU (flow check, not NVLink)" if role == "both"
                                            else "NCCL p2p, one op per batch, page-block gather / scatter",
-                              "overlap": f"transfer on the comm stream while {DISAGG_STEPS_PER_ROUND} verify steps run"}
+                              "overlap": f"transfer on the comm stream while {DISAGG_STEPS_PER_ROUND} verify steps run",
+                              "producer_prefill": prefill_ms}
     elapsed, tokens = svdist.reduce_region(elapsed, tokens, device=dev if world > 1 else None)
     sv.nccl_comm_destroy(comm)
     steps = rounds * DISAGG_STEPS_PER_ROUND

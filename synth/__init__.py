@@ -265,3 +265,35 @@ def planted_masks_req(n_steps, batch, kmax, alphas, vocab, seed):
 def as_f64(t):
     """bf16/fp32 torch tensor -> numpy fp64 (exact)."""
     return t.detach().to("cpu").to(torch.float64).numpy()
+
+
+# ---------------------------------------------------------------- config 5: mixed serving trace
+# BASELINE configs[4] / SURVEY.md §8(d) config 5: 80 queries each of ALPACA (prompt 256), GSM8K and
+# HUMANEVAL (prompt U[1k, 2k]) and SUM (prompt 8k); output lengths lognormal with the SPEC.md:420
+# medians 60 / 150 / 220 / 90 and sigma 0.5 (our choice); planted acceptance profiles
+# p0 = 0.70 / 0.72 / 0.75 / 0.85 (SPEC.md:420). Seeded; no method arithmetic.
+TRACE_PROFILES = {            # dataset: (prompt_lo, prompt_hi, output median, acceptance p0)
+    "ALPACA": (256, 256, 60, 0.70),
+    "GSM8K": (1024, 2048, 150, 0.72),
+    "HUMANEVAL": (1024, 2048, 220, 0.75),
+    "SUM": (8192, 8192, 90, 0.85),
+}
+
+
+def mixed_trace(n_per_dataset=80, seed=0, sigma=0.5, max_out=1024):
+    """The 320-query trace as a list of dicts (qid, dataset, prompt_len, out_len, alpha, prompt_seed),
+    datasets interleaved in a seeded random order."""
+    g = _gen(seed)
+    qs = []
+    for name, (lo, hi, med, p0) in TRACE_PROFILES.items():
+        plen = torch.randint(lo, hi + 1, (n_per_dataset,), generator=g)
+        z = torch.randn(n_per_dataset, generator=g, dtype=torch.float64)
+        out = torch.clamp((med * torch.exp(sigma * z)).round(), 1, max_out).to(torch.int64)
+        for i in range(n_per_dataset):
+            qs.append(dict(dataset=name, prompt_len=int(plen[i]), out_len=int(out[i]), alpha=p0))
+    order = torch.randperm(len(qs), generator=g).tolist()
+    trace = [qs[i] for i in order]
+    for qid, q in enumerate(trace):
+        q["qid"] = qid
+        q["prompt_seed"] = 1_000_003 * (seed + 1) + qid
+    return trace
