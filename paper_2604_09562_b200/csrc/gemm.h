@@ -22,6 +22,8 @@ GemmPlan* gemm_plan_create(const LaneDev& d, void* ws, cudaStream_t s);
 void gemm_plan_destroy(GemmPlan* p);
 // a3 verify attention: tcgen05 kernel when the shape allows (page 64, d_h 64/128), else SIMT
 cudaError_t attn_run(GemmPlan* p, int layer, int batch, int tree, cudaStream_t s);
+// true when attn_run's kernel writes O itself for requests with a single split-KV item
+bool attn_writes_single_split(GemmPlan* p);
 // NEXT-3 long-chunk prefill attention (tcgen05 rows-on-lanes, G in {1, 2, 4})
 bool attn_prefill_supported(GemmPlan* p);
 cudaError_t attn_prefill_run(GemmPlan* p, int layer, int n_items, cudaStream_t s);

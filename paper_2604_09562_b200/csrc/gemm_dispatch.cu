@@ -158,6 +158,8 @@ cudaError_t attn_run(GemmPlan* p, int layer, int batch, int tree, cudaStream_t s
   return launch_attention(d, layer, batch, s);
 }
 
+bool attn_writes_single_split(GemmPlan* p) { return p->use_tc2_attn && p->attn_maps_ok; }
+
 bool attn_prefill_supported(GemmPlan* p) {
   const LaneDev& d = p->d;
   const int G = d.Hq / d.Hkv;

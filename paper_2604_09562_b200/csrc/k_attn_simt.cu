@@ -139,7 +139,7 @@ cudaError_t launch_attention(const LaneDev& d, int layer, int batch, cudaStream_
 // d_h = 128, float2 for 64); the loads of up to 8 splits are issued together, with an online
 // rescale between chunks. O = sum_s e^(m_s - M) O_s / sum_s e^(m_s - M) l_s, M = max m_s.
 template <int DH>
-__global__ void __launch_bounds__(256) attn_combine_kernel(LaneDev d, int T) {
+__global__ void __launch_bounds__(256) attn_combine_kernel(LaneDev d, int T, int skip_single) {
   pdl_trigger();
   pdl_wait();
   constexpr int V = DH / 32;                       // floats per lane
@@ -154,6 +154,7 @@ __global__ void __launch_bounds__(256) attn_combine_kernel(LaneDev d, int T) {
   }
   __syncthreads();
   const int j = s_j, ns = s_ns;
+  if (skip_single && ns == 1) return;              // the attention kernel wrote this row's O
   const int G = d.Hq / d.Hkv;
   for (int hq = warp; hq < d.Hq; hq += 8) {
     const int h = hq / G, g = hq % G, rl = j * G + g;
@@ -203,10 +204,10 @@ __global__ void __launch_bounds__(256) attn_combine_kernel(LaneDev d, int T) {
   }
 }
 
-cudaError_t launch_attn_combine(const LaneDev& d, int T, cudaStream_t s) {
+cudaError_t launch_attn_combine(const LaneDev& d, int T, bool skip_single, cudaStream_t s) {
   SV_COUNT_LAUNCH();
-  if (d.dh == 128) return launch_pdl(attn_combine_kernel<128>, dim3(T), dim3(256), 0, s, 1, d, T);
-  return launch_pdl(attn_combine_kernel<64>, dim3(T), dim3(256), 0, s, 1, d, T);
+  if (d.dh == 128) return launch_pdl(attn_combine_kernel<128>, dim3(T), dim3(256), 0, s, 1, d, T, (int)skip_single);
+  return launch_pdl(attn_combine_kernel<64>, dim3(T), dim3(256), 0, s, 1, d, T, (int)skip_single);
 }
 
 }  // namespace sv

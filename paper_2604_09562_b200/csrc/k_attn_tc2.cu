@@ -543,20 +543,42 @@ __global__ void __launch_bounds__(THREADS, 1)
       float ltot = __uint_as_float(lv[0]);
 #pragma unroll
       for (int c = 1; c < 32; ++c) ltot = lane == c ? __uint_as_float(lv[c]) : ltot;
-      float* po = d.part_o + (size_t)it * kAttnRows * DH + q * 32 + lane;
+      const size_t ldo = (size_t)d.Hq * DH;
+      const int dcol = q * 32 + lane;                 // this thread's d_h index (TMEM lane of O^T)
+      if (I.ns == 1) {
+        // one split: the item holds every key of its rows; normalise and write O (bf16) directly
+        tc::fence_before();
+        tc::mbar_arrive(&o_empty[ob]);                // O^T / L^T are in registers
 #pragma unroll
-      for (int c = 0; c < 32; ++c) {
-        const int r = ch * 32 + c;
-        if (r < RG) po[(size_t)r * DH] = __uint_as_float(ov[c]);
+        for (int c = 0; c < 32; ++c) {
+          const int r = ch * 32 + c;
+          if (r < RG) {
+            const float l = __uint_as_float(lv[c]);
+            d.o[(size_t)(I.row0 + (r >> lg)) * ldo + (size_t)(I.h * G + (r & (G - 1))) * DH + dcol] =
+                __float2bfloat16_rn(__uint_as_float(ov[c]) / l);
+          }
+        }
+        tc::named_bar(bar_id, 128);                   // exchange slots are reused by the next item
+      } else {
+        float* po = d.part_o + (size_t)it * kAttnRows * DH + dcol;
+#pragma unroll
+        for (int c = 0; c < 32; ++c) {
+          const int r = ch * 32 + c;
+          if (r < RG) po[(size_t)r * DH] = __uint_as_float(ov[c]);
+        }
+        const int my_slot = ch * 32 + lane;
+        if (q == 0 && my_slot < RG) {
+          d.part_ml[((size_t)it * kAttnRows + my_slot) * 2 + 0] = my_init ? my_m * 0.69314718055994531f : -INFINITY;
+          d.part_ml[((size_t)it * kAttnRows + my_slot) * 2 + 1] = ltot;
+        }
+        tc::named_bar(bar_id, 128);                   // exchange slots are reused by the next item
+        tc::fence_before();
+        tc::mbar_arrive(&o_empty[ob]);
       }
-      const int my_slot = ch * 32 + lane;
-      if (q == 0 && my_slot < RG) {
-        d.part_ml[((size_t)it * kAttnRows + my_slot) * 2 + 0] = my_init ? my_m * 0.69314718055994531f : -INFINITY;
-        d.part_ml[((size_t)it * kAttnRows + my_slot) * 2 + 1] = ltot;
-      }
-      tc::named_bar(bar_id, 128);                     // exchange slots are reused by the next item
-      tc::fence_before();
-      tc::mbar_arrive(&o_empty[ob]);
+      // Items of a split request leave partials for attn_combine_kernel. A fused merge in the last
+      // item of each (request, kv head) to finish was measured (scripts/ab_live.sh, ns, serial ncu):
+      // 337 us against 198 + 16 us for this kernel + the combine — the per-thread release fence alone
+      // cost 36 us and the merge's L2 round trips stalled the softmax pipeline — so it is not used.
       if (warp == 4 && lane == 0) SV_TR2(7, iter);
     }
   }

@@ -136,7 +136,8 @@ cudaError_t launch_residual_epilogue(const float* hin, const float* c, float* ho
 cudaError_t launch_swiglu_epilogue(const LaneDev& d, int T, cudaStream_t s);
 cudaError_t launch_tile_stats(const LaneDev& d, int T, float inv_temp, cudaStream_t s);
 cudaError_t launch_attention(const LaneDev& d, int layer, int batch, cudaStream_t s);
-cudaError_t launch_attn_combine(const LaneDev& d, int T, cudaStream_t s);
+// skip_single: rows of requests with one split-KV item were written by the attention kernel itself
+cudaError_t launch_attn_combine(const LaneDev& d, int T, bool skip_single, cudaStream_t s);
 cudaError_t launch_finalize(const LaneDev& d, int batch, const int* draft_tokens, const int* parents,
                             const float* draft_probs, const float* logits, uint64_t seed, int mode, float inv_temp,
                             int* accepted_len, int* out_tokens, int* accepted_nodes, cudaStream_t s);

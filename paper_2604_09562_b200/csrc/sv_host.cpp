@@ -527,7 +527,7 @@ static sv_status verify_impl(sv_ctx* c, int32_t batch, const int32_t* slots, con
     STAGE(c, ST_QKV, gemm(c, d.a, d.wqkv + (size_t)layer * d.qkv_rows * d.D, d.cbuf, T, d.qkv_rows, d.D,
                           sv::EPI_QKV_ROPE, e));
     STAGE(c, ST_ATTN, sv::attn_run(c->gemm, layer, batch, d.tree, s));
-    STAGE(c, ST_COMBINE, sv::launch_attn_combine(d, T, s));
+    STAGE(c, ST_COMBINE, sv::launch_attn_combine(d, T, sv::attn_writes_single_split(c->gemm), s));
     float* hattn = d.F > 0 ? d.h1 : d.h2;
     e.resid_in = hin;
     e.resid_out = hattn;

@@ -10,6 +10,6 @@ print('$so ncu', [(r[ki][:8], int(r[vi])//100/10) for r in rows[1:] if 'attn' in
 done
 for rep in 1 2; do
   for so in "$@"; do
-    SV_LIBSV=$PWD/$so timeout 300 python bench.py --steps ${STEPS:-200} --warmup 10 --e2e-steps 0 --no-cpu-baseline 2>/dev/null | python -c "import json,sys; d=json.load(sys.stdin); k=d['kernels']; print('$so live', d['value'], d['ms_per_step'], k['attention']['us_per_launch'], k['attention']['frac'], d['clocks']['sm_mhz'])"
+    SV_LIBSV=$PWD/$so timeout 300 python bench.py --steps ${STEPS:-200} --warmup 10 --e2e-steps 0 --no-cpu-baseline --steady-s 0 --check-steps 0 2>/dev/null | python -c "import json,sys; d=json.load(sys.stdin); k=d['kernels']; print('$so live', d['value'], d['ms_per_step'], k['attention']['us_per_launch'], k['attention']['frac'], d['clocks']['sm_mhz'])"
   done
 done
