@@ -418,6 +418,27 @@ sv_status sv_kv_pack(const void* k, const void* v, int32_t n_layers, int32_t n_k
                      int32_t head_dim, int32_t n_tokens, int32_t pending_token, void* kv_packed,
                      sv_stream_t stream);
 
+/* ---------------- fp32-SIMT exactness instantiation (NEXT-4; S19) ----------------
+ * The verify step's model arithmetic (a2-a5: embed, RMSNorm, QKV, RoPE, chain-causal GQA attention over
+ * the cache, O-proj + residual, RMSNorm, SwiGLU MLP + residual, final RMSNorm, lm-head) with fp32
+ * operands, fp32 accumulation and NO bf16 rounding anywhere: its logits sit within fp32 accumulation
+ * error of the fp64 definition (the oracle with its bf16 rounding points switched off). Plain SIMT
+ * kernels, stateless; decisions on the logits go through sv_verify_logits (the same finalize). */
+typedef struct { /* device pointers, fp32, the layouts of sv_weights; BORROWED */
+  const float *embed, *attn_norm, *wqkv, *wo, *ffn_norm, *w_gate_up, *w_down, *final_norm, *lm_head;
+} sv_weights_f32;
+/* Workspace bytes for T chain rows (the RoPE table covers positions < cfg->max_pos). */
+sv_status sv_exact_query_sizes(const sv_config* cfg, int32_t T, size_t* workspace_bytes);
+/* logits [T][V] fp32 (device) of the chain rows of `batch` requests: request b's rows
+ * row_off[b]..row_off[b+1]-1 (host, row_off[0] = 0, T = row_off[batch]) hold tokens chain_tok (device
+ * [T]) at positions ctx_len[b] + j (host ctx_len); its context K/V (post-RoPE) are the first ctx_len[b]
+ * rows of cache_k / cache_v (device fp32 [n_layers][batch][max_ctx][H_kv][d_h], dense; NULL when every
+ * ctx_len is 0). Enqueued on `stream`. EINVAL on bad sizes, positions >= max_pos or a short workspace. */
+sv_status sv_exact_forward(const sv_config* cfg, const sv_weights_f32* w, int32_t batch, const int32_t* row_off,
+                           const int32_t* chain_tok, const int32_t* ctx_len, const float* cache_k,
+                           const float* cache_v, int32_t max_ctx, void* workspace, size_t workspace_bytes,
+                           float* logits, sv_stream_t stream);
+
 /* ---------------- SpecuStream depth controller (NEXT-1; host code, no device work) ----------------
  * PAPER.md §3.5, Alg. 4 "SpecuStream Adaptation", eq:acceptance_gradient ..
  * eq_exponential_smoothing, readings DESIGN.md R21-R24. One sv_flow_state per

@@ -29,7 +29,7 @@ EXPORTED = [
     "sv_draft_planted", "sv_nccl_unique_id", "sv_nccl_comm_init", "sv_nccl_comm_destroy", "sv_kv_send",
     "sv_kv_recv_append", "sv_kv_packed_bytes", "sv_kv_pack", "sv_profile_enable", "sv_profile_num_stages",
     "sv_profile_stage_name", "sv_profile_read", "sv_launch_count", "sv_debug_gemm", "sv_kv_append_packed",
-    "sv_kv_loopback_append", "sv_kv_send_slots", "sv_kv_recv_slots", "sv_kv_loopback_slots", "sv_comm_stream", "sv_kv_slots_bytes", "sv_spec_default_config", "sv_spec_reset", "sv_spec_adapt", "sv_spec_step",
+    "sv_kv_loopback_append", "sv_kv_send_slots", "sv_kv_recv_slots", "sv_kv_loopback_slots", "sv_comm_stream", "sv_kv_slots_bytes", "sv_exact_query_sizes", "sv_exact_forward", "sv_spec_default_config", "sv_spec_reset", "sv_spec_adapt", "sv_spec_step",
     "sv_route_default_config", "sv_route_select", "sv_lane_occupancy", "sv_kv_pack_slot", "sv_prefill",
     "sv_verify_tree", "sv_verify_tree_logits", "sv_set_filter", "sv_draft_planted_tree", "sv_graph_begin",
     "sv_graph_end", "sv_graph_launch", "sv_graph_destroy",
@@ -133,6 +133,8 @@ def load():
         "sv_kv_recv_slots": ([vp, i32, vp, vp, vp, vp, ctypes.c_int, vp], ctypes.c_int),
         "sv_kv_loopback_slots": ([vp, vp, i32, vp, vp, vp, vp, vp, vp, ctypes.c_int, vp], ctypes.c_int),
         "sv_kv_slots_bytes": ([P(Config), i32, vp], sz),
+        "sv_exact_query_sizes": ([P(Config), i32, P(sz)], ctypes.c_int),
+        "sv_exact_forward": ([P(Config), P(Weights), i32, vp, vp, vp, vp, vp, i32, vp, sz, vp, vp], ctypes.c_int),
         "sv_kv_packed_bytes": ([P(Config), i32], sz),
         "sv_kv_pack": ([vp, vp, i32, i32, i32, i32, i32, vp, vp], ctypes.c_int),
         "sv_profile_enable": ([vp, ctypes.c_int32], ctypes.c_int),
@@ -496,3 +498,30 @@ def kv_send(packed, n_layers, n_kv_heads, head_dim, n_tokens, peer, comm, stream
 def packed_bytes(cfg, n_tokens):
     c = Config.from_any(cfg)
     return int(load().sv_kv_packed_bytes(ctypes.byref(c), n_tokens))
+
+
+def exact_forward(cfg, weights_f32, row_off, chain_tok, ctx_len, cache_k=None, cache_v=None, stream=None):
+    """fp32-SIMT exactness instantiation (sv_exact_forward, NEXT-4): logits [T][V] fp32 of the chain rows.
+    weights_f32: dict of fp32 device tensors (sv_weights names); chain_tok: device int32 [T];
+    row_off / ctx_len: host lists; cache_k / cache_v: device fp32 [n_layers][batch][max_ctx][Hkv][dh]."""
+    lib = load()
+    c = Config.from_any(cfg)
+    T = int(row_off[-1])
+    dev = chain_tok.device
+    for k, v in weights_f32.items():
+        assert v.dtype == torch.float32 and v.is_contiguous() and v.device == dev, k
+    wts = Weights(*[ctypes.c_void_p(weights_f32[n].data_ptr()) if n in weights_f32 else None for n in WEIGHT_NAMES])
+    need = ctypes.c_size_t()
+    _check(lib.sv_exact_query_sizes(ctypes.byref(c), T, ctypes.byref(need)), "sv_exact_query_sizes")
+    ws = torch.empty(need.value, dtype=torch.uint8, device=dev)
+    logits = torch.empty(T, c.vocab, dtype=torch.float32, device=dev)
+    ro, _ = _i32_array(row_off)
+    cl, batch = _i32_array(ctx_len)
+    max_ctx = int(cache_k.shape[2]) if cache_k is not None else 0
+    st = stream if stream is not None else torch.cuda.current_stream(dev)
+    _check(lib.sv_exact_forward(ctypes.byref(c), ctypes.byref(wts), batch, ro, _ptr(chain_tok), cl,
+                                None if cache_k is None else ctypes.c_void_p(cache_k.data_ptr()),
+                                None if cache_v is None else ctypes.c_void_p(cache_v.data_ptr()), max_ctx,
+                                ctypes.c_void_p(ws.data_ptr()), ws.numel(), ctypes.c_void_p(logits.data_ptr()),
+                                ctypes.c_void_p(st.cuda_stream)), "sv_exact_forward")
+    return logits, ws
