@@ -132,8 +132,9 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int G = d.Hq / d.Hkv;
   const size_t nkv = (size_t)d.Hkv * DH;
 
-  // zero the K/V ring and Q once: skipped second pages / unloaded slots must hold finite values
-  for (int i = threadIdx.x; i < ((KST + VST) * KV_BYTES + Q_BYTES) / 16; i += THREADS)
+  // zero the K/V ring, Q and P^T once: skipped second pages / unloaded slots / the P^T columns a
+  // narrow slot half does not write must hold finite values
+  for (int i = threadIdx.x; i < ((KST + VST) * KV_BYTES + Q_BYTES + 2 * P_BYTES) / 16; i += THREADS)
     reinterpret_cast<uint4*>(sK)[i] = make_uint4(0, 0, 0, 0);
   tc::fence_proxy_async();
   if (warp == 0 && lane == 0) {
@@ -389,6 +390,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       float* fac = fs + ch * 32;
       float* thr = thr_s + ch * 32;
       uint32_t minit = 0;
+      const bool narrow = RG - ch * 32 <= 8;          // warp-uniform for the whole item (empty halves too)
       if (q == 0) {
         mref[lane] = 0.f;
         thr[lane] = -INFINITY;                        // no reference yet: any finite score raises
@@ -399,131 +401,264 @@ __global__ void __launch_bounds__(THREADS, 1)
         tc::mbar_wait(&s_full[sb], (g >> 1) & 1);
         if (warp == 4 && lane == 0) SV_TR2(5, g);
         tc::fence_after();
-        uint32_t sv[32];
-        __syncwarp();
-        tc::tmem_ld32(tmem + lane_off + S_COL + sb * NQ + ch * 32, sv);
-        tc::tmem_ld_wait();
-        tc::fence_before();
-        tc::mbar_arrive(&s_read[sb]);                 // the MMA may write S^T(g+2) into this buffer
-        if (warp == 4 && lane == 0) SV_TR2(8, g);
-        const bool chain_tile = t >= I.n_page_tiles;
-        const int key = (chain_tile ? I.L : I.t0 + t * KT) + kidx;
-        const bool kvalid = key < (chain_tile ? I.L + I.R : I.kend);
-        // visibility mask over this lane's 32 slots: key valid, slot exists, and (chain tile) causal:
-        // chain key kidx is visible to slot r iff kidx <= r / G  <=>  r >= kidx * G
-        uint32_t vm = kvalid ? colok : 0u;
-        if (chain_tile) {
-          if (d.tree) {
-            // token tree (R30): chain key kidx is visible to row j iff kidx is an
-            // ancestor-or-self of node j (row_anc bit); rows j of this half hold slots jG..jG+G-1
-            uint32_t tm = 0;
-            if (kvalid) {
-              const int j0 = (ch * 32) >> lg, j1 = min(I.R, (ch * 32 + 32) >> lg);
-              for (int j = j0; j < j1; ++j)
-                if ((d.row_anc[I.row0 + j] >> kidx) & 1ull) tm |= uint32_t((1ull << G) - 1ull) << ((j << lg) - ch * 32);
-            }
-            vm &= tm;
-          } else {
-            const int first = (kidx << lg) - ch * 32;
-            vm &= first <= 0 ? 0xffffffffu : (first >= 32 ? 0u : (0xffffffffu << first));
-          }
-        }
-        float x[32];
-        bool need = false;
-#pragma unroll
-        for (int c = 0; c < 32; c += 4) {
-          const float4 t4 = *reinterpret_cast<const float4*>(thr + c);
-          const float th[4] = {t4.x, t4.y, t4.z, t4.w};
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float s = __uint_as_float(sv[c + e]) * sl2e;
-            x[c + e] = ((vm >> (c + e)) & 1u) ? s : -INFINITY;
-            need |= x[c + e] > th[e];
-          }
-        }
-        // does any of the 128 keys push a column beyond its reference (+2^8)? (4-warp vote)
-        float* xc = xcol + ((sb * 2 + ch) * 4) * 32;
-        const bool wneed = __any_sync(0xffffffffu, need);
-        if (lane == 0) xc[q * 32] = wneed ? 1.f : 0.f;
-        tc::named_bar(bar_id, 128);
-        const bool raise_any = xc[0] + xc[32] + xc[64] + xc[96] > 0.f;   // uniform in the 4 warps
-        if (warp == 4 && lane == 0) SV_TR2(9, g);
-        if (g > 1) {                                   // PV(g-2) has released this P^T buffer
-          const uint32_t pg = g - 2;
-          tc::mbar_wait(&s_free[pg & 1], (pg >> 1) & 1);
-          tc::fence_after();
-        }
-        if (warp == 4 && lane == 0) SV_TR2(10, g);
-        if (raise_any) {
-          // exact column max over the 128 keys: transpose-reduce inside the warp (lane c ends with
-          // column c), then across the 4 quadrant warps through shared memory
-          float v[32];
-#pragma unroll
-          for (int c = 0; c < 32; ++c) v[c] = x[c];
-#pragma unroll
-          for (int s = 16; s >= 1; s >>= 1) {
-            const bool up = lane & s;
-#pragma unroll
-            for (int i = 0; i < s; ++i) {
-              const float send = up ? v[i] : v[i + s];
-              const float keep = up ? v[i + s] : v[i];
-              v[i] = fmaxf(keep, __shfl_xor_sync(0xffffffffu, send, s));
+        // The columns this warp computes: all 32, or only the first 8 when this slot half holds at most
+        // 8 real slots (k = 8 at G = 4: 36 slots, 4 in the second half; k <= 7: an empty half). The
+        // other columns of a narrow half are masked slots whose P^T entries stay finite stale values and
+        // whose O^T / L^T columns are never read. Two textual copies (a shared generic lambda made the
+        // 32-column path ~25 % slower at k = 11 / 15).
+        if (narrow) {
+          uint32_t sv[8];
+          __syncwarp();
+          tc::tmem_ld8(tmem + lane_off + S_COL + sb * NQ + ch * 32, sv);
+          tc::tmem_ld_wait();
+          tc::fence_before();
+          tc::mbar_arrive(&s_read[sb]);               // the MMA may write S^T(g+2) into this buffer
+          if (warp == 4 && lane == 0) SV_TR2(8, g);
+          const bool chain_tile = t >= I.n_page_tiles;
+          const int key = (chain_tile ? I.L : I.t0 + t * KT) + kidx;
+          const bool kvalid = key < (chain_tile ? I.L + I.R : I.kend);
+          // visibility mask over this lane's 32 slots: key valid, slot exists, and (chain tile) causal:
+          // chain key kidx is visible to slot r iff kidx <= r / G  <=>  r >= kidx * G
+          uint32_t vm = kvalid ? colok : 0u;
+          if (chain_tile) {
+            if (d.tree) {
+              // token tree (R30): chain key kidx is visible to row j iff kidx is an
+              // ancestor-or-self of node j (row_anc bit); rows j of this half hold slots jG..jG+G-1
+              uint32_t tm = 0;
+              if (kvalid) {
+                const int j0 = (ch * 32) >> lg, j1 = min(I.R, (ch * 32 + 32) >> lg);
+                for (int j = j0; j < j1; ++j)
+                  if ((d.row_anc[I.row0 + j] >> kidx) & 1ull) tm |= uint32_t((1ull << G) - 1ull) << ((j << lg) - ch * 32);
+              }
+              vm &= tm;
+            } else {
+              const int first = (kidx << lg) - ch * 32;
+              vm &= first <= 0 ? 0xffffffffu : (first >= 32 ? 0u : (0xffffffffu << first));
             }
           }
-          float* xm = xcol + (((sb ^ 1) * 2 + ch) * 4) * 32;   // other parity: free this tile
-          xm[q * 32 + lane] = v[0];
+          float x[8];
+          bool need = false;
+#pragma unroll
+          for (int c = 0; c < 8; c += 4) {
+            const float4 t4 = *reinterpret_cast<const float4*>(thr + c);
+            const float th[4] = {t4.x, t4.y, t4.z, t4.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float sc = __uint_as_float(sv[c + e]) * sl2e;
+              x[c + e] = ((vm >> (c + e)) & 1u) ? sc : -INFINITY;
+              need |= x[c + e] > th[e];
+            }
+          }
+          // does any of the 128 keys push a column beyond its reference (+2^8)? (4-warp vote)
+          float* xc = xcol + ((sb * 2 + ch) * 4) * 32;
+          const bool wneed = __any_sync(0xffffffffu, need);
+          if (lane == 0) xc[q * 32] = wneed ? 1.f : 0.f;
           tc::named_bar(bar_id, 128);
-          // lane c decides column c (identically in the 4 warps)
-          const float cm = fmaxf(fmaxf(xm[lane], xm[32 + lane]), fmaxf(xm[64 + lane], xm[96 + lane]));
-          const float old = mref[lane];
-          const bool init = (minit >> lane) & 1u;
-          const bool raise = init ? cm > old + kRescaleLog2 : cm > -INFINITY;
-          const float f = (raise && init) ? tc::ex2(old - cm) : 1.0f;
-          const bool any_resc = __any_sync(0xffffffffu, raise && init);
-          minit |= __ballot_sync(0xffffffffu, raise);
-          tc::named_bar(bar_id, 128);                 // all reads of the old references are done
-          if (q == 0) {
-            if (raise) {
-              mref[lane] = cm;
-              thr[lane] = cm + kRescaleLog2;
-            }
-            fac[lane] = f;
-          }
-          tc::named_bar(bar_id, 128);                 // new references / factors visible
-          if (any_resc) {                             // uniform: every warp sees the same factors
-            // O^T and the column sums L^T (this warp's 32 lanes x 32 slots) *= f(slot), once
-            // PV(g-1) has landed in them
-            const uint32_t pg = g - 1;
+          const bool raise_any = xc[0] + xc[32] + xc[64] + xc[96] > 0.f;   // uniform in the 4 warps
+          if (warp == 4 && lane == 0) SV_TR2(9, g);
+          if (g > 1) {                                 // PV(g-2) has released this P^T buffer
+            const uint32_t pg = g - 2;
             tc::mbar_wait(&s_free[pg & 1], (pg >> 1) & 1);
             tc::fence_after();
-            for (int buf = 0; buf < 2; ++buf) {
-              const uint32_t a = tmem + lane_off + (buf ? L_COL : O_COL) + (iter & 1) * NQ + ch * 32;
-              uint32_t ov[32];
-              tc::tmem_ld32(a, ov);
-              tc::tmem_ld_wait();
-#pragma unroll
-              for (int c = 0; c < 32; ++c) ov[c] = __float_as_uint(__uint_as_float(ov[c]) * fac[c]);
-              tc::tmem_st32(a, ov);
-            }
-            tc::tmem_st_wait();
           }
-        }
-        // P^T row (this key) for 32 slots -> bf16 -> swizzled st.shared
-        uint32_t pk[16];
+          if (warp == 4 && lane == 0) SV_TR2(10, g);
+          if (raise_any) {
+            // exact column max over the 128 keys inside the warp (lane c ends with column c), then
+            // across the 4 quadrant warps through shared memory
+            float cmw;
+            {                                          // 8 columns: one redux per column
+              cmw = -INFINITY;
 #pragma unroll
-        for (int c = 0; c < 32; c += 2) {
-          const float2 m2 = *reinterpret_cast<const float2*>(mref + c);
-          const float p0 = tc::ex2(x[c] - m2.x);           // x = -inf -> 0 (mref finite: 0 if unset)
-          const float p1 = tc::ex2(x[c + 1] - m2.y);
-          const __nv_bfloat162 pp = __floats2bfloat162_rn(p0, p1);
-          pk[c / 2] = *reinterpret_cast<const uint32_t*>(&pp);
-        }
-        if (warp == 4 && lane == 0) SV_TR2(11, g);
-        uint8_t* prow = sP + sb * P_BYTES + kidx * 128;
+              for (int c = 0; c < 8; ++c) {
+                const float m = redux_max(x[c]);
+                cmw = lane == c ? m : cmw;
+              }
+            }
+            float* xm = xcol + (((sb ^ 1) * 2 + ch) * 4) * 32;   // other parity: free this tile
+            xm[q * 32 + lane] = cmw;
+            tc::named_bar(bar_id, 128);
+            // lane c decides column c (identically in the 4 warps)
+            const float cm = fmaxf(fmaxf(xm[lane], xm[32 + lane]), fmaxf(xm[64 + lane], xm[96 + lane]));
+            const float old = mref[lane];
+            const bool init = (minit >> lane) & 1u;
+            const bool raise = init ? cm > old + kRescaleLog2 : cm > -INFINITY;
+            const float f = (raise && init) ? tc::ex2(old - cm) : 1.0f;
+            const bool any_resc = __any_sync(0xffffffffu, raise && init);
+            minit |= __ballot_sync(0xffffffffu, raise);
+            tc::named_bar(bar_id, 128);               // all reads of the old references are done
+            if (q == 0) {
+              if (raise) {
+                mref[lane] = cm;
+                thr[lane] = cm + kRescaleLog2;
+              }
+              fac[lane] = f;
+            }
+            tc::named_bar(bar_id, 128);               // new references / factors visible
+            if (any_resc) {                           // uniform: every warp sees the same factors
+              // O^T and the column sums L^T (this warp's 32 lanes x 32 slots) *= f(slot), once
+              // PV(g-1) has landed in them
+              const uint32_t pg = g - 1;
+              tc::mbar_wait(&s_free[pg & 1], (pg >> 1) & 1);
+              tc::fence_after();
+              for (int buf = 0; buf < 2; ++buf) {
+                const uint32_t a = tmem + lane_off + (buf ? L_COL : O_COL) + (iter & 1) * NQ + ch * 32;
+                uint32_t ov[32];
+                tc::tmem_ld32(a, ov);
+                tc::tmem_ld_wait();
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
-          *reinterpret_cast<uint4*>(prow + (((ch * 4 + i) ^ (kidx & 7)) * 16)) =
-              make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+                for (int c = 0; c < 32; ++c) ov[c] = __float_as_uint(__uint_as_float(ov[c]) * fac[c]);
+                tc::tmem_st32(a, ov);
+              }
+              tc::tmem_st_wait();
+            }
+          }
+          // P^T row (this key) for the NC slots -> bf16 -> swizzled st.shared
+          uint32_t pk[4];
+#pragma unroll
+          for (int c = 0; c < 8; c += 2) {
+            const float2 m2 = *reinterpret_cast<const float2*>(mref + c);
+            const float p0 = tc::ex2(x[c] - m2.x);         // x = -inf -> 0 (mref finite: 0 if unset)
+            const float p1 = tc::ex2(x[c + 1] - m2.y);
+            const __nv_bfloat162 pp = __floats2bfloat162_rn(p0, p1);
+            pk[c / 2] = *reinterpret_cast<const uint32_t*>(&pp);
+          }
+          if (warp == 4 && lane == 0) SV_TR2(11, g);
+          uint8_t* prow = sP + sb * P_BYTES + kidx * 128;
+#pragma unroll
+          for (int i = 0; i < 1; ++i)
+            *reinterpret_cast<uint4*>(prow + (((ch * 4 + i) ^ (kidx & 7)) * 16)) =
+                make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+        } else {
+          uint32_t sv[32];
+          __syncwarp();
+          tc::tmem_ld32(tmem + lane_off + S_COL + sb * NQ + ch * 32, sv);
+          tc::tmem_ld_wait();
+          tc::fence_before();
+          tc::mbar_arrive(&s_read[sb]);               // the MMA may write S^T(g+2) into this buffer
+          if (warp == 4 && lane == 0) SV_TR2(8, g);
+          const bool chain_tile = t >= I.n_page_tiles;
+          const int key = (chain_tile ? I.L : I.t0 + t * KT) + kidx;
+          const bool kvalid = key < (chain_tile ? I.L + I.R : I.kend);
+          // visibility mask over this lane's 32 slots: key valid, slot exists, and (chain tile) causal:
+          // chain key kidx is visible to slot r iff kidx <= r / G  <=>  r >= kidx * G
+          uint32_t vm = kvalid ? colok : 0u;
+          if (chain_tile) {
+            if (d.tree) {
+              // token tree (R30): chain key kidx is visible to row j iff kidx is an
+              // ancestor-or-self of node j (row_anc bit); rows j of this half hold slots jG..jG+G-1
+              uint32_t tm = 0;
+              if (kvalid) {
+                const int j0 = (ch * 32) >> lg, j1 = min(I.R, (ch * 32 + 32) >> lg);
+                for (int j = j0; j < j1; ++j)
+                  if ((d.row_anc[I.row0 + j] >> kidx) & 1ull) tm |= uint32_t((1ull << G) - 1ull) << ((j << lg) - ch * 32);
+              }
+              vm &= tm;
+            } else {
+              const int first = (kidx << lg) - ch * 32;
+              vm &= first <= 0 ? 0xffffffffu : (first >= 32 ? 0u : (0xffffffffu << first));
+            }
+          }
+          float x[32];
+          bool need = false;
+#pragma unroll
+          for (int c = 0; c < 32; c += 4) {
+            const float4 t4 = *reinterpret_cast<const float4*>(thr + c);
+            const float th[4] = {t4.x, t4.y, t4.z, t4.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float sc = __uint_as_float(sv[c + e]) * sl2e;
+              x[c + e] = ((vm >> (c + e)) & 1u) ? sc : -INFINITY;
+              need |= x[c + e] > th[e];
+            }
+          }
+          // does any of the 128 keys push a column beyond its reference (+2^8)? (4-warp vote)
+          float* xc = xcol + ((sb * 2 + ch) * 4) * 32;
+          const bool wneed = __any_sync(0xffffffffu, need);
+          if (lane == 0) xc[q * 32] = wneed ? 1.f : 0.f;
+          tc::named_bar(bar_id, 128);
+          const bool raise_any = xc[0] + xc[32] + xc[64] + xc[96] > 0.f;   // uniform in the 4 warps
+          if (warp == 4 && lane == 0) SV_TR2(9, g);
+          if (g > 1) {                                 // PV(g-2) has released this P^T buffer
+            const uint32_t pg = g - 2;
+            tc::mbar_wait(&s_free[pg & 1], (pg >> 1) & 1);
+            tc::fence_after();
+          }
+          if (warp == 4 && lane == 0) SV_TR2(10, g);
+          if (raise_any) {
+            // exact column max over the 128 keys inside the warp (lane c ends with column c), then
+            // across the 4 quadrant warps through shared memory
+            float cmw;
+            {                                          // transpose-reduce
+              float v[32];
+#pragma unroll
+              for (int c = 0; c < 32; ++c) v[c] = x[c];
+#pragma unroll
+              for (int s2 = 16; s2 >= 1; s2 >>= 1) {
+                const bool up = lane & s2;
+#pragma unroll
+                for (int i = 0; i < s2; ++i) {
+                  const float send = up ? v[i] : v[i + s2];
+                  const float keep = up ? v[i + s2] : v[i];
+                  v[i] = fmaxf(keep, __shfl_xor_sync(0xffffffffu, send, s2));
+                }
+              }
+              cmw = v[0];
+            }
+            float* xm = xcol + (((sb ^ 1) * 2 + ch) * 4) * 32;   // other parity: free this tile
+            xm[q * 32 + lane] = cmw;
+            tc::named_bar(bar_id, 128);
+            // lane c decides column c (identically in the 4 warps)
+            const float cm = fmaxf(fmaxf(xm[lane], xm[32 + lane]), fmaxf(xm[64 + lane], xm[96 + lane]));
+            const float old = mref[lane];
+            const bool init = (minit >> lane) & 1u;
+            const bool raise = init ? cm > old + kRescaleLog2 : cm > -INFINITY;
+            const float f = (raise && init) ? tc::ex2(old - cm) : 1.0f;
+            const bool any_resc = __any_sync(0xffffffffu, raise && init);
+            minit |= __ballot_sync(0xffffffffu, raise);
+            tc::named_bar(bar_id, 128);               // all reads of the old references are done
+            if (q == 0) {
+              if (raise) {
+                mref[lane] = cm;
+                thr[lane] = cm + kRescaleLog2;
+              }
+              fac[lane] = f;
+            }
+            tc::named_bar(bar_id, 128);               // new references / factors visible
+            if (any_resc) {                           // uniform: every warp sees the same factors
+              // O^T and the column sums L^T (this warp's 32 lanes x 32 slots) *= f(slot), once
+              // PV(g-1) has landed in them
+              const uint32_t pg = g - 1;
+              tc::mbar_wait(&s_free[pg & 1], (pg >> 1) & 1);
+              tc::fence_after();
+              for (int buf = 0; buf < 2; ++buf) {
+                const uint32_t a = tmem + lane_off + (buf ? L_COL : O_COL) + (iter & 1) * NQ + ch * 32;
+                uint32_t ov[32];
+                tc::tmem_ld32(a, ov);
+                tc::tmem_ld_wait();
+#pragma unroll
+                for (int c = 0; c < 32; ++c) ov[c] = __float_as_uint(__uint_as_float(ov[c]) * fac[c]);
+                tc::tmem_st32(a, ov);
+              }
+              tc::tmem_st_wait();
+            }
+          }
+          // P^T row (this key) for the NC slots -> bf16 -> swizzled st.shared
+          uint32_t pk[16];
+#pragma unroll
+          for (int c = 0; c < 32; c += 2) {
+            const float2 m2 = *reinterpret_cast<const float2*>(mref + c);
+            const float p0 = tc::ex2(x[c] - m2.x);         // x = -inf -> 0 (mref finite: 0 if unset)
+            const float p1 = tc::ex2(x[c + 1] - m2.y);
+            const __nv_bfloat162 pp = __floats2bfloat162_rn(p0, p1);
+            pk[c / 2] = *reinterpret_cast<const uint32_t*>(&pp);
+          }
+          if (warp == 4 && lane == 0) SV_TR2(11, g);
+          uint8_t* prow = sP + sb * P_BYTES + kidx * 128;
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            *reinterpret_cast<uint4*>(prow + (((ch * 4 + i) ^ (kidx & 7)) * 16)) =
+                make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+        }
         tc::fence_proxy_async();
         tc::fence_before();
         if (warp == 4 && lane == 0) SV_TR2(6, g);
