@@ -13,6 +13,7 @@ struct GemmEpi {
   float* resid_out;        // RESIDUAL: h_out (fp32 [M][N]); may alias resid_in
   float inv_temp;          // LOGITS: statistics are of l * inv_temp
   bool write_out;          // LOGITS: also store the fp32 logits (tensor-core paths; SIMT always does)
+  unsigned long long* row_best;   // LOGITS: per-row argmax keys (only when gemm_fills_row_best)
 };
 
 struct GemmPlan;
@@ -24,6 +25,8 @@ void gemm_plan_destroy(GemmPlan* p);
 cudaError_t attn_run(GemmPlan* p, int layer, int batch, int tree, cudaStream_t s);
 // true when attn_run's kernel writes O itself for requests with a single split-KV item
 bool attn_writes_single_split(GemmPlan* p);
+// true when the lm-head GEMM (EPI_LOGITS) also fills GemmEpi::row_best (the weight-major kernel)
+bool gemm_fills_row_best(GemmPlan* p);
 // NEXT-3 long-chunk prefill attention (tcgen05 rows-on-lanes, G in {1, 2, 4})
 bool attn_prefill_supported(GemmPlan* p);
 cudaError_t attn_prefill_run(GemmPlan* p, int layer, int n_items, cudaStream_t s);

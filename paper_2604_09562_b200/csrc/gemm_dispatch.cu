@@ -160,6 +160,8 @@ cudaError_t attn_run(GemmPlan* p, int layer, int batch, int tree, cudaStream_t s
 
 bool attn_writes_single_split(GemmPlan* p) { return p->use_tc2_attn && p->attn_maps_ok; }
 
+bool gemm_fills_row_best(GemmPlan* p) { return p->use_tc && !p->use_2sm && !p->use_1sm && !p->use_streamk; }
+
 bool attn_prefill_supported(GemmPlan* p) {
   const LaneDev& d = p->d;
   const int G = d.Hq / d.Hkv;
@@ -266,6 +268,7 @@ cudaError_t gemm_run(GemmPlan* p, const bf16* A, const bf16* B, float* C, int M,
       g.targ = d.tile_arg;
       g.nt = d.nt;
       g.inv_temp = e.inv_temp;
+      g.row_best = e.row_best;
       if (!e.write_out) g.out = nullptr;
       break;
     default:

@@ -30,6 +30,9 @@ struct GemmTcArgs {
   int* targ;
   int nt;
   float inv_temp;
+  // LOGITS (weight-major kernel, greedy): per token row, atomicMax of (order-preserving max bits << 32 |
+  // ~argmax) over the vocab tiles = the row's lowest-index argmax (finalize reads it; zero between steps)
+  unsigned long long* row_best;
   // stream-K (decided at launch): partial-tile buffers [grid][2][128 x 256] fp32 and per-tile
   // arrival counters (zero between launches)
   int streamk, sk_w;

@@ -595,7 +595,8 @@ __global__ void __launch_bounds__(FIN_THREADS) finalize_kernel(LaneDev d, const 
                                                                 const float* __restrict__ probs,
                                                                 const float* __restrict__ logits, uint64_t seed,
                                                                 int mode, float inv_temp, int* __restrict__ acc_out,
-                                                                int* __restrict__ tok_out, int* __restrict__ nodes_out) {
+                                                                int* __restrict__ tok_out, int* __restrict__ nodes_out,
+                                                                int use_row_best) {
   __shared__ float s_m[kMaxDepth + 1], s_S[kMaxDepth + 1];
   __shared__ int s_top[kMaxDepth + 1];
   __shared__ int s_a, s_indep, s_y, s_resid;
@@ -616,9 +617,18 @@ __global__ void __launch_bounds__(FIN_THREADS) finalize_kernel(LaneDev d, const 
   // an intermediate prefill chunk (no lm-head ran): every row is kept and no token is predicted
   const bool nohead = mode == kPrefillNoHead;
   if (nohead) mode = SV_PREFILL;
-  // 1. combine the vocab-tile statistics of each chain row (warp per row): one online pass,
-  //    loads batched 8 deep per lane so the memory round trips overlap
-  for (int j = warp; j <= (nohead ? -1 : k); j += nw) {
+  // 1. each chain row's argmax (and, for sampled decisions, max and sum of exp). Greedy / prefill
+  //    with use_row_best: one word per row from the lm-head epilogue's atomicMax key (lowest-index
+  //    argmax over the vocab tiles), reset here for the next verify. Otherwise combine the row's
+  //    vocab-tile statistics (warp per row): one online pass, loads batched 8 deep per lane.
+  if (use_row_best && !nohead && mode != SV_SAMPLE) {
+    for (int j = tid; j <= k; j += FIN_THREADS) {
+      const unsigned long long key = d.row_best[r0 + j];
+      s_top[j] = (int)(0xFFFFFFFFu - (uint32_t)key);
+      d.row_best[r0 + j] = 0ull;
+    }
+  }
+  for (int j = warp; j <= ((nohead || (use_row_best && mode != SV_SAMPLE)) ? -1 : k); j += nw) {
     const float* tm = d.tile_max + (size_t)(r0 + j) * d.nt;
     const float* ts = d.tile_sum + (size_t)(r0 + j) * d.nt;
     const int* ta = d.tile_arg + (size_t)(r0 + j) * d.nt;
@@ -838,7 +848,8 @@ __global__ void __launch_bounds__(FIN_THREADS) finalize_kernel(LaneDev d, const 
 
 cudaError_t launch_finalize(const LaneDev& d, int batch, const int* draft_tokens, const int* parents,
                             const float* draft_probs, const float* logits, uint64_t seed, int mode, float inv_temp,
-                            int* accepted_len, int* out_tokens, int* accepted_nodes, cudaStream_t s) {
+                            int* accepted_len, int* out_tokens, int* accepted_nodes, cudaStream_t s,
+                            bool use_row_best) {
   SV_COUNT_LAUNCH();
   // sampled chains: the race over the vocabulary is split across RS CTAs per request so the grid
   // fills the resident CTA slots once; the other modes need one CTA per request
@@ -854,7 +865,7 @@ cudaError_t launch_finalize(const LaneDev& d, int batch, const int* draft_tokens
   int RS = 1;
   if (mode == SV_SAMPLE && !parents) RS = std::min(kMaxRaceSplits, std::max(1, slots / batch));
   return launch_pdl(finalize_kernel, dim3(batch, RS), dim3(FIN_THREADS), 0, s, 1, d, draft_tokens, parents, draft_probs,
-                    logits, seed, mode, inv_temp, accepted_len, out_tokens, accepted_nodes);
+                    logits, seed, mode, inv_temp, accepted_len, out_tokens, accepted_nodes, (int)use_row_best);
 }
 
 }  // namespace sv

@@ -223,6 +223,12 @@ __device__ __forceinline__ void sw_epi_logits(const SwEpi& e, const SwTile& tl) 
       g.tmax[o] = m;
       g.tsum[o] = s;
       g.targ[o] = am;
+      if (g.row_best && m != -INFINITY) {
+        // order-preserving bits of m (larger m -> larger key), ties -> the lower token id wins
+        const uint32_t u = __float_as_uint(m);
+        const uint32_t ou = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+        atomicMax(g.row_best + t, ((unsigned long long)ou << 32) | (0xFFFFFFFFu - (uint32_t)am));
+      }
     }
   }
   tc::named_bar(EPI_BAR, EPI_THREADS);                    // RED is reused by the next tile

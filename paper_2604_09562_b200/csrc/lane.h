@@ -59,6 +59,7 @@ struct LaneDev {
   int* path_int;                     // [max_batch][max_depth+1] accepted path's chain rows (commit)
   unsigned long long* row_anc;       // [Tmax] ancestor-or-self node mask of each chain row
   int* fin_cnt;                      // [max_batch] finished race slices (zero between verifies)
+  unsigned long long* row_best;      // [Tmax] greedy argmax keys from the lm-head epilogue (zero between verifies)
   RacePart* fin_part;                // [max_batch][kMaxRaceSplits]
   unsigned* filt_key;                // [Tmax] R31 filter: threshold key of the scaled logit
   int* filt_tie;                     // [Tmax] largest kept token id among threshold ties
@@ -138,9 +139,11 @@ cudaError_t launch_tile_stats(const LaneDev& d, int T, float inv_temp, cudaStrea
 cudaError_t launch_attention(const LaneDev& d, int layer, int batch, cudaStream_t s);
 // skip_single: rows of requests with one split-KV item were written by the attention kernel itself
 cudaError_t launch_attn_combine(const LaneDev& d, int T, bool skip_single, cudaStream_t s);
+// use_row_best: greedy / prefill argmaxes come from d.row_best (filled by the lm-head epilogue)
 cudaError_t launch_finalize(const LaneDev& d, int batch, const int* draft_tokens, const int* parents,
                             const float* draft_probs, const float* logits, uint64_t seed, int mode, float inv_temp,
-                            int* accepted_len, int* out_tokens, int* accepted_nodes, cudaStream_t s);
+                            int* accepted_len, int* out_tokens, int* accepted_nodes, cudaStream_t s,
+                            bool use_row_best = false);
 cudaError_t launch_filter(const LaneDev& d, int T, float inv_temp, int top_k, float top_p, cudaStream_t s);
 cudaError_t launch_commit(const LaneDev& d, const int* n_keep, int batch, cudaStream_t s);
 cudaError_t launch_append(const LaneDev& d, int slot, unsigned long long rid, const bf16* k, const bf16* v,

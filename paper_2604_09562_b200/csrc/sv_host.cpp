@@ -25,7 +25,7 @@ struct Layout {
   size_t slots, depths, row_off, row_req, row_pos, chain_tok, req_err;
   size_t h0, h1, h2, cbuf, logits, tile_max, tile_sum, tile_arg;
   size_t a, b, z, q, kc, vc, o, u;
-  size_t items, item_start, n_items, part_o, part_ml, acc_int, tok_int, batch_n, path_int, row_anc, filt, fin_cnt, fin_part;
+  size_t items, item_start, n_items, part_o, part_ml, acc_int, tok_int, batch_n, path_int, row_anc, filt, fin_cnt, fin_part, row_best;
   size_t gemm_ws, trace, prefill, handoff;
   size_t max_items;
 
@@ -114,6 +114,7 @@ Layout make_layout(const sv_config& c) {
   L.row_anc = L.take(8 * T);
   L.filt = L.take(16 * T);
   L.fin_cnt = L.take(4 * c.max_batch);
+  L.row_best = L.take(8 * T);
   L.fin_part = L.take(sizeof(sv::RacePart) * sv::kMaxRaceSplits * c.max_batch);
   L.gemm_ws = L.take(sv::gemm_workspace_bytes((int)T, (int)cmax));
   L.trace = L.take(8 * 16 * 256);
@@ -385,6 +386,7 @@ sv_status sv_create(const sv_config* cfg, const sv_weights* w, void* kv_pool, vo
   d.tree = 0;
   d.filt_on = 0;
   d.fin_cnt = (int*)(ws + L.fin_cnt);
+  d.row_best = (unsigned long long*)(ws + L.row_best);
   d.fin_part = (sv::RacePart*)(ws + L.fin_part);
   d.filt_key = (unsigned*)(ws + L.filt);
   d.filt_tie = (int*)(ws + L.filt + 4 * (size_t)d.Tmax);
@@ -411,6 +413,7 @@ sv_status sv_create(const sv_config* cfg, const sv_weights* w, void* kv_pool, vo
       (st = cuda_ok(cudaMemsetAsync(ws + L.page_table, 0xff, 4 * (size_t)cfg->max_slots * d.max_pages_per_slot,
                                     c->stream))) ||
       (st = cuda_ok(cudaMemsetAsync(ws + L.fin_cnt, 0, 4 * (size_t)cfg->max_batch, c->stream))) ||
+      (st = cuda_ok(cudaMemsetAsync(ws + L.row_best, 0, 8 * (size_t)d.Tmax, c->stream))) ||
       (st = cuda_ok(sv::launch_init_state(d, c->stream)))) {
     delete c;
     return st;
@@ -515,6 +518,7 @@ static sv_status verify_impl(sv_ctx* c, int32_t batch, const int32_t* slots, con
   const int T = p.T;
   cudaStream_t s = c->stream;
   const float inv_temp = mode == SV_SAMPLE ? 1.0f / temperature : 1.0f;
+  bool row_best = false;
   wait_comm_slots(c, batch, slots);
   STAGE(c, ST_PLAN, sv::launch_plan(d, p, draft_tokens, parents, true, s));
   STAGE(c, ST_EMBED, sv::launch_embed_norm(d, T, s));
@@ -548,13 +552,18 @@ static sv_status verify_impl(sv_ctx* c, int32_t batch, const int32_t* slots, con
     // greedy decisions need only the vocab-tile statistics: the fp32 logits (T x V x 4 bytes)
     // are stored only when something reads them
     e.write_out = c->taps || mode == SV_SAMPLE || logits_out != nullptr;
+    // greedy / prefill decisions need only each row's argmax: the lm-head epilogue folds it into
+    // row_best (atomicMax of order-preserving keys, deterministic) and finalize reads 1 word per row
+    row_best = mode != SV_SAMPLE && sv::gemm_fills_row_best(c->gemm);
+    e.row_best = row_best ? d.row_best : nullptr;
     STAGE(c, ST_LM_HEAD, gemm(c, d.z, d.lm_head, d.logits, T, d.V, d.D, sv::EPI_LOGITS, e));
   }
   d.filt_on = mode == SV_SAMPLE && filter_active(c);
   if (d.filt_on) STAGE(c, ST_FILTER, sv::launch_filter(d, T, inv_temp, c->top_k, c->top_p, s));
+  if (!head) row_best = false;
   STAGE(c, ST_FINALIZE, sv::launch_finalize(d, batch, draft_tokens, parents, draft_probs, d.logits, seed,
                                             head ? (int)mode : sv::kPrefillNoHead, inv_temp, accepted_len,
-                                            out_tokens, accepted_nodes, s));
+                                            out_tokens, accepted_nodes, s, row_best));
   if (logits_out)
     SV_CUDA(cudaMemcpyAsync(logits_out, d.logits, (size_t)T * d.V * 4, cudaMemcpyDeviceToDevice, s));
   for (int b = 0; b < batch; ++b) c->state[slots[b]] = PENDING;
