@@ -515,24 +515,33 @@ def _run_gpu(args, wl, rank, world, dev, stream):
 
 
 def run_graph(args, wl, rank, world, dev):
-    """--graph: the step (planted drafter + verify + commit) captured once as a CUDA graph
-    (sv_graph_*) and replayed; each step's drafter inputs are copied into the buffers the graph
-    reads. Depths are fixed per request (the graph freezes kernel arguments): k_max for fixed-depth
-    workloads, request i drafting 1 + i % k_max for toy (BASELINE configs[0]: k = {1, 2, 3, 4}).
-    For launch-bound small configurations; no per-kernel events (no roofline) in this mode."""
+    """--graph: the step (planted drafter + verify + commit) captured once as a CUDA graph and replayed;
+    each step's drafter inputs are copied into the buffers the graph reads. Fixed-depth workloads use a
+    plain graph (sv_graph_begin); workloads whose depths change per step (c2: k ~ U{1..8} per request,
+    c3: SpecuStream's depth every window) use ONE dynamic-depth graph (sv_graph_begin_dynamic) with
+    each replay's depth vector staged by sv_graph_set_batch. No per-kernel events
+    (no roofline) in this mode."""
     from paper_2604_09562_b200 import sv
     import torch.distributed as dist
-    if wl.controller or (wl.kmin != wl.kmax and wl.name != "toy"):
-        raise SystemExit(f"--graph needs fixed depths (workload {wl.name} draws them per step)")
+    dynamic = wl.controller or wl.kmin != wl.kmax
+    if wl.tree and dynamic:
+        raise SystemExit("--graph: token-tree workloads need fixed depths")
     stream = torch.cuda.Stream(dev)
     with torch.cuda.stream(stream):
         lane, w, succ, reqs = build_lane(wl, rank, dev, stream)
         cfg, B = wl.cfg, wl.batch
         total = args.warmup + args.steps
-        ks = [wl.kmax] * B if wl.kmin == wl.kmax else [1 + i % wl.kmax for i in range(B)]
-        depths = [ks] * total
+        if dynamic:
+            depths = depths_for(wl, total, seed=7 + rank)
+        else:
+            ks = [wl.kmax] * B
+            depths = [ks] * total
         rows = B * wl.kmax
         masks, devtok = synth.planted_masks(total, rows, wl.alpha, cfg.vocab, seed=9 + rank)
+        ctl = None
+        if wl.controller:
+            ctl = ControlledDepths(wl, total, seed=11 + rank)
+            depths, masks, devtok = ctl.depths, ctl.masks, ctl.devtok
         masks_d, devtok_d, succ_d = masks.to(dev), devtok.to(dev), succ.to(dev)
         m_stage = torch.empty(rows, dtype=masks.dtype, device=dev)
         t_stage = torch.empty(rows, dtype=torch.int32, device=dev)
@@ -542,19 +551,31 @@ def run_graph(args, wl, rank, world, dev):
         slots = list(range(B))
         par_d = tree_parents(wl, dev)
 
-        def eager():
+        def stage(i):
+            if ctl:
+                ctl.prepare(i, masks_d, devtok_d)
+            m_stage.copy_(masks_d[i])
+            t_stage.copy_(devtok_d[i])
+
+        def eager(ks):
             draft_and_verify(lane, wl, slots, ks, succ_d, m_stage, t_stage, drafts, 1234, (acc, tok), par_d)
             lane.commit()
 
         for i in range(args.warmup):
-            m_stage.copy_(masks_d[i])
-            t_stage.copy_(devtok_d[i])
-            eager()
-        lane.graph_begin()
-        eager()                                       # captured, not run
+            stage(i)
+            eager(depths[i])
+            if ctl:
+                ctl.tick(lane, i)
+        if dynamic:
+            lane.graph_begin_dynamic(B)
+        else:
+            lane.graph_begin()
+        eager(depths[args.warmup - 1])                # captured, not run
         g = lane.graph_end()
         torch.cuda.synchronize(dev)
         lane.stats(reset=True)
+        if ctl:
+            ctl.restart(lane)
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
         launches0 = sv.launch_count()
         if world > 1:
@@ -563,10 +584,14 @@ def run_graph(args, wl, rank, world, dev):
         with Clocks(dev.index) as clk:
             ev[0].record(stream)
             for i in range(args.steps):
-                m_stage.copy_(masks_d[args.warmup + i])
-                t_stage.copy_(devtok_d[args.warmup + i])
+                j = args.warmup + i
+                stage(j)
+                if dynamic:
+                    lane.graph_set_batch(g, slots, depths[j])
                 lane.graph_launch(g)
                 ev[i + 1].record(stream)
+                if ctl:
+                    ctl.tick(lane, j)
             torch.cuda.synchronize(dev)
         if world > 1:
             dist.barrier()
@@ -576,7 +601,9 @@ def run_graph(args, wl, rank, world, dev):
     return dict(elapsed_ms=ev[0].elapsed_time(ev[-1]), tokens=st["emitted"],
                 per_step=[ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)], prof={}, roof={}, dominant=None,
                 launches=launches, clocks=clk.summary(), stats=st, e2e=None, e2e_host=None, w=w, succ=succ, reqs=reqs,
-                depths=depths, masks=masks, devtok=devtok, alg=None, controller=None, graph=True)
+                depths=depths, masks=masks, devtok=devtok, alg=None,
+                controller=({"window_steps": ControlledDepths.WINDOW, "final_depth": ctl.d, "trace": ctl.trace[-6:]}
+                            if ctl else None), graph="dynamic" if dynamic else "static")
 
 
 DISAGG_STEPS_PER_ROUND = 8   # decode steps per hand-off batch (the transfer of the next batch overlaps them)
@@ -1080,8 +1107,9 @@ def main():
         line["config"]["disagg"] = f"hand-off of {wl.batch} x {wl.ctx[1]}-token KV every {DISAGG_STEPS_PER_ROUND} steps"
         line["scaling"] = "weak"
     if res.get("graph"):
-        line["config"]["graph"] = "CUDA graph replay of drafter + verify + commit; depths fixed per request"
-        line["config"]["depth"] = sorted(set(res["depths"][0]))
+        line["config"]["graph"] = ("one dynamic-depth CUDA graph (sv_graph_begin_dynamic) replayed with each step's "
+                                   "depth vector" if res["graph"] == "dynamic" else
+                                   "CUDA graph replay of drafter + verify + commit; depths fixed per request")
     if args.detail:
         line["stages"] = {k: {"us": round(v["ms_per_launch"] * 1e3, 1), "share": round(v["share"], 4)}
                           for k, v in res["prof"].items()}

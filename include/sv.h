@@ -211,6 +211,18 @@ sv_status sv_verify_tree_logits(sv_ctx* ctx, int32_t batch, const int32_t* slots
  * the captured calls. sv_graph_destroy frees the instantiated graph. */
 typedef struct sv_graph sv_graph;
 sv_status sv_graph_begin(sv_ctx* ctx);
+/* One graph for ANY depth vector (slots / depths go through a pinned staging buffer
+ * that the captured graph's H2D node reads). Like sv_graph_begin, for a step of exactly `batch`
+ * requests: the captured calls (sv_draft_planted, sv_verify in GREEDY / SAMPLE mode of chains, without
+ * logits_out, and sv_commit) take their slots and depths from the device copy made by the graph's
+ * first node; row-gridded kernels are launched for batch * (max_depth + 1) rows and return beyond the
+ * plan's device row count, the GEMMs read their rows from it. The slots / depths given at capture only
+ * need to be valid then. Before each replay, sv_graph_set_batch stages that replay's slots and
+ * depths (host-checked like sv_verify's; it waits until the previous replay has copied its values).
+ * ESTATE if the lane's GEMM / attention configuration cannot read rows from the device (SV_GEMM /
+ * SV_ATTN overrides). One dynamic graph per lane at a time (they share the staging buffer). */
+sv_status sv_graph_begin_dynamic(sv_ctx* ctx, int32_t batch);
+sv_status sv_graph_set_batch(sv_ctx* ctx, const sv_graph* graph, const int32_t* slots, const int32_t* depths);
 sv_status sv_graph_end(sv_ctx* ctx, sv_graph** graph);
 sv_status sv_graph_launch(sv_ctx* ctx, const sv_graph* graph);
 sv_status sv_graph_destroy(sv_graph* graph);

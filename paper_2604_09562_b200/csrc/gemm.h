@@ -14,6 +14,8 @@ struct GemmEpi {
   float inv_temp;          // LOGITS: statistics are of l * inv_temp
   bool write_out;          // LOGITS: also store the fp32 logits (tensor-core paths; SIMT always does)
   unsigned long long* row_best;   // LOGITS: per-row argmax keys (only when gemm_fills_row_best)
+  const int* M_dev;        // rows from the device (dynamic-depth graph; M = the upper bound), or nullptr
+  int M_hint;              // with M_dev: typical rows, for the token-tile width (0: use M)
 };
 
 struct GemmPlan;
@@ -27,6 +29,9 @@ cudaError_t attn_run(GemmPlan* p, int layer, int batch, int tree, cudaStream_t s
 bool attn_writes_single_split(GemmPlan* p);
 // true when the lm-head GEMM (EPI_LOGITS) also fills GemmEpi::row_best (the weight-major kernel)
 bool gemm_fills_row_best(GemmPlan* p);
+// true when every GEMM of the step honours GemmEpi::M_dev and the attention reads its work list from
+// the device (the dynamic-depth CUDA graph's requirements)
+bool supports_dynamic_rows(GemmPlan* p);
 // NEXT-3 long-chunk prefill attention (tcgen05 rows-on-lanes, G in {1, 2, 4})
 bool attn_prefill_supported(GemmPlan* p);
 cudaError_t attn_prefill_run(GemmPlan* p, int layer, int n_items, cudaStream_t s);

@@ -162,6 +162,8 @@ bool attn_writes_single_split(GemmPlan* p) { return p->use_tc2_attn && p->attn_m
 
 bool gemm_fills_row_best(GemmPlan* p) { return p->use_tc && !p->use_2sm && !p->use_1sm && !p->use_streamk; }
 
+bool supports_dynamic_rows(GemmPlan* p) { return gemm_fills_row_best(p) && p->use_tc_attn && p->attn_maps_ok; }
+
 bool attn_prefill_supported(GemmPlan* p) {
   const LaneDev& d = p->d;
   const int G = d.Hq / d.Hkv;
@@ -199,10 +201,11 @@ static cudaError_t gemm_simt(GemmPlan* p, const bf16* A, const bf16* B, float* C
 }
 
 // weight-major 2-SM kernel: weights (B) on the MMA's M side, the M tokens of A on its N side
-static cudaError_t gemm_sw(GemmPlan* p, const bf16* A, const bf16* B, int M, int K, GemmTcArgs& g, cudaStream_t s) {
+static cudaError_t gemm_sw(GemmPlan* p, const bf16* A, const bf16* B, int M, int K, GemmTcArgs& g, cudaStream_t s,
+                           int M_hint = 0) {
   const bool swiglu = g.kind == GEMM_EPI_SWIGLU;
   const int num_mp = swiglu ? g.F / 128 : (g.N + 255) / 256;
-  g.nt_tok = gemm_sw_choose_nt(M, num_mp, p->num_sms / 2);
+  g.nt_tok = M_hint > 0 ? gemm_sw_choose_nt(M_hint, num_mp, p->num_sms / 2, M) : gemm_sw_choose_nt(M, num_mp, p->num_sms / 2);
   if (const char* nt = getenv("SV_SW_NT")) g.nt_tok = atoi(nt);   // experiment override
   if (const char* dg = getenv("SV_SW_DIAG")) g.diag = atoi(dg);    // experiment: 1 no loads, 2 no epilogue
   {                                                                  // tile timeline (SV_TRACE): lm-head by
@@ -230,6 +233,7 @@ cudaError_t gemm_run(GemmPlan* p, const bf16* A, const bf16* B, float* C, int M,
   g.n_tiles = (N + 255) / 256;
   g.out = C;
   g.ldo = N;
+  g.M_dev = e.M_dev;
   if (p->use_streamk) {
     g.partials = p->partials;
     g.sk_counters = p->sk_counters;
@@ -276,7 +280,7 @@ cudaError_t gemm_run(GemmPlan* p, const bf16* A, const bf16* B, float* C, int M,
   }
   if (p->use_2sm && !g.partials) return launch_gemm_tc2(*ma, *mb, g, p->num_sms, s);
   if (p->use_1sm || g.partials) return launch_gemm_tc(*ma, *mb, g, p->num_sms, s);
-  return gemm_sw(p, A, B, M, K, g, s);
+  return gemm_sw(p, A, B, M, K, g, s, e.M_dev ? e.M_hint : 0);
 }
 
 }  // namespace sv

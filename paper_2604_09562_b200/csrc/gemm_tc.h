@@ -33,6 +33,9 @@ struct GemmTcArgs {
   // LOGITS (weight-major kernel, greedy): per token row, atomicMax of (order-preserving max bits << 32 |
   // ~argmax) over the vocab tiles = the row's lowest-index argmax (finalize reads it; zero between steps)
   unsigned long long* row_best;
+  // weight-major kernel: when set, the rows M are read from the device after the dependency wait (the
+  // grid is sized for the g.M given, an upper bound; dynamic-depth CUDA graphs)
+  const int* M_dev;
   // stream-K (decided at launch): partial-tile buffers [grid][2][128 x 256] fp32 and per-tile
   // arrival counters (zero between launches)
   int streamk, sk_w;
@@ -51,7 +54,7 @@ cudaError_t launch_gemm_tc2(const CUtensorMap& map_a, const CUtensorMap& map_b, 
                             cudaStream_t s);
 // weight-major 2-SM variant (k_gemm_sw.cu): map_w = weights [N][K] box (64, 128) (box rows 64 for
 // SWIGLU), map_x = tokens [>= M][K] box (64, nt_tok / 2)
-int gemm_sw_choose_nt(int T, int num_mp, int n_pairs);
+int gemm_sw_choose_nt(int T, int num_mp, int n_pairs, int T2 = 0);
 int gemm_sw_smem_bytes();
 cudaError_t launch_gemm_sw(const CUtensorMap& map_w, const CUtensorMap& map_x, const GemmTcArgs& g, int num_sms,
                            cudaStream_t s);

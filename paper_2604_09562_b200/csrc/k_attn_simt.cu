@@ -146,6 +146,7 @@ __global__ void __launch_bounds__(256) attn_combine_kernel(LaneDev d, int T, int
   constexpr int MS = 8;
   __shared__ int s_j, s_ns, s_base;
   const int r = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (r >= *d.T_dev) return;                       // launched for Tmax rows (dynamic-depth graph)
   if (threadIdx.x == 0) {
     const int b = d.row_req[r];
     s_j = r - d.row_off[b];

@@ -90,6 +90,7 @@ __global__ void __launch_bounds__(FLT_THREADS) filter_kernel(LaneDev d, float in
   pdl_trigger();
   pdl_wait();
   const int r = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = FLT_THREADS / 32;
+  if (r >= *d.T_dev) return;                       // launched for Tmax rows (dynamic-depth graph)
   const int V = d.V, nt = d.nt;
   const float* row = d.logits + (size_t)r * V;
   const float* tmax = d.tile_max + (size_t)r * nt;

@@ -75,6 +75,7 @@ struct SwEpi {
   int* pos;          // POS region
   uint32_t tbase;    // TMEM address of this warp's lanes, current accumulator
   int NT;
+  int M;             // token rows (the launch's, or the device value of a dynamic-depth graph)
 };
 
 // 16 accumulator columns of this warp's 32 rows
@@ -107,7 +108,7 @@ __device__ __forceinline__ void sw_epi_f32(const SwEpi& e, const SwTile& tl) {
     for (int it = 0; it < 4; ++it) {
       const int t = t0 + c + it * 4 + (e.lane >> 3);
       h[it] = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (resid && vec && c < e.NT && t < g.M) h[it] = __ldcg(reinterpret_cast<const float4*>(g.resid_in + (size_t)t * g.ldo + fcol));
+      if (resid && vec && c < e.NT && t < e.M) h[it] = __ldcg(reinterpret_cast<const float4*>(g.resid_in + (size_t)t * g.ldo + fcol));
     }
   };
   float4 hn[4];
@@ -125,7 +126,7 @@ __device__ __forceinline__ void sw_epi_f32(const SwEpi& e, const SwTile& tl) {
 #pragma unroll
     for (int it = 0; it < 4; ++it) {
       const int tok = it * 4 + (e.lane >> 3), t = t0 + c + tok;
-      if (t >= g.M) continue;
+      if (t >= e.M) continue;
       const float4 v = *reinterpret_cast<const float4*>(st + tok * 32 + part * 4);
       const size_t o = (size_t)t * g.ldo + fcol;
       if (vec) {
@@ -173,7 +174,7 @@ __device__ __forceinline__ void sw_epi_logits(const SwEpi& e, const SwTile& tl) 
     for (int i = 0; i < 16; ++i) {
       const int t = t0 + c + i;
       const float l = sw_u2f(r[i]);
-      if (g.out && valid && t < g.M) g.out[(size_t)t * g.ldo + f] = l;
+      if (g.out && valid && t < e.M) g.out[(size_t)t * g.ldo + f] = l;
       x[i] = valid ? l * g.inv_temp : -INFINITY;
     }
     // column max over the warp's 32 rows: one redux per column, result in every lane;
@@ -218,7 +219,7 @@ __device__ __forceinline__ void sw_epi_logits(const SwEpi& e, const SwTile& tl) 
       const float v = rmax[w * 256 + col];
       if (v != -INFINITY) s += rsum[w * 256 + col] * tc::ex2((v - m) * kLog2e);
     }
-    if (t < g.M && tile < g.nt) {
+    if (t < e.M && tile < g.nt) {
       const size_t o = (size_t)t * g.nt + tile;
       g.tmax[o] = m;
       g.tsum[o] = s;
@@ -294,7 +295,7 @@ __device__ __forceinline__ void sw_epi_qkv(const SwEpi& e, const SwTile& tl) {
   const int t0 = tl.n_blk * e.NT;
   for (int col = e.tid; col < e.NT; col += EPI_THREADS) {     // the tile's token positions
     const int t = t0 + col;
-    e.pos[col] = t < g.M ? g.row_pos[t] : 0;
+    e.pos[col] = t < e.M ? g.row_pos[t] : 0;
   }
   tc::named_bar(EPI_BAR, EPI_THREADS);
   // RoPE table values of the next chunk are loaded while this chunk's accumulators come out of
@@ -329,7 +330,7 @@ __device__ __forceinline__ void sw_epi_qkv(const SwEpi& e, const SwTile& tl) {
       const float x = sw_u2f(r[i]);
       y[i] = f2bf(!rope ? x : lo ? x * cs[i] - p[i] * sn[i] : x * cs[i] + p[i] * sn[i]);
     }
-    sw_store_bf16(e, y, dst + (size_t)(t0 + c) * ld, ld, min(16, g.M - (t0 + c)));
+    sw_store_bf16(e, y, dst + (size_t)(t0 + c) * ld, ld, min(16, e.M - (t0 + c)));
   }
   tc::named_bar(EPI_BAR, EPI_THREADS);                    // XCH / POS are reused by the next tile
 }
@@ -353,7 +354,7 @@ __device__ __forceinline__ void sw_epi_swiglu(const SwEpi& e, const SwTile& tl) 
       const float x = sw_u2f(r[i]);
       y[i] = f2bf(__fdividef(x, 1.0f + __expf(-x)) * p[i]);
     }
-    const int ntok = min(16, g.M - (t0 + c));
+    const int ntok = min(16, e.M - (t0 + c));
     sw_store_bf16(e, y, g.u + (size_t)(t0 + c) * g.F + j0, g.F, ntok);
   }
   tc::named_bar(EPI_BAR, EPI_THREADS);                    // XCH / POS are reused by the next tile
@@ -382,8 +383,9 @@ __global__ void __launch_bounds__(THREADS, 1)
   const bool swiglu = g.kind == GEMM_EPI_SWIGLU;
   const int NT = g.nt_tok;
   const int num_mp = swiglu ? g.F / 128 : (g.N + 255) / 256;
-  const int n_tok = (g.M + NT - 1) / NT;
-  const int num_tiles = num_mp * n_tok;
+  int M = g.M;                                            // g.M_dev: read after the dependency wait
+  int n_tok = (M + NT - 1) / NT;
+  int num_tiles = num_mp * n_tok;
   const int nk = g.K / BK;
   const int cluster = blockIdx.x >> 1, n_clusters = gridDim.x >> 1;
 
@@ -410,8 +412,14 @@ __global__ void __launch_bounds__(THREADS, 1)
   // step, so the producer also prefetches the first tile's weight stages before waiting; every other
   // global access (tokens, residuals, outputs) comes after pdl_wait.
   pdl_trigger();
-  const int npre = (g.diag & 1) || cluster >= num_tiles ? 0 : (nk < STAGES ? nk : STAGES);
+  // (no pre-wait prefetch with a device M: the tile -> weight-tile map depends on it)
+  const int npre = (g.diag & 1) || g.M_dev || cluster >= num_tiles ? 0 : (nk < STAGES ? nk : STAGES);
   if (warp != 0) pdl_wait();
+  if (g.M_dev && warp != 0) {
+    M = *g.M_dev;
+    n_tok = (M + NT - 1) / NT;
+    num_tiles = num_mp * n_tok;
+  }
   if (g.trace && threadIdx.x == 0 && blockIdx.x < 512) g.trace[10 * 256 + blockIdx.x / 2 + (rank ? 128 : 0)] = sw_gtimer();
 
   // Producer and MMA roles run as whole, converged warps with one elected lane issuing: the
@@ -444,6 +452,11 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     __syncwarp();
     pdl_wait();
+    if (g.M_dev) {
+      M = *g.M_dev;
+      n_tok = (M + NT - 1) / NT;
+      num_tiles = num_mp * n_tok;
+    }
     for (int t = cluster; t < num_tiles; t += n_clusters) {
       const int n_blk = t % n_tok, m_pair = t / n_tok;    // token tiles of one weight tile run together
       const int xrow = n_blk * NT + (int)rank * (NT / 2);
@@ -516,7 +529,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       tc::mbar_wait(&tfull[acc], acc_phase);
       tc::fence_after();
       if (warp == 4 && lane == 0) SW_TR(g, 14, (t - cluster) / n_clusters);
-      const SwEpi e{&g, (int)rank, q, h, lane, h * 128 + q * 32 + lane, aux, pos_s, tmem_base + (uint32_t(q * 32) << 16) + acc * 256, NT};
+      const SwEpi e{&g, (int)rank, q, h, lane, h * 128 + q * 32 + lane, aux, pos_s, tmem_base + (uint32_t(q * 32) << 16) + acc * 256, NT, M};
       switch ((g.diag & 2) ? -1 : g.kind) {
         case -1: break;                                   // diagnostic: no epilogue
         case GEMM_EPI_LOGITS: sw_epi_logits(e, tl); break;
@@ -543,21 +556,40 @@ __global__ void __launch_bounds__(THREADS, 1)
 
 // Token tile width: the N = 16k <= 256 that splits T into equal tiles with the fewest
 // pair-waves x (width + a fixed per-tile cost); T = 576 -> 192 (3 tiles) for 24+ weight tiles.
-int gemm_sw_choose_nt(int T, int num_mp, int n_pairs) {
+static int sw_nt_cost(int T, int nt, int num_mp, int n_pairs) {
+  const int tiles = num_mp * ((T + nt - 1) / nt);
+  const int waves = (tiles + n_pairs - 1) / n_pairs;
+  return waves * (nt + 48);
+}
+
+// T2 > 0 (dynamic-depth graphs: the rows vary per replay around the capture's T, up to the bound T2):
+// the width minimising 2 cost(T) + cost(T2)
+int gemm_sw_choose_nt(int T, int num_mp, int n_pairs, int T2) {
   int best = 256, best_cost = 0x7fffffff;
   for (int k = 1; k <= 64; ++k) {
     int nt = (T + k - 1) / k;
     nt = (nt + 15) / 16 * 16;
     if (nt > 256) continue;
     if (nt < 16) nt = 16;
-    const int tiles = num_mp * ((T + nt - 1) / nt);
-    const int waves = (tiles + n_pairs - 1) / n_pairs;
-    const int cost = waves * (nt + 48);
+    const int cost = (T2 > 0 ? 2 : 1) * sw_nt_cost(T, nt, num_mp, n_pairs) + (T2 > 0 ? sw_nt_cost(T2, nt, num_mp, n_pairs) : 0);
     if (cost < best_cost) {
       best_cost = cost;
       best = nt;
     }
     if (nt == 16) break;
+  }
+  if (T2 > 0) {                                           // the widths chosen for T2 alone are candidates too
+    for (int k = 1; k <= 64; ++k) {
+      int nt = ((T2 + k - 1) / k + 15) / 16 * 16;
+      if (nt > 256) continue;
+      if (nt < 16) nt = 16;
+      const int cost = 2 * sw_nt_cost(T, nt, num_mp, n_pairs) + sw_nt_cost(T2, nt, num_mp, n_pairs);
+      if (cost < best_cost) {
+        best_cost = cost;
+        best = nt;
+      }
+      if (nt == 16) break;
+    }
   }
   return best;
 }

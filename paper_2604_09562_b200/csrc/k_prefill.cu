@@ -55,6 +55,7 @@ __global__ void __launch_bounds__(256) prefill_plan_kernel(LaneDev d, int slot, 
     d.slots[0] = slot;
     d.depths[0] = C - 1;
     *d.batch_n = 1;
+    *d.T_dev = C;
   }
   __syncthreads();
   for (int i = threadIdx.x; i < s_cnt; i += blockDim.x)

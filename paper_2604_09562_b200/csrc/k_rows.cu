@@ -50,10 +50,20 @@ __global__ void plan_kernel(LaneDev d, PlanArgs p, const int* __restrict__ draft
   __shared__ int s_item[kMaxBatch + 1];
   __shared__ int s_err[kMaxBatch];
   __shared__ int s_len[kMaxBatch];
+  __shared__ int s_slot[kMaxBatch], s_dep[kMaxBatch];
   const int B = p.batch;
   for (int b = threadIdx.x; b < B; b += blockDim.x) {   // the per-request loads, in parallel
-    s_len[b] = d.len[p.slots[b]];
-    s_err[b] = 0;
+    int slot = p.slots[b], k = p.depths[b], e = 0;
+    if (d.dyn_ctrl) {                                    // dynamic-depth graph: this replay's batch
+      slot = d.dyn_ctrl[b];
+      k = d.dyn_ctrl[B + b];
+      if (slot < 0 || slot >= d.max_slots) { slot = 0; e = 1; }
+      if (k < 0 || k > d.max_depth) { k = 0; e = 1; }
+    }
+    s_slot[b] = slot;
+    s_dep[b] = k;
+    s_len[b] = d.len[slot];
+    s_err[b] = e;
   }
   __syncthreads();
   if (threadIdx.x == 0) {                                // prefix sums over shared memory only
@@ -61,30 +71,32 @@ __global__ void plan_kernel(LaneDev d, PlanArgs p, const int* __restrict__ draft
     for (int b = 0; b < B; ++b) {
       s_off[b] = o;
       s_item[b] = it;
-      o += p.depths[b] + 1;
+      o += s_dep[b] + 1;
       if (attn) it += num_splits(s_len[b]) * d.Hkv;
     }
     s_off[B] = o;
     s_item[B] = it;
     *d.n_items = it;
     *d.batch_n = B;
+    *d.T_dev = o;
   }
   __syncthreads();
   for (int b = threadIdx.x; b <= B; b += blockDim.x) {
     d.row_off[b] = s_off[b];
     d.item_start[b] = s_item[b];
     if (b < B) {
-      d.slots[b] = p.slots[b];
-      d.depths[b] = p.depths[b];
+      d.slots[b] = s_slot[b];
+      d.depths[b] = s_dep[b];
     }
   }
-  for (int r = threadIdx.x; r < p.T; r += blockDim.x) {
+  const int T = s_off[B];
+  for (int r = threadIdx.x; r < T; r += blockDim.x) {
     int lo = 0, hi = B - 1;                      // last b with s_off[b] <= r
     while (lo < hi) {
       const int mid = (lo + hi + 1) >> 1;
       if (s_off[mid] <= r) lo = mid; else hi = mid - 1;
     }
-    const int b = lo, j = r - s_off[b], slot = p.slots[b];
+    const int b = lo, j = r - s_off[b], slot = s_slot[b];
     int tok = j == 0 ? d.pending[slot] : draft_tokens[s_off[b] - b + j - 1];
     if (tok < 0 || tok >= d.V) {
       atomicOr(&s_err[b], 1);
@@ -165,6 +177,7 @@ __global__ void __launch_bounds__(256) embed_norm_kernel(LaneDev d) {
   pdl_trigger();
   pdl_wait();
   const int r = blockIdx.x;
+  if (r >= *d.T_dev) return;                       // launched for Tmax rows (dynamic-depth graph)
   const int tok = d.chain_tok[r];
   const bf16* e = d.embed + (size_t)tok * d.D;
   float* h = d.h0 + (size_t)r * d.D;
@@ -203,6 +216,7 @@ __global__ void __launch_bounds__(256) embed_norm_vec_kernel(LaneDev d) {
   pdl_trigger();
   pdl_wait();
   const int r = blockIdx.x;
+  if (r >= *d.T_dev) return;                       // launched for Tmax rows (dynamic-depth graph)
   const int nv = d.D / 8;
   const uint4* e = reinterpret_cast<const uint4*>(d.embed + (size_t)d.chain_tok[r] * d.D);
   float4* h = reinterpret_cast<float4*>(d.h0 + (size_t)r * d.D);
@@ -236,10 +250,11 @@ __global__ void __launch_bounds__(256) embed_norm_vec_kernel(LaneDev d) {
 }
 
 __global__ void __launch_bounds__(256) rmsnorm_vec_kernel(const float* __restrict__ x, const bf16* __restrict__ g,
-                                                          bf16* __restrict__ out, int D, float eps) {
+                                                          bf16* __restrict__ out, int D, float eps, const int* __restrict__ Tdev) {
   pdl_trigger();
   pdl_wait();
   const int r = blockIdx.x;
+  if (Tdev && r >= *Tdev) return;                 // launched for Tmax rows (dynamic-depth graph)
   const int nv = D / 8;
   const float4* xr = reinterpret_cast<const float4*>(x + (size_t)r * D);
   float v8[kNormMaxVec][8];
@@ -282,10 +297,11 @@ cudaError_t launch_embed_norm(const LaneDev& d, int T, cudaStream_t s) {
 }
 
 __global__ void __launch_bounds__(256) rmsnorm_kernel(const float* __restrict__ x, const bf16* __restrict__ g,
-                                                      bf16* __restrict__ out, int D, float eps) {
+                                                      bf16* __restrict__ out, int D, float eps, const int* __restrict__ Tdev) {
   pdl_trigger();
   pdl_wait();
   const int r = blockIdx.x;
+  if (Tdev && r >= *Tdev) return;                 // launched for Tmax rows (dynamic-depth graph)
   const float* xr = x + (size_t)r * D;
   float ss = 0.f;
   for (int i = threadIdx.x; i < D; i += 256) ss += xr[i] * xr[i];
@@ -293,12 +309,14 @@ __global__ void __launch_bounds__(256) rmsnorm_kernel(const float* __restrict__ 
   for (int i = threadIdx.x; i < D; i += 256) out[(size_t)r * D + i] = f2bf(xr[i] * rstd * bf2f(g[i]));
 }
 
-cudaError_t launch_rmsnorm(const LaneDev& d, const float* x, const bf16* g, bf16* out, int T, cudaStream_t s) {
+cudaError_t launch_rmsnorm(const LaneDev& d, const float* x, const bf16* g, bf16* out, int T, cudaStream_t s,
+                           bool bound_by_T_dev) {
   SV_COUNT_LAUNCH();
+  const int* Tdev = bound_by_T_dev ? d.T_dev : nullptr;
   if (d.D <= 256 * 8 * kNormMaxVec && aligned16(g))
-    return launch_pdl(rmsnorm_vec_kernel, dim3(T), dim3(256), 0, s, 1, x, g, out, d.D, d.eps);
+    return launch_pdl(rmsnorm_vec_kernel, dim3(T), dim3(256), 0, s, 1, x, g, out, d.D, d.eps, Tdev);
   else
-    return launch_pdl(rmsnorm_kernel, dim3(T), dim3(256), 0, s, 1, x, g, out, d.D, d.eps);
+    return launch_pdl(rmsnorm_kernel, dim3(T), dim3(256), 0, s, 1, x, g, out, d.D, d.eps, Tdev);
 }
 
 // ------------------------------------------------------------------ a2: QKV + RoPE epilogue
@@ -434,11 +452,15 @@ __global__ void draft_planted_kernel(LaneDev d, PlanArgs p, const int* __restric
   pdl_wait();
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= p.batch) return;
+  const int* dep = d.dyn_ctrl ? d.dyn_ctrl + p.batch : p.depths;   // dynamic-depth graph: device copies
+  const int* slt = d.dyn_ctrl ? d.dyn_ctrl : p.slots;
   int off = 0;
-  for (int i = 0; i < b; ++i) off += p.depths[i];
+  for (int i = 0; i < b; ++i) off += min(max(dep[i], 0), d.max_depth);
+  const int kb = min(max(dep[b], 0), d.max_depth);
   int tok[kMaxDepth + 1];                          // node tokens (node 0 = the pending token)
-  tok[0] = d.pending[p.slots[b]];
-  for (int j = 0; j < p.depths[b]; ++j) {
+  const int sl = slt[b];
+  tok[0] = d.pending[sl >= 0 && sl < d.max_slots ? sl : 0];
+  for (int j = 0; j < kb; ++j) {
     int par = parents ? parents[off + j] : j;      // tree: the node's parent; chain: the previous node
     if (par < 0 || par > j) par = j;               // (the verify flags a bad tree; keep reads in range)
     int t = succ[tok[par]];

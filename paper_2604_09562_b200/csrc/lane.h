@@ -65,6 +65,10 @@ struct LaneDev {
   int* filt_tie;                     // [Tmax] largest kept token id among threshold ties
   float *filt_inv, *filt_m;          // [Tmax] 1 / kept mass, row max (scaled logits)
   int* batch_n;                      // [1] batch of the pending verify (device copy)
+  int* T_dev;                        // [1] chain rows of the current verify / prefill chunk (plan writes it);
+                                     // row-gridded kernels launched for Tmax rows return beyond it
+  const int* dyn_ctrl;               // dynamic-depth CUDA graph (sv_graph_begin_dynamic): device copies of
+                                     // this verify's slots [batch] then depths [batch]; nullptr otherwise
   unsigned long long* trace;         // [16][256] clock64 trace of CTA 0 (SV_TRACE=1) or nullptr
 };
 
@@ -129,7 +133,8 @@ struct PlanArgs {
 cudaError_t launch_plan(const LaneDev& d, const PlanArgs& p, const int* draft_tokens, const int* parents, bool attn,
                         cudaStream_t s);
 cudaError_t launch_embed_norm(const LaneDev& d, int T, cudaStream_t s);
-cudaError_t launch_rmsnorm(const LaneDev& d, const float* x, const bf16* g, bf16* out, int T, cudaStream_t s);
+cudaError_t launch_rmsnorm(const LaneDev& d, const float* x, const bf16* g, bf16* out, int T, cudaStream_t s,
+                           bool bound_by_T_dev = true);
 // C[M][N] (fp32) = A[M][K] (bf16) * B[N][K]^T (bf16)
 cudaError_t launch_gemm_simt(const bf16* A, const bf16* B, float* C, int M, int N, int K, cudaStream_t s);
 cudaError_t launch_qkv_rope_epilogue(const LaneDev& d, int layer, int T, cudaStream_t s);

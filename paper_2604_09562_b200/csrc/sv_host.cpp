@@ -26,7 +26,7 @@ struct Layout {
   size_t h0, h1, h2, cbuf, logits, tile_max, tile_sum, tile_arg;
   size_t a, b, z, q, kc, vc, o, u;
   size_t items, item_start, n_items, part_o, part_ml, acc_int, tok_int, batch_n, path_int, row_anc, filt, fin_cnt, fin_part, row_best;
-  size_t gemm_ws, trace, prefill, handoff;
+  size_t gemm_ws, trace, prefill, handoff, tdev, dctrl;
   size_t max_items;
 
   size_t take(size_t bytes) {
@@ -123,6 +123,8 @@ Layout make_layout(const sv_config& c) {
   // batched hand-off (sv_kv_send_slots / sv_kv_recv_slots): slots, token counts, block starts [max_slots + 1]
   // i32 + request ids [max_slots] u64
   L.handoff = L.take(4 * (4 * (size_t)c.max_slots + 4) + 8 * (size_t)c.max_slots);
+  L.tdev = L.take(16);                                  // rows of the current verify (plan writes it)
+  L.dctrl = L.take(8 * (size_t)c.max_batch);            // dynamic-depth graph: slots | depths of a replay
   L.total = (L.total + 1023) & ~size_t(1023);
   return L;
 }
@@ -185,6 +187,12 @@ struct sv_ctx {
   std::vector<char> comm_slot;       // slots whose pages / pending token a posted transfer reads or writes
   std::vector<cudaEvent_t> rel_ev;   // per slot: recorded after its last release (a receive into it waits)
   std::vector<char> rel_pending;
+  // dynamic-depth CUDA graph (sv_graph_begin_dynamic): a replay's slots | depths are staged in one of
+  // two pinned host buffers [2][2 max_batch] and copied to the device by the graph's first node
+  int* pin_ctrl = nullptr;
+  cudaEvent_t ctrl_consumed = nullptr;
+  bool dyn_capture = false;
+  int dyn_batch = 0;
 };
 
 // make the lane's stream wait for the posted hand-off transfers (sends read pages, receives write
@@ -386,6 +394,8 @@ sv_status sv_create(const sv_config* cfg, const sv_weights* w, void* kv_pool, vo
   d.tree = 0;
   d.filt_on = 0;
   d.fin_cnt = (int*)(ws + L.fin_cnt);
+  d.T_dev = (int*)(ws + L.tdev);
+  d.dyn_ctrl = nullptr;
   d.row_best = (unsigned long long*)(ws + L.row_best);
   d.fin_part = (sv::RacePart*)(ws + L.fin_part);
   d.filt_key = (unsigned*)(ws + L.filt);
@@ -422,7 +432,9 @@ sv_status sv_create(const sv_config* cfg, const sv_weights* w, void* kv_pool, vo
   if ((st = cuda_ok(cudaStreamSynchronize(c->stream))) ||
       (st = cuda_ok(cudaStreamCreateWithFlags(&c->comm, cudaStreamNonBlocking))) ||
       (st = cuda_ok(cudaEventCreateWithFlags(&c->comm_done, cudaEventDisableTiming))) ||
-      (st = cuda_ok(cudaEventCreateWithFlags(&c->lane_mark, cudaEventDisableTiming)))) {
+      (st = cuda_ok(cudaEventCreateWithFlags(&c->lane_mark, cudaEventDisableTiming))) ||
+      (st = cuda_ok(cudaEventCreateWithFlags(&c->ctrl_consumed, cudaEventDisableTiming))) ||
+      (st = cuda_ok(cudaHostAlloc((void**)&c->pin_ctrl, 16 * (size_t)cfg->max_batch, cudaHostAllocDefault)))) {
     sv::gemm_plan_destroy(c->gemm);
     if (c->comm) cudaStreamDestroy(c->comm);
     if (c->comm_done) cudaEventDestroy(c->comm_done);
@@ -441,6 +453,8 @@ sv_status sv_destroy(sv_ctx* c) {
   cudaStreamDestroy(c->comm);
   cudaEventDestroy(c->comm_done);
   cudaEventDestroy(c->lane_mark);
+  if (c->ctrl_consumed) cudaEventDestroy(c->ctrl_consumed);
+  if (c->pin_ctrl) cudaFreeHost(c->pin_ctrl);
   for (cudaEvent_t e : c->rel_ev)
     if (e) cudaEventDestroy(e);
   sv::gemm_plan_destroy(c->gemm);
@@ -515,7 +529,17 @@ static sv_status verify_impl(sv_ctx* c, int32_t batch, const int32_t* slots, con
   sv::LaneDev d = c->d;
   d.tree = parents != nullptr && p.T > batch;
   if (!d.tree) parents = nullptr;                   // no drafts: a tree of roots is the chain
-  const int T = p.T;
+  // dynamic-depth graph capture: every replay's slots / depths come from the device copy the graph's
+  // first node makes; row-gridded launches cover Tmax = batch (max_depth + 1) rows and return beyond
+  // the plan's device T, the GEMMs read their rows from it
+  const bool dyn = c->dyn_capture;
+  if (dyn) {
+    if (batch != c->dyn_batch || parents || mode == SV_PREFILL || logits_out || !draft_tokens || !head)
+      return SV_EINVAL;
+    d.dyn_ctrl = (const int*)(c->ws + c->lay.dctrl);
+  }
+  const int* Mdev = dyn ? d.T_dev : nullptr;
+  const int T = dyn ? batch * (c->cfg.max_depth + 1) : p.T;
   cudaStream_t s = c->stream;
   const float inv_temp = mode == SV_SAMPLE ? 1.0f / temperature : 1.0f;
   bool row_best = false;
@@ -528,6 +552,8 @@ static sv_status verify_impl(sv_ctx* c, int32_t batch, const int32_t* slots, con
     if (layer > 0) STAGE(c, ST_ATTN_NORM, sv::launch_rmsnorm(d, hin, d.attn_norm + (size_t)layer * d.D, d.a, T, s));
     sv::GemmEpi e{};
     e.layer = layer;
+    e.M_dev = Mdev;
+    e.M_hint = p.T;
     STAGE(c, ST_QKV, gemm(c, d.a, d.wqkv + (size_t)layer * d.qkv_rows * d.D, d.cbuf, T, d.qkv_rows, d.D,
                           sv::EPI_QKV_ROPE, e));
     STAGE(c, ST_ATTN, sv::attn_run(c->gemm, layer, batch, d.tree, s));
@@ -549,6 +575,8 @@ static sv_status verify_impl(sv_ctx* c, int32_t batch, const int32_t* slots, con
     STAGE(c, ST_FINAL_NORM, sv::launch_rmsnorm(d, d.h2, d.final_norm, d.z, T, s));
     sv::GemmEpi e{};
     e.inv_temp = inv_temp;
+    e.M_dev = Mdev;
+    e.M_hint = p.T;
     // greedy decisions need only the vocab-tile statistics: the fp32 logits (T x V x 4 bytes)
     // are stored only when something reads them
     e.write_out = c->taps || mode == SV_SAMPLE || logits_out != nullptr;
@@ -570,7 +598,7 @@ static sv_status verify_impl(sv_ctx* c, int32_t batch, const int32_t* slots, con
   c->pending_verify = true;
   c->pending_batch = batch;
   c->pending_slots.assign(slots, slots + batch);
-  c->last_T = T;
+  c->last_T = dyn ? T : p.T;
   c->last_batch = batch;
   return SV_OK;
 }
@@ -600,7 +628,7 @@ static sv_status verify_logits_impl(sv_ctx* c, int32_t batch, const int32_t* slo
   if (mode != SV_GREEDY && mode != SV_SAMPLE && mode != SV_PREFILL) return SV_EINVAL;
   if (parents && mode == SV_PREFILL) return SV_EINVAL;
   if (mode == SV_SAMPLE && !(temperature > 0.f)) return SV_EINVAL;
-  if (c->pending_verify) return SV_ESTATE;
+  if (c->pending_verify || c->dyn_capture) return SV_ESTATE;
   sv::PlanArgs p;
   sv_status st = check_batch(c, batch, slots, depths, p);
   if (st) return st;
@@ -788,7 +816,12 @@ static sv_status draft_planted_impl(sv_ctx* c, int32_t batch, const int32_t* slo
     p.depths[b] = depths[b];
     p.T += depths[b] + 1;
   }
-  STAGE(c, ST_DRAFT, sv::launch_draft_planted(c->d, p, succ, dev_mask, dev_tok, parents, draft_tokens, c->stream));
+  sv::LaneDev d = c->d;
+  if (c->dyn_capture) {                            // dynamic-depth graph: this replay's slots / depths
+    if (batch != c->dyn_batch || parents) return SV_EINVAL;
+    d.dyn_ctrl = (const int*)(c->ws + c->lay.dctrl);
+  }
+  STAGE(c, ST_DRAFT, sv::launch_draft_planted(d, p, succ, dev_mask, dev_tok, parents, draft_tokens, c->stream));
   return SV_OK;
 }
 
@@ -970,6 +1003,13 @@ uint64_t sv_launch_count(void) { return sv::g_launch_count; }
 struct sv_graph {
   cudaGraphExec_t exec;
   unsigned long long kernels;        // kernel launches captured (added to sv_launch_count per replay)
+  bool dynamic;                      // sv_graph_begin_dynamic: slots / depths staged per replay
+  int batch;
+  cudaGraph_t tmpl = nullptr;        // dynamic: the captured graph (its H2D node is retargeted per replay)
+  cudaGraphNode_t h2d = nullptr;
+  mutable long long replays = 0;     // dynamic: replay r stages into pinned buffer r & 1 ...
+  mutable cudaEvent_t done[2] = {nullptr, nullptr};   // ... once replay r - 2 (same buffer) has finished
+  mutable bool done_set[2] = {false, false};
 };
 
 sv_status sv_graph_begin(sv_ctx* c) {
@@ -982,12 +1022,56 @@ sv_status sv_graph_begin(sv_ctx* c) {
   return SV_OK;
 }
 
+sv_status sv_graph_begin_dynamic(sv_ctx* c, int32_t batch) {
+  if (!c || !c->stream || batch < 1 || batch > c->cfg.max_batch) return SV_EINVAL;
+  if (c->capturing || c->pending_verify || c->prof.mask) return SV_ESTATE;
+  if (!sv::supports_dynamic_rows(c->gemm)) return SV_ESTATE;
+  wait_comm(c);
+  SV_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+  c->capturing = true;
+  c->dyn_capture = true;
+  c->dyn_batch = batch;
+  c->capture_launches0 = sv::g_launch_count;
+  // the graph's first node: this replay's slots | depths, pinned host -> device (its source buffer is
+  // switched between two pinned buffers per replay, sv_graph_set_batch)
+  cudaError_t e = cudaMemcpyAsync(c->ws + c->lay.dctrl, c->pin_ctrl, 8 * (size_t)batch, cudaMemcpyHostToDevice,
+                                  c->stream);
+  if (e != cudaSuccess) {
+    cudaGraph_t g = nullptr;
+    cudaStreamEndCapture(c->stream, &g);
+    if (g) cudaGraphDestroy(g);
+    c->capturing = c->dyn_capture = false;
+    return cuda_ok(e);
+  }
+  return SV_OK;
+}
+
+sv_status sv_graph_set_batch(sv_ctx* c, const sv_graph* g, const int32_t* slots, const int32_t* depths) {
+  if (!c || !g || !slots || !depths) return SV_EINVAL;
+  if (!g->dynamic) return SV_ESTATE;
+  if (c->capturing || c->pending_verify) return SV_ESTATE;
+  sv::PlanArgs p;
+  sv_status st = check_batch(c, g->batch, slots, depths, p);   // distinct, in range, ACTIVE, depth <= max
+  if (st) return st;
+  const int buf = (int)(g->replays & 1);
+  if (g->done_set[buf]) SV_CUDA(cudaEventSynchronize(g->done[buf]));   // replay r - 2 read this buffer
+  int* pin = c->pin_ctrl + (size_t)buf * 2 * c->cfg.max_batch;
+  memcpy(pin, slots, 4 * (size_t)g->batch);
+  memcpy(pin + g->batch, depths, 4 * (size_t)g->batch);
+  SV_CUDA(cudaGraphExecMemcpyNodeSetParams1D(g->exec, g->h2d, c->ws + c->lay.dctrl, pin, 8 * (size_t)g->batch,
+                                             cudaMemcpyHostToDevice));
+  return SV_OK;
+}
+
 sv_status sv_graph_end(sv_ctx* c, sv_graph** out) {
   if (!c || !out) return SV_EINVAL;
   if (!c->capturing) return SV_ESTATE;
   cudaGraph_t g = nullptr;
   const cudaError_t e = cudaStreamEndCapture(c->stream, &g);
   c->capturing = false;
+  const bool dyn = c->dyn_capture;
+  const int dyn_batch = c->dyn_batch;
+  c->dyn_capture = false;
   if (e != cudaSuccess) return SV_ECUDA;
   if (c->pending_verify) {                                // a captured verify must be committed in it
     cudaGraphDestroy(g);
@@ -995,9 +1079,24 @@ sv_status sv_graph_end(sv_ctx* c, sv_graph** out) {
   }
   cudaGraphExec_t x = nullptr;
   const cudaError_t e2 = cudaGraphInstantiate(&x, g, 0);
-  cudaGraphDestroy(g);
+  if (!dyn || e2 != cudaSuccess) cudaGraphDestroy(g);
   if (e2 != cudaSuccess) return SV_ECUDA;
-  *out = new sv_graph{x, sv::g_launch_count - c->capture_launches0};
+  sv_graph* gr = new sv_graph{x, sv::g_launch_count - c->capture_launches0, dyn, dyn_batch};
+  if (dyn) {                                              // keep the template: its H2D root is retargeted
+    gr->tmpl = g;
+    size_t nroot = 1;
+    cudaGraphNode_t root = nullptr;
+    cudaGraphNodeType ty;
+    if (cudaGraphGetRootNodes(g, &root, &nroot) != cudaSuccess || nroot < 1 ||
+        cudaGraphNodeGetType(root, &ty) != cudaSuccess || ty != cudaGraphNodeTypeMemcpy ||
+        cudaEventCreateWithFlags(&gr->done[0], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&gr->done[1], cudaEventDisableTiming) != cudaSuccess) {
+      sv_graph_destroy(gr);
+      return SV_ECUDA;
+    }
+    gr->h2d = root;
+  }
+  *out = gr;
   sv::g_launch_count = c->capture_launches0;              // captured launches run at replay
   return SV_OK;
 }
@@ -1007,12 +1106,21 @@ sv_status sv_graph_launch(sv_ctx* c, const sv_graph* g) {
   if (c->capturing || c->pending_verify) return SV_ESTATE;
   SV_CUDA(cudaGraphLaunch(g->exec, c->stream));
   sv::g_launch_count += g->kernels;
+  if (g->dynamic) {
+    const int buf = (int)(g->replays & 1);
+    SV_CUDA(cudaEventRecord(g->done[buf], c->stream));
+    g->done_set[buf] = true;
+    ++g->replays;
+  }
   return SV_OK;
 }
 
 sv_status sv_graph_destroy(sv_graph* g) {
   if (!g) return SV_EINVAL;
   cudaGraphExecDestroy(g->exec);
+  if (g->tmpl) cudaGraphDestroy(g->tmpl);
+  for (cudaEvent_t e : g->done)
+    if (e) cudaEventDestroy(e);
   delete g;
   return SV_OK;
 }

@@ -29,7 +29,7 @@ EXPORTED = [
     "sv_draft_planted", "sv_nccl_unique_id", "sv_nccl_comm_init", "sv_nccl_comm_destroy", "sv_kv_send",
     "sv_kv_recv_append", "sv_kv_packed_bytes", "sv_kv_pack", "sv_profile_enable", "sv_profile_num_stages",
     "sv_profile_stage_name", "sv_profile_read", "sv_launch_count", "sv_debug_gemm", "sv_kv_append_packed",
-    "sv_kv_loopback_append", "sv_kv_send_slots", "sv_kv_recv_slots", "sv_kv_loopback_slots", "sv_comm_stream", "sv_kv_slots_bytes", "sv_exact_query_sizes", "sv_exact_forward", "sv_spec_default_config", "sv_spec_reset", "sv_spec_adapt", "sv_spec_step",
+    "sv_kv_loopback_append", "sv_kv_send_slots", "sv_kv_recv_slots", "sv_kv_loopback_slots", "sv_comm_stream", "sv_kv_slots_bytes", "sv_exact_query_sizes", "sv_exact_forward", "sv_graph_begin_dynamic", "sv_graph_set_batch", "sv_spec_default_config", "sv_spec_reset", "sv_spec_adapt", "sv_spec_step",
     "sv_route_default_config", "sv_route_select", "sv_lane_occupancy", "sv_kv_pack_slot", "sv_prefill",
     "sv_verify_tree", "sv_verify_tree_logits", "sv_set_filter", "sv_draft_planted_tree", "sv_graph_begin",
     "sv_graph_end", "sv_graph_launch", "sv_graph_destroy",
@@ -134,6 +134,8 @@ def load():
         "sv_kv_loopback_slots": ([vp, vp, i32, vp, vp, vp, vp, vp, vp, ctypes.c_int, vp], ctypes.c_int),
         "sv_kv_slots_bytes": ([P(Config), i32, vp], sz),
         "sv_exact_query_sizes": ([P(Config), i32, P(sz)], ctypes.c_int),
+        "sv_graph_begin_dynamic": ([vp, i32], ctypes.c_int),
+        "sv_graph_set_batch": ([vp, vp, vp, vp], ctypes.c_int),
         "sv_exact_forward": ([P(Config), P(Weights), i32, vp, vp, vp, vp, vp, i32, vp, sz, vp, vp], ctypes.c_int),
         "sv_kv_packed_bytes": ([P(Config), i32], sz),
         "sv_kv_pack": ([vp, vp, i32, i32, i32, i32, i32, vp, vp], ctypes.c_int),
@@ -322,6 +324,16 @@ class Lane:
     def graph_begin(self):
         """Capture the lane's next calls into a CUDA graph (sv_graph_begin; needs a created stream)."""
         _check(self.lib.sv_graph_begin(self.ctx), "sv_graph_begin")
+
+    def graph_begin_dynamic(self, batch):
+        """Capture a step that serves any depth vector of `batch` requests (sv_graph_begin_dynamic)."""
+        _check(self.lib.sv_graph_begin_dynamic(self.ctx, int(batch)), "sv_graph_begin_dynamic")
+
+    def graph_set_batch(self, g, slots, depths):
+        """Stage the next replay's slots / depths of a dynamic graph (sv_graph_set_batch)."""
+        s, _ = _i32_array(slots)
+        d, _ = _i32_array(depths)
+        _check(self.lib.sv_graph_set_batch(self.ctx, g, s, d), "sv_graph_set_batch")
 
     def graph_end(self):
         g = ctypes.c_void_p()

@@ -143,3 +143,67 @@ def test_graph_capture_rules():
         with pytest.raises(sv.SvError):
             lane.graph_end()
         lane.close()
+
+
+@pytest.mark.parametrize("cfgname,mode", [("toy_mlp", "sample"), ("llama", "greedy"), ("llama", "sample")])
+def test_dynamic_graph_any_depth_vector(cfgname, mode):
+    """sv_graph_begin_dynamic: ONE captured drafter + verify + commit step replayed with a different
+    depth vector (and slot order) every step (sv_graph_set_batch) gives exactly the outputs, counters
+    and cache lengths of the same steps run eagerly — SURVEY.md §8(b) "one CUDA graph must serve any
+    depth vector"."""
+    if cfgname == "llama":
+        cfg = synth.LLAMA.with_(n_pages=64, max_slots=4, max_batch=4, max_pos=1024)
+    else:
+        cfg = synth.TOY_MLP
+    w = synth.model_weights(cfg, seed=0, norm_one=False, embed_std=4.0)
+    w, succ = synth.planted_successor(cfg, w, seed=1, beta=0.3)
+    n = 7
+    g_ = torch.Generator().manual_seed(5)
+    depths = [[int(x) for x in torch.randint(0, cfg.max_depth + 1, (4,), generator=g_)] for _ in range(n)]
+    depths[2] = [cfg.max_depth] * 4
+    depths[3] = [0, 0, 0, 0]
+    orders = [[0, 1, 2, 3], [2, 0, 3, 1], [3, 2, 1, 0], [1, 3, 0, 2]] * 2
+    rows = 4 * cfg.max_depth
+    masks, devtok = synth.planted_masks(n, rows, 0.7, cfg.vocab, seed=2)
+    outs = {}
+    for kind in ("eager", "graph"):
+        stream = torch.cuda.Stream()
+        with torch.cuda.stream(stream):
+            lane = _lane(cfg, w, stream)
+            succ_d = succ.cuda()
+            m_stage = torch.empty(rows, dtype=torch.uint8, device="cuda")
+            t_stage = torch.empty(rows, dtype=torch.int32, device="cuda")
+            drafts = torch.empty(rows, dtype=torch.int32, device="cuda")
+            acc = torch.empty(4, dtype=torch.int32, device="cuda")
+            tok = torch.empty(4, cfg.max_depth + 1, dtype=torch.int32, device="cuda")
+
+            def step(slots, ks):
+                lane.draft_planted(slots, ks, succ_d, m_stage, t_stage, drafts)
+                lane.verify(slots, ks, drafts, None, seed=77, mode=mode, temperature=0.9, out=(acc, tok))
+                lane.commit()
+
+            res, g = [], None
+            for i in range(n):
+                m_stage.copy_(masks[i].cuda())
+                t_stage.copy_(devtok[i].cuda())
+                if kind == "eager":
+                    step(orders[i], depths[i])
+                else:
+                    if g is None:
+                        lane.graph_begin_dynamic(4)
+                        step([0, 1, 2, 3], [1, 1, 1, 1])        # captured, not run
+                        g = lane.graph_end()
+                    lane.graph_set_batch(g, orders[i], depths[i])
+                    lane.graph_launch(g)
+                torch.cuda.synchronize()
+                res.append((acc.cpu().clone(), tok.cpu().clone(),
+                            lane.tap("len", torch.int32, (cfg.max_slots,)).cpu().clone()))
+            st = lane.stats()
+            if g is not None:
+                lane.graph_destroy(g)
+            outs[kind] = (res, st)
+    for i, (a, b) in enumerate(zip(outs["eager"][0], outs["graph"][0])):
+        for x, y in zip(a, b):
+            assert torch.equal(x, y), (i, depths[i], x, y)
+    assert outs["eager"][1] == outs["graph"][1]
+    assert outs["eager"][1]["drafted"] == sum(sum(k) for k in depths)
