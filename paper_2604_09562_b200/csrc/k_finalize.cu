@@ -64,7 +64,7 @@ SV_DEV uint32_t flt_key(float v) {
 }
 SV_DEV float key_flt(uint32_t k) { return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k); }
 
-constexpr int FLT_CAP = 2048;                     // fast path: candidate capacity (shared memory)
+constexpr int FLT_CAP = kFiltCap;                 // fast path: candidate capacity (shared memory)
 constexpr size_t FLT_SMEM = (FLT_THREADS / 32) * 256 * (8 + 4);   // 48 KB: private histograms / candidates
 static_assert(FLT_CAP * 16 + SORT_N * 4 <= FLT_SMEM, "filter candidate buffers exceed the smem budget");
 
@@ -86,7 +86,7 @@ __global__ void __launch_bounds__(FLT_THREADS) filter_kernel(LaneDev d, float in
   __shared__ unsigned int s_cnt_above, s_nc;
   __shared__ unsigned long long s_mass_above, s_target, s_cmass;
   __shared__ int s_tie_lim, s_nkeep, s_fast;
-  __shared__ float s_tau;
+  __shared__ float s_tau, s_S;
   pdl_trigger();
   pdl_wait();
   const int r = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = FLT_THREADS / 32;
@@ -132,7 +132,8 @@ __global__ void __launch_bounds__(FLT_THREADS) filter_kernel(LaneDev d, float in
     float tau = -INFINITY;
     if (use_k && top_k <= nt) tau = srt[top_k - 1];
     if (use_p) {
-      // S estimate from the tile statistics; prefix sums of e(tile max) in sorted order (warp scans)
+      // S from the tile statistics (fixed summation order: strided per thread, warp butterfly, warps in
+      // order), and prefix sums of e(tile max) in sorted order (warp scans)
       float se = 0.f;
       for (int t = tid; t < nt; t += FLT_THREADS) se += tsum[t] * expf(tmax[t] - m);
       se = warp_sum(se);
@@ -140,6 +141,7 @@ __global__ void __launch_bounds__(FLT_THREADS) filter_kernel(LaneDev d, float in
       __syncthreads();
       float S = 0.f;
       for (int i = 0; i < nw; ++i) S += s_redf[i];
+      if (tid == 0) s_S = S;
       static_assert(SORT_N == 2 * FLT_THREADS, "the scan gives each thread two sorted maxima");
       const int i0 = 2 * tid, i1 = i0 + 1;            // a contiguous pair per thread
       const float e0 = i0 < nt ? expf(srt[i0] - m) : 0.f, e1 = i1 < nt ? expf(srt[i1] - m) : 0.f;
@@ -170,12 +172,15 @@ __global__ void __launch_bounds__(FLT_THREADS) filter_kernel(LaneDev d, float in
   __syncthreads();
   const float tau = s_tau;
 
-  // 2. one pass over the row: fixed-point total mass; candidates >= tau into shared memory
+  // 2. one pass over the row: candidates >= tau into shared memory. The total mass for the top-p
+  //    target is the tile statistics' S (sortable rows: computed above, in a fixed order), so only
+  //    candidates evaluate exp; otherwise every element's fixed-point mass is summed.
+  const bool tot_from_tiles = sortable && use_p;
   unsigned long long tot = 0;
   auto visit = [&](float v, int x) {
-    const unsigned long long e = v == -INFINITY ? 0ull : fx_mass(expf(v - m));
-    tot += e;
+    if (!tot_from_tiles) tot += v == -INFINITY ? 0ull : fx_mass(expf(v - m));
     if (tau > -INFINITY && v >= tau) {
+      const unsigned long long e = fx_mass(expf(v - m));
       const unsigned pos = atomicAdd(&s_nc, 1u);
       if (pos < FLT_CAP) {
         c_key[pos] = flt_key(v);
@@ -227,6 +232,7 @@ __global__ void __launch_bounds__(FLT_THREADS) filter_kernel(LaneDev d, float in
   if (tid == 0) {
     unsigned long long t2 = 0;
     for (int i = 0; i < nw; ++i) t2 += s_redu[i];
+    if (tot_from_tiles) t2 = (unsigned long long)((double)s_S * kFx);
     const unsigned long long target = use_p ? (unsigned long long)((double)top_p * (double)t2) : ~0ull;
     s_target = target;
     // the kept set lies inside the candidates iff a limit is reached inside them
@@ -294,28 +300,66 @@ __global__ void __launch_bounds__(FLT_THREADS) filter_kernel(LaneDev d, float in
       }
       __syncthreads();
     }
-    if (tid == 0) {
-      unsigned int c = s_cnt_above;
-      unsigned long long ms = s_mass_above;
-      int D = -1;
-      for (int dg = 255; dg >= 0; --dg) {
-        if (!h_cnt[dg]) continue;
-        const unsigned int c2 = c + h_cnt[dg];
+    if (warp == 0) {
+      // walk the digits from the top in parallel: lane l owns digits 255 - 8l .. 248 - 8l; an exclusive
+      // warp scan of the lanes' (count, mass) gives the totals above each lane's group, then the lane
+      // holding the first digit at which a limit is reached (or the lowest non-empty digit) decides
+      const unsigned int c0 = s_cnt_above;
+      const unsigned long long ms0 = s_mass_above;
+      unsigned int lc = 0;
+      unsigned long long lm = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int dg = 255 - 8 * lane - i;
+        lc += h_cnt[dg];
+        lm += h_mass[dg];
+      }
+      unsigned int ec = lc;
+      unsigned long long em = lm;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {               // inclusive scan over lanes (top digits first)
+        const unsigned int yc = __shfl_up_sync(0xffffffffu, ec, o);
+        const unsigned long long ym = __shfl_up_sync(0xffffffffu, em, o);
+        if (lane >= o) { ec += yc; em += ym; }
+      }
+      unsigned int c = c0 + ec - lc;                   // above this lane's group
+      unsigned long long ms = ms0 + em - lm;
+      int D = -1;                                      // the digit this lane would decide
+      bool hit = false;
+      int last_nz = -1;
+      unsigned int c_last = 0;
+      unsigned long long m_last = 0;
+      for (int i = 0; i < 8 && !hit; ++i) {
+        const int dg = 255 - 8 * lane - i;
+        const unsigned int hc = h_cnt[dg];
+        if (!hc) continue;
+        const unsigned int c2 = c + hc;
         const unsigned long long m2 = ms + h_mass[dg];
-        D = dg;
-        if ((use_k && c2 >= (unsigned)top_k) || (use_p && m2 >= target)) break;
-        c = c2;
-        ms = m2;
+        if ((use_k && c2 >= (unsigned)top_k) || (use_p && m2 >= target)) {
+          hit = true;
+          D = dg;
+        } else {
+          last_nz = dg;
+          c_last = c;
+          m_last = ms;
+          c = c2;
+          ms = m2;
+        }
       }
-      if (D < 0) D = 0;                                // (unreachable: a limit is always reached)
-      else if (!((use_k && c + h_cnt[D] >= (unsigned)top_k) || (use_p && ms + h_mass[D] >= target))) {
-        c -= h_cnt[D];                                 // no limit reached: the lowest bin is the cut
-        ms -= h_mass[D];
+      const unsigned hits = __ballot_sync(0xffffffffu, hit);
+      const unsigned nz = __ballot_sync(0xffffffffu, last_nz >= 0);
+      // the first hit in digit order, else the lowest non-empty digit (no limit reached there)
+      const int src = hits ? __ffs(hits) - 1 : (nz ? 31 - __clz(nz) : 0);
+      const int Dw = __shfl_sync(0xffffffffu, hit ? D : last_nz, src);
+      const unsigned int cw = __shfl_sync(0xffffffffu, hit ? c : c_last, src);
+      const unsigned long long mw = __shfl_sync(0xffffffffu, hit ? ms : m_last, src);
+      if (lane == 0) {
+        const int Dd = (hits || nz) ? Dw : 0;          // (Dd = 0 unreachable: a limit is always reached)
+        s_cnt_above = (hits || nz) ? cw : c0;
+        s_mass_above = (hits || nz) ? mw : ms0;
+        s_prefix = prefix | (uint32_t(Dd) << shift);
+        s_D = Dd;
       }
-      s_cnt_above = c;
-      s_mass_above = ms;
-      s_prefix = prefix | (uint32_t(D) << shift);
-      s_D = D;
     }
     __syncthreads();
   }
@@ -389,6 +433,24 @@ __global__ void __launch_bounds__(FLT_THREADS) filter_kernel(LaneDev d, float in
     __syncthreads();
   }
   if (tid == 0) d.filt_tie[r] = s_tie_lim;
+  // the kept ids (fast path: a subset of the candidates), so finalize races over them only — every
+  // other token has p' = 0 and can win neither the bonus nor the residual race
+  if (fast) {
+    __shared__ unsigned int s_nk;
+    if (tid == 0) s_nk = 0;
+    __syncthreads();
+    const uint32_t kstar = s_prefix;
+    const int tl = s_tie_lim;
+    for (unsigned i = tid; i < nc; i += FLT_THREADS) {
+      const uint32_t k = c_key[i];
+      const int id = c_id[i];
+      if (k > kstar || (k == kstar && id <= tl)) d.filt_ids[(size_t)r * FLT_CAP + atomicAdd(&s_nk, 1u)] = id;
+    }
+    __syncthreads();
+    if (tid == 0) d.filt_cnt[r] = (int)s_nk;
+  } else if (tid == 0) {
+    d.filt_cnt[r] = -1;                               // slow path: finalize scans the whole row
+  }
 }
 
 cudaError_t launch_filter(const LaneDev& d, int T, float inv_temp, int top_k, float top_p, cudaStream_t s) {
@@ -784,7 +846,28 @@ __global__ void __launch_bounds__(FIN_THREADS) finalize_kernel(LaneDev d, const 
       return make_float4(t[0], t[1], t[2], t[3]);
     };
     const float4 zero4 = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (vec && !filt) {
+    const int nkept = filt ? d.filt_cnt[r0 + a] : -1;
+    if (filt && nkept >= 0) {
+      // filtered target with a kept-id list (the filter's fast path): race over those ids only; this
+      // CTA takes slice sidx of the list. Ties keep the lower id (better()), so the list order is moot.
+      const int* ids = d.filt_ids + (size_t)(r0 + a) * FLT_CAP;
+      const int per_l = (nkept + RS - 1) / RS, lo_l = sidx * per_l, hi_l = min(nkept, lo_l + per_l);
+      for (int i = lo_l + tid; i < hi_l; i += FIN_THREADS) {
+        const int x = ids[i];
+        const float lv = lrow[x];
+        const float p = filt_p(fr, x, lv * inv_temp);
+        const u32x4 w = race_words(seed, rid, z, uint32_t(x >> 2));
+        const uint32_t wl = (x & 3) == 0 ? w.x : ((x & 3) == 1 ? w.y : ((x & 3) == 2 ? w.z : w.w));
+        const float invE = __frcp_rn(-logf(word_to_uniform(wl)));
+        bP = better(bP, Best{p > 0.f ? p * invE : -INFINITY, x});
+        if (resid) {
+          const float q = qrow ? qrow[x] : (x == dnext ? 1.0f : 0.0f);
+          const float R = fmaxf(0.f, p - q);
+          sumR += R;
+          bR = better(bR, Best{R > 0.f ? R * invE : -INFINITY, x});
+        }
+      }
+    } else if (vec && !filt) {
       // fast path (16-byte rows, no filter): p = 2^(l*it*log2e - m*log2e) / S with ex2.approx, 1 / E by
       // rcp.approx (the race is decided against the oracle's fp64 scores; both approximations are ~1e-7
       // relative, far inside the borderline band), and strict > comparisons (a thread visits x in

@@ -19,6 +19,7 @@ constexpr int kAttnRows = 64;      // max (k+1) * G query rows per (request, kv 
 constexpr int kSplitKeys = SV_SPLIT_KEYS;   // page keys per split-KV work item
 constexpr int kNumStats = 6 + 3 * (kMaxDepth + 1);
 constexpr int kMaxRaceSplits = 16;
+constexpr int kFiltCap = 2048;     // top-k / top-p filter: candidate capacity (= FLT_CAP, k_finalize.cu)
 constexpr int kPrefillNoHead = 3;  // internal finalize mode: a prefill chunk whose lm-head was skipped  // finalize: CTAs per request sharing a sampled row's race
 
 struct RacePart { float rs; int rx; float ps; int px; float sr; int pad[3]; };   // one race slice's result
@@ -64,6 +65,8 @@ struct LaneDev {
   unsigned* filt_key;                // [Tmax] R31 filter: threshold key of the scaled logit
   int* filt_tie;                     // [Tmax] largest kept token id among threshold ties
   float *filt_inv, *filt_m;          // [Tmax] 1 / kept mass, row max (scaled logits)
+  int* filt_ids;                     // [Tmax][kFiltCap] kept token ids (filter fast path), any order
+  int* filt_cnt;                     // [Tmax] their number, or -1 (slow path: no list)
   int* batch_n;                      // [1] batch of the pending verify (device copy)
   int* T_dev;                        // [1] chain rows of the current verify / prefill chunk (plan writes it);
                                      // row-gridded kernels launched for Tmax rows return beyond it

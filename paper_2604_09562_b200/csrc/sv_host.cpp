@@ -25,7 +25,7 @@ struct Layout {
   size_t slots, depths, row_off, row_req, row_pos, chain_tok, req_err;
   size_t h0, h1, h2, cbuf, logits, tile_max, tile_sum, tile_arg;
   size_t a, b, z, q, kc, vc, o, u;
-  size_t items, item_start, n_items, part_o, part_ml, acc_int, tok_int, batch_n, path_int, row_anc, filt, fin_cnt, fin_part, row_best;
+  size_t items, item_start, n_items, part_o, part_ml, acc_int, tok_int, batch_n, path_int, row_anc, filt, fin_cnt, fin_part, row_best, filt_ids;
   size_t gemm_ws, trace, prefill, handoff, tdev, dctrl;
   size_t max_items;
 
@@ -113,6 +113,7 @@ Layout make_layout(const sv_config& c) {
   L.path_int = L.take(4 * c.max_batch * (c.max_depth + 1));
   L.row_anc = L.take(8 * T);
   L.filt = L.take(16 * T);
+  L.filt_ids = L.take(4 * T * sv::kFiltCap + 4 * T);
   L.fin_cnt = L.take(4 * c.max_batch);
   L.row_best = L.take(8 * T);
   L.fin_part = L.take(sizeof(sv::RacePart) * sv::kMaxRaceSplits * c.max_batch);
@@ -402,6 +403,8 @@ sv_status sv_create(const sv_config* cfg, const sv_weights* w, void* kv_pool, vo
   d.filt_tie = (int*)(ws + L.filt + 4 * (size_t)d.Tmax);
   d.filt_inv = (float*)(ws + L.filt + 8 * (size_t)d.Tmax);
   d.filt_m = (float*)(ws + L.filt + 12 * (size_t)d.Tmax);
+  d.filt_ids = (int*)(ws + L.filt_ids);
+  d.filt_cnt = (int*)(ws + L.filt_ids + 4 * (size_t)d.Tmax * sv::kFiltCap);
   d.trace = getenv("SV_TRACE") ? (unsigned long long*)(ws + L.trace) : nullptr;
 
   // RoPE table: fp64 angles pos * theta^(-2m/d_h), stored fp32 (SURVEY.md §8(c) "Model details")
