@@ -377,6 +377,7 @@ __global__ void __launch_bounds__(FLT_THREADS) filter_kernel(LaneDev d, float in
       const int Dw = __shfl_sync(0xffffffffu, hit ? D : last_nz, src);
       const unsigned int cw = __shfl_sync(0xffffffffu, hit ? c : c_last, src);
       const unsigned long long mw = __shfl_sync(0xffffffffu, hit ? ms : m_last, src);
+      __syncwarp();                                    // every lane has read s_cnt_above / s_mass_above
       if (lane == 0) {
         const int Dd = (hits || nz) ? Dw : 0;          // (Dd = 0 unreachable: a limit is always reached)
         s_cnt_above = (hits || nz) ? cw : c0;
