@@ -115,7 +115,9 @@ const char* sv_strerror(sv_status s);
 /* Bytes the caller must allocate for the KV pool and the workspace for cfg.
  * Both buffers must be 1024-byte aligned. EINVAL on an invalid cfg
  * (non-positive sizes, n_q_heads % n_kv_heads != 0, head_dim not in {64,128},
- * d_model % 64 != 0, max_depth > 32, (max_depth + 1) * group > 64). */
+ * d_model % 64 != 0, max_depth > 32, (max_depth + 1) * group > 64 unless group <= 4 and max_depth < 32:
+ * verifies whose deepest chain has (k + 1) * group <= 64 query rows per kv head run the keys-on-lanes
+ * attention kernel, deeper ones (up to k = 31 at group 4) the rows-on-lanes kernel). */
 sv_status sv_query_sizes(const sv_config* cfg, size_t* kv_pool_bytes, size_t* workspace_bytes);
 
 /* Create a lane on the current CUDA device. Builds the fp32 RoPE table

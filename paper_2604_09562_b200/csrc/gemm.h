@@ -24,9 +24,9 @@ size_t gemm_workspace_bytes(int Tmax, int max_n);
 GemmPlan* gemm_plan_create(const LaneDev& d, void* ws, cudaStream_t s);
 void gemm_plan_destroy(GemmPlan* p);
 // a3 verify attention: tcgen05 kernel when the shape allows (page 64, d_h 64/128), else SIMT
-cudaError_t attn_run(GemmPlan* p, int layer, int batch, int tree, cudaStream_t s);
-// true when attn_run's kernel writes O itself for requests with a single split-KV item
-bool attn_writes_single_split(GemmPlan* p);
+// max_rows: the deepest chain of this verify + 1 (picks the kernel); used_tc2 (optional): the keys-on-lanes
+// kernel ran (it writes O itself for single-split requests)
+cudaError_t attn_run(GemmPlan* p, int layer, int batch, int tree, int max_rows, cudaStream_t s, bool* used_tc2);
 // true when the lm-head GEMM (EPI_LOGITS) also fills GemmEpi::row_best (the weight-major kernel)
 bool gemm_fills_row_best(GemmPlan* p);
 // true when every GEMM of the step honours GemmEpi::M_dev and the attention reads its work list from

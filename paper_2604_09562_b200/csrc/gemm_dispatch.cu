@@ -107,8 +107,8 @@ GemmPlan* gemm_plan_create(const LaneDev& d, void* ws, cudaStream_t s) {
   const int G = d.Hq / d.Hkv;
   p->use_tc_attn = p->encode && !(aenv && !strcmp(aenv, "simt")) && d.page == 64 && (d.dh == 64 || d.dh == 128) &&
                    G <= 4 && d.max_depth + 1 <= 32;
-  p->use_tc2_attn = p->use_tc_attn && d.dh == 128 && (d.max_depth + 1) * G <= 64 && (64 % G) == 0 &&
-                    !(aenv && !strcmp(aenv, "tc1"));
+  // keys-on-lanes kernel: chosen per verify when its (max k + 1) G <= 64 query slots fit (attn_run)
+  p->use_tc2_attn = p->use_tc_attn && d.dh == 128 && (64 % G) == 0 && !(aenv && !strcmp(aenv, "tc1"));
   if (p->use_tc_attn) p->attn_maps_ok = encode_attn_maps(p);
   return p;
 }
@@ -148,17 +148,22 @@ static bool encode_attn_maps(GemmPlan* p) {
   return true;
 }
 
-cudaError_t attn_run(GemmPlan* p, int layer, int batch, int tree, cudaStream_t s) {
+cudaError_t attn_run(GemmPlan* p, int layer, int batch, int tree, int max_rows, cudaStream_t s, bool* used_tc2) {
   LaneDev d = p->d;
   d.tree = tree;
-  if (p->use_tc2_attn && p->attn_maps_ok)
+  const int G = d.Hq / d.Hkv;
+  if (used_tc2) *used_tc2 = false;
+  // keys-on-lanes when this verify's deepest chain fits its 64 query slots per kv head; the rows-on-
+  // lanes kernel up to 32 rows x G <= 4 (deeper chains, e.g. SpecuStream's d* up to 20); else SIMT
+  if (p->use_tc2_attn && p->attn_maps_ok && max_rows * G <= kAttnRows) {
+    if (used_tc2) *used_tc2 = true;
     return launch_attention_tc2(p->map_q2, p->map_kv, d, layer, p->num_sms, s);
-  if (p->use_tc_attn && p->attn_maps_ok)
+  }
+  if (p->use_tc_attn && p->attn_maps_ok && max_rows <= p->q_box_tokens)
     return launch_attention_tc(p->map_q, p->map_kv, d, layer, p->num_sms, p->q_box_tokens, s);
+  if (max_rows * G > kAttnRows) return cudaErrorInvalidValue;
   return launch_attention(d, layer, batch, s);
 }
-
-bool attn_writes_single_split(GemmPlan* p) { return p->use_tc2_attn && p->attn_maps_ok; }
 
 bool gemm_fills_row_best(GemmPlan* p) { return p->use_tc && !p->use_2sm && !p->use_1sm && !p->use_streamk; }
 

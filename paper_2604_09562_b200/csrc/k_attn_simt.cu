@@ -109,15 +109,15 @@ __global__ void __launch_bounds__(128) attn_simt_kernel(LaneDev d, int layer) {
       }
     }
     __syncthreads();
-    float* po = d.part_o + (size_t)it * kAttnRows * dh;
+    float* po = d.part_o + (size_t)it * kPartRows * dh;
 #pragma unroll
     for (int i = 0; i < kAttnRows; ++i) {
       const int rl = rg + i * groups;
       if (i * groups < kAttnRows && rl < nr) po[rl * dh + dd_own] = acc[i];
     }
     for (int rl = tid; rl < nr; rl += 128) {
-      d.part_ml[((size_t)it * kAttnRows + rl) * 2 + 0] = Ms[rl];
-      d.part_ml[((size_t)it * kAttnRows + rl) * 2 + 1] = Ls[rl];
+      d.part_ml[((size_t)it * kPartRows + rl) * 2 + 0] = Ms[rl];
+      d.part_ml[((size_t)it * kPartRows + rl) * 2 + 1] = Ls[rl];
     }
   }
 }
@@ -169,7 +169,7 @@ __global__ void __launch_bounds__(256) attn_combine_kernel(LaneDev d, int T, int
 #pragma unroll
       for (int k = 0; k < MS; ++k) {
         const int s = s0 + k;
-        const size_t it = (size_t)(base + s) * kAttnRows + rl;
+        const size_t it = (size_t)(base + s) * kPartRows + rl;
         ml[k] = s < ns ? *reinterpret_cast<const float2*>(d.part_ml + it * 2) : make_float2(-INFINITY, 0.f);
         const float* src = d.part_o + it * DH + lane * V;
         if constexpr (V == 4) {

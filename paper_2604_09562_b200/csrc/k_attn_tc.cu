@@ -384,7 +384,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         tc::named_bar(bar_id, 64);
         const float l_tot = l + xl[ob * 256 + (hf ^ 1) * 128 + tl];
         const int rl = j * G + q;                     // partial-buffer row (combine's layout)
-        float* po = d.part_o + ((size_t)it * kAttnRows + rl) * DH + hf * (DH / 2);
+        float* po = d.part_o + ((size_t)it * kPartRows + rl) * DH + hf * (DH / 2);
         for (int c = 0; c < DH / 2; c += 32) {
           uint32_t ov[32];
           __syncwarp();
@@ -399,8 +399,8 @@ __global__ void __launch_bounds__(THREADS, 1)
           }
         }
         if (row_valid && hf == 0) {
-          d.part_ml[((size_t)it * kAttnRows + rl) * 2 + 0] = m == -INFINITY ? -INFINITY : m * 0.69314718055994531f;
-          d.part_ml[((size_t)it * kAttnRows + rl) * 2 + 1] = l_tot;
+          d.part_ml[((size_t)it * kPartRows + rl) * 2 + 0] = m == -INFINITY ? -INFINITY : m * 0.69314718055994531f;
+          d.part_ml[((size_t)it * kPartRows + rl) * 2 + 1] = l_tot;
         }
       }
       tc::fence_before();

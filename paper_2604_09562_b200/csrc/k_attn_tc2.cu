@@ -695,7 +695,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         tc::named_bar(bar_id, 128);                   // exchange slots are reused by the next item
       } else {
-        float* po = d.part_o + (size_t)it * kAttnRows * DH + dcol;
+        float* po = d.part_o + (size_t)it * kPartRows * DH + dcol;
 #pragma unroll
         for (int c = 0; c < 32; ++c) {
           const int r = ch * 32 + c;
@@ -703,8 +703,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         const int my_slot = ch * 32 + lane;
         if (q == 0 && my_slot < RG) {
-          d.part_ml[((size_t)it * kAttnRows + my_slot) * 2 + 0] = my_init ? my_m * 0.69314718055994531f : -INFINITY;
-          d.part_ml[((size_t)it * kAttnRows + my_slot) * 2 + 1] = ltot;
+          d.part_ml[((size_t)it * kPartRows + my_slot) * 2 + 0] = my_init ? my_m * 0.69314718055994531f : -INFINITY;
+          d.part_ml[((size_t)it * kPartRows + my_slot) * 2 + 1] = ltot;
         }
         tc::named_bar(bar_id, 128);                   // exchange slots are reused by the next item
         tc::fence_before();

@@ -12,7 +12,8 @@ typedef __nv_bfloat16 bf16;
 constexpr int kMaxBatch = 256;     // PlanArgs capacity (requests per verify)
 constexpr int kMaxDepth = 32;      // k_i <= 32 (sv_lane_stats histograms have 33 bins)
 constexpr int kVocabTile = 128;    // lm-head epilogue statistics tile
-constexpr int kAttnRows = 64;      // max (k+1) * G query rows per (request, kv head)
+constexpr int kAttnRows = 64;      // (k+1) * G query rows per (request, kv head) of the keys-on-lanes / SIMT kernels
+constexpr int kPartRows = 128;     // split-KV partial rows per work item (rows-on-lanes kernel: <= 32 rows x G <= 4)
 #ifndef SV_SPLIT_KEYS
 #define SV_SPLIT_KEYS 1024
 #endif

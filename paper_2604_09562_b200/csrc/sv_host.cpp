@@ -6,6 +6,7 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <algorithm>
 #include <string>
 #include <vector>
 
@@ -49,7 +50,10 @@ bool valid_cfg(const sv_config* c) {
   if (c->page_size < 8 || c->page_size % 8 || c->n_pages < 1 || c->max_slots < 1) return false;
   if (c->max_batch < 1 || c->max_batch > sv::kMaxBatch) return false;
   if (c->max_depth < 0 || c->max_depth > sv::kMaxDepth) return false;
-  if ((c->max_depth + 1) * (c->n_q_heads / c->n_kv_heads) > sv::kAttnRows) return false;
+  {                                           // query rows per (request, kv head): keys-on-lanes / SIMT
+    const int G = c->n_q_heads / c->n_kv_heads;   // kernels take (k+1) G <= 64, the rows-on-lanes one
+    if ((c->max_depth + 1) * G > sv::kAttnRows && !(G <= 4 && c->max_depth + 1 <= 32)) return false;   // k+1 <= 32, G <= 4
+  }
   if (c->max_pos < c->max_depth + 2) return false;
   if (!(c->rope_theta > 0.f) || !(c->norm_eps >= 0.f)) return false;
   return true;
@@ -105,8 +109,8 @@ Layout make_layout(const sv_config& c) {
   L.items = L.take(16 * L.max_items);
   L.item_start = L.take(4 * (c.max_batch + 1));
   L.n_items = L.take(16);
-  L.part_o = L.take(4 * L.max_items * sv::kAttnRows * c.head_dim);
-  L.part_ml = L.take(8 * L.max_items * sv::kAttnRows);
+  L.part_o = L.take(4 * L.max_items * sv::kPartRows * c.head_dim);
+  L.part_ml = L.take(8 * L.max_items * sv::kPartRows);
   L.acc_int = L.take(4 * c.max_batch);
   L.tok_int = L.take(4 * c.max_batch * (c.max_depth + 1));
   L.batch_n = L.take(4);
@@ -542,6 +546,9 @@ static sv_status verify_impl(sv_ctx* c, int32_t batch, const int32_t* slots, con
     d.dyn_ctrl = (const int*)(c->ws + c->lay.dctrl);
   }
   const int* Mdev = dyn ? d.T_dev : nullptr;
+  int max_rows = 1;                                 // deepest chain + 1 (a dynamic graph: any depth)
+  for (int b = 0; b < batch; ++b) max_rows = std::max(max_rows, p.depths[b] + 1);
+  if (dyn) max_rows = c->cfg.max_depth + 1;
   const int T = dyn ? batch * (c->cfg.max_depth + 1) : p.T;
   cudaStream_t s = c->stream;
   const float inv_temp = mode == SV_SAMPLE ? 1.0f / temperature : 1.0f;
@@ -559,8 +566,9 @@ static sv_status verify_impl(sv_ctx* c, int32_t batch, const int32_t* slots, con
     e.M_hint = p.T;
     STAGE(c, ST_QKV, gemm(c, d.a, d.wqkv + (size_t)layer * d.qkv_rows * d.D, d.cbuf, T, d.qkv_rows, d.D,
                           sv::EPI_QKV_ROPE, e));
-    STAGE(c, ST_ATTN, sv::attn_run(c->gemm, layer, batch, d.tree, s));
-    STAGE(c, ST_COMBINE, sv::launch_attn_combine(d, T, sv::attn_writes_single_split(c->gemm), s));
+    bool tc2 = false;
+    STAGE(c, ST_ATTN, sv::attn_run(c->gemm, layer, batch, d.tree, max_rows, s, &tc2));
+    STAGE(c, ST_COMBINE, sv::launch_attn_combine(d, T, tc2, s));
     float* hattn = d.F > 0 ? d.h1 : d.h2;
     e.resid_in = hin;
     e.resid_out = hattn;

@@ -54,7 +54,7 @@ def test_query_sizes(lib):
 
 
 @pytest.mark.parametrize("field,value", [("n_q_heads", 3), ("head_dim", 96), ("max_depth", 33),
-                                         ("max_batch", 0), ("d_model", 100), ("max_depth", 16)])
+                                         ("max_batch", 0), ("d_model", 100), ("n_kv_heads", 4)])
 def test_query_sizes_rejects_bad_config(lib, field, value):
     cfg = synth.LLAMA.with_(**{field: value})
     c = sv.Config.from_any(cfg)
@@ -91,3 +91,12 @@ def test_handoff_batch_bytes():
     t = (ctypes.c_int32 * 3)(1, 65, 128)
     assert lib.sv_kv_slots_bytes(ctypes.byref(c), 3, t) == 2 * (1 + 2 + 2) * blk + 16
     assert lib.sv_kv_slots_bytes(ctypes.byref(c), 0, t) == 0
+
+
+def test_query_sizes_deep_chains(lib):
+    """G = 4: chains up to k = 31 (rows-on-lanes attention for (k + 1) G > 64); G = 8 caps at k = 7."""
+    kv, ws = ctypes.c_size_t(), ctypes.c_size_t()
+    ok = sv.Config.from_any(synth.LLAMA.with_(max_depth=31, max_batch=8, max_slots=8, n_pages=64))
+    assert lib.sv_query_sizes(ctypes.byref(ok), ctypes.byref(kv), ctypes.byref(ws)) == sv.SV_OK
+    g8 = sv.Config.from_any(synth.LLAMA.with_(n_kv_heads=4, max_depth=7))
+    assert lib.sv_query_sizes(ctypes.byref(g8), ctypes.byref(kv), ctypes.byref(ws)) == sv.SV_OK

@@ -266,3 +266,16 @@ def test_llama_long_contexts_split_kv():
     drafts = synth.random_tokens(sum(depths), cfg.vocab, seed=12)
     rep, _, _ = run_and_check(S, slots, depths, drafts, "greedy")
     print("llama long contexts", rep)
+
+
+def test_llama_deep_chains_rows_on_lanes():
+    """max_depth 20 at G = 4 (SpecuStream's d* reaches 20, Alg. 4): a verify whose deepest chain
+    has (k + 1) G > 64 query rows per kv head runs the rows-on-lanes tcgen05 kernel (32 rows x 4 heads per
+    item), one within 64 the keys-on-lanes kernel, on the same lane; every stage within the contract."""
+    cfg = synth.LLAMA.with_(n_pages=96, max_slots=6, max_batch=6, max_depth=20, max_pos=2048)
+    for slots, depths, seed in (([0, 1, 2, 3, 4, 5], [20, 9, 15, 0, 3, 17], 18), ([1, 3], [8, 2], 19)):
+        S = Setup(cfg, [256, 1100, 40, 700, 2000, 1], seed=17)
+        drafts = synth.random_tokens(sum(depths), cfg.vocab, seed=seed)
+        rep, _, _ = run_and_check(S, slots, depths, drafts, "greedy")
+        print("deep chains", depths, rep["o"])
+        S.lane.close()
