@@ -492,19 +492,22 @@ def _run_gpu(args, wl, rank, world, dev, stream):
     roof = roofline(kern, alg, pk, capped, traffic)
     dominant = max(kern.items(), key=lambda kv: kv[1]["ms_per_launch"] * kv[1]["launches"])[0] if kern else None
     vg_depths = depths[total - 1]
-    # verify-step µs as SURVEY.md §8(d) defines it, right after the timed region (same power state)
-    vgraph = verify_step_graph(lane, wl, slots, vg_depths, drafts, 4321, (acc, tok), par_d, dev, VERIFY_GRAPH_REPLAYS)
-    steady = steady_state(args, wl, lane, depths, elapsed_ms / args.steps, pk, dev, stream)
-    # ----- e2e through host buffers: pinned H2D inputs and D2H results every step (see run_e2e)
+    # ----- e2e through host buffers (pinned H2D inputs and D2H results every step, see run_e2e), right
+    # after the timed region so it runs in the same power state (the steady phase below is power-capped)
     e2e = e2e_host = None
     if ctl:                                           # later regions draft at the controller's last depth
         for i in range(total, total + args.e2e_steps + HOST_DRAFTER_STEPS):
             ctl.prepare(i)
     if args.e2e_steps > 0:
-        e2e = run_e2e(args, wl, lane, succ, depths, masks, devtok, dev, total)
+        with Clocks(dev.index) as eclk:
+            e2e = run_e2e(args, wl, lane, succ, depths, masks, devtok, dev, total)
+        e2e["clocks"] = eclk.summary()
         if not wl.tree:                               # the host drafter variant drafts chains only
             e2e_host = run_e2e_host_drafter(args, wl, lane, succ, depths, masks, devtok, dev,
                                             total + args.e2e_steps, HOST_DRAFTER_STEPS)
+    # verify-step µs as SURVEY.md §8(d) defines it (graph replay, drafting excluded), then the steady phase
+    vgraph = verify_step_graph(lane, wl, slots, vg_depths, drafts, 4321, (acc, tok), par_d, dev, VERIFY_GRAPH_REPLAYS)
+    steady = steady_state(args, wl, lane, depths, elapsed_ms / args.steps, pk, dev, stream)
     check = decision_check(wl, lane, reqs, succ, masks, devtok, depths, total + args.e2e_steps + HOST_DRAFTER_STEPS,
                            dev) if args.check_steps > 0 else None
     return dict(check=check, steady=steady, elapsed_ms=elapsed_ms, tokens=tokens, per_step=per_step, prof=kern, roof=roof, dominant=dominant,
