@@ -35,7 +35,7 @@ for name, N, K in (("qkv", 6144, 4096), ("o", 4096, 4096), ("down", 4096, 14336)
     row = []
     os.environ.pop("SV_SW_NT", None)
     row.append(("auto", t(lambda: lane.debug_gemm(a, b, c, 5))))
-    for nt in (48, 64, 96, 144, 192):
+    for nt in (96, 128, 144, 160, 176, 192, 224, 256):
         os.environ["SV_SW_NT"] = str(nt)
         row.append((nt, t(lambda: lane.debug_gemm(a, b, c, 5))))
     os.environ.pop("SV_SW_NT", None)
