@@ -134,74 +134,94 @@ cudaError_t launch_attention(const LaneDev& d, int layer, int batch, cudaStream_
   return cudaGetLastError();
 }
 
-// combine split-KV partials. One CTA per chain row (the row's request, position and split count
-// are looked up once), each warp merges q heads w, w + 8, ...: lanes over d_h (float4 each for
-// d_h = 128, float2 for 64); the loads of up to 8 splits are issued together, with an online
-// rescale between chunks. O = sum_s e^(m_s - M) O_s / sum_s e^(m_s - M) l_s, M = max m_s.
+// combine split-KV partials. One CTA per chain row (the row's chain index, split count and first
+// item come from the plan's row table), each warp merges q heads w, w + 8, ...: lanes over d_h
+// (float4 each for d_h = 128, float2 for 64); the loads of up to 4 splits of 2 heads are issued
+// together, with an online rescale between chunks of 4 splits. O = sum_s e^(m_s - M) O_s / sum_s e^(m_s - M) l_s, M = max m_s.
 template <int DH>
-__global__ void __launch_bounds__(256) attn_combine_kernel(LaneDev d, int T, int skip_single) {
+__global__ void __launch_bounds__(256, 3) attn_combine_kernel(LaneDev d, int T, int skip_single) {
   pdl_trigger();
   pdl_wait();
   constexpr int V = DH / 32;                       // floats per lane
-  constexpr int MS = 8;
-  __shared__ int s_j, s_ns, s_base;
+  constexpr int MS = 4;
   const int r = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (r >= *d.T_dev) return;                       // launched for Tmax rows (dynamic-depth graph)
-  if (threadIdx.x == 0) {
-    const int b = d.row_req[r];
-    s_j = r - d.row_off[b];
-    s_ns = num_splits(d.len[d.slots[b]]);
-    s_base = d.item_start[b];
-  }
-  __syncthreads();
-  const int j = s_j, ns = s_ns;
+  // the row's (chain row, splits, first item) from the plan's table: one load, issued with the T bound
+  const int Tn = *d.T_dev;
+  const int4 rc = d.row_comb[r];
+  if (r >= Tn) return;                             // launched for Tmax rows (dynamic-depth graph)
+  const int j = rc.x, ns = rc.y, s_base = rc.z;
   if (skip_single && ns == 1) return;              // the attention kernel wrote this row's O
   const int G = d.Hq / d.Hkv;
-  for (int hq = warp; hq < d.Hq; hq += 8) {
-    const int h = hq / G, g = hq % G, rl = j * G + g;
-    const int base = s_base + h * ns;
-    float M = -INFINITY, l = 0.f, o[V];
+  // HB q heads per warp iteration (w + 8 i), their split loads issued together: a row's loads are
+  // then in flight at once instead of one head's after another
+  constexpr int HB = 2;
+  for (int hq0 = warp; hq0 < d.Hq; hq0 += 8 * HB) {
+    float M[HB], l[HB], o[HB][V];
+    const float* po[HB];                           // split s of head hb: po[hb] + s * kPartRows * DH
+    const float* pm[HB];
+    bool hok[HB];
 #pragma unroll
-    for (int i = 0; i < V; ++i) o[i] = 0.f;
+    for (int hb = 0; hb < HB; ++hb) {
+      const int hq = hq0 + 8 * hb, h = hq / G, g = hq % G;
+      hok[hb] = hq < d.Hq;
+      const size_t it0 = (size_t)(s_base + h * ns) * kPartRows + j * G + g;
+      po[hb] = d.part_o + it0 * DH + lane * V;
+      pm[hb] = d.part_ml + it0 * 2;
+      M[hb] = -INFINITY;
+      l[hb] = 0.f;
+#pragma unroll
+      for (int i = 0; i < V; ++i) o[hb][i] = 0.f;
+    }
     for (int s0 = 0; s0 < ns; s0 += MS) {
-      float2 ml[MS];
-      float v[MS][V];
+      float2 ml[HB][MS];
+      float v[HB][MS][V];
 #pragma unroll
-      for (int k = 0; k < MS; ++k) {
-        const int s = s0 + k;
-        const size_t it = (size_t)(base + s) * kPartRows + rl;
-        ml[k] = s < ns ? *reinterpret_cast<const float2*>(d.part_ml + it * 2) : make_float2(-INFINITY, 0.f);
-        const float* src = d.part_o + it * DH + lane * V;
-        if constexpr (V == 4) {
-          const float4 x = s < ns ? *reinterpret_cast<const float4*>(src) : make_float4(0.f, 0.f, 0.f, 0.f);
-          v[k][0] = x.x; v[k][1] = x.y; v[k][2] = x.z; v[k][3] = x.w;
-        } else {
-          const float2 x = s < ns ? *reinterpret_cast<const float2*>(src) : make_float2(0.f, 0.f);
-          v[k][0] = x.x; v[k][1] = x.y;
+      for (int hb = 0; hb < HB; ++hb) {
+#pragma unroll
+        for (int k = 0; k < MS; ++k) {
+          const int s = s0 + k;
+          const bool ok = hok[hb] && s < ns;
+          ml[hb][k] = ok ? *reinterpret_cast<const float2*>(pm[hb] + (size_t)s * kPartRows * 2) : make_float2(-INFINITY, 0.f);
+          const float* src = po[hb] + (size_t)s * kPartRows * DH;
+          if constexpr (V == 4) {
+            const float4 x = ok ? *reinterpret_cast<const float4*>(src) : make_float4(0.f, 0.f, 0.f, 0.f);
+            v[hb][k][0] = x.x; v[hb][k][1] = x.y; v[hb][k][2] = x.z; v[hb][k][3] = x.w;
+          } else {
+            const float2 x = ok ? *reinterpret_cast<const float2*>(src) : make_float2(0.f, 0.f);
+            v[hb][k][0] = x.x; v[hb][k][1] = x.y;
+          }
         }
       }
-      float Mn = M;
 #pragma unroll
-      for (int k = 0; k < MS; ++k) Mn = fmaxf(Mn, ml[k].x);
-      if (Mn == -INFINITY) continue;
-      const float sc = M == -INFINITY ? 0.f : expf(M - Mn);
-      l *= sc;
+      for (int hb = 0; hb < HB; ++hb) {
+        float Mn = M[hb];
 #pragma unroll
-      for (int i = 0; i < V; ++i) o[i] *= sc;
+        for (int k = 0; k < MS; ++k) Mn = fmaxf(Mn, ml[hb][k].x);
+        if (Mn == -INFINITY) continue;
+        const float sc = M[hb] == -INFINITY ? 0.f : expf(M[hb] - Mn);
+        l[hb] *= sc;
 #pragma unroll
-      for (int k = 0; k < MS; ++k) {
-        const float w = ml[k].x == -INFINITY ? 0.f : expf(ml[k].x - Mn);
-        l += ml[k].y * w;
+        for (int i = 0; i < V; ++i) o[hb][i] *= sc;
 #pragma unroll
-        for (int i = 0; i < V; ++i) o[i] += v[k][i] * w;
+        for (int k = 0; k < MS; ++k) {
+          const float w = ml[hb][k].x == -INFINITY ? 0.f : expf(ml[hb][k].x - Mn);
+          l[hb] += ml[hb][k].y * w;
+#pragma unroll
+          for (int i = 0; i < V; ++i) o[hb][i] += v[hb][k][i] * w;
+        }
+        M[hb] = Mn;
       }
-      M = Mn;
     }
-    const float inv = 1.0f / l;
-    bf16* dst = d.o + (size_t)r * d.Hq * DH + (size_t)hq * DH + lane * V;
 #pragma unroll
-    for (int i = 0; i < V; i += 2)
-      *reinterpret_cast<__nv_bfloat162*>(dst + i) = __floats2bfloat162_rn(o[i] * inv, o[i + 1] * inv);
+    for (int hb = 0; hb < HB; ++hb) {
+      const int hq = hq0 + 8 * hb;
+      if (hq >= d.Hq) break;
+      const float inv = 1.0f / l[hb];
+      bf16* dst = d.o + (size_t)r * d.Hq * DH + (size_t)hq * DH + lane * V;
+#pragma unroll
+      for (int i = 0; i < V; i += 2)
+        *reinterpret_cast<__nv_bfloat162*>(dst + i) = __floats2bfloat162_rn(o[hb][i] * inv, o[hb][i + 1] * inv);
+    }
   }
 }
 

@@ -19,6 +19,17 @@
 namespace sv {
 
 constexpr int FIN_THREADS = 512;
+// phase timeline of every CTA (SV_TRACE=1; global timer, rows e of the lane trace buffer, index
+// request * 4 + slice < 256): 0 start, 1 after the dependency wait, 2 row statistics, 3 accept scan,
+// 4 race loop, 5 slice merge
+#define FIN_TR(e)                                                                                 \
+  do {                                                                                            \
+    if (d.trace && threadIdx.x == 0 && blockIdx.x * 4 + blockIdx.y < 256) {                       \
+      unsigned long long t_;                                                                      \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                      \
+      d.trace[(e)*256 + blockIdx.x * 4 + blockIdx.y] = t_;                                        \
+    }                                                                                             \
+  } while (0)
 
 SV_DEV float tc_ex2(float x) {
   float r;
@@ -691,7 +702,66 @@ __device__ void tree_walk(const LaneDev& d, const int* __restrict__ drafts, cons
   }
 }
 
-__global__ void __launch_bounds__(FIN_THREADS) finalize_kernel(LaneDev d, const int* __restrict__ drafts,
+// Greedy chain decisions from the row_best keys (one warp): lane j < 32 holds chain row j (and j + 32
+// for k = 32); draft j + 1 = drafts[doff + j] is accepted iff it equals row j's argmax; a = the first
+// rejection (k if none), the emitted token after the accepted drafts = row a's argmax (SURVEY.md
+// §8(a) a6, greedy). Outputs and counters as the generic path below writes them.
+__device__ __forceinline__ void finalize_greedy_warp(const LaneDev& d, const int* __restrict__ drafts, int b,
+                                                  int* __restrict__ acc_out, int* __restrict__ tok_out,
+                                                  int* __restrict__ nodes_out) {
+  const int lane = threadIdx.x & 31;
+  const int k = d.depths[b], r0 = d.row_off[b], doff = r0 - b, err = d.req_err[b];
+  const int K1 = d.max_depth + 1;
+  int top[2], drf[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int j = lane + 32 * h;
+    top[h] = -1;
+    drf[h] = -1;
+    if (j <= k) {
+      const unsigned long long key = d.row_best[r0 + j];
+      top[h] = (int)(0xFFFFFFFFu - (uint32_t)key);
+    }
+    if (j < k) drf[h] = drafts[doff + j];
+  }
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+    if (lane + 32 * h <= k) d.row_best[r0 + lane + 32 * h] = 0ull;   // zero for the next verify
+  const bool acc = lane < k && drf[0] == top[0];                       // k <= 32: tests j = 1..k on lanes 0..k-1
+  const unsigned kmask = k >= 32 ? 0xffffffffu : ((1u << k) - 1u);
+  const unsigned okm = __ballot_sync(0xffffffffu, acc) & kmask;
+  const unsigned fail = ~okm & kmask;
+  const int a = fail ? __ffs(fail) - 1 : k;
+  const int y = a < 32 ? __shfl_sync(0xffffffffu, top[0], a & 31) : __shfl_sync(0xffffffffu, top[1], 0);
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int i = lane + 32 * h;
+    if (i >= K1) continue;
+    const int t = err ? -1 : (i < a ? drf[h] : (i == a ? y : -1));
+    const int nd = (!err && i <= a) ? i : -1;
+    tok_out[(size_t)b * K1 + i] = t;
+    if (d.tok_int) d.tok_int[(size_t)b * K1 + i] = t;
+    if (d.path_int) d.path_int[(size_t)b * K1 + i] = nd;
+    if (nodes_out) nodes_out[(size_t)b * K1 + i] = nd;
+  }
+  if (lane == 0) {
+    acc_out[b] = err ? -1 : a;
+    if (d.acc_int) d.acc_int[b] = err ? -1 : a;
+    if (b == 0) atomicAdd(&d.stats[ST_STEPS], 1ull);
+    if (!err) {
+      atomicAdd(&d.stats[ST_ROWS], (unsigned long long)(k + 1));
+      atomicAdd(&d.stats[ST_DRAFTED], (unsigned long long)k);
+      atomicAdd(&d.stats[ST_ACCEPTED], (unsigned long long)a);
+      atomicAdd(&d.stats[ST_EMITTED], (unsigned long long)(a + 1));
+      atomicAdd(&d.stats[ST_INDEP], (unsigned long long)__popc(okm));
+      atomicAdd(&d.stats[ST_HIST + a], 1ull);
+      atomicAdd(&d.stats[ST_DRAFTED_BY_K + k], (unsigned long long)k);
+      atomicAdd(&d.stats[ST_ACCEPTED_BY_K + k], (unsigned long long)a);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(FIN_THREADS, 2) finalize_kernel(LaneDev d, const int* __restrict__ drafts,
                                                                 const int* __restrict__ parents,
                                                                 const float* __restrict__ probs,
                                                                 const float* __restrict__ logits, uint64_t seed,
@@ -704,10 +774,22 @@ __global__ void __launch_bounds__(FIN_THREADS) finalize_kernel(LaneDev d, const 
   __shared__ Best s_bestR[FIN_THREADS / 32], s_bestP[FIN_THREADS / 32];
   __shared__ float s_sumR[FIN_THREADS / 32];
   __shared__ int s_path[kMaxDepth + 1];             // accepted path (chain rows); identity for chains
+  __shared__ int s_tb[kMaxDepth + 1];               // row statistics: tile of each row's max
+  __shared__ float s_rm[FIN_THREADS / 32][8], s_rs[FIN_THREADS / 32][8];
+  __shared__ int s_rt[FIN_THREADS / 32][8];
 
+  FIN_TR(0);
   pdl_trigger();
   pdl_wait();
+  FIN_TR(1);
   const int b = blockIdx.x;
+  if (!parents && mode == SV_GREEDY && use_row_best) {
+    // greedy chains (the lm-head epilogue left each row's argmax key): warp 0 alone, lane j holding
+    // row j's argmax and draft j, the accept scan by one ballot (every load in one round trip)
+    if (threadIdx.x >= 32) return;
+    finalize_greedy_warp(d, drafts, b, acc_out, tok_out, nodes_out);
+    return;
+  }
   const int k = d.depths[b], slot = d.slots[b], r0 = d.row_off[b], doff = r0 - b;
   const int L = d.len[slot];
   const unsigned long long rid = d.rid[slot];
@@ -729,50 +811,106 @@ __global__ void __launch_bounds__(FIN_THREADS) finalize_kernel(LaneDev d, const 
       d.row_best[r0 + j] = 0ull;
     }
   }
-  for (int j = warp; j <= ((nohead || (use_row_best && mode != SV_SAMPLE)) ? -1 : k); j += nw) {
-    const float* tm = d.tile_max + (size_t)(r0 + j) * d.nt;
-    const float* ts = d.tile_sum + (size_t)(r0 + j) * d.nt;
-    const int* ta = d.tile_arg + (size_t)(r0 + j) * d.nt;
-    float m = -INFINITY, S = 0.f;
-    int am = 0x7fffffff;
-    constexpr int U = 8;
-    for (int t0 = lane; t0 < d.nt; t0 += 32 * U) {
-      float vm[U], vs[U];
-      int va[U];
+  // Otherwise the whole CTA combines the vocab-tile statistics of up to 8 rows at a time: thread t
+  // takes tiles t, t + 512, ... of every row (all loads of a group in flight together), folds them
+  // online, then a warp butterfly and an in-order merge of the 16 warps; the row's argmax is the tile
+  // argmax of its lowest max tile (tiles are in vocabulary order), looked up at the end.
+  if (!(nohead || (use_row_best && mode != SV_SAMPLE))) {
+    // per row: the block max M first (fmax trees: no exponentials), then sum_t s_t e^(m_t - M) with
+    // one exponential per tile, and the lowest tile attaining M (its tile argmax is the row's argmax)
+    const int nt = d.nt;
+    constexpr int RG = 5;                                 // rows per group (loads of a group in flight together)
+    constexpr int TPT = 2;                                // tiles per thread per sweep
+    for (int j0 = 0; j0 <= k; j0 += RG) {
+      float mt[RG];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int t = t0 + 32 * u;
-        const bool ok = t < d.nt;
-        vm[u] = ok ? tm[t] : -INFINITY;
-        vs[u] = ok ? ts[t] : 0.f;
-        va[u] = ok ? ta[t] : 0x7fffffff;
+      for (int jj = 0; jj < RG; ++jj) mt[jj] = -INFINITY;
+      // pass 1: maxima (the loads stay in registers when nt <= TPT * FIN_THREADS)
+      float vm[RG][TPT], vs[RG][TPT];
+      const bool one_sweep = nt <= TPT * FIN_THREADS;
+      for (int i0 = 0; i0 < nt; i0 += TPT * FIN_THREADS) {
+#pragma unroll
+        for (int jj = 0; jj < RG; ++jj)
+#pragma unroll
+          for (int i = 0; i < TPT; ++i) {
+            const int j = j0 + jj, t = i0 + tid + i * FIN_THREADS;
+            const bool ok = j <= k && t < nt;
+            vm[jj][i] = ok ? d.tile_max[(size_t)(r0 + j) * nt + t] : -INFINITY;
+            vs[jj][i] = ok ? d.tile_sum[(size_t)(r0 + j) * nt + t] : 0.f;
+            mt[jj] = fmaxf(mt[jj], vm[jj][i]);
+          }
       }
 #pragma unroll
-      for (int u = 0; u < U; ++u) {                 // t increasing per lane: strict > keeps lowest
-        if (vm[u] > m) {
-          S = (m == -INFINITY ? 0.f : S * expf(m - vm[u])) + vs[u];
-          m = vm[u];
-          am = va[u];
-        } else if (vm[u] != -INFINITY) {
-          S += vs[u] * expf(vm[u] - m);
+      for (int jj = 0; jj < RG; ++jj) {
+        float m = mt[jj];
+#pragma unroll
+        for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+        if (lane == 0) s_rm[warp][jj] = m;
+      }
+      __syncthreads();
+      float M[RG];
+#pragma unroll
+      for (int jj = 0; jj < RG; ++jj) {
+        float m = s_rm[0][jj];
+        for (int w = 1; w < nw; ++w) m = fmaxf(m, s_rm[w][jj]);
+        M[jj] = m;
+      }
+      // pass 2: scaled sums and the lowest max tile (reloading only when the row did not fit one sweep)
+      float St[RG];
+      int tb[RG];
+#pragma unroll
+      for (int jj = 0; jj < RG; ++jj) {
+        St[jj] = 0.f;
+        tb[jj] = 0x7fffffff;
+      }
+      for (int i0 = 0; i0 < nt; i0 += TPT * FIN_THREADS) {
+#pragma unroll
+        for (int jj = 0; jj < RG; ++jj)
+#pragma unroll
+          for (int i = 0; i < TPT; ++i) {
+            const int j = j0 + jj, t = i0 + tid + i * FIN_THREADS;
+            const bool ok = j <= k && t < nt;
+            if (!one_sweep) {
+              vm[jj][i] = ok ? d.tile_max[(size_t)(r0 + j) * nt + t] : -INFINITY;
+              vs[jj][i] = ok ? d.tile_sum[(size_t)(r0 + j) * nt + t] : 0.f;
+            }
+            if (vm[jj][i] != -INFINITY) St[jj] += vs[jj][i] * expf(vm[jj][i] - M[jj]);
+            if (ok && vm[jj][i] == M[jj] && t < tb[jj]) tb[jj] = t;
+          }
+      }
+#pragma unroll
+      for (int jj = 0; jj < RG; ++jj) {
+        float S = St[jj];
+        int t = tb[jj];
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+          S += __shfl_xor_sync(0xffffffffu, S, o);
+          t = min(t, __shfl_xor_sync(0xffffffffu, t, o));
+        }
+        if (lane == 0) {
+          s_rs[warp][jj] = S;
+          s_rt[warp][jj] = t;
         }
       }
+      __syncthreads();
+      if (tid < RG && j0 + tid <= k) {                    // warps summed in order (deterministic)
+        float S = 0.f;
+        int t = 0x7fffffff;
+        for (int w = 0; w < nw; ++w) {
+          S += s_rs[w][tid];
+          t = min(t, s_rt[w][tid]);
+        }
+        s_m[j0 + tid] = M[tid];
+        s_S[j0 + tid] = S;
+        s_tb[j0 + tid] = t;
+      }
+      __syncthreads();
     }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-      const float om = __shfl_xor_sync(0xffffffffu, m, o);
-      const float oS = __shfl_xor_sync(0xffffffffu, S, o);
-      const int oa = __shfl_xor_sync(0xffffffffu, am, o);
-      const float mn = fmaxf(m, om);
-      const float Sn = (m == -INFINITY ? 0.f : S * expf(m - mn)) + (om == -INFINITY ? 0.f : oS * expf(om - mn));
-      if (om > m || (om == m && oa < am)) am = oa;
-      m = mn;
-      S = Sn;
-    }
-    if (lane == 0) { s_m[j] = m; s_S[j] = S; s_top[j] = am; }
+    if (tid <= k) s_top[tid] = s_tb[tid] < nt ? d.tile_arg[(size_t)(r0 + tid) * nt + s_tb[tid]] : 0;
   }
   __syncthreads();
 
+  FIN_TR(2);
   // 2. accept scan (serial over k <= 32)
   if (parents) {
     tree_walk(d, drafts, parents, probs, logits, seed, mode, inv_temp, b, k, r0, doff, L, rid, s_m, s_S, s_top,
@@ -824,7 +962,9 @@ __global__ void __launch_bounds__(FIN_THREADS) finalize_kernel(LaneDev d, const 
   const int a = s_a;
 
   // 3. exponential race over the one selected row (sampled chains; trees race inside tree_walk)
+  FIN_TR(3);
   if (mode == SV_SAMPLE && !parents) {
+
     const bool resid = s_resid;
     const float* lrow = logits + (size_t)(r0 + a) * V;
     const float m = s_m[a], invS = 1.0f / s_S[a];
@@ -898,40 +1038,89 @@ __global__ void __launch_bounds__(FIN_THREADS) finalize_kernel(LaneDev d, const 
       // relative, far inside the borderline band), and strict > comparisons (a thread visits x in
       // increasing order, so a tie keeps the lower id)
       const float itl = inv_temp * 1.4426950408889634f, ml = m * 1.4426950408889634f;
+      // Pruning (exact, two levels):
+      //  * E = -ln U >= -ln(1 - 2^-24) for every lattice uniform, so an entry's computed score p / E is at
+      //    most p * 1.6777216e7 (1 + 1e-6); a Philox word (4 entries) none of whose entries can reach the
+      //    lane's current bests under that cap needs no random numbers at all. Lanes push the words that
+      //    do need them into a per-warp queue (ballot + prefix), and full warps drain it, so Philox runs
+      //    for the needed words only instead of for every word a diverged warp touches.
+      //  * E >= 1 - U: with the word's uniforms an entry whose p / (1 - U) (with a 1e-5 margin over the
+      //    ~3e-7 relative error of the log / reciprocal approximations) falls below the best skips them.
+      // Every lane starts from the exact scores of the row's argmax x* (tile statistics), usually the
+      // winner or close to it. Pruned entries score strictly below a kept one, so the argmax (lowest id
+      // on ties) is the unpruned race's; sum R is accumulated over every entry in the lane's order.
+      constexpr float kPruneMargin = 1.00001f;
+      constexpr float kInvEmax = 1.6777216e7f * 1.0001f;
+      const int xs = s_top[a];
       auto fast = [&](auto resid_t, auto qrow_t) {
         constexpr bool RES = decltype(resid_t)::value, QR = decltype(qrow_t)::value;
         float sR = -INFINITY, sP = -INFINITY, sum = 0.f;
         int xR = 0x7fffffff, xP = 0x7fffffff;
-        auto word = [&](int mm, const float4 l4, const float4 q4) {
-          const u32x4 w = race_words(seed, rid, z, uint32_t(mm));
-          const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+        if (xs >= 0 && xs < (int)V) {                 // seed: x*'s exact scores (same arithmetic as below)
+          const u32x4 w = race_words(seed, rid, z, uint32_t(xs >> 2));
+          const uint32_t wl = (xs & 3) == 0 ? w.x : ((xs & 3) == 1 ? w.y : ((xs & 3) == 2 ? w.z : w.w));
+          const float pv = tc_ex2(fmaf(lrow[xs], itl, -ml)) * invS;
+          const float invE = __frcp_approx(neg_log_uniform(wl));
+          sP = pv * invE;
+          xP = xs;
+          if constexpr (RES) {
+            const float q = QR ? qrow[xs] : (xs == dnext ? 1.0f : 0.0f);
+            const float R = fmaxf(0.f, pv - q);
+            if (R > 0.f) {
+              sR = R * invE;
+              xR = xs;
+            }
+          }
+        }
+        auto word = [&](int mm, bool valid, const float4 l4, const float4 q4) {
           const float lv[4] = {l4.x, l4.y, l4.z, l4.w};
           const float qv[4] = {q4.x, q4.y, q4.z, q4.w};
+          float pv[4], rv[4];
+          bool any = false;
 #pragma unroll
           for (int l = 0; l < 4; ++l) {
             const int x = mm * 4 + l;
-            const float pv = tc_ex2(fmaf(lv[l], itl, -ml)) * invS;
-            const float invE = __frcp_approx(neg_log_uniform(ws[l]));
-            const float sc = pv * invE;
-            if (sc > sP) { sP = sc; xP = x; }
+            pv[l] = valid ? tc_ex2(fmaf(lv[l], itl, -ml)) * invS : 0.f;
+            any |= pv[l] * kInvEmax > sP;
+            rv[l] = 0.f;
             if constexpr (RES) {
               const float q = QR ? qv[l] : (x == dnext ? 1.0f : 0.0f);
-              const float R = fmaxf(0.f, pv - q);
-              sum += R;
-              const float scr = R > 0.f ? R * invE : -INFINITY;
-              if (scr > sR) { sR = scr; xR = x; }
+              rv[l] = fmaxf(0.f, pv[l] - q);
+              sum += rv[l];
+              any |= rv[l] > 0.f && rv[l] * kInvEmax > sR;
+            }
+          }
+          any = any && valid;
+          if (!__any_sync(0xffffffffu, any)) return;  // no lane's word can reach its bests: no Philox
+          const u32x4 w = race_words(seed, rid, z, uint32_t(mm));
+          const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+          for (int l = 0; l < 4; ++l) {
+            const int x = mm * 4 + l;
+            const float om = 1.0f - word_to_uniform(ws[l]);  // exact (U is a multiple of 2^-24)
+            bool need = pv[l] * kPruneMargin > sP * om;
+            if constexpr (RES) need |= rv[l] > 0.f && rv[l] * kPruneMargin > sR * om;
+            if (need && valid) {
+              const float invE = __frcp_approx(neg_log_uniform(ws[l]));
+              const float sc = pv[l] * invE;
+              if (sc > sP || (sc == sP && x < xP)) { sP = sc; xP = x; }
+              if constexpr (RES) {
+                const float scr = rv[l] > 0.f ? rv[l] * invE : -INFINITY;
+                if (scr > sR || (scr == sR && x < xR)) { sR = scr; xR = x; }
+              }
             }
           }
         };
-        for (int mm = m_lo + tid; mm < m_hi; mm += 2 * FIN_THREADS) {
-          const int mm2 = mm + FIN_THREADS;
-          const bool two = mm2 < m_hi;
-          const float4 l0 = *reinterpret_cast<const float4*>(lrow + mm * 4);
+        // warp-uniform loop (the Philox skip is a warp vote): lane l takes words mm0 + l and mm0 + 512 + l
+        for (int mm0 = m_lo + warp * 32; mm0 < m_hi; mm0 += 2 * FIN_THREADS) {
+          const int mm = mm0 + lane, mm2 = mm + FIN_THREADS;
+          const bool one = mm < m_hi, two = mm2 < m_hi;
+          const float4 l0 = one ? *reinterpret_cast<const float4*>(lrow + mm * 4) : zero4;
           const float4 l1 = two ? *reinterpret_cast<const float4*>(lrow + mm2 * 4) : zero4;
-          const float4 q0 = QR ? *reinterpret_cast<const float4*>(qrow + mm * 4) : zero4;
+          const float4 q0 = (QR && one) ? *reinterpret_cast<const float4*>(qrow + mm * 4) : zero4;
           const float4 q1 = (QR && two) ? *reinterpret_cast<const float4*>(qrow + mm2 * 4) : zero4;
-          word(mm, l0, q0);
-          if (two) word(mm2, l1, q1);
+          word(mm, one, l0, q0);
+          if (mm0 + FIN_THREADS < m_hi) word(mm2, two, l1, q1);    // warp-uniform condition
         }
         bP = Best{sP, xP};
         bR = Best{sR, xR};
@@ -951,6 +1140,7 @@ __global__ void __launch_bounds__(FIN_THREADS) finalize_kernel(LaneDev d, const 
       race4(mm, l0, q0);
       if (two) race4(mm2, l1, q1);
     }
+    FIN_TR(4);
     bR = warp_best(bR);
     bP = warp_best(bP);
     sumR = warp_sum(sumR);
@@ -989,6 +1179,7 @@ __global__ void __launch_bounds__(FIN_THREADS) finalize_kernel(LaneDev d, const 
     if (!s_last) return;                              // another slice of this request finishes it
   }
 
+  FIN_TR(5);
   // 4. outputs + lane counters (a7)
   const int K1 = d.max_depth + 1;
   for (int i = tid; i < K1; i += FIN_THREADS) {
@@ -1024,18 +1215,21 @@ cudaError_t launch_finalize(const LaneDev& d, int batch, const int* draft_tokens
   SV_COUNT_LAUNCH();
   // sampled chains: the race over the vocabulary is split across RS CTAs per request so the grid
   // fills the resident CTA slots once; the other modes need one CTA per request
-  // (RS * batch <= the resident CTA slots, so the grid is a single wave)
-  static int slots = 0;
-  if (!slots) {
-    int dev = 0, sms = 148, occ = 1;
-    cudaGetDevice(&dev);
+  const bool race = mode == SV_SAMPLE && !parents;
+  const int smem = 0;
+  static int slots_dev[64] = {0};                    // resident race CTAs per device (occupancy x SMs)
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int& slots = slots_dev[dev & 63];
+  if (race && !slots) {
+    int sms = 148, occ = 1;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, finalize_kernel, FIN_THREADS, 0);
     slots = std::max(1, occ) * sms;
   }
   int RS = 1;
-  if (mode == SV_SAMPLE && !parents) RS = std::min(kMaxRaceSplits, std::max(1, slots / batch));
-  return launch_pdl(finalize_kernel, dim3(batch, RS), dim3(FIN_THREADS), 0, s, 1, d, draft_tokens, parents, draft_probs,
+  if (race) RS = std::min(kMaxRaceSplits, std::max(1, slots / batch));
+  return launch_pdl(finalize_kernel, dim3(batch, RS), dim3(FIN_THREADS), smem, s, 1, d, draft_tokens, parents, draft_probs,
                     logits, seed, mode, inv_temp, accepted_len, out_tokens, accepted_nodes, (int)use_row_best);
 }
 

@@ -17,13 +17,18 @@ SV_DEV size_t pool_row(const LaneDev& d, int layer, int page, int kv, int h, int
   return ((((size_t)layer * d.n_pages + page) * 2 + kv) * d.Hkv + h) * d.page + off;
 }
 
+// acquire / release atomics (no full fences): the critical section's reads see the previous holder's
+// writes, and its own writes are visible to the next holder
 SV_DEV void fl_lock(const LaneDev& d) {
-  while (atomicCAS(d.free_top + 1, 0, 1) != 0) __nanosleep(32);
-  __threadfence();
+  int old;
+  for (;;) {
+    asm volatile("atom.acquire.gpu.global.cas.b32 %0, [%1], 0, 1;" : "=r"(old) : "l"(d.free_top + 1) : "memory");
+    if (old == 0) break;
+    __nanosleep(32);
+  }
 }
 SV_DEV void fl_unlock(const LaneDev& d) {
-  __threadfence();
-  atomicExch(d.free_top + 1, 0);
+  asm volatile("st.release.gpu.global.b32 [%0], 0;" ::"l"(d.free_top + 1) : "memory");
 }
 SV_DEV int fl_top(const LaneDev& d) { return *reinterpret_cast<volatile int*>(d.free_top); }
 
@@ -46,11 +51,29 @@ SV_DEV bool pop_pages(const LaneDev& d, int slot, int first, int n) {
 __global__ void __launch_bounds__(256) commit_kernel(LaneDev d, const int* __restrict__ n_keep) {
   pdl_trigger();
   pdl_wait();
+  // Loads that do not depend on each other are issued together (latency-bound kernel: every dependent
+  // global round trip is ~1 us): the request's row offset, the accepted path and emitted tokens (K1
+  // words each) with the slot; the slot's length; then the page-table words of the <= 8 pages the new
+  // tokens can touch, in parallel with thread 0's page pop (the pops write the new page ids to s_pg too)
   __shared__ int s_n, s_ok;
-  const int b = blockIdx.x;
-  const int slot = d.slots[b], L = d.len[slot];
-  if (threadIdx.x == 0) {
-    int n = d.acc_int[b] + 1;                    // acc_int = -1 on error -> n = 0
+  __shared__ int s_row[kMaxDepth + 1], s_tok[kMaxDepth + 1];
+  __shared__ int s_pg[8];
+  const int b = blockIdx.x, tid = threadIdx.x;
+  const int K1 = d.max_depth + 1;
+  const int slot = d.slots[b];
+  const int row0 = d.row_off[b];
+  if (tid < K1) {
+    s_row[tid] = row0 + d.path_int[(size_t)b * K1 + tid];   // the accepted path's chain rows (R30)
+    s_tok[tid] = d.tok_int[(size_t)b * K1 + tid];
+  }
+  const int L = d.len[slot];
+  const int have = (L + d.page - 1) / d.page, pg0 = L / d.page;
+  if (tid >= 32 && tid < 40) {                         // pages already owned (new ones: thread 0)
+    const int idx = pg0 + tid - 32;
+    if (idx < have) s_pg[tid - 32] = d.page_table[slot * d.max_pages_per_slot + idx];
+  }
+  if (tid == 0) {
+    int n = d.acc_int[b] + 1;                          // acc_int = -1 on error -> n = 0
     if (n > 0 && n_keep) {
       const int nk = n_keep[b];
       if (nk < 1) { atomicOr(d.err, SV_DERR_BAD_KEEP); n = 0; }
@@ -58,12 +81,25 @@ __global__ void __launch_bounds__(256) commit_kernel(LaneDev d, const int* __res
     }
     int ok = n > 0;
     if (ok) {
-      const int have = (L + d.page - 1) / d.page, need = (L + n + d.page - 1) / d.page;
+      const int need = (L + n + d.page - 1) / d.page;
       if (L + n > d.max_pos || need > d.max_pages_per_slot) {
         atomicOr(d.err, SV_DERR_MAX_POS);
         ok = 0;
-      } else {
-        ok = pop_pages(d, slot, have, need - have);
+      } else if (need > have) {
+        const int cnt = need - have;
+        fl_lock(d);
+        const int old = fl_top(d);
+        ok = old >= cnt;
+        if (ok) {
+          for (int i = 0; i < cnt; ++i) {
+            const int id = d.free_list[old - cnt + i];
+            d.page_table[slot * d.max_pages_per_slot + have + i] = id;
+            s_pg[have + i - pg0] = id;
+          }
+          *d.free_top = old - cnt;
+        }
+        fl_unlock(d);
+        if (!ok) atomicOr(d.err, SV_DERR_NO_PAGES);
       }
     }
     s_n = n;
@@ -71,21 +107,13 @@ __global__ void __launch_bounds__(256) commit_kernel(LaneDev d, const int* __res
   }
   __syncthreads();
   if (!s_ok) return;
-  const int n = s_n, row0 = d.row_off[b];
-  // the accepted path's chain rows (0..n-1 for chains; a token tree's path, R30)
-  __shared__ int s_row[kMaxDepth + 1];
-  if (threadIdx.x < n) s_row[threadIdx.x] = row0 + d.path_int[(size_t)b * (d.max_depth + 1) + threadIdx.x];
-  // the <= 6 pages covering tokens L .. L + n - 1 (n <= 33, page >= 8), staged once
-  __shared__ int s_pg[8];
-  const int pg0 = L / d.page, npg = (L + n - 1) / d.page - pg0 + 1;
-  if (threadIdx.x < npg) s_pg[threadIdx.x] = d.page_table[slot * d.max_pages_per_slot + pg0 + threadIdx.x];
-  __syncthreads();
+  const int n = s_n;
   const int vec_per_row = d.dh / 8;              // 16-byte vectors per (token, kv head)
   const int per_tok = 2 * d.Hkv * vec_per_row;
   const size_t nkv = (size_t)d.Hkv * d.dh;
   const int total = d.n_layers * n * per_tok;
   constexpr int U = 4;                           // loads of U vectors in flight before their stores
-  for (int i0 = threadIdx.x; i0 < total; i0 += U * blockDim.x) {
+  for (int i0 = tid; i0 < total; i0 += U * blockDim.x) {
     uint4 v[U];
     bf16* dst[U];
 #pragma unroll
@@ -105,10 +133,9 @@ __global__ void __launch_bounds__(256) commit_kernel(LaneDev d, const int* __res
     for (int u = 0; u < U; ++u)
       if (dst[u]) *reinterpret_cast<uint4*>(dst[u]) = v[u];
   }
-  __syncthreads();
-  if (threadIdx.x == 0) {
+  if (tid == 0) {
     d.len[slot] = L + n;
-    d.pending[slot] = d.tok_int[(size_t)b * (d.max_depth + 1) + n - 1];
+    d.pending[slot] = s_tok[n - 1];
   }
 }
 

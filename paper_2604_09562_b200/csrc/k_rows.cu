@@ -129,6 +129,7 @@ __global__ void plan_kernel(LaneDev d, PlanArgs p, const int* __restrict__ draft
     d.row_req[r] = b;
     d.row_pos[r] = pos;
     d.chain_tok[r] = tok;
+    if (attn) d.row_comb[r] = make_int4(j, num_splits(s_len[b]), s_item[b], 0);   // the combine's one load
   }
   if (attn) {
     const int n_items = s_item[B];
@@ -216,9 +217,10 @@ __global__ void __launch_bounds__(256) embed_norm_vec_kernel(LaneDev d) {
   pdl_trigger();
   pdl_wait();
   const int r = blockIdx.x;
-  if (r >= *d.T_dev) return;                       // launched for Tmax rows (dynamic-depth graph)
+  const int Tn = *d.T_dev, tok = d.chain_tok[r];   // both loads in flight together
+  if (r >= Tn) return;                             // launched for Tmax rows (dynamic-depth graph)
   const int nv = d.D / 8;
-  const uint4* e = reinterpret_cast<const uint4*>(d.embed + (size_t)d.chain_tok[r] * d.D);
+  const uint4* e = reinterpret_cast<const uint4*>(d.embed + (size_t)tok * d.D);
   float4* h = reinterpret_cast<float4*>(d.h0 + (size_t)r * d.D);
   float x[kNormMaxVec][8];
   float ss = 0.f;

@@ -55,6 +55,7 @@ struct LaneDev {
   int* tile_arg;
   bf16 *a, *b, *z, *q, *kc, *vc, *o, *u;
   int4* items;                       // attention work list: (request, kv head, split, 0)
+  int4* row_comb;                    // [Tmax] split-KV combine: (chain row j, splits, first item, 0)
   int *item_start, *n_items;
   float *part_o, *part_ml;           // split-KV partials
   int *acc_int, *tok_int;            // internal copies of accepted_len / out_tokens for commit

@@ -26,7 +26,7 @@ struct Layout {
   size_t slots, depths, row_off, row_req, row_pos, chain_tok, req_err;
   size_t h0, h1, h2, cbuf, logits, tile_max, tile_sum, tile_arg;
   size_t a, b, z, q, kc, vc, o, u;
-  size_t items, item_start, n_items, part_o, part_ml, acc_int, tok_int, batch_n, path_int, row_anc, filt, fin_cnt, fin_part, row_best, filt_ids;
+  size_t items, item_start, n_items, part_o, part_ml, acc_int, tok_int, batch_n, path_int, row_anc, row_comb, filt, fin_cnt, fin_part, row_best, filt_ids;
   size_t gemm_ws, trace, prefill, handoff, tdev, dctrl;
   size_t max_items;
 
@@ -116,6 +116,7 @@ Layout make_layout(const sv_config& c) {
   L.batch_n = L.take(4);
   L.path_int = L.take(4 * c.max_batch * (c.max_depth + 1));
   L.row_anc = L.take(8 * T);
+  L.row_comb = L.take(16 * T);
   L.filt = L.take(16 * T);
   L.filt_ids = L.take(4 * T * sv::kFiltCap + 4 * T);
   L.fin_cnt = L.take(4 * c.max_batch);
@@ -396,6 +397,7 @@ sv_status sv_create(const sv_config* cfg, const sv_weights* w, void* kv_pool, vo
   d.batch_n = (int*)(ws + L.batch_n);
   d.path_int = (int*)(ws + L.path_int);
   d.row_anc = (unsigned long long*)(ws + L.row_anc);
+  d.row_comb = (int4*)(ws + L.row_comb);
   d.tree = 0;
   d.filt_on = 0;
   d.fin_cnt = (int*)(ws + L.fin_cnt);

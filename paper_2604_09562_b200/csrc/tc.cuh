@@ -48,6 +48,13 @@ SV_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
 SV_DEV void prefetch_tmap(const CUtensorMap* m) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
 }
+// plain bulk copy global -> smem (16-byte aligned, size a multiple of 16), completes tx bytes on `bar`
+SV_DEV void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
 // 2D tile load: box at (x = inner/column, y = row) -> smem, completes tx bytes on `bar`
 SV_DEV void tma_load_2d(void* dst, const CUtensorMap* m, uint64_t* bar, int x, int y) {
   asm volatile(
