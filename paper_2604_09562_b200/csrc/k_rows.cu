@@ -290,6 +290,205 @@ __global__ void __launch_bounds__(256) rmsnorm_vec_kernel(const float* __restric
 
 static bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
 
+// ------------------------------------------------------------------ a1 + a2 fused: plan + embed
+// One CTA per chain row (Tmax rows for a dynamic-depth graph). Every CTA reads the batch's slots /
+// depths (kernel parameters, or the graph's device copy) and lengths and scans them itself, so no CTA
+// waits for another: row r finds its request, writes its row tables, gathers its token's embedding
+// and normalises it (a2); the CTA of each request's first row also writes the request's tables, its
+// split-KV work items and the request's error bits (every row of the request checked there, as
+// plan_kernel does), and CTA 0 the batch totals. Same outputs as plan_kernel + embed_norm_vec_kernel.
+__device__ __forceinline__ int block_excl_scan256(int v, int* s_w, int* total) {
+  // exclusive scan over the 256 threads of the block (8 warps)
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s_w[w] = x;
+  __syncthreads();
+  int off = 0, tot = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    off += i < w ? s_w[i] : 0;
+    tot += s_w[i];
+  }
+  __syncthreads();
+  *total = tot;
+  return off + x - v;
+}
+
+__global__ void __launch_bounds__(256) plan_embed_kernel(LaneDev d, PlanArgs p, const int* __restrict__ draft_tokens,
+                                                         const int* __restrict__ parents) {
+  pdl_trigger();
+  pdl_wait();
+  __shared__ int s_off[kMaxBatch + 1], s_item[kMaxBatch + 1], s_len[kMaxBatch], s_slot[kMaxBatch];
+  __shared__ int s_w[8], s_err;
+  const int B = p.batch, tid = threadIdx.x;
+  // per-request state: thread t < B holds request t (B <= kMaxBatch = 256)
+  int k1 = 0, nit = 0;
+  if (tid < B) {
+    int slot = p.slots[tid], k = p.depths[tid];
+    if (d.dyn_ctrl) {
+      slot = d.dyn_ctrl[tid];
+      k = d.dyn_ctrl[B + tid];
+      if (slot < 0 || slot >= d.max_slots) slot = 0;
+      if (k < 0 || k > d.max_depth) k = 0;
+    }
+    const int L = d.len[slot];
+    s_slot[tid] = slot;
+    s_len[tid] = L;
+    k1 = k + 1;
+    nit = num_splits(L) * d.Hkv;
+  }
+  int T = 0, NI = 0;
+  const int off = block_excl_scan256(k1, s_w, &T);
+  const int ito = block_excl_scan256(nit, s_w, &NI);
+  if (tid < B) {
+    s_off[tid] = off;
+    s_item[tid] = ito;
+  }
+  if (tid == 0) {
+    s_off[B] = T;
+    s_item[B] = NI;
+  }
+  __syncthreads();
+  const int r = blockIdx.x;
+  if (r == 0 && tid == 0) {
+    *d.n_items = NI;
+    *d.batch_n = B;
+    *d.T_dev = T;
+    d.row_off[B] = T;
+    d.item_start[B] = NI;
+  }
+  if (r >= T) return;                              // launched for Tmax rows (dynamic-depth graph)
+  int lo = 0, hi = B - 1;                          // last b with s_off[b] <= r
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (s_off[mid] <= r) lo = mid; else hi = mid - 1;
+  }
+  const int b = lo, j = r - s_off[b], slot = s_slot[b], L = s_len[b];
+  const int R = s_off[b + 1] - s_off[b];
+  const int doff = s_off[b] - b;                   // first draft token of request b
+  // this CTA's row (thread 0) and, for the request's first row, every row's validity (threads t < R)
+  if (tid == 0) s_err = 0;
+  __syncthreads();
+  auto row_info = [&](int jj, int& tok, int& pos, unsigned long long& anc, int& e) {
+    e = 0;
+    tok = jj == 0 ? d.pending[slot] : draft_tokens[doff + jj - 1];
+    if (tok < 0 || tok >= d.V) {
+      e |= 1;
+      tok = 0;
+    }
+    int depth = jj;
+    anc = jj >= 63 ? ~0ull : (2ull << jj) - 1ull;
+    if (parents && jj > 0) {
+      const int* par = parents + doff;               // parent of node n at par[n - 1]
+      anc = 1ull << jj;
+      depth = 0;
+      for (int n = jj; n != 0; ++depth) {
+        const int pn = par[n - 1];
+        if (pn < 0 || pn >= n) {                     // not topological: the request is invalid
+          e |= 4;
+          break;
+        }
+        n = pn;
+        anc |= 1ull << n;
+      }
+    }
+    pos = L + depth;
+    if (pos >= d.max_pos) {
+      e |= 2;
+      pos = d.max_pos - 1;
+    }
+  };
+  __shared__ int s_tok;
+  if (j == 0) {
+    if (tid < R) {
+      int tok, pos, e;
+      unsigned long long anc;
+      row_info(tid, tok, pos, anc, e);
+      if (e) atomicOr(&s_err, e);
+    }
+    if (tid == 0) {
+      int e0 = 0;
+      if (d.dyn_ctrl) {
+        const int s0 = d.dyn_ctrl[b], k0 = d.dyn_ctrl[B + b];
+        if (s0 < 0 || s0 >= d.max_slots || k0 < 0 || k0 > d.max_depth) e0 = 1;
+      }
+      if (e0) atomicOr(&s_err, e0);
+      d.row_off[b] = s_off[b];
+      d.item_start[b] = s_item[b];
+      d.slots[b] = slot;
+      d.depths[b] = R - 1;
+    }
+    const int ns = num_splits(L);
+    for (int i = tid; i < ns * d.Hkv; i += blockDim.x)
+      d.items[s_item[b] + i] = make_int4(b, i / ns, i % ns, ns);
+  }
+  if (tid == 0) {
+    int tok, pos, e;
+    unsigned long long anc;
+    row_info(j, tok, pos, anc, e);
+    d.row_anc[r] = anc;
+    d.row_req[r] = b;
+    d.row_pos[r] = pos;
+    d.chain_tok[r] = tok;
+    d.row_comb[r] = make_int4(j, num_splits(L), s_item[b], 0);
+    s_tok = tok;
+  }
+  __syncthreads();
+  if (j == 0 && tid == 0) {
+    const int e = s_err;
+    d.req_err[b] = e;
+    if (e & 1) atomicOr(d.err, SV_DERR_BAD_TOKEN);
+    if (e & 2) atomicOr(d.err, SV_DERR_MAX_POS);
+    if (e & 4) atomicOr(d.err, SV_DERR_BAD_TREE);
+  }
+  // a2: h0 = E[c]; a = bf16(RMSNorm(h0) * g)
+  const int nv = d.D / 8;
+  const uint4* e = reinterpret_cast<const uint4*>(d.embed + (size_t)s_tok * d.D);
+  float4* h = reinterpret_cast<float4*>(d.h0 + (size_t)r * d.D);
+  float x[kNormMaxVec][8];
+  float ss = 0.f;
+#pragma unroll
+  for (int kk = 0; kk < kNormMaxVec; ++kk) {
+    const int v = tid + kk * 256;
+    if (v < nv) {
+      bf16x8_to_f32(e[v], x[kk]);
+      h[2 * v] = make_float4(x[kk][0], x[kk][1], x[kk][2], x[kk][3]);
+      h[2 * v + 1] = make_float4(x[kk][4], x[kk][5], x[kk][6], x[kk][7]);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) ss += x[kk][i] * x[kk][i];
+    }
+  }
+  const float rstd = 1.0f / sqrtf(block_sum<256>(ss) / float(d.D) + d.eps);
+  const uint4* gw = reinterpret_cast<const uint4*>(d.attn_norm);
+  uint4* out = reinterpret_cast<uint4*>(d.a + (size_t)r * d.D);
+#pragma unroll
+  for (int kk = 0; kk < kNormMaxVec; ++kk) {
+    const int v = tid + kk * 256;
+    if (v < nv) {
+      float g[8], y[8];
+      bf16x8_to_f32(gw[v], g);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) y[i] = x[kk][i] * rstd * g[i];
+      out[v] = f32x8_to_bf16(y);
+    }
+  }
+}
+
+bool plan_embed_supported(const LaneDev& d) {
+  return d.D <= 256 * 8 * kNormMaxVec && (d.D % 8) == 0 && aligned16(d.embed) && aligned16(d.attn_norm);
+}
+
+cudaError_t launch_plan_embed(const LaneDev& d, const PlanArgs& p, const int* draft_tokens, const int* parents,
+                              int rows, cudaStream_t s) {
+  SV_COUNT_LAUNCH();
+  return launch_pdl(plan_embed_kernel, dim3(rows), dim3(256), 0, s, 1, d, p, draft_tokens, parents);
+}
+
 cudaError_t launch_embed_norm(const LaneDev& d, int T, cudaStream_t s) {
   SV_COUNT_LAUNCH();
   if (d.D <= 256 * 8 * kNormMaxVec && aligned16(d.embed) && aligned16(d.attn_norm))

@@ -138,6 +138,11 @@ struct PlanArgs {
 cudaError_t launch_plan(const LaneDev& d, const PlanArgs& p, const int* draft_tokens, const int* parents, bool attn,
                         cudaStream_t s);
 cudaError_t launch_embed_norm(const LaneDev& d, int T, cudaStream_t s);
+// a1 + a2 in one launch (plan tables, work items and the embed + RMSNorm of each row; `rows` = T, or
+// Tmax for a dynamic-depth graph); requires plan_embed_supported(d)
+bool plan_embed_supported(const LaneDev& d);
+cudaError_t launch_plan_embed(const LaneDev& d, const PlanArgs& p, const int* draft_tokens, const int* parents,
+                              int rows, cudaStream_t s);
 cudaError_t launch_rmsnorm(const LaneDev& d, const float* x, const bf16* g, bf16* out, int T, cudaStream_t s,
                            bool bound_by_T_dev = true);
 // C[M][N] (fp32) = A[M][K] (bf16) * B[N][K]^T (bf16)

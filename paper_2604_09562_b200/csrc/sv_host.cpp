@@ -556,8 +556,13 @@ static sv_status verify_impl(sv_ctx* c, int32_t batch, const int32_t* slots, con
   const float inv_temp = mode == SV_SAMPLE ? 1.0f / temperature : 1.0f;
   bool row_best = false;
   wait_comm_slots(c, batch, slots);
-  STAGE(c, ST_PLAN, sv::launch_plan(d, p, draft_tokens, parents, true, s));
-  STAGE(c, ST_EMBED, sv::launch_embed_norm(d, T, s));
+  if (sv::plan_embed_supported(d) && !getenv("SV_SPLIT_PLAN")) {
+    // plan + embed in one launch (each row's CTA scans the batch itself)
+    STAGE(c, ST_EMBED, sv::launch_plan_embed(d, p, draft_tokens, parents, T, s));
+  } else {
+    STAGE(c, ST_PLAN, sv::launch_plan(d, p, draft_tokens, parents, true, s));
+    STAGE(c, ST_EMBED, sv::launch_embed_norm(d, T, s));
+  }
   const size_t nq = (size_t)d.Hq * d.dh;
   for (int layer = 0; layer < d.n_layers; ++layer) {
     const float* hin = layer == 0 ? d.h0 : d.h2;
