@@ -14,6 +14,7 @@ struct GemmEpi {
   float inv_temp;          // LOGITS: statistics are of l * inv_temp
   bool write_out;          // LOGITS: also store the fp32 logits (tensor-core paths; SIMT always does)
   unsigned long long* row_best;   // LOGITS: per-row argmax keys (only when gemm_fills_row_best)
+  bool argmax_only;                // LOGITS with row_best: only the argmax keys (no tile statistics)
   const int* M_dev;        // rows from the device (dynamic-depth graph; M = the upper bound), or nullptr
   int M_hint;              // with M_dev: typical rows, for the token-tile width (0: use M)
 };

@@ -278,6 +278,7 @@ cudaError_t gemm_run(GemmPlan* p, const bf16* A, const bf16* B, float* C, int M,
       g.nt = d.nt;
       g.inv_temp = e.inv_temp;
       g.row_best = e.row_best;
+      g.argmax_only = e.row_best && e.argmax_only ? 1 : 0;
       if (!e.write_out) g.out = nullptr;
       break;
     default:

@@ -33,6 +33,7 @@ struct GemmTcArgs {
   // LOGITS (weight-major kernel, greedy): per token row, atomicMax of (order-preserving max bits << 32 |
   // ~argmax) over the vocab tiles = the row's lowest-index argmax (finalize reads it; zero between steps)
   unsigned long long* row_best;
+  int argmax_only;        // LOGITS with row_best: skip sum exp and the per-tile statistics (greedy, no taps)
   // weight-major kernel: when set, the rows M are read from the device after the dependency wait (the
   // grid is sized for the g.M given, an upper bound; dynamic-depth CUDA graphs)
   const int* M_dev;

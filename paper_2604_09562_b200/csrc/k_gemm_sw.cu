@@ -156,6 +156,56 @@ __device__ __forceinline__ void bfly_sum(float (&s)[16], int lane) {
   }
 }
 
+// greedy decisions (argmax_only): per column the max and lowest argmax over this warp's 32 rows, the
+// 4 warps combined through shared memory, one atomicMax key per (token, 128-row tile) into row_best
+__device__ __forceinline__ void sw_epi_argmax(const SwEpi& e, const SwTile& tl) {
+  const GemmTcArgs& g = *e.g;
+  const int fb = tl.m_pair * 256 + e.rank * 128;          // first vocab row of this CTA
+  const int f = fb + e.q * 32 + e.lane;
+  const bool valid = f < g.N;
+  const int t0 = tl.n_blk * e.NT;
+  float* rmax = e.aux;                                    // [4][256]
+  int* rarg = reinterpret_cast<int*>(e.aux + 8 * 256);
+  for (int c = e.h * 16; c < e.NT; c += 32) {
+    uint32_t r[16];
+    sw_ld16(e.tbase + c, r);
+    float M[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) M[i] = tc::redux_max(valid ? sw_u2f(r[i]) : -INFINITY);
+    unsigned hit[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) hit[i] = __ballot_sync(0xffffffffu, valid && sw_u2f(r[i]) == M[i]);
+    if (e.lane < 16) {                                    // lane i publishes column c + i
+      float mi = M[0];
+      unsigned hi = hit[0];
+#pragma unroll
+      for (int i = 1; i < 16; ++i) {
+        mi = e.lane == i ? M[i] : mi;
+        hi = e.lane == i ? hit[i] : hi;
+      }
+      rmax[e.q * 256 + c + e.lane] = mi;
+      rarg[e.q * 256 + c + e.lane] = hi ? fb + e.q * 32 + (__ffs(hi) - 1) : 0x7fffffff;
+    }
+  }
+  tc::named_bar(EPI_BAR, EPI_THREADS);
+  for (int col = e.tid; col < e.NT; col += EPI_THREADS) {
+    const int t = t0 + col;
+    float m = -INFINITY;
+    int am = 0x7fffffff;
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      const float v = rmax[w * 256 + col];
+      if (v > m) { m = v; am = rarg[w * 256 + col]; }    // warps in feature order: first = lowest
+    }
+    if (t < e.M && m != -INFINITY) {
+      const uint32_t u = __float_as_uint(m);
+      const uint32_t ou = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+      atomicMax(g.row_best + t, ((unsigned long long)ou << 32) | (0xFFFFFFFFu - (uint32_t)am));
+    }
+  }
+  tc::named_bar(EPI_BAR, EPI_THREADS);                    // RED is reused by the next tile
+}
+
 __device__ __forceinline__ void sw_epi_logits(const SwEpi& e, const SwTile& tl) {
   const GemmTcArgs& g = *e.g;
   const int fb = tl.m_pair * 256 + e.rank * 128;          // first vocab row of this CTA
@@ -532,7 +582,10 @@ __global__ void __launch_bounds__(THREADS, 1)
       const SwEpi e{&g, (int)rank, q, h, lane, h * 128 + q * 32 + lane, aux, pos_s, tmem_base + (uint32_t(q * 32) << 16) + acc * 256, NT, M};
       switch ((g.diag & 2) ? -1 : g.kind) {
         case -1: break;                                   // diagnostic: no epilogue
-        case GEMM_EPI_LOGITS: sw_epi_logits(e, tl); break;
+        case GEMM_EPI_LOGITS:
+          if (g.argmax_only && !g.out) sw_epi_argmax(e, tl);
+          else sw_epi_logits(e, tl);
+          break;
         case GEMM_EPI_QKV_ROPE: sw_epi_qkv(e, tl); break;
         case GEMM_EPI_SWIGLU: sw_epi_swiglu(e, tl); break;
         default: sw_epi_f32(e, tl); break;

@@ -602,6 +602,9 @@ static sv_status verify_impl(sv_ctx* c, int32_t batch, const int32_t* slots, con
     // row_best (atomicMax of order-preserving keys, deterministic) and finalize reads 1 word per row
     row_best = mode != SV_SAMPLE && sv::gemm_fills_row_best(c->gemm);
     e.row_best = row_best ? d.row_best : nullptr;
+    // greedy decisions read only row_best: the epilogue skips sum exp and the tile statistics unless
+    // something inspects them (taps)
+    e.argmax_only = row_best && !c->taps && mode == SV_GREEDY;
     STAGE(c, ST_LM_HEAD, gemm(c, d.z, d.lm_head, d.logits, T, d.V, d.D, sv::EPI_LOGITS, e));
   }
   d.filt_on = mode == SV_SAMPLE && filter_active(c);
