@@ -30,6 +30,9 @@ void gemm_plan_destroy(GemmPlan* p);
 cudaError_t attn_run(GemmPlan* p, int layer, int batch, int tree, int max_rows, cudaStream_t s, bool* used_tc2);
 // true when the lm-head GEMM (EPI_LOGITS) also fills GemmEpi::row_best (the weight-major kernel)
 bool gemm_fills_row_best(GemmPlan* p);
+// true when attn_run will pick the keys-on-lanes kernel for this verify's deepest chain (the only
+// attention kernel that plan_embed's wide 2048-key splits are enabled for)
+bool attn_uses_tc2(GemmPlan* p, int max_rows);
 // true when every GEMM of the step honours GemmEpi::M_dev and the attention reads its work list from
 // the device (the dynamic-depth CUDA graph's requirements)
 bool supports_dynamic_rows(GemmPlan* p);

@@ -165,6 +165,11 @@ cudaError_t attn_run(GemmPlan* p, int layer, int batch, int tree, int max_rows, 
   return launch_attention(d, layer, batch, s);
 }
 
+bool attn_uses_tc2(GemmPlan* p, int max_rows) {
+  const int G = p->d.Hq / p->d.Hkv;
+  return p->use_tc2_attn && p->attn_maps_ok && max_rows * G <= kAttnRows;
+}
+
 bool gemm_fills_row_best(GemmPlan* p) { return p->use_tc && !p->use_2sm && !p->use_1sm && !p->use_streamk; }
 
 bool supports_dynamic_rows(GemmPlan* p) { return gemm_fills_row_best(p) && p->use_tc_attn && p->attn_maps_ok; }

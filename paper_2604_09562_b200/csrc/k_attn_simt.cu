@@ -33,8 +33,9 @@ __global__ void __launch_bounds__(128) attn_simt_kernel(LaneDev d, int layer) {
     const int slot = d.slots[b], R = d.depths[b] + 1, L = d.len[slot];
     const int row0 = d.row_off[b];
     const int nr = R * G;
-    const int t0 = split_t0(split);
-    const int t1 = split_t1(split, item.w, L, R);
+    const int sk = item_split_keys(item.w);
+    const int t0 = split * sk;
+    const int t1 = split_t1_k(split, item_ns(item.w), L, R, sk);
     __syncthreads();
     for (int i = tid; i < nr * dh; i += 128) {
       const int rl = i / dh, dd = i % dh, j = rl / G, g = rl % G;

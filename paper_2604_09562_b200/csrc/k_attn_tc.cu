@@ -70,13 +70,14 @@ __device__ __forceinline__ ItemInfo item_info(const LaneDev& d, int it) {
   I.b = w.x;
   I.h = w.y;
   I.s = w.z;
-  I.ns = w.w;
+  I.ns = item_ns(w.w);
+  const int sk = item_split_keys(w.w);
   I.slot = d.slots[I.b];
   I.L = d.len[I.slot];
   I.R = d.depths[I.b] + 1;
   I.row0 = d.row_off[I.b];
-  I.t0 = split_t0(I.s);
-  I.t1 = split_t1(I.s, I.ns, I.L, I.R);
+  I.t0 = I.s * sk;
+  I.t1 = split_t1_k(I.s, I.ns, I.L, I.R, sk);
   const int page_end = min(I.t1, I.L);
   I.n_page_tiles = page_end > I.t0 ? (page_end - I.t0 + KT - 1) / KT : 0;
   I.n_tiles = I.n_page_tiles + (I.s == I.ns - 1 ? 1 : 0);

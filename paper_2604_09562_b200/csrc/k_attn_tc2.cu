@@ -54,7 +54,7 @@ constexpr int P_BYTES = KT * NQ * 2;       // 16 KB per P^T buffer (two buffers)
 constexpr int XCOL_FLOATS = 2 * 2 * 4 * 32;  // [tile parity][slot half][quadrant][32]
 constexpr int SMEM = (KST + VST) * KV_BYTES + Q_BYTES + 2 * P_BYTES + 4 * XCOL_FLOATS + 512 + 512;
 static_assert(SMEM <= 232448, "attention smem exceeds the 227 KB per-CTA limit");
-static_assert(kSplitKeys / 64 <= 32, "an item's pages are held one per producer lane");
+static_assert(2 * kSplitKeys / 64 <= 32, "an item's pages (wide splits too) are held one per producer lane");
 constexpr uint32_t IDESC_QK = tc::idesc_bf16(128, NQ);          // A = K (K-major), B = Q (K-major)
 constexpr uint32_t IDESC_PV = tc::idesc_bf16(128, NQ, 1, 1);    // A = V^T (MN-major), B = P^T (MN-major)
 constexpr uint32_t IDESC_L = tc::idesc_bf16(128, NQ, 0, 1);     // A = ones (TMEM), B = P^T (MN-major)
@@ -75,13 +75,14 @@ __device__ __forceinline__ Item2 item2(const LaneDev& d, int it) {
   I.b = w.x;
   I.h = w.y;
   I.s = w.z;
-  I.ns = w.w;
+  I.ns = item_ns(w.w);
+  const int sk = item_split_keys(w.w);                        // 1024, or 2048 for a wide-split verify
   I.slot = d.slots[I.b];
   I.L = d.len[I.slot];
   I.R = d.depths[I.b] + 1;
   I.row0 = d.row_off[I.b];
-  I.t0 = split_t0(I.s);
-  I.kend = min(split_t1(I.s, I.ns, I.L, I.R), I.L);         // page keys of this item: [t0, kend)
+  I.t0 = I.s * sk;
+  I.kend = min(split_t1_k(I.s, I.ns, I.L, I.R, sk), I.L);   // page keys of this item: [t0, kend)
   I.n_pages = I.kend > I.t0 ? (I.kend - I.t0 + 63) / 64 : 0;
   I.n_page_tiles = (I.n_pages + 1) / 2;
   I.n_tiles = I.n_page_tiles + (I.s == I.ns - 1 ? 1 : 0);

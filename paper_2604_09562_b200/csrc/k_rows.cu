@@ -320,12 +320,13 @@ __device__ __forceinline__ int block_excl_scan256(int v, int* s_w, int* total) {
 }
 
 __global__ void __launch_bounds__(256) plan_embed_kernel(LaneDev d, PlanArgs p, const int* __restrict__ draft_tokens,
-                                                         const int* __restrict__ parents) {
+                                                         const int* __restrict__ parents, int allow_wide) {
   pdl_trigger();
   pdl_wait();
   __shared__ int s_off[kMaxBatch + 1], s_item[kMaxBatch + 1], s_len[kMaxBatch], s_slot[kMaxBatch];
-  __shared__ int s_w[8], s_err;
+  __shared__ int s_w[8], s_err, s_minL;
   const int B = p.batch, tid = threadIdx.x;
+  if (tid == 0) s_minL = 0x7fffffff;
   // per-request state: thread t < B holds request t (B <= kMaxBatch = 256)
   int k1 = 0, nit = 0;
   if (tid < B) {
@@ -340,8 +341,16 @@ __global__ void __launch_bounds__(256) plan_embed_kernel(LaneDev d, PlanArgs p, 
     s_slot[tid] = slot;
     s_len[tid] = L;
     k1 = k + 1;
-    nit = num_splits(L) * d.Hkv;
   }
+  __syncthreads();
+  if (tid < B) atomicMin(&s_minL, s_len[tid]);
+  __syncthreads();
+  // wide (2048-key) splits when every context holds at least two of them: half the items, half the
+  // split-KV partials the combine reads (ns 4096-token contexts); shorter or mixed contexts keep
+  // 1024-key items, which balance better over the persistent grid (c3: 1-2k contexts measured worse wide)
+  const int wide = allow_wide && s_minL >= 4 * kSplitKeys ? 1 : 0;
+  const int sk = kSplitKeys << wide;
+  if (tid < B) nit = num_splits_k(s_len[tid], sk) * d.Hkv;
   int T = 0, NI = 0;
   const int off = block_excl_scan256(k1, s_w, &T);
   const int ito = block_excl_scan256(nit, s_w, &NI);
@@ -423,9 +432,9 @@ __global__ void __launch_bounds__(256) plan_embed_kernel(LaneDev d, PlanArgs p, 
       d.slots[b] = slot;
       d.depths[b] = R - 1;
     }
-    const int ns = num_splits(L);
+    const int ns = num_splits_k(L, sk);
     for (int i = tid; i < ns * d.Hkv; i += blockDim.x)
-      d.items[s_item[b] + i] = make_int4(b, i / ns, i % ns, ns);
+      d.items[s_item[b] + i] = make_int4(b, i / ns, i % ns, ns | (wide << kItemWideShift));
   }
   if (tid == 0) {
     int tok, pos, e;
@@ -435,7 +444,7 @@ __global__ void __launch_bounds__(256) plan_embed_kernel(LaneDev d, PlanArgs p, 
     d.row_req[r] = b;
     d.row_pos[r] = pos;
     d.chain_tok[r] = tok;
-    d.row_comb[r] = make_int4(j, num_splits(L), s_item[b], 0);
+    d.row_comb[r] = make_int4(j, num_splits_k(L, sk), s_item[b], 0);
     s_tok = tok;
   }
   __syncthreads();
@@ -484,9 +493,9 @@ bool plan_embed_supported(const LaneDev& d) {
 }
 
 cudaError_t launch_plan_embed(const LaneDev& d, const PlanArgs& p, const int* draft_tokens, const int* parents,
-                              int rows, cudaStream_t s) {
+                              int rows, bool allow_wide, cudaStream_t s) {
   SV_COUNT_LAUNCH();
-  return launch_pdl(plan_embed_kernel, dim3(rows), dim3(256), 0, s, 1, d, p, draft_tokens, parents);
+  return launch_pdl(plan_embed_kernel, dim3(rows), dim3(256), 0, s, 1, d, p, draft_tokens, parents, allow_wide ? 1 : 0);
 }
 
 cudaError_t launch_embed_norm(const LaneDev& d, int T, cudaStream_t s) {

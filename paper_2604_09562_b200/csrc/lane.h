@@ -85,6 +85,15 @@ __host__ __device__ inline int split_t0(int s) { return s * kSplitKeys; }
 __host__ __device__ inline int split_t1(int s, int ns, int L, int R) {
   return s == ns - 1 ? L + R : (s + 1) * kSplitKeys;
 }
+// Wide splits (per verify, chosen by plan_embed_kernel): items of (kSplitKeys << wide) page keys. An
+// item's .w holds ns | wide << 24; the helpers below take the split size explicitly.
+constexpr int kItemWideShift = 24;
+__host__ __device__ inline int item_ns(int w) { return w & ((1 << kItemWideShift) - 1); }
+__host__ __device__ inline int item_split_keys(int w) { return kSplitKeys << (w >> kItemWideShift); }
+__host__ __device__ inline int num_splits_k(int L, int sk) { return L <= 0 ? 1 : (L + sk - 1) / sk; }
+__host__ __device__ inline int split_t1_k(int s, int ns, int L, int R, int sk) {
+  return s == ns - 1 ? L + R : (s + 1) * sk;
+}
 
 // kernels launched by the library so far (measurement hook, sv_launch_count)
 extern unsigned long long g_launch_count;
@@ -142,7 +151,7 @@ cudaError_t launch_embed_norm(const LaneDev& d, int T, cudaStream_t s);
 // Tmax for a dynamic-depth graph); requires plan_embed_supported(d)
 bool plan_embed_supported(const LaneDev& d);
 cudaError_t launch_plan_embed(const LaneDev& d, const PlanArgs& p, const int* draft_tokens, const int* parents,
-                              int rows, cudaStream_t s);
+                              int rows, bool allow_wide, cudaStream_t s);
 cudaError_t launch_rmsnorm(const LaneDev& d, const float* x, const bf16* g, bf16* out, int T, cudaStream_t s,
                            bool bound_by_T_dev = true);
 // C[M][N] (fp32) = A[M][K] (bf16) * B[N][K]^T (bf16)

@@ -558,7 +558,8 @@ static sv_status verify_impl(sv_ctx* c, int32_t batch, const int32_t* slots, con
   wait_comm_slots(c, batch, slots);
   if (sv::plan_embed_supported(d) && !getenv("SV_SPLIT_PLAN")) {
     // plan + embed in one launch (each row's CTA scans the batch itself)
-    STAGE(c, ST_EMBED, sv::launch_plan_embed(d, p, draft_tokens, parents, T, s));
+    const bool wide = sv::attn_uses_tc2(c->gemm, max_rows) && !getenv("SV_NO_WIDE_SPLIT");
+    STAGE(c, ST_EMBED, sv::launch_plan_embed(d, p, draft_tokens, parents, T, wide, s));
   } else {
     STAGE(c, ST_PLAN, sv::launch_plan(d, p, draft_tokens, parents, true, s));
     STAGE(c, ST_EMBED, sv::launch_embed_norm(d, T, s));
