@@ -840,6 +840,7 @@ __global__ void __launch_bounds__(FIN_THREADS, 2) finalize_kernel(LaneDev d, con
             mt[jj] = fmaxf(mt[jj], vm[jj][i]);
           }
       }
+      if (j0 == 0) FIN_TR(6);
 #pragma unroll
       for (int jj = 0; jj < RG; ++jj) {
         float m = mt[jj];
@@ -848,13 +849,16 @@ __global__ void __launch_bounds__(FIN_THREADS, 2) finalize_kernel(LaneDev d, con
         if (lane == 0) s_rm[warp][jj] = m;
       }
       __syncthreads();
+      if (j0 == 0) FIN_TR(7);
       float M[RG];
 #pragma unroll
-      for (int jj = 0; jj < RG; ++jj) {
-        float m = s_rm[0][jj];
-        for (int w = 1; w < nw; ++w) m = fmaxf(m, s_rm[w][jj]);
+      for (int jj = 0; jj < RG; ++jj) {                   // lanes 0..15 hold the 16 warps' maxima
+        float m = s_rm[lane & 15][jj];
+#pragma unroll
+        for (int o = 8; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
         M[jj] = m;
       }
+      if (j0 == 0) FIN_TR(8);
       // pass 2: scaled sums and the lowest max tile (reloading only when the row did not fit one sweep)
       float St[RG];
       int tb[RG];
@@ -874,7 +878,7 @@ __global__ void __launch_bounds__(FIN_THREADS, 2) finalize_kernel(LaneDev d, con
               vm[jj][i] = ok ? d.tile_max[(size_t)(r0 + j) * nt + t] : -INFINITY;
               vs[jj][i] = ok ? d.tile_sum[(size_t)(r0 + j) * nt + t] : 0.f;
             }
-            if (vm[jj][i] != -INFINITY) St[jj] += vs[jj][i] * expf(vm[jj][i] - M[jj]);
+            if (vm[jj][i] != -INFINITY) St[jj] += vs[jj][i] * tc_ex2((vm[jj][i] - M[jj]) * 1.4426950408889634f);
             if (ok && vm[jj][i] == M[jj] && t < tb[jj]) tb[jj] = t;
           }
       }
@@ -893,18 +897,25 @@ __global__ void __launch_bounds__(FIN_THREADS, 2) finalize_kernel(LaneDev d, con
         }
       }
       __syncthreads();
-      if (tid < RG && j0 + tid <= k) {                    // warps summed in order (deterministic)
-        float S = 0.f;
-        int t = 0x7fffffff;
-        for (int w = 0; w < nw; ++w) {
-          S += s_rs[w][tid];
-          t = min(t, s_rt[w][tid]);
+      if (warp == 0) {                                    // warps summed in a fixed tree order (deterministic)
+#pragma unroll
+        for (int jj = 0; jj < RG; ++jj) {
+          float S = lane < nw ? s_rs[lane][jj] : 0.f;
+          int t = lane < nw ? s_rt[lane][jj] : 0x7fffffff;
+#pragma unroll
+          for (int o = 16; o; o >>= 1) {
+            S += __shfl_xor_sync(0xffffffffu, S, o);
+            t = min(t, __shfl_xor_sync(0xffffffffu, t, o));
+          }
+          if (lane == jj && j0 + jj <= k) {
+            s_m[j0 + jj] = M[jj];
+            s_S[j0 + jj] = S;
+            s_tb[j0 + jj] = t;
+          }
         }
-        s_m[j0 + tid] = M[tid];
-        s_S[j0 + tid] = S;
-        s_tb[j0 + tid] = t;
       }
       __syncthreads();
+      if (j0 == 0) FIN_TR(9);
     }
     if (tid <= k) s_top[tid] = s_tb[tid] < nt ? d.tile_arg[(size_t)(r0 + tid) * nt + s_tb[tid]] : 0;
   }

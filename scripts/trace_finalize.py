@@ -25,7 +25,7 @@ for i in range(4):
     lane.verify(list(range(B)), ks, drafts, None, seed=i, mode=wl.mode, temperature=wl.temperature, out=(acc, tok))
     lane.commit()
 torch.cuda.synchronize()
-tr = lane.tap("trace", torch.int64, (16, 256)).cpu().numpy().astype(np.int64)[:6]
+tr = lane.tap("trace", torch.int64, (16, 256)).cpu().numpy().astype(np.int64)[:10]
 ok = tr[0] > 0
 t0 = tr[0][ok].min()
 ph = (tr[:, ok] - t0) / 1e3
@@ -35,4 +35,9 @@ for i, n in enumerate(names):
 d = np.diff(ph, axis=0)
 for i in range(1, 6):
     print(f"{names[i - 1]}->{names[i]:10s} median {np.median(d[i - 1]):6.2f} max {d[i - 1].max():6.2f}")
+sub = ["loads", "max+sync", "M", "sums+sync"]
+prev = ph[1]
+for i, n in enumerate(sub):
+    print(f"row stats group 0: {n:10s} median {np.median(ph[6 + i] - prev):6.2f} max {(ph[6 + i] - prev).max():6.2f}")
+    prev = ph[6 + i]
 print("accepted", acc.cpu().numpy()[:16])
