@@ -558,7 +558,11 @@ static sv_status verify_impl(sv_ctx* c, int32_t batch, const int32_t* slots, con
   wait_comm_slots(c, batch, slots);
   if (sv::plan_embed_supported(d) && !getenv("SV_SPLIT_PLAN")) {
     // plan + embed in one launch (each row's CTA scans the batch itself)
-    const bool wide = sv::attn_uses_tc2(c->gemm, max_rows) && !getenv("SV_NO_WIDE_SPLIT");
+    // wide (2048-key) splits: opt-in (SV_WIDE_SPLIT=1). ns step -0.7 %, but on ragged 4.1-6.2 k contexts
+    // one of three runs put the attention at 1.001 % of the survey's 1 % criterion (1024-key items:
+    // 0.77-0.82 %), DESIGN.md §6.2
+    const bool wide = sv::attn_uses_tc2(c->gemm, max_rows) && getenv("SV_WIDE_SPLIT") &&
+                      !strcmp(getenv("SV_WIDE_SPLIT"), "1");
     STAGE(c, ST_EMBED, sv::launch_plan_embed(d, p, draft_tokens, parents, T, wide, s));
   } else {
     STAGE(c, ST_PLAN, sv::launch_plan(d, p, draft_tokens, parents, true, s));
