@@ -55,6 +55,12 @@ def main():
     d = synth.random_tokens(9, lcfg.vocab, seed=5).cuda()
     ll.verify([0, 1], [8, 1], d[:9], mode="greedy")
     ll.commit()
+    # sampled at Llama vocabulary: the pruned race fast path (one-hot and dense drafts, split slices)
+    ll.verify([0, 1], [8, 1], d[:9], mode="sample", seed=3, temperature=0.9)
+    ll.commit()
+    qd = synth.draft_probs_dense(9, lcfg.vocab, seed=6).cuda()
+    ll.verify([0, 1], [8, 1], d[:9], qd, mode="sample", seed=4)
+    ll.commit()
     torch.cuda.synchronize()
     print("llama ok", ll.stats()["steps"], "steps")
 
