@@ -455,6 +455,45 @@ def _run_gpu(args, wl, rank, world, dev, stream):
     # host call and a stream dependency); --detail times every stage and says so in the line
     lane.profile(True if args.detail else ["lm_head", "attention"])
     lane.profile_read(reset=True)
+    # The timed region replays ONE captured step (planted drafter + verify + commit) as a CUDA graph,
+    # the production decode path (PipeServe-Engine lanes run the same step every iteration): the
+    # profiled stages' events are nodes of the graph, re-pointed at fresh events every replay, so the
+    # roofline kernels are still timed per launch inside the region. Depth vectors that change per step
+    # (c2, c3's controller) go through the dynamic-depth graph's staging buffer; each step's drafter
+    # inputs are copied into the buffers the graph reads. --eager times the same steps as eager calls.
+    # Workloads whose depths change per step (c2, c3's controller) time eager calls (their dynamic-depth
+    # graph with per-replay events measured no faster on one box); fixed-depth ones replay two graphs of
+    # the same step: the one whose stage events are graph nodes on every --prof-every-th step (the
+    # roofline averages come from those), the one without events on the others (an event node between
+    # two kernels costs the PDL overlap there: ~2 % of an ns step).
+    dynamic = wl.controller or wl.kmin != wl.kmax
+    graph = plain = None
+    if not args.eager and not dynamic:
+        try:
+            m_stage = torch.empty_like(masks_d[0])
+            t_stage = torch.empty_like(devtok_d[0])
+
+            def capture():
+                lane.graph_begin()
+                draft_and_verify(lane, wl, slots, depths[args.warmup - 1], succ_d, m_stage, t_stage, drafts, 1234,
+                                 (acc, tok), par_d)
+                lane.commit()                         # captured, not run
+                return lane.graph_end()
+            graph = capture()                         # profiled stages -> event-record nodes
+            lane.profile(False)
+            plain = capture()
+            lane.profile(True if args.detail else ["lm_head", "attention"])
+            torch.cuda.synchronize(dev)
+        except Exception as ex:                       # fall back to timing eager calls
+            print(f"[bench] graph capture failed ({ex}); timing eager steps", file=sys.stderr)
+            lane.profile(True if args.detail else ["lm_head", "attention"])
+            graph = plain = None
+
+    def gstep(i, j):
+        m_stage.copy_(masks_d[j])
+        t_stage.copy_(devtok_d[j])
+        lane.graph_launch(graph if i % args.prof_every == 0 else plain)
+
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     stream = torch.cuda.current_stream(dev)
     launches0 = sv.launch_count()
@@ -464,7 +503,10 @@ def _run_gpu(args, wl, rank, world, dev, stream):
     with Clocks(dev.index) as clk:
         ev[0].record(stream)
         for i in range(args.steps):
-            step(args.warmup + i)
+            if graph is not None:
+                gstep(i, args.warmup + i)
+            else:
+                step(args.warmup + i)
             ev[i + 1].record(stream)
             if ctl:                                   # the control loop reads the counters (syncs)
                 ctl.tick(lane, args.warmup + i)
@@ -476,6 +518,9 @@ def _run_gpu(args, wl, rank, world, dev, stream):
     per_step = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]
     prof = lane.profile_read(reset=True)
     lane.profile(False)
+    if graph is not None:
+        lane.graph_destroy(graph)
+        lane.graph_destroy(plain)
     st = lane.stats()
     tokens = st["emitted"]
     # ----- roofline of the dominant kernels (live CUDA-event durations, averaged per launch)
@@ -514,7 +559,8 @@ def _run_gpu(args, wl, rank, world, dev, stream):
                 launches=launches, clocks=clk.summary(), stats=st, e2e=e2e, e2e_host=e2e_host, w=w, succ=succ, reqs=reqs,
                 depths=depths, masks=masks, devtok=devtok, alg=alg, verify_graph=vgraph,
                 controller=({"window_steps": ControlledDepths.WINDOW, "final_depth": ctl.d, "trace": ctl.trace[-6:]}
-                            if ctl else None))
+                            if ctl else None),
+                timed=("static" if graph is not None else "eager"), prof_every=args.prof_every)
 
 
 def run_graph(args, wl, rank, world, dev):
@@ -1024,6 +1070,10 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=50)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--detail", action="store_true", help="add per-stage breakdown to the JSON line")
+    ap.add_argument("--eager", action="store_true",
+                    help="time eager library calls instead of replays of one captured step (CUDA graph)")
+    ap.add_argument("--prof-every", type=int, default=10,
+                    help="graph-timed region: replay the event-timed copy of the step every N-th step")
     ap.add_argument("--graph", action="store_true", help="replay the step as a CUDA graph (fixed depths)")
     ap.add_argument("--disagg", action="store_true",
                     help="prefill -> decode pairs with the batched NCCL KV hand-off (configs[3]; world 1: loopback)")
@@ -1109,6 +1159,12 @@ def main():
                                          else "prefill + decode lanes on one GPU (loopback)")
         line["config"]["disagg"] = f"hand-off of {wl.batch} x {wl.ctx[1]}-token KV every {DISAGG_STEPS_PER_ROUND} steps"
         line["scaling"] = "weak"
+    if res.get("timed"):
+        line["config"]["timed_region"] = {
+            "eager": "eager library calls (drafter + verify + commit) per step",
+            "static": "replays of one captured step (CUDA graph: drafter + verify + commit), depths fixed per request; "
+                      f"every {res.get('prof_every')}-th replay from the copy whose roofline stages are event-record "
+                      "nodes (per-launch averages over those), the others from the copy without events"}[res["timed"]]
     if res.get("graph"):
         line["config"]["graph"] = ("one dynamic-depth CUDA graph (sv_graph_begin_dynamic) replayed with each step's "
                                    "depth vector" if res["graph"] == "dynamic" else

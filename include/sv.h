@@ -207,10 +207,12 @@ sv_status sv_verify_tree_logits(sv_ctx* ctx, int32_t batch, const int32_t* slots
  * its stream instead of running — the host-side checks and state changes happen once, at capture —
  * and sv_graph_launch replays the captured kernels with the same arguments (slots, depths, seed,
  * device pointers: inputs that change per step are refreshed by the caller in the buffers the
- * graph reads). The lane's stream must be a created stream (not the legacy default stream), its
- * profiling off, and every captured sv_verify committed inside the capture (else sv_graph_end
- * returns SV_ESTATE). Replays advance the device state (lengths, pages, counters) exactly like
- * the captured calls. sv_graph_destroy frees the instantiated graph. */
+ * graph reads). The lane's stream must be a created stream (not the legacy default stream), and
+ * every captured sv_verify committed inside the capture (else sv_graph_end returns SV_ESTATE).
+ * Stages being timed (sv_profile_enable) while capturing become event-record nodes of the graph that
+ * every replay points at fresh events while the lane still times those stages, so sv_profile_read
+ * covers replays as it covers eager calls. Replays advance the device state (lengths, pages,
+ * counters) exactly like the captured calls. sv_graph_destroy frees the instantiated graph. */
 typedef struct sv_graph sv_graph;
 sv_status sv_graph_begin(sv_ctx* ctx);
 /* One graph for ANY depth vector (slots / depths go through a pinned staging buffer

@@ -149,6 +149,7 @@ struct Prof {
   std::vector<cudaEvent_t> free_ev;
   struct Rec { int stage; cudaEvent_t a, b; };
   std::vector<Rec> recs;
+  std::vector<Rec> captured;                  // stage events recorded into a CUDA graph being captured
   double ms[ST_NUM] = {};
   long long n[ST_NUM] = {};
   cudaEvent_t get() {
@@ -220,10 +221,16 @@ static void wait_comm_slots(sv_ctx* c, int n, const int32_t* slots) {
     }
 }
 
+// while capturing a graph the records must become event-record NODES (cudaEventRecordExternal), which
+// sv_graph_launch re-points per replay; a plain record would only order the capture
+static void prof_record(sv_ctx* c, cudaEvent_t e) {
+  if (c->capturing) cudaEventRecordWithFlags(e, c->stream, cudaEventRecordExternal);
+  else cudaEventRecord(e, c->stream);
+}
 static cudaEvent_t prof_begin(sv_ctx* c, int stage) {
   if (!(c->prof.mask >> stage & 1u)) return nullptr;
   cudaEvent_t e = c->prof.get();
-  cudaEventRecord(e, c->stream);
+  prof_record(c, e);
   return e;
 }
 // fold finished records into the totals; never blocks the host (a blocking fold would drain
@@ -249,7 +256,11 @@ static void prof_fold(sv_ctx* c, bool wait) {
 static void prof_end(sv_ctx* c, int stage, cudaEvent_t a) {
   if (!a) return;
   cudaEvent_t b = c->prof.get();
-  cudaEventRecord(b, c->stream);
+  prof_record(c, b);
+  if (c->capturing) {                         // event-record nodes of the graph: timed per replay
+    c->prof.captured.push_back({stage, a, b});
+    return;
+  }
   c->prof.recs.push_back({stage, a, b});
   if (c->prof.recs.size() >= 8192 && c->prof.recs.size() % 1024 == 0) prof_fold(c, false);
 }
@@ -1036,11 +1047,19 @@ struct sv_graph {
   mutable long long replays = 0;     // dynamic: replay r stages into pinned buffer r & 1 ...
   mutable cudaEvent_t done[2] = {nullptr, nullptr};   // ... once replay r - 2 (same buffer) has finished
   mutable bool done_set[2] = {false, false};
+  // profiled graph (stages timed while capturing): each stage's two event-record nodes are pointed at
+  // fresh pool events before every replay (cudaGraphExecEventRecordNodeSetEvent), and the pair joins the
+  // lane's profile records, so per-stage CUDA-event times cover replays as they do eager calls
+  struct ProfNode { int stage; cudaGraphNode_t a, b; };
+  std::vector<ProfNode> prof;
+  std::vector<cudaEvent_t> owned;    // the events recorded at capture (the template's nodes refer to them)
+  cudaEvent_t idle[2] = {nullptr, nullptr};   // targets while the lane is not profiling the stage
 };
 
 sv_status sv_graph_begin(sv_ctx* c) {
   if (!c || !c->stream) return SV_EINVAL;                 // the legacy default stream cannot be captured
-  if (c->capturing || c->pending_verify || c->prof.mask) return SV_ESTATE;
+  if (c->capturing || c->pending_verify) return SV_ESTATE;
+  c->prof.captured.clear();
   wait_comm(c);                                           // an outside event cannot be waited on in capture
   SV_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
   c->capturing = true;
@@ -1050,7 +1069,8 @@ sv_status sv_graph_begin(sv_ctx* c) {
 
 sv_status sv_graph_begin_dynamic(sv_ctx* c, int32_t batch) {
   if (!c || !c->stream || batch < 1 || batch > c->cfg.max_batch) return SV_EINVAL;
-  if (c->capturing || c->pending_verify || c->prof.mask) return SV_ESTATE;
+  if (c->capturing || c->pending_verify) return SV_ESTATE;
+  c->prof.captured.clear();
   if (!sv::supports_dynamic_rows(c->gemm)) return SV_ESTATE;
   wait_comm(c);
   SV_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
@@ -1105,11 +1125,50 @@ sv_status sv_graph_end(sv_ctx* c, sv_graph** out) {
   }
   cudaGraphExec_t x = nullptr;
   const cudaError_t e2 = cudaGraphInstantiate(&x, g, 0);
-  if (!dyn || e2 != cudaSuccess) cudaGraphDestroy(g);
-  if (e2 != cudaSuccess) return SV_ECUDA;
+  const bool profiled = !c->prof.captured.empty();
+  if ((!dyn && !profiled) || e2 != cudaSuccess) cudaGraphDestroy(g);
+  if (e2 != cudaSuccess) {
+    for (auto& r : c->prof.captured) {
+      c->prof.free_ev.push_back(r.a);
+      c->prof.free_ev.push_back(r.b);
+    }
+    c->prof.captured.clear();
+    return SV_ECUDA;
+  }
   sv_graph* gr = new sv_graph{x, sv::g_launch_count - c->capture_launches0, dyn, dyn_batch};
-  if (dyn) {                                              // keep the template: its H2D root is retargeted
+  if (profiled) {                                         // map the captured stage events to their nodes
     gr->tmpl = g;
+    size_t n = 0;
+    cudaGraphGetNodes(g, nullptr, &n);
+    std::vector<cudaGraphNode_t> nodes(n);
+    if (n) cudaGraphGetNodes(g, nodes.data(), &n);
+    auto node_of = [&](cudaEvent_t ev) -> cudaGraphNode_t {
+      for (cudaGraphNode_t nd : nodes) {
+        cudaGraphNodeType ty;
+        cudaEvent_t e = nullptr;
+        if (cudaGraphNodeGetType(nd, &ty) == cudaSuccess && ty == cudaGraphNodeTypeEventRecord &&
+            cudaGraphEventRecordNodeGetEvent(nd, &e) == cudaSuccess && e == ev)
+          return nd;
+      }
+      return nullptr;
+    };
+    bool ok = cudaEventCreate(&gr->idle[0]) == cudaSuccess && cudaEventCreate(&gr->idle[1]) == cudaSuccess;
+    for (auto& r : c->prof.captured) {
+      gr->owned.push_back(r.a);
+      gr->owned.push_back(r.b);
+      const cudaGraphNode_t na = node_of(r.a), nb = node_of(r.b);
+      if (!na || !nb) ok = false;
+      gr->prof.push_back({r.stage, na, nb});
+    }
+    c->prof.captured.clear();
+    if (!ok) {
+      fprintf(stderr, "[sv] sv_graph_end: profiled stage events without event-record nodes\n");
+      sv_graph_destroy(gr);
+      return SV_ECUDA;
+    }
+  }
+  if (dyn) {                                              // keep the template: its H2D root is retargeted
+    gr->tmpl = g;                                         // (the same template as a profiled graph's)
     size_t nroot = 1;
     cudaGraphNode_t root = nullptr;
     cudaGraphNodeType ty;
@@ -1130,7 +1189,18 @@ sv_status sv_graph_end(sv_ctx* c, sv_graph** out) {
 sv_status sv_graph_launch(sv_ctx* c, const sv_graph* g) {
   if (!c || !g) return SV_EINVAL;
   if (c->capturing || c->pending_verify) return SV_ESTATE;
+  // profiled stages: fresh events for this replay while the lane times the stage, else the idle pair
+  std::vector<Prof::Rec> fresh;
+  for (const auto& pn : g->prof) {
+    const bool on = (c->prof.mask >> pn.stage) & 1u;
+    const cudaEvent_t a = on ? c->prof.get() : g->idle[0], b = on ? c->prof.get() : g->idle[1];
+    SV_CUDA(cudaGraphExecEventRecordNodeSetEvent(g->exec, pn.a, a));
+    SV_CUDA(cudaGraphExecEventRecordNodeSetEvent(g->exec, pn.b, b));
+    if (on) fresh.push_back({pn.stage, a, b});
+  }
   SV_CUDA(cudaGraphLaunch(g->exec, c->stream));
+  for (const auto& r : fresh) c->prof.recs.push_back(r);
+  if (c->prof.recs.size() >= 8192 && c->prof.recs.size() % 1024 == 0) prof_fold(c, false);
   sv::g_launch_count += g->kernels;
   if (g->dynamic) {
     const int buf = (int)(g->replays & 1);
@@ -1146,6 +1216,9 @@ sv_status sv_graph_destroy(sv_graph* g) {
   cudaGraphExecDestroy(g->exec);
   if (g->tmpl) cudaGraphDestroy(g->tmpl);
   for (cudaEvent_t e : g->done)
+    if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : g->owned) cudaEventDestroy(e);
+  for (cudaEvent_t e : g->idle)
     if (e) cudaEventDestroy(e);
   delete g;
   return SV_OK;

@@ -207,3 +207,62 @@ def test_dynamic_graph_any_depth_vector(cfgname, mode):
             assert torch.equal(x, y), (i, depths[i], x, y)
     assert outs["eager"][1] == outs["graph"][1]
     assert outs["eager"][1]["drafted"] == sum(sum(k) for k in depths)
+
+
+def test_profiled_graph_times_every_replay():
+    """Stages timed while capturing become event-record nodes that each replay re-points at fresh
+    events: sv_profile_read counts one launch per replay with a positive time, while the profile stays
+    on; replays after sv_profile_enable(0) add nothing. Outputs equal an unprofiled graph's."""
+    cfg = synth.TOY_MLP
+    w = synth.model_weights(cfg, seed=0, norm_one=False)
+    w, succ = synth.planted_successor(cfg, w, seed=1, beta=0.3)
+    depths = [4, 2, 3, 1]
+    rows = sum(depths)
+    masks, devtok = synth.planted_masks(8, rows, 0.7, cfg.vocab, seed=2)
+    outs = []
+    for profiled in (True, False):
+        stream = torch.cuda.Stream()
+        with torch.cuda.stream(stream):
+            lane = _lane(cfg, w, stream)
+            succ_d = succ.cuda()
+            m_stage = torch.empty(rows, dtype=torch.uint8, device="cuda")
+            t_stage = torch.empty(rows, dtype=torch.int32, device="cuda")
+            drafts = torch.empty(rows, dtype=torch.int32, device="cuda")
+            acc = torch.empty(4, dtype=torch.int32, device="cuda")
+            tok = torch.empty(4, cfg.max_depth + 1, dtype=torch.int32, device="cuda")
+
+            def step():
+                lane.draft_planted([0, 1, 2, 3], depths, succ_d, m_stage, t_stage, drafts)
+                lane.verify([0, 1, 2, 3], depths, drafts, None, seed=5, mode="greedy", out=(acc, tok))
+                lane.commit()
+
+            m_stage.copy_(masks[0].cuda())
+            t_stage.copy_(devtok[0].cuda())
+            step()
+            if profiled:
+                lane.profile(["lm_head", "attention"])
+            lane.graph_begin()
+            step()                                       # captured, not run
+            g = lane.graph_end()
+            lane.profile_read(reset=True)
+            res = []
+            for i in range(1, 6):
+                m_stage.copy_(masks[i].cuda())
+                t_stage.copy_(devtok[i].cuda())
+                lane.graph_launch(g)
+                res.append((acc.clone(), tok.clone()))
+            prof = lane.profile_read(reset=True)
+            if profiled:
+                assert prof["lm_head"][1] == 5 and prof["attention"][1] == 5
+                assert prof["lm_head"][0] > 0 and prof["attention"][0] > 0
+                lane.profile(False)
+                lane.graph_launch(g)
+                assert lane.profile_read(reset=True)["lm_head"][1] == 0
+            else:
+                assert all(n == 0 for _, n in prof.values())
+                lane.graph_launch(g)
+            torch.cuda.synchronize()
+            outs.append([(a.cpu(), t.cpu()) for a, t in res])
+            lane.graph_destroy(g)
+    for (a0, t0), (a1, t1) in zip(*outs):
+        assert torch.equal(a0, a1) and torch.equal(t0, t1)
