@@ -6,7 +6,7 @@ tag=${1:-r02s3}
 o=gpurun_out
 python bench.py > $o/${tag}_bench_ns.json 2> $o/${tag}_bench_ns.err
 for w in c2 c3 c4 ns_tree c2_filter toy; do
-  python bench.py --workload $w --steps 100 --detail > $o/${tag}_bench_$w.json 2> $o/${tag}_bench_$w.err
+  python bench.py --workload $w --steps 100 > $o/${tag}_bench_$w.json 2> $o/${tag}_bench_$w.err
 done
 for w in ns c2 c3 toy; do
   python bench.py --workload $w --steps 100 --graph --no-cpu-baseline --e2e-steps 0 > $o/${tag}_bench_${w}_graph.json 2> $o/${tag}_bench_${w}_graph.err
