@@ -805,11 +805,14 @@ def run_e2e(args, wl, lane, succ, depths, masks, devtok, dev, start):
     every step. The drafter is the device one (`sv_draft_planted`); each step's drafter inputs
     (deviation mask + replacement tokens) are copied H2D from pinned memory and each step's
     accepted lengths + emitted tokens are copied D2H into a pinned double buffer and consumed on
-    the host one step later (event-ordered), so host work overlaps the next step's kernels."""
+    the host one step later (event-ordered), so host work overlaps the next step's kernels. Fixed-depth
+    workloads (unless --eager) run the step as replays of one captured graph (sv_graph_launch, public API)
+    that reads the device copies of the drafter inputs, as the timed region does."""
     cfg = wl.cfg
     B = wl.batch
     slots = list(range(B))
     n = args.e2e_steps
+    fixed = not (wl.controller or wl.kmin != wl.kmax)
     kr = B * wl.kmax
     h_mask = masks[start:start + n].clone().pin_memory()
     h_dev = devtok[start:start + n].clone().pin_memory()
@@ -832,16 +835,32 @@ def run_e2e(args, wl, lane, succ, depths, masks, devtok, dev, start):
         a = h_acc[slot].numpy()
         emitted_host += int((a + 1).sum())
 
+    graph = None
+    if fixed and not args.eager:
+        try:                                      # the inputs land in d_mask[0] / d_dev[0] (stream-ordered)
+            lane.graph_begin()
+            draft_and_verify(lane, wl, slots, depths[start], succ_d, d_mask[0], d_dev[0], drafts, 99 + start,
+                             (acc, tok), par_d)
+            lane.commit()                         # captured, not run
+            graph = lane.graph_end()
+        except Exception as ex:
+            print(f"[bench] e2e graph capture failed ({ex}); eager calls", file=sys.stderr)
+            graph = None
     lane.stats(reset=True)
     torch.cuda.synchronize(dev)
     t0 = time.perf_counter()
     for s_ in range(n):
         i = start + s_
-        sl = s_ & 1
-        d_mask[sl].copy_(h_mask[s_], non_blocking=True)
-        d_dev[sl].copy_(h_dev[s_], non_blocking=True)
-        draft_and_verify(lane, wl, slots, depths[i], succ_d, d_mask[sl], d_dev[sl], drafts, 99 + i, (acc, tok), par_d)
-        lane.commit()
+        sl = s_ & 1                               # read-back double buffer
+        ib = 0 if graph is not None else sl       # input buffers (the graph reads buffer 0)
+        d_mask[ib].copy_(h_mask[s_], non_blocking=True)
+        d_dev[ib].copy_(h_dev[s_], non_blocking=True)
+        if graph is not None:
+            lane.graph_launch(graph)
+        else:
+            draft_and_verify(lane, wl, slots, depths[i], succ_d, d_mask[ib], d_dev[ib], drafts, 99 + i, (acc, tok),
+                             par_d)
+            lane.commit()
         h_acc[sl].copy_(acc, non_blocking=True)
         h_tok[sl].copy_(tok, non_blocking=True)
         done[sl].record(stream)
@@ -849,12 +868,15 @@ def run_e2e(args, wl, lane, succ, depths, masks, devtok, dev, start):
             consume(sl ^ 1)                       # previous step's results, while this step runs
     consume((n - 1) & 1)
     el = time.perf_counter() - t0
+    if graph is not None:
+        lane.graph_destroy(graph)
     st = lane.stats(reset=True)
     assert st["emitted"] == emitted_host, (st["emitted"], emitted_host)
     h2d = kr * (h_mask.element_size() + 4)
     d2h = B * 4 + B * (cfg.max_depth + 1) * 4
     return {"value": emitted_host / el, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
             "steps": n, "ms_per_step": 1e3 * el / n, "drafter": "device (sv_draft_planted), pipelined read-back",
+            "path": "sv_graph_launch of the captured step" if graph is not None else "eager sv_* calls",
             "tokens": emitted_host, "seconds": el}
 
 
