@@ -87,6 +87,13 @@ class Clocks:
             self.nv = pynvml
             self.h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
             self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            # the driver's cumulative power-policy violation time: unlike the sampled reason bits it
+            # cannot miss a cap that engages between two samples
+            try:
+                self.v0 = pynvml.nvmlDeviceGetViolationStatus(self.h, pynvml.NVML_PERF_POLICY_POWER).violationTime
+            except Exception:
+                self.v0 = None
+            self.w0 = time.perf_counter()
             self.t = threading.Thread(target=self._run, daemon=True)
             self.t.start()
         except Exception:
@@ -109,20 +116,34 @@ class Clocks:
 
     def __exit__(self, *a):
         self.stop.set()
+        self.power_violation = None
         if self.nv:
             self.t.join(timeout=1)
+            if self.v0 is not None:
+                try:
+                    v1 = self.nv.nvmlDeviceGetViolationStatus(self.h, self.nv.NVML_PERF_POLICY_POWER).violationTime
+                    span_ns = (time.perf_counter() - self.w0) * 1e9
+                    self.power_violation = max(0.0, min(1.0, (v1 - self.v0) / span_ns)) if span_ns > 0 else None
+                    if self.power_violation:
+                        self.reasons.add("sw_power_cap")
+                except Exception:
+                    pass
 
     def summary(self):
         if not self.sm:
             return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"], "samples": 0}
-        return {"sm_mhz": statistics.median(self.sm), "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
-                "samples": len(self.sm),
-                "reason_frac": {k: round(v / len(self.sm), 3) for k, v in sorted(self.reason_count.items())}}
+        out = {"sm_mhz": statistics.median(self.sm), "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+               "samples": len(self.sm),
+               "reason_frac": {k: round(v / len(self.sm), 3) for k, v in sorted(self.reason_count.items())}}
+        if getattr(self, "power_violation", None) is not None:
+            out["power_cap_violation_frac"] = round(self.power_violation, 3)   # NVML power-policy violation time
+        return out
 
     def power_capped(self):
         """True when sw_power_cap held for most of the region: the kernels then ran at the clocks
         the sustained peak was measured at, so that is the roofline denominator; else the burst."""
-        return bool(self.sm) and self.reason_count.get("sw_power_cap", 0) > 0.5 * len(self.sm)
+        sampled = bool(self.sm) and self.reason_count.get("sw_power_cap", 0) > 0.5 * len(self.sm)
+        return sampled or (getattr(self, "power_violation", None) or 0.0) > 0.5
 
 
 # ------------------------------------------------------------------ workload setup
