@@ -296,3 +296,29 @@ def test_lane_occupancy():
     assert active == 3 and free == 32 - 4
     S.lane.release(1)
     assert S.lane.occupancy() == (2, 32 - 3)
+
+
+@pytest.mark.parametrize("mode", ["greedy", "sample"])
+def test_fused_plan_embed_equals_separate_launches(mode, monkeypatch):
+    """plan_embed_kernel (a1 + a2 in one launch, each row CTA scanning the batch itself) writes the same
+    row tables, work items and h0 / a as plan_kernel + embed_norm_vec_kernel (SV_SPLIT_PLAN=1): the
+    verify's outputs and every tapped intermediate agree bit for bit."""
+    cfg = synth.TOY_MLP
+    d = synth.random_tokens(2 + 5 + 0 + 3, cfg.vocab, seed=21)
+    res = []
+    for split in (False, True):
+        if split:
+            monkeypatch.setenv("SV_SPLIT_PLAN", "1")
+        else:
+            monkeypatch.delenv("SV_SPLIT_PLAN", raising=False)
+        S = Setup(cfg, [50, 90, 7, 130], seed=12)
+        a, t = [x.cpu().clone() for x in S.lane.verify([0, 1, 2, 3], [2, 5, 0, 3], d.cuda(), mode=mode, seed=8)]
+        T = 2 + 5 + 0 + 3 + 4
+        taps = [S.tap("h0", torch.float32, (T, cfg.d_model)), S.tap("a", torch.bfloat16, (T, cfg.d_model)),
+                S.tap("o", torch.bfloat16, (T, cfg.n_q_heads * cfg.head_dim))]
+        S.lane.commit()
+        res.append((a, t, taps))
+    (a0, t0, x0), (a1, t1, x1) = res
+    assert torch.equal(a0, a1) and torch.equal(t0, t1)
+    for u, v in zip(x0, x1):
+        assert torch.equal(u, v)
