@@ -489,21 +489,27 @@ def _run_gpu(args, wl, rank, world, dev, stream):
     # two kernels costs the PDL overlap there: ~2 % of an ns step).
     dynamic = wl.controller or wl.kmin != wl.kmax
     graph = plain = None
-    if not args.eager and not dynamic:
+    if not args.eager and (not dynamic or args.graph_dynamic) and not (dynamic and wl.tree):
         try:
             m_stage = torch.empty_like(masks_d[0])
             t_stage = torch.empty_like(devtok_d[0])
 
             def capture():
-                lane.graph_begin()
+                if dynamic:
+                    lane.graph_begin_dynamic(B)
+                else:
+                    lane.graph_begin()
                 draft_and_verify(lane, wl, slots, depths[args.warmup - 1], succ_d, m_stage, t_stage, drafts, 1234,
                                  (acc, tok), par_d)
                 lane.commit()                         # captured, not run
                 return lane.graph_end()
             graph = capture()                         # profiled stages -> event-record nodes
-            lane.profile(False)
-            plain = capture()
-            lane.profile(True if args.detail else ["lm_head", "attention"])
+            if dynamic:                               # one dynamic graph per lane (shared staging buffer)
+                plain = graph
+            else:
+                lane.profile(False)
+                plain = capture()
+                lane.profile(True if args.detail else ["lm_head", "attention"])
             torch.cuda.synchronize(dev)
         except Exception as ex:                       # fall back to timing eager calls
             print(f"[bench] graph capture failed ({ex}); timing eager steps", file=sys.stderr)
@@ -511,9 +517,14 @@ def _run_gpu(args, wl, rank, world, dev, stream):
             graph = plain = None
 
     def gstep(i, j):
+        if ctl:
+            ctl.prepare(j, masks_d, devtok_d)
         m_stage.copy_(masks_d[j])
         t_stage.copy_(devtok_d[j])
-        lane.graph_launch(graph if i % args.prof_every == 0 else plain)
+        g = graph if i % args.prof_every == 0 else plain
+        if dynamic:
+            lane.graph_set_batch(g, slots, depths[j])
+        lane.graph_launch(g)
 
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     stream = torch.cuda.current_stream(dev)
@@ -541,7 +552,8 @@ def _run_gpu(args, wl, rank, world, dev, stream):
     lane.profile(False)
     if graph is not None:
         lane.graph_destroy(graph)
-        lane.graph_destroy(plain)
+        if plain is not graph:
+            lane.graph_destroy(plain)
     st = lane.stats()
     tokens = st["emitted"]
     # ----- roofline of the dominant kernels (live CUDA-event durations, averaged per launch)
@@ -581,7 +593,8 @@ def _run_gpu(args, wl, rank, world, dev, stream):
                 depths=depths, masks=masks, devtok=devtok, alg=alg, verify_graph=vgraph,
                 controller=({"window_steps": ControlledDepths.WINDOW, "final_depth": ctl.d, "trace": ctl.trace[-6:]}
                             if ctl else None),
-                timed=("static" if graph is not None else "eager"), prof_every=args.prof_every)
+                timed=(("dynamic" if dynamic else "static") if graph is not None else "eager"),
+                prof_every=args.prof_every)
 
 
 def run_graph(args, wl, rank, world, dev):
@@ -1115,6 +1128,8 @@ def main():
     ap.add_argument("--detail", action="store_true", help="add per-stage breakdown to the JSON line")
     ap.add_argument("--eager", action="store_true",
                     help="time eager library calls instead of replays of one captured step (CUDA graph)")
+    ap.add_argument("--graph-dynamic", action="store_true",
+                    help="depth-varying workloads: time replays of one profiled dynamic-depth graph")
     ap.add_argument("--prof-every", type=int, default=10,
                     help="graph-timed region: replay the event-timed copy of the step every N-th step")
     ap.add_argument("--graph", action="store_true", help="replay the step as a CUDA graph (fixed depths)")
@@ -1207,7 +1222,9 @@ def main():
             "eager": "eager library calls (drafter + verify + commit) per step",
             "static": "replays of one captured step (CUDA graph: drafter + verify + commit), depths fixed per request; "
                       f"every {res.get('prof_every')}-th replay from the copy whose roofline stages are event-record "
-                      "nodes (per-launch averages over those), the others from the copy without events"}[res["timed"]]
+                      "nodes (per-launch averages over those), the others from the copy without events",
+            "dynamic": "replays of one dynamic-depth CUDA graph (sv_graph_begin_dynamic) with each step's depth "
+                       "vector; its roofline stages are event-record nodes timed on every replay"}[res["timed"]]
     if res.get("graph"):
         line["config"]["graph"] = ("one dynamic-depth CUDA graph (sv_graph_begin_dynamic) replayed with each step's "
                                    "depth vector" if res["graph"] == "dynamic" else
