@@ -482,14 +482,16 @@ def _run_gpu(args, wl, rank, world, dev, stream):
     # roofline kernels are still timed per launch inside the region. Depth vectors that change per step
     # (c2, c3's controller) go through the dynamic-depth graph's staging buffer; each step's drafter
     # inputs are copied into the buffers the graph reads. --eager times the same steps as eager calls.
-    # Workloads whose depths change per step (c2, c3's controller) time eager calls (their dynamic-depth
-    # graph with per-replay events measured no faster on one box); fixed-depth ones replay two graphs of
-    # the same step: the one whose stage events are graph nodes on every --prof-every-th step (the
-    # roofline averages come from those), the one without events on the others (an event node between
-    # two kernels costs the PDL overlap there: ~2 % of an ns step).
+    # The timed steps replay two graphs of the same step: the one whose stage events are graph nodes on
+    # every --prof-every-th step (the roofline averages come from those), the one without events on the
+    # others (an event node between two kernels costs the PDL overlap there: ~2 % of an ns step).
+    # Depth-varying workloads use two dynamic-depth graphs (sharing the lane's staging buffers).
     dynamic = wl.controller or wl.kmin != wl.kmax
     graph = plain = None
-    if not args.eager and (not dynamic or args.graph_dynamic) and not (dynamic and wl.tree):
+    # depth-varying workloads: graphs only where launches bound the step (toy: 0.080 -> 0.065 ms); at
+    # Llama shape their event-timed replays measured 1 % slower (c2) or even (c3) than eager calls
+    launch_bound = cfg.d_model <= 1024
+    if not args.eager and (not dynamic or args.graph_dynamic or launch_bound) and not (dynamic and wl.tree):
         try:
             m_stage = torch.empty_like(masks_d[0])
             t_stage = torch.empty_like(devtok_d[0])
@@ -504,12 +506,9 @@ def _run_gpu(args, wl, rank, world, dev, stream):
                 lane.commit()                         # captured, not run
                 return lane.graph_end()
             graph = capture()                         # profiled stages -> event-record nodes
-            if dynamic:                               # one dynamic graph per lane (shared staging buffer)
-                plain = graph
-            else:
-                lane.profile(False)
-                plain = capture()
-                lane.profile(True if args.detail else ["lm_head", "attention"])
+            lane.profile(False)
+            plain = capture()                         # (dynamic graphs share the lane's staging buffers)
+            lane.profile(True if args.detail else ["lm_head", "attention"])
             torch.cuda.synchronize(dev)
         except Exception as ex:                       # fall back to timing eager calls
             print(f"[bench] graph capture failed ({ex}); timing eager steps", file=sys.stderr)
@@ -847,6 +846,7 @@ def run_e2e(args, wl, lane, succ, depths, masks, devtok, dev, start):
     slots = list(range(B))
     n = args.e2e_steps
     fixed = not (wl.controller or wl.kmin != wl.kmax)
+    dyn_graph = not fixed and cfg.d_model <= 1024 and not wl.tree   # launch-bound: dynamic-depth graph
     kr = B * wl.kmax
     h_mask = masks[start:start + n].clone().pin_memory()
     h_dev = devtok[start:start + n].clone().pin_memory()
@@ -870,9 +870,12 @@ def run_e2e(args, wl, lane, succ, depths, masks, devtok, dev, start):
         emitted_host += int((a + 1).sum())
 
     graph = None
-    if fixed and not args.eager:
+    if (fixed or dyn_graph) and not args.eager:
         try:                                      # the inputs land in d_mask[0] / d_dev[0] (stream-ordered)
-            lane.graph_begin()
+            if dyn_graph:
+                lane.graph_begin_dynamic(B)
+            else:
+                lane.graph_begin()
             draft_and_verify(lane, wl, slots, depths[start], succ_d, d_mask[0], d_dev[0], drafts, 99 + start,
                              (acc, tok), par_d)
             lane.commit()                         # captured, not run
@@ -890,6 +893,8 @@ def run_e2e(args, wl, lane, succ, depths, masks, devtok, dev, start):
         d_mask[ib].copy_(h_mask[s_], non_blocking=True)
         d_dev[ib].copy_(h_dev[s_], non_blocking=True)
         if graph is not None:
+            if dyn_graph:
+                lane.graph_set_batch(graph, slots, depths[i])
             lane.graph_launch(graph)
         else:
             draft_and_verify(lane, wl, slots, depths[i], succ_d, d_mask[ib], d_dev[ib], drafts, 99 + i, (acc, tok),
@@ -1129,7 +1134,7 @@ def main():
     ap.add_argument("--eager", action="store_true",
                     help="time eager library calls instead of replays of one captured step (CUDA graph)")
     ap.add_argument("--graph-dynamic", action="store_true",
-                    help="depth-varying workloads: time replays of one profiled dynamic-depth graph")
+                    help="depth-varying Llama-shape workloads: time dynamic-depth graph replays (default: eager)")
     ap.add_argument("--prof-every", type=int, default=10,
                     help="graph-timed region: replay the event-timed copy of the step every N-th step")
     ap.add_argument("--graph", action="store_true", help="replay the step as a CUDA graph (fixed depths)")
@@ -1223,8 +1228,9 @@ def main():
             "static": "replays of one captured step (CUDA graph: drafter + verify + commit), depths fixed per request; "
                       f"every {res.get('prof_every')}-th replay from the copy whose roofline stages are event-record "
                       "nodes (per-launch averages over those), the others from the copy without events",
-            "dynamic": "replays of one dynamic-depth CUDA graph (sv_graph_begin_dynamic) with each step's depth "
-                       "vector; its roofline stages are event-record nodes timed on every replay"}[res["timed"]]
+            "dynamic": "replays of two dynamic-depth CUDA graphs of the step (sv_graph_begin_dynamic) with each "
+                       f"step's depth vector; every {res.get('prof_every')}-th replay from the copy whose roofline "
+                       "stages are event-record nodes, the others from the copy without events"}[res["timed"]]
     if res.get("graph"):
         line["config"]["graph"] = ("one dynamic-depth CUDA graph (sv_graph_begin_dynamic) replayed with each step's "
                                    "depth vector" if res["graph"] == "dynamic" else

@@ -222,9 +222,13 @@ sv_status sv_graph_begin(sv_ctx* ctx);
  * first node; row-gridded kernels are launched for batch * (max_depth + 1) rows and return beyond the
  * plan's device row count, the GEMMs read their rows from it. The slots / depths given at capture only
  * need to be valid then. Before each replay, sv_graph_set_batch stages that replay's slots and
- * depths (host-checked like sv_verify's; it waits until the previous replay has copied its values).
+ * depths (host-checked like sv_verify's); every replay of a dynamic graph takes a freshly staged batch
+ * (sv_graph_launch returns SV_ESTATE otherwise). The lane owns two pinned staging buffers that its
+ * dynamic graphs share: sv_graph_set_batch takes the next one once the replay that last read it has
+ * finished, and refuses (SV_ESTATE) while a staging of that buffer, or of the same graph, awaits its
+ * launch — so several dynamic graphs of a lane may alternate (stage one, launch it, stage the next).
  * ESTATE if the lane's GEMM / attention configuration cannot read rows from the device (SV_GEMM /
- * SV_ATTN overrides). One dynamic graph per lane at a time (they share the staging buffer). */
+ * SV_ATTN overrides). */
 sv_status sv_graph_begin_dynamic(sv_ctx* ctx, int32_t batch);
 sv_status sv_graph_set_batch(sv_ctx* ctx, const sv_graph* graph, const int32_t* slots, const int32_t* depths);
 sv_status sv_graph_end(sv_ctx* ctx, sv_graph** graph);

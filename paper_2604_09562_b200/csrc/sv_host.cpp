@@ -198,6 +198,13 @@ struct sv_ctx {
   // two pinned host buffers [2][2 max_batch] and copied to the device by the graph's first node
   int* pin_ctrl = nullptr;
   cudaEvent_t ctrl_consumed = nullptr;
+  // the two pinned staging buffers belong to the lane, so several dynamic graphs can alternate: each
+  // sv_graph_set_batch takes the next buffer (once the replay that last read it has finished) and the
+  // graph's next launch consumes it
+  long long dyn_stage_seq = 0;
+  cudaEvent_t dyn_done[2] = {nullptr, nullptr};
+  bool dyn_done_set[2] = {false, false};
+  bool dyn_unlaunched[2] = {false, false};
   bool dyn_capture = false;
   int dyn_batch = 0;
 };
@@ -454,6 +461,8 @@ sv_status sv_create(const sv_config* cfg, const sv_weights* w, void* kv_pool, vo
       (st = cuda_ok(cudaEventCreateWithFlags(&c->comm_done, cudaEventDisableTiming))) ||
       (st = cuda_ok(cudaEventCreateWithFlags(&c->lane_mark, cudaEventDisableTiming))) ||
       (st = cuda_ok(cudaEventCreateWithFlags(&c->ctrl_consumed, cudaEventDisableTiming))) ||
+      (st = cuda_ok(cudaEventCreateWithFlags(&c->dyn_done[0], cudaEventDisableTiming))) ||
+      (st = cuda_ok(cudaEventCreateWithFlags(&c->dyn_done[1], cudaEventDisableTiming))) ||
       (st = cuda_ok(cudaHostAlloc((void**)&c->pin_ctrl, 16 * (size_t)cfg->max_batch, cudaHostAllocDefault)))) {
     sv::gemm_plan_destroy(c->gemm);
     if (c->comm) cudaStreamDestroy(c->comm);
@@ -474,6 +483,8 @@ sv_status sv_destroy(sv_ctx* c) {
   cudaEventDestroy(c->comm_done);
   cudaEventDestroy(c->lane_mark);
   if (c->ctrl_consumed) cudaEventDestroy(c->ctrl_consumed);
+  for (cudaEvent_t e : c->dyn_done)
+    if (e) cudaEventDestroy(e);
   if (c->pin_ctrl) cudaFreeHost(c->pin_ctrl);
   for (cudaEvent_t e : c->rel_ev)
     if (e) cudaEventDestroy(e);
@@ -1044,9 +1055,8 @@ struct sv_graph {
   int batch;
   cudaGraph_t tmpl = nullptr;        // dynamic: the captured graph (its H2D node is retargeted per replay)
   cudaGraphNode_t h2d = nullptr;
-  mutable long long replays = 0;     // dynamic: replay r stages into pinned buffer r & 1 ...
-  mutable cudaEvent_t done[2] = {nullptr, nullptr};   // ... once replay r - 2 (same buffer) has finished
-  mutable bool done_set[2] = {false, false};
+  mutable int staged_buf = -1;       // dynamic: the lane staging buffer its next launch consumes
+  sv_ctx* ctx = nullptr;             // the lane (its staging buffers are released if the graph dies staged)
   // profiled graph (stages timed while capturing): each stage's two event-record nodes are pointed at
   // fresh pool events before every replay (cudaGraphExecEventRecordNodeSetEvent), and the pair joins the
   // lane's profile records, so per-stage CUDA-event times cover replays as they do eager calls
@@ -1099,13 +1109,18 @@ sv_status sv_graph_set_batch(sv_ctx* c, const sv_graph* g, const int32_t* slots,
   sv::PlanArgs p;
   sv_status st = check_batch(c, g->batch, slots, depths, p);   // distinct, in range, ACTIVE, depth <= max
   if (st) return st;
-  const int buf = (int)(g->replays & 1);
-  if (g->done_set[buf]) SV_CUDA(cudaEventSynchronize(g->done[buf]));   // replay r - 2 read this buffer
+  const int buf = (int)(c->dyn_stage_seq & 1);
+  if (c->dyn_unlaunched[buf]) return SV_ESTATE;           // staged for a launch that has not happened
+  if (g->staged_buf >= 0) return SV_ESTATE;               // this graph's previous staging is unlaunched
+  if (c->dyn_done_set[buf]) SV_CUDA(cudaEventSynchronize(c->dyn_done[buf]));   // its last reader finished
   int* pin = c->pin_ctrl + (size_t)buf * 2 * c->cfg.max_batch;
   memcpy(pin, slots, 4 * (size_t)g->batch);
   memcpy(pin + g->batch, depths, 4 * (size_t)g->batch);
   SV_CUDA(cudaGraphExecMemcpyNodeSetParams1D(g->exec, g->h2d, c->ws + c->lay.dctrl, pin, 8 * (size_t)g->batch,
                                              cudaMemcpyHostToDevice));
+  c->dyn_unlaunched[buf] = true;
+  g->staged_buf = buf;
+  ++c->dyn_stage_seq;
   return SV_OK;
 }
 
@@ -1136,6 +1151,7 @@ sv_status sv_graph_end(sv_ctx* c, sv_graph** out) {
     return SV_ECUDA;
   }
   sv_graph* gr = new sv_graph{x, sv::g_launch_count - c->capture_launches0, dyn, dyn_batch};
+  gr->ctx = c;
   if (profiled) {                                         // map the captured stage events to their nodes
     gr->tmpl = g;
     size_t n = 0;
@@ -1173,9 +1189,7 @@ sv_status sv_graph_end(sv_ctx* c, sv_graph** out) {
     cudaGraphNode_t root = nullptr;
     cudaGraphNodeType ty;
     if (cudaGraphGetRootNodes(g, &root, &nroot) != cudaSuccess || nroot < 1 ||
-        cudaGraphNodeGetType(root, &ty) != cudaSuccess || ty != cudaGraphNodeTypeMemcpy ||
-        cudaEventCreateWithFlags(&gr->done[0], cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&gr->done[1], cudaEventDisableTiming) != cudaSuccess) {
+        cudaGraphNodeGetType(root, &ty) != cudaSuccess || ty != cudaGraphNodeTypeMemcpy) {
       sv_graph_destroy(gr);
       return SV_ECUDA;
     }
@@ -1189,6 +1203,7 @@ sv_status sv_graph_end(sv_ctx* c, sv_graph** out) {
 sv_status sv_graph_launch(sv_ctx* c, const sv_graph* g) {
   if (!c || !g) return SV_EINVAL;
   if (c->capturing || c->pending_verify) return SV_ESTATE;
+  if (g->dynamic && g->staged_buf < 0) return SV_ESTATE;  // every replay takes a freshly staged batch
   // profiled stages: fresh events for this replay while the lane times the stage, else the idle pair
   std::vector<Prof::Rec> fresh;
   for (const auto& pn : g->prof) {
@@ -1202,21 +1217,21 @@ sv_status sv_graph_launch(sv_ctx* c, const sv_graph* g) {
   for (const auto& r : fresh) c->prof.recs.push_back(r);
   if (c->prof.recs.size() >= 8192 && c->prof.recs.size() % 1024 == 0) prof_fold(c, false);
   sv::g_launch_count += g->kernels;
-  if (g->dynamic) {
-    const int buf = (int)(g->replays & 1);
-    SV_CUDA(cudaEventRecord(g->done[buf], c->stream));
-    g->done_set[buf] = true;
-    ++g->replays;
+  if (g->dynamic) {                                       // the staged buffer is free once this replay ran
+    const int buf = g->staged_buf;
+    SV_CUDA(cudaEventRecord(c->dyn_done[buf], c->stream));
+    c->dyn_done_set[buf] = true;
+    c->dyn_unlaunched[buf] = false;
+    g->staged_buf = -1;
   }
   return SV_OK;
 }
 
 sv_status sv_graph_destroy(sv_graph* g) {
   if (!g) return SV_EINVAL;
+  if (g->dynamic && g->staged_buf >= 0 && g->ctx) g->ctx->dyn_unlaunched[g->staged_buf] = false;
   cudaGraphExecDestroy(g->exec);
   if (g->tmpl) cudaGraphDestroy(g->tmpl);
-  for (cudaEvent_t e : g->done)
-    if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : g->owned) cudaEventDestroy(e);
   for (cudaEvent_t e : g->idle)
     if (e) cudaEventDestroy(e);

@@ -266,3 +266,65 @@ def test_profiled_graph_times_every_replay():
             lane.graph_destroy(g)
     for (a0, t0), (a1, t1) in zip(*outs):
         assert torch.equal(a0, a1) and torch.equal(t0, t1)
+
+
+def test_two_dynamic_graphs_alternate():
+    """Two dynamic-depth graphs of the same step (one with event-timed stages, one without) share the
+    lane's two staging buffers: alternating them with per-replay depth vectors gives exactly the eager
+    steps; a second staging of a graph before its launch is refused, and so is a launch without one."""
+    cfg = synth.TOY_MLP
+    w = synth.model_weights(cfg, seed=0, norm_one=False)
+    w, succ = synth.planted_successor(cfg, w, seed=1, beta=0.3)
+    n = 8
+    g_ = torch.Generator().manual_seed(5)
+    depths = [[int(x) for x in torch.randint(0, 5, (4,), generator=g_)] for _ in range(n)]
+    orders = [[int(x) for x in torch.randperm(4, generator=g_)] for _ in range(n)]
+    masks, devtok = synth.planted_masks(n, 4 * 4, 0.7, cfg.vocab, seed=2)
+    outs = {}
+    for kind in ("eager", "graphs"):
+        stream = torch.cuda.Stream()
+        with torch.cuda.stream(stream):
+            lane = _lane(cfg, w, stream)
+            succ_d = succ.cuda()
+            m_stage = torch.empty(16, dtype=torch.uint8, device="cuda")
+            t_stage = torch.empty(16, dtype=torch.int32, device="cuda")
+            drafts = torch.empty(16, dtype=torch.int32, device="cuda")
+            acc = torch.empty(4, dtype=torch.int32, device="cuda")
+            tok = torch.empty(4, cfg.max_depth + 1, dtype=torch.int32, device="cuda")
+
+            def step(sl, ks):
+                lane.draft_planted(sl, ks, succ_d, m_stage, t_stage, drafts)
+                lane.verify(sl, ks, drafts, None, seed=3, mode="greedy", out=(acc, tok))
+                lane.commit()
+
+            gs = []
+            if kind == "graphs":
+                lane.profile(["lm_head"])
+                for _ in range(2):
+                    lane.graph_begin_dynamic(4)
+                    step([0, 1, 2, 3], [1, 1, 1, 1])      # captured, not run
+                    gs.append(lane.graph_end())
+                    lane.profile(False)
+                with pytest.raises(sv.SvError):
+                    lane.graph_launch(gs[0])             # nothing staged
+            res = []
+            for i in range(n):
+                m_stage.copy_(masks[i].cuda())
+                t_stage.copy_(devtok[i].cuda())
+                if kind == "eager":
+                    step(orders[i], depths[i])
+                else:
+                    g = gs[i % 2]
+                    lane.graph_set_batch(g, orders[i], depths[i])
+                    if i == 0:
+                        with pytest.raises(sv.SvError):
+                            lane.graph_set_batch(g, orders[i], depths[i])   # staged, not yet launched
+                    lane.graph_launch(g)
+                torch.cuda.synchronize()
+                res.append((acc.cpu().clone(), tok.cpu().clone()))
+            for g in gs:
+                lane.graph_destroy(g)
+            outs[kind] = (res, lane.stats())
+    for (a0, t0), (a1, t1) in zip(outs["eager"][0], outs["graphs"][0]):
+        assert torch.equal(a0, a1) and torch.equal(t0, t1)
+    assert outs["eager"][1] == outs["graphs"][1]
