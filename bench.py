@@ -846,7 +846,8 @@ def run_e2e(args, wl, lane, succ, depths, masks, devtok, dev, start):
     slots = list(range(B))
     n = args.e2e_steps
     fixed = not (wl.controller or wl.kmin != wl.kmax)
-    dyn_graph = not fixed and cfg.d_model <= 1024 and not wl.tree   # launch-bound: dynamic-depth graph
+    # depth-varying workloads: a dynamic-depth graph where launches bound the step, or with --graph-dynamic
+    dyn_graph = not fixed and not wl.tree and (cfg.d_model <= 1024 or args.graph_dynamic or args.e2e_graph)
     kr = B * wl.kmax
     h_mask = masks[start:start + n].clone().pin_memory()
     h_dev = devtok[start:start + n].clone().pin_memory()
@@ -1135,6 +1136,7 @@ def main():
                     help="time eager library calls instead of replays of one captured step (CUDA graph)")
     ap.add_argument("--graph-dynamic", action="store_true",
                     help="depth-varying Llama-shape workloads: time dynamic-depth graph replays (default: eager)")
+    ap.add_argument("--e2e-graph", action="store_true", help="e2e of depth-varying workloads through a dynamic graph")
     ap.add_argument("--prof-every", type=int, default=10,
                     help="graph-timed region: replay the event-timed copy of the step every N-th step")
     ap.add_argument("--graph", action="store_true", help="replay the step as a CUDA graph (fixed depths)")
